@@ -1,0 +1,127 @@
+/* fuseplan-b200 — C ABI of the B200 experience-collection engine.
+ *
+ * Same conventions as fp_sched.h (status codes FP_OK / FP_EINVAL /
+ * FP_EINFEASIBLE / FP_EINTERNAL, fp_last_error(), caller-owned host buffers,
+ * engine-owned device memory, no exceptions across the boundary).
+ *
+ * What it replaces in the reference: simulate_serial / simulate_fused
+ * (proj/include/fuseplan/genfuse.hpp:113-121, proj/src/genfuse.cpp:469-515)
+ * model generation and scoring with cost formulas (prefill_seconds /
+ * score_seconds / decode_step_base, genfuse.cpp:26-41, 243-245); fp_execute
+ * runs the same schedule for real on B200s and returns the experience batch,
+ * measured times, and the decision-clock result it executed (which is exactly
+ * what simulate_* return, so reference callers keep their outputs).
+ *
+ * Multi-GPU: one process per GPU; every rank calls fp_execute with the same
+ * batch / config and fp_comm{rank, world, shm_name}. cfg->num_instances must
+ * equal world. Rank 0's experience is the gathered batch.
+ *
+ * The fp_k_* entry points expose single kernels on caller-provided device
+ * pointers for parity tests (stream = cudaStream_t or NULL).
+ */
+#ifndef FP_ENGINE_H_
+#define FP_ENGINE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "fp_sched.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fp_model_dims {
+  int32_t num_layers, hidden, num_heads, num_kv_heads, head_dim, ffn, vocab;
+} fp_model_dims;
+
+typedef struct fp_engine_setup {
+  fp_model_dims actor, ref, critic, reward; /* critic/reward: vocab = embedding size only */
+  uint64_t weight_seed;
+  int32_t max_prompt, max_new, max_samples, max_live;
+  int64_t kv_pool_bytes; /* 0: max_live x (max_prompt + max_new) tokens */
+  int32_t max_prefill_tokens, max_infer_tokens;
+  float rope_theta;
+  int32_t device;
+} fp_engine_setup;
+
+enum { FP_TOKENS_FORCED = 0, FP_TOKENS_GREEDY = 1, FP_TOKENS_SAMPLE = 2 };
+enum { FP_SCHEDULE_STAGE_BARRIER = 0, FP_SCHEDULE_FUSED = 1 };
+
+typedef struct fp_run_options {
+  int32_t token_mode, schedule;
+  float temperature;
+  uint64_t token_seed, sample_seed;
+  float kl_beta, gamma, lam;
+  int32_t claim_tokens, run_ahead;
+} fp_run_options;
+
+typedef struct fp_comm {
+  int32_t rank, world;
+  const char* shm_name; /* POSIX shm name shared by all ranks ("/..."); NULL if world == 1 */
+} fp_comm;
+
+typedef struct fp_exec_stats {
+  double wall_seconds, gen_seconds, trigger_seconds, migrate_seconds, infer_busy_seconds, decode_gpu_seconds;
+  int64_t decode_steps, decode_rows, decode_ctx_tokens, prefill_tokens, infer_tokens, infer_samples;
+  int64_t migrated_in, migrated_bytes;
+  int64_t total_resp;
+} fp_exec_stats;
+
+typedef struct fp_engine fp_engine;
+typedef struct fp_exec fp_exec;
+
+int fp_engine_create(const fp_engine_setup* setup, fp_engine** out);
+void fp_engine_destroy(fp_engine* e);
+/* model: 0 actor, 1 ref, 2 critic, 3 reward. Weight bytes (device) and parameter count. */
+int fp_engine_model_size(const fp_engine* e, int32_t model, int64_t* bytes, int64_t* params);
+/* Physical KV bytes per token of the actor (bf16 K + V, GQA-aware). */
+int fp_engine_kv_bytes_per_token(const fp_engine* e, int64_t* bytes);
+/* Synthetic prompt ids [n][max_prompt] for token_seed. */
+int fp_synthetic_prompts(const fp_engine* e, int32_t n, uint64_t token_seed, int32_t* out);
+
+/* Run the stage. prompts: [n][max_prompt] ids or NULL (synthetic). */
+int fp_execute(fp_engine* e, const fp_gen_sample* batch, int32_t n, const fp_gen_config* cfg, int32_t r_t,
+               const fp_run_options* opts, const fp_comm* comm, const int32_t* prompts, fp_exec** out);
+int fp_exec_stats_get(const fp_exec* x, fp_exec_stats* s);
+/* Experience, response-aligned (total_resp entries; sample i owns
+ * [resp_off[i], resp_off[i+1])) plus score[n]. Any pointer may be NULL. */
+int fp_exec_experience(const fp_exec* x, int64_t* resp_off, int32_t* tokens, float* logp_actor, float* logp_ref,
+                       float* values, float* kl, float* reward, float* adv, float* ret, float* score);
+/* Per sample: GPU-clock finish time (s) and the instance it finished on (-1: other rank). */
+int fp_exec_finish(const fp_exec* x, double* finish_seconds, int32_t* finish_instance);
+/* Decision-clock GenStageResult of the executed schedule (free with fp_result_free). */
+int fp_exec_decision(const fp_exec* x, fp_result** out);
+/* Trigger / plan actually executed (fused, world > 1); moves in application order. */
+int fp_exec_moves(const fp_exec* x, int32_t* n_moves, int32_t* sample, int32_t* from, int32_t* to);
+void fp_exec_free(fp_exec* x);
+
+/* ---- single-kernel entry points (device pointers) ---- */
+int fp_k_init_bf16(void* w, int64_t n, uint64_t seed, uint64_t tag, float scale, void* stream);
+int fp_k_gemm_bf16(const void* W, int32_t N, int32_t K, const void* X, int32_t M, void* out, int32_t ld,
+                   void* stream);
+int fp_k_gemm_f32(const void* W, int32_t N, int32_t K, const void* X, int32_t M, float* out, int32_t splits,
+                  void* stream); /* splits <= 0: fp_k_gemm_splits(N, K) */
+int fp_k_gemm_splits(int32_t N, int32_t K);
+int fp_k_gemm_swiglu(const void* Wgu, int32_t F, int32_t K, const void* X, int32_t M, void* out, void* stream);
+/* LM head + token choice: token[M], logp[M]. mode: FP_TOKENS_*; target/sample_id/step: [M] (device). */
+int fp_k_vocab(const void* X, int32_t M, int32_t K, const void* W, int32_t V, int32_t mode, float inv_temp,
+               const int32_t* target, const int32_t* sample_id, const int32_t* step, uint64_t seed, int32_t* token,
+               float* logp, void* stream);
+int fp_k_add_norm(float* x, const float* parts, int32_t nsplit, const float* gain, void* y, int32_t M, int32_t d,
+                  void* stream);
+/* Paged decode attention. pool: [pages][L][KVH][2][64][hd] bf16; block_table [slots][bt_stride]. */
+int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t hd, const void* pool,
+                     int32_t num_layers, int32_t layer, const int32_t* block_table, int32_t bt_stride,
+                     const int32_t* slot, const int32_t* ctx, int32_t max_ctx, void* out, void* stream);
+/* Varlen causal attention; cu_host: n_seq+1 offsets (host), cu_dev the same on device. */
+int fp_k_attn_varlen(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
+                     const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream);
+int fp_k_postprocess(int32_t n, const int32_t* off, const float* logp_actor, const float* logp_ref,
+                     const float* values, const float* score, float beta, float gamma, float lam, float* kl,
+                     float* reward, float* adv, float* ret, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FP_ENGINE_H_ */

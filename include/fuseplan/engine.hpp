@@ -1,0 +1,104 @@
+// fuseplan-b200 — GPU execution of the gen+inf stage (extension of genfuse.hpp).
+//
+// execute() runs the experience-collection stage for real on B200s: the
+// actor's batched decode (paged KV, retire-on-finish, KV-gated admission with
+// the reference's reservation rule, genfuse.cpp:226-236), sample-level
+// streaming of finished samples into Reference/Critic/Reward scoring, per-token
+// post-processing (KL, reward, GAE, returns), and — in the fused schedule on
+// G > 1 instances — the one-shot long-tail migration at the trigger.
+//
+// Decisions (sample -> instance assignment, trigger, m, destinations,
+// migrated set, mechanism, in-flight placement) are taken on the decision
+// clock (simulate_fused / fused_trigger), so they are bit-exact with the
+// reference; the engine then executes them and measures wall time separately.
+// One process per GPU: rank r executes instance r of cfg.num_instances.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "fuseplan/genfuse.hpp"
+
+namespace fuseplan {
+
+/// Transformer shape of one engine model (Llama-style: RMSNorm, RoPE, GQA, SwiGLU).
+struct EngineModelDims {
+  int num_layers = 0, hidden = 0, num_heads = 0, num_kv_heads = 0, head_dim = 0, ffn = 0, vocab = 0;
+};
+
+struct EngineSetup {
+  EngineModelDims actor, ref, critic, reward;
+  std::uint64_t weight_seed = 1234;
+  int max_prompt = 128;
+  int max_new = 1024;
+  int max_samples = 512;
+  int max_live = 512;
+  std::int64_t kv_pool_bytes = 0;
+  int max_prefill_tokens = 16384;
+  int max_infer_tokens = 16384;
+  float rope_theta = 10000.f;
+  int device = 0;
+};
+
+enum class TokenMode : int { kForced = 0, kGreedy = 1, kSample = 2 };
+enum class Schedule : int { kStageBarrier = 0, kFused = 1 };
+
+struct EngineOptions {
+  TokenMode token_mode = TokenMode::kForced;
+  Schedule schedule = Schedule::kFused;
+  float temperature = 1.0f;
+  std::uint64_t token_seed = 7;    // synthetic prompts / forced responses
+  std::uint64_t sample_seed = 11;  // Philox streams of the sampler
+  float kl_beta = 0.05f, gamma = 1.0f, lam = 0.95f;
+  int claim_tokens = 8192;         // scoring batch granularity (tokens)
+  int run_ahead = 4;               // decode steps the host may enqueue ahead of the GPU
+};
+
+/// Multi-process coordination (G > 1): every rank passes the same shm name.
+struct CommSetup {
+  int rank = 0;
+  int world = 1;
+  std::string shm_name;  // empty when world == 1
+};
+
+struct ExperienceBatch {
+  std::vector<std::int64_t> resp_off;  // n + 1 response offsets
+  std::vector<int> tokens;             // response token ids
+  std::vector<float> logp_actor, logp_ref, values, kl, reward, adv, ret;
+  std::vector<float> score;            // per sample
+};
+
+struct ExecStats {
+  double wall_seconds = 0.0;        // whole stage on this rank (host clock, start barrier -> end)
+  double gen_seconds = 0.0;         // this rank's last decode step end (GPU clock from start)
+  double trigger_seconds = -1.0;    // trigger reached (GPU clock), -1 if none
+  double migrate_seconds = 0.0;     // migration exchange (host clock)
+  double infer_busy_seconds = 0.0;  // GPU time of this rank's scoring batches
+  std::int64_t decode_steps = 0, decode_rows = 0, decode_ctx_tokens = 0;
+  std::int64_t prefill_tokens = 0, infer_tokens = 0, infer_samples = 0;
+  std::int64_t migrated_in = 0, migrated_bytes = 0;
+  double decode_gpu_seconds = 0.0;  // sum of decode-step GPU durations
+};
+
+struct ExecResult {
+  GenStageResult decision;          // decision-clock result of the same schedule
+  TriggerSnapshot trigger;          // plan taken (fused, G > 1)
+  std::vector<double> finish_wall;  // per sample: GPU-clock finish time (seconds), on its final instance
+  std::vector<int> finish_instance;
+  ExperienceBatch experience;       // complete on rank 0 (gathered), local part elsewhere
+  ExecStats stats;
+};
+
+class GpuEngine;  // opaque
+
+GpuEngine* create_engine(const EngineSetup& setup);
+void destroy_engine(GpuEngine* e);
+
+/// Synthetic prompts (hash of token_seed) of shape [n][max_prompt].
+std::vector<int> synthetic_prompts(const GpuEngine* e, int n, std::uint64_t token_seed);
+
+ExecResult execute(GpuEngine* e, const std::vector<GenSample>& batch, const GenSimConfig& cfg, int r_t,
+                   const EngineOptions& opts, const CommSetup& comm, const std::vector<int>* prompts = nullptr);
+
+}  // namespace fuseplan

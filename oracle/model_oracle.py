@@ -1,0 +1,306 @@
+"""ORACLE — test infrastructure only (never imported by the product path).
+
+CPU restatement (numpy, fp32 activations, bf16-rounded weights) of what the
+B200 engine computes for the experience-collection path:
+
+  * synthetic weights / prompts / forced responses from the same integer hash
+    as csrc/kernels/philox.cuh (bit-identical bf16 weights);
+  * Llama-style forward: RMSNorm (eps 1e-5, fp32 gain), rotate-half RoPE
+    (theta 1e4), causal softmax attention with GQA, SwiGLU MLP, untied LM head
+    (actor / reference) or a d -> 1 value head (critic / reward);
+  * actor log-probs of the response tokens (teacher-forced: the full causal
+    forward equals incremental decode), greedy incremental decode with a KV
+    cache (for the token agreement rate), Gumbel-max sampling with the same
+    Philox4x32-10 streams as the GPU sampler;
+  * reference log-probs, critic values at positions P-1 .. P+R-2, reward score
+    at position P+R-1;
+  * post-processing: KL, reward shaping, GAE (the recursion of
+    proj/src/numerics.cpp:27-34 with the explicit V_R = 0 bootstrap), returns
+    (oracle/post_oracle.c restates the same in C).
+
+PPO/KL and transformer math do not exist in the reference (SPEC.md:512 — an
+explicit non-goal), so for those quantities parity is pinned only by this
+oracle ("parity unpinned by the reference"); the GAE part is pinned against
+the reference's golden vectors and library (tests/test_oracle.py).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+M64 = (1 << 64) - 1
+GOLDEN = 0x9E3779B97F4A7C15
+TAG_EMBED, TAG_WQKV, TAG_WO, TAG_WGU, TAG_WD, TAG_LN1, TAG_LN2, TAG_LNF, TAG_HEAD, TAG_VHEAD = range(1, 11)
+TAG_PROMPT, TAG_RESPONSE = 0xF1, 0xF2
+ACTOR, REF, CRITIC, REWARD = 0, 1, 2, 3
+
+
+def weight_tag(model: int, layer: int, kind: int) -> int:
+    return (model << 24) | (layer << 8) | kind
+
+
+def hash3(seed: int, tag: int, idx: np.ndarray) -> np.ndarray:
+    """splitmix64 finaliser of (seed, tag, index) — philox.cuh:hash3."""
+    z0 = (seed ^ ((tag * 0xD1B54A32D192ED03) & M64)) & M64
+    z = np.uint64(z0) + (idx.astype(np.uint64) + np.uint64(1)) * np.uint64(GOLDEN)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def unit24(h: np.ndarray) -> np.ndarray:
+    return (h >> np.uint64(40)).astype(np.float32) * np.float32(1.0 / 16777216.0)
+
+
+def to_bf16(x: np.ndarray) -> np.ndarray:
+    """Round-to-nearest-even fp32 -> bf16, returned as fp32 values."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = (b + np.uint64(0x7FFF) + ((b >> np.uint64(16)) & np.uint64(1))) & np.uint64(0xFFFF0000)
+    return b.astype(np.uint32).view(np.float32)
+
+
+def uniform_weight(seed, tag, n, scale) -> np.ndarray:
+    t = unit24(hash3(seed, tag, np.arange(n, dtype=np.uint64))) * np.float32(2.0) - np.float32(1.0)
+    return to_bf16(t * np.float32(scale))
+
+
+def gain(seed, tag, n) -> np.ndarray:
+    t = unit24(hash3(seed, tag, np.arange(n, dtype=np.uint64))) * np.float32(2.0) - np.float32(1.0)
+    return np.float32(1.0) + np.float32(0.1) * t
+
+
+def fsqrt(x) -> np.float32:
+    return np.sqrt(np.float32(x))
+
+
+def make_weights(dims, model: int, seed: int) -> dict:
+    """Same tensors, same bits as Engine::init_model (engine.cpp)."""
+    L, d, H, KVH, hd, F, V = (dims.num_layers, dims.hidden, dims.num_heads, dims.num_kv_heads, dims.head_dim,
+                              dims.ffn, dims.vocab)
+    qw, ao = (H + 2 * KVH) * hd, H * hd
+    W = {"dims": dims, "embed": uniform_weight(seed, weight_tag(model, 0, TAG_EMBED), V * d, 1.0).reshape(V, d),
+         "layers": []}
+    for l in range(L):
+        gu = uniform_weight(seed, weight_tag(model, l, TAG_WGU), 2 * F * d, fsqrt(np.float32(3.0) / np.float32(d)))
+        gu = gu.reshape(2 * F, d)
+        W["layers"].append({
+            "wqkv": uniform_weight(seed, weight_tag(model, l, TAG_WQKV), qw * d,
+                                   fsqrt(np.float32(3.0) / np.float32(d))).reshape(qw, d),
+            "wo": uniform_weight(seed, weight_tag(model, l, TAG_WO), d * ao,
+                                 fsqrt(np.float32(3.0) / np.float32(ao))).reshape(d, ao),
+            "wg": gu[:F], "wu": gu[F:],
+            "wd": uniform_weight(seed, weight_tag(model, l, TAG_WD), d * F,
+                                 fsqrt(np.float32(3.0) / np.float32(F))).reshape(d, F),
+            "ln1": gain(seed, weight_tag(model, l, TAG_LN1), d),
+            "ln2": gain(seed, weight_tag(model, l, TAG_LN2), d),
+        })
+    W["lnf"] = gain(seed, weight_tag(model, 0, TAG_LNF), d)
+    if model in (ACTOR, REF):
+        W["head"] = uniform_weight(seed, weight_tag(model, 0, TAG_HEAD), V * d,
+                                   fsqrt(np.float32(3.0) / np.float32(d))).reshape(V, d)
+    else:
+        W["vhead"] = uniform_weight(seed, weight_tag(model, 0, TAG_VHEAD), d, fsqrt(np.float32(3.0) / np.float32(d)))
+    return W
+
+
+def synthetic_prompts(n: int, max_prompt: int, vocab: int, token_seed: int) -> np.ndarray:
+    h = hash3(token_seed, TAG_PROMPT, np.arange(n * max_prompt, dtype=np.uint64))
+    return ((h >> np.uint64(32)) % np.uint64(vocab)).astype(np.int64).reshape(n, max_prompt)
+
+
+def forced_response(sid: int, R: int, max_new: int, vocab: int, token_seed: int) -> np.ndarray:
+    idx = np.uint64(sid * max_new) + np.arange(R, dtype=np.uint64)
+    return ((hash3(token_seed, TAG_RESPONSE, idx) >> np.uint64(32)) % np.uint64(vocab)).astype(np.int64)
+
+
+# ---------------------------------------------------------------------------
+# forward pieces (fp32)
+
+def rmsnorm(x, g):
+    return x / np.sqrt(np.mean(x * x, axis=-1, keepdims=True) + np.float32(1e-5)) * g
+
+
+def rope(x, pos, theta=10000.0):
+    """x [T, heads, hd] fp32, pos [T]; rotate-half pairs (i, i + hd/2)."""
+    hd = x.shape[-1]
+    half = hd // 2
+    i = np.arange(half, dtype=np.float32)
+    inv = np.exp2(-(np.float32(2.0) * i / np.float32(hd)) * np.float32(math.log2(theta))).astype(np.float32)
+    ang = pos.astype(np.float32)[:, None] * inv[None, :]
+    c, s = np.cos(ang)[:, None, :], np.sin(ang)[:, None, :]
+    x1, x2 = x[..., :half], x[..., half:]
+    return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+
+def silu(x):
+    return x / (np.float32(1.0) + np.exp(-x))
+
+
+def forward(W, tokens: np.ndarray) -> np.ndarray:
+    """Full causal forward of one sequence; returns the final normed hidden [T, d]."""
+    D = W["dims"]
+    H, KVH, hd = D.num_heads, D.num_kv_heads, D.head_dim
+    T = len(tokens)
+    x = W["embed"][tokens].astype(np.float32)
+    pos = np.arange(T)
+    mask = np.triu(np.full((T, T), -np.inf, dtype=np.float32), 1)
+    for Lw in W["layers"]:
+        h = rmsnorm(x, Lw["ln1"])
+        qkv = h @ Lw["wqkv"].T
+        q = qkv[:, :H * hd].reshape(T, H, hd)
+        k = qkv[:, H * hd:(H + KVH) * hd].reshape(T, KVH, hd)
+        v = qkv[:, (H + KVH) * hd:].reshape(T, KVH, hd)
+        q, k = rope(q, pos), rope(k, pos)
+        g = H // KVH
+        k = np.repeat(k, g, axis=1)
+        v = np.repeat(v, g, axis=1)
+        s = np.einsum("thd,shd->hts", q, k) / np.float32(math.sqrt(hd)) + mask[None]
+        s = s - s.max(-1, keepdims=True)
+        p = np.exp(s)
+        p /= p.sum(-1, keepdims=True)
+        o = np.einsum("hts,shd->thd", p, v).reshape(T, H * hd)
+        x = x + o @ Lw["wo"].T
+        h = rmsnorm(x, Lw["ln2"])
+        x = x + (silu(h @ Lw["wg"].T) * (h @ Lw["wu"].T)) @ Lw["wd"].T
+    return rmsnorm(x, W["lnf"])
+
+
+def log_softmax(z):
+    m = z.max(-1, keepdims=True)
+    return z - m - np.log(np.exp(z - m).sum(-1, keepdims=True))
+
+
+# ---------------------------------------------------------------------------
+# Philox4x32-10 + Gumbel (the GPU sampler's streams)
+
+def philox4x32_10(ctr: np.ndarray, k0: int, k1: int) -> np.ndarray:
+    """ctr uint32 [..., 4] -> uint32 [..., 4]."""
+    c = ctr.astype(np.uint64)
+    k0 = np.uint64(k0 & 0xFFFFFFFF)
+    k1 = np.uint64(k1 & 0xFFFFFFFF)
+    m32 = np.uint64(0xFFFFFFFF)
+    for _ in range(10):
+        p0 = np.uint64(0xD2511F53) * c[..., 0]
+        p1 = np.uint64(0xCD9E8D57) * c[..., 2]
+        hi0, lo0 = p0 >> np.uint64(32), p0 & m32
+        hi1, lo1 = p1 >> np.uint64(32), p1 & m32
+        c = np.stack([(hi1 ^ c[..., 1] ^ k0) & m32, lo1, (hi0 ^ c[..., 3] ^ k1) & m32, lo0], axis=-1)
+        k0 = (k0 + np.uint64(0x9E3779B9)) & m32
+        k1 = (k1 + np.uint64(0xBB67AE85)) & m32
+    return c.astype(np.uint32)
+
+
+def gumbel_noise(seed: int, sample_id: int, step: int, vocab: int) -> np.ndarray:
+    nq = (vocab + 3) // 4
+    ctr = np.zeros((nq, 4), dtype=np.uint32)
+    ctr[:, 0] = np.arange(nq, dtype=np.uint32)
+    ctr[:, 1] = step
+    ctr[:, 2] = sample_id
+    ctr[:, 3] = 0xF00D
+    w = philox4x32_10(ctr, seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF).reshape(-1)[:vocab]
+    u = ((w >> np.uint32(8)).astype(np.float32) + np.float32(0.5)) * np.float32(1.0 / 16777216.0)
+    return -np.log(-np.log(u))
+
+
+# ---------------------------------------------------------------------------
+# experience
+
+def postprocess(logp_actor, logp_ref, values, score, beta, gamma, lam):
+    """fp64 KL / reward / GAE / returns of one sample (numerics.cpp:27-34 recursion)."""
+    la, lr, v = (np.asarray(a, dtype=np.float64) for a in (logp_actor, logp_ref, values))
+    R = len(la)
+    kl = la - lr
+    rew = -beta * kl
+    rew[-1] += score
+    v_next = np.append(v[1:], 0.0)
+    adv = rew + gamma * v_next - v
+    c = gamma * lam
+    for t in range(R - 2, -1, -1):
+        adv[t] += c * adv[t + 1]
+    return {"kl": kl, "reward": rew, "adv": adv, "ret": adv + v}
+
+
+class Oracle:
+    """The four synthetic models of one workload."""
+
+    def __init__(self, workload, weight_seed: int = 1234):
+        self.w = workload
+        self.models = [make_weights(workload.actor, ACTOR, weight_seed), make_weights(workload.ref, REF, weight_seed),
+                       make_weights(workload.critic, CRITIC, weight_seed),
+                       make_weights(workload.reward, REWARD, weight_seed)]
+
+    def score_sample(self, prompt: np.ndarray, response: np.ndarray, temperature: float = 1.0) -> dict:
+        """Teacher-forced pass of one (prompt, response): every per-token quantity."""
+        toks = np.concatenate([prompt, response])
+        P, R = len(prompt), len(response)
+        rows = np.arange(P - 1, P + R - 1)
+        out = {}
+        for name, m in (("logp_actor", ACTOR), ("logp_ref", REF)):
+            h = forward(self.models[m], toks)[rows]
+            z = (h @ self.models[m]["head"].T) / np.float32(temperature if name == "logp_actor" else 1.0)
+            out[name] = log_softmax(z)[np.arange(R), response]
+        hc = forward(self.models[CRITIC], toks)
+        out["values"] = hc[rows] @ self.models[CRITIC]["vhead"]
+        hr = forward(self.models[REWARD], toks)
+        out["score"] = float(hr[-1] @ self.models[REWARD]["vhead"])
+        return out
+
+    def experience(self, prompt, response, beta, gamma, lam, temperature=1.0) -> dict:
+        s = self.score_sample(prompt, response, temperature)
+        s.update(postprocess(s["logp_actor"], s["logp_ref"], s["values"], s["score"], beta, gamma, lam))
+        s["tokens"] = np.asarray(response)
+        return s
+
+    def decode(self, prompt: np.ndarray, R: int, mode: str = "greedy", sample_id: int = 0, seed: int = 11,
+               temperature: float = 1.0) -> tuple:
+        """Incremental decode of R tokens (KV cache); returns (tokens, logps)."""
+        W = self.models[ACTOR]
+        D = W["dims"]
+        H, KVH, hd = D.num_heads, D.num_kv_heads, D.head_dim
+        g = H // KVH
+        toks = list(prompt)
+        out_t, out_lp = [], []
+        K = [np.zeros((0, KVH, hd), np.float32) for _ in W["layers"]]
+        Vc = [np.zeros((0, KVH, hd), np.float32) for _ in W["layers"]]
+
+        def step(tok_ids, pos0):
+            T = len(tok_ids)
+            x = W["embed"][np.asarray(tok_ids)].astype(np.float32)
+            pos = np.arange(pos0, pos0 + T)
+            for li, Lw in enumerate(W["layers"]):
+                h = rmsnorm(x, Lw["ln1"])
+                qkv = h @ Lw["wqkv"].T
+                q = rope(qkv[:, :H * hd].reshape(T, H, hd), pos)
+                k = rope(qkv[:, H * hd:(H + KVH) * hd].reshape(T, KVH, hd), pos)
+                v = qkv[:, (H + KVH) * hd:].reshape(T, KVH, hd)
+                K[li] = np.concatenate([K[li], k])
+                Vc[li] = np.concatenate([Vc[li], v])
+                kk, vv = np.repeat(K[li], g, axis=1), np.repeat(Vc[li], g, axis=1)
+                S = K[li].shape[0]
+                s = np.einsum("thd,shd->hts", q, kk) / np.float32(math.sqrt(hd))
+                s = s + np.triu(np.full((T, S), -np.inf, np.float32), S - T + 1)[None]
+                s = s - s.max(-1, keepdims=True)
+                p = np.exp(s)
+                p /= p.sum(-1, keepdims=True)
+                o = np.einsum("hts,shd->thd", p, vv).reshape(T, H * hd)
+                x = x + o @ Lw["wo"].T
+                h = rmsnorm(x, Lw["ln2"])
+                x = x + (silu(h @ Lw["wg"].T) * (h @ Lw["wu"].T)) @ Lw["wd"].T
+            return rmsnorm(x[-1:], W["lnf"])[0]
+
+        if len(toks) > 1:
+            step(toks[:-1], 0)
+        cur, pos = toks[-1], len(toks) - 1
+        for k in range(R):
+            h = step([cur], pos)
+            z = (h @ W["head"].T) / np.float32(temperature)
+            lp = log_softmax(z)
+            if mode == "greedy":
+                t = int(np.argmax(z))
+            else:
+                t = int(np.argmax(z + gumbel_noise(seed, sample_id, k, len(z))))
+            out_t.append(t)
+            out_lp.append(float(lp[t]))
+            cur, pos = t, pos + 1
+        return np.asarray(out_t), np.asarray(out_lp)

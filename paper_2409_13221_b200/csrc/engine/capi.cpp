@@ -1,0 +1,407 @@
+// fuseplan-b200 — C ABI of the engine (include/fp_engine.h).
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "fp_engine.h"
+#include "fuseplan/engine.hpp"
+#include "fuseplan/errors.hpp"
+#include "ops.h"
+
+void fp_set_last_error_internal(const char* msg);             // sched_capi.cpp
+const fpe::Engine& fp_engine_internal(const fuseplan::GpuEngine* g);  // executor.cpp
+
+struct fp_engine {
+  fuseplan::GpuEngine* g = nullptr;
+  fuseplan::EngineSetup setup;
+};
+struct fp_exec {
+  fuseplan::ExecResult r;
+};
+// fp_result is defined by sched_capi.cpp with this exact layout.
+struct fp_result {
+  fuseplan::GenStageResult r;
+};
+
+namespace {
+
+// fp_last_error() lives in sched_capi.cpp; its storage is shared through a setter.
+template <typename F>
+int guarded(F&& body) {
+  try {
+    body();
+    return FP_OK;
+  } catch (const fuseplan::InfeasibleError& e) {
+    fp_set_last_error_internal(e.what());
+    return FP_EINFEASIBLE;
+  } catch (const fuseplan::ConfigError& e) {
+    fp_set_last_error_internal(e.what());
+    return FP_EINVAL;
+  } catch (const std::invalid_argument& e) {
+    fp_set_last_error_internal(e.what());
+    return FP_EINVAL;
+  } catch (const std::exception& e) {
+    fp_set_last_error_internal(e.what());
+    return FP_EINTERNAL;
+  } catch (...) {
+    fp_set_last_error_internal("unknown error");
+    return FP_EINTERNAL;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw std::invalid_argument(std::string("null argument: ") + what);
+}
+
+fuseplan::EngineModelDims dims(const fp_model_dims& m) {
+  return {m.num_layers, m.hidden, m.num_heads, m.num_kv_heads, m.head_dim, m.ffn, m.vocab};
+}
+
+fuseplan::ModelSpec model_of(const fp_model_spec& m) {
+  fuseplan::ModelSpec s;
+  s.name = m.name ? m.name : "";
+  s.num_layers = m.num_layers;
+  s.num_heads = m.num_heads;
+  s.hidden_size = m.hidden_size;
+  s.intermediate_size = m.intermediate_size;
+  return s;
+}
+
+fuseplan::GenSimConfig config_of(const fp_gen_config* c) {
+  need(c, "cfg");
+  fuseplan::GenSimConfig g;
+  g.actor = model_of(c->actor);
+  g.num_instances = c->num_instances;
+  g.instance_gpus = c->instance_gpus;
+  for (int i = 0; i < c->num_tasks; ++i) {
+    fuseplan::InferenceTask t;
+    t.model = model_of(c->tasks[i]);
+    t.name = (c->task_names && c->task_names[i]) ? c->task_names[i] : t.model.name;
+    g.tasks.push_back(t);
+  }
+  g.cluster.num_gpus = c->cluster.num_gpus;
+  g.cluster.gpus_per_node = c->cluster.gpus_per_node;
+  g.cluster.activation_capacity_per_stage = c->cluster.activation_capacity_per_stage;
+  g.cluster.kv_capacity_per_instance = c->cluster.kv_capacity_per_instance;
+  g.cluster.bs_max = c->cluster.bs_max;
+  g.cluster.interconnect_bandwidth = c->cluster.interconnect_bandwidth;
+  g.cost.time_per_token_coeff = c->cost.time_per_token_coeff;
+  g.cost.backward_forward_ratio = c->cost.backward_forward_ratio;
+  g.cost.activation_bytes_coeff = c->cost.activation_bytes_coeff;
+  g.cost.decode_step_base = c->cost.decode_step_base;
+  g.cost.comm_bandwidth = c->cost.comm_bandwidth;
+  return g;
+}
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+using bf16 = __nv_bfloat16;
+
+void after_launch() {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw fpe::CudaError(std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+extern "C" {
+
+int fp_engine_create(const fp_engine_setup* s, fp_engine** out) {
+  return guarded([&] {
+    need(s, "setup");
+    need(out, "out");
+    fuseplan::EngineSetup es;
+    es.actor = dims(s->actor);
+    es.ref = dims(s->ref);
+    es.critic = dims(s->critic);
+    es.reward = dims(s->reward);
+    es.weight_seed = s->weight_seed;
+    es.max_prompt = s->max_prompt;
+    es.max_new = s->max_new;
+    es.max_samples = s->max_samples;
+    es.max_live = s->max_live;
+    es.kv_pool_bytes = s->kv_pool_bytes;
+    es.max_prefill_tokens = s->max_prefill_tokens;
+    es.max_infer_tokens = s->max_infer_tokens;
+    es.rope_theta = s->rope_theta;
+    es.device = s->device;
+    if (es.max_prompt < 1 || es.max_new < 1 || es.max_samples < 1 || es.max_live < 1)
+      throw std::invalid_argument("engine setup: sizes must be positive");
+    auto* e = new fp_engine;
+    e->setup = es;
+    try {
+      e->g = fuseplan::create_engine(es);
+    } catch (...) {
+      delete e;
+      throw;
+    }
+    *out = e;
+  });
+}
+
+void fp_engine_destroy(fp_engine* e) {
+  if (!e) return;
+  fuseplan::destroy_engine(e->g);
+  delete e;
+}
+
+int fp_engine_model_size(const fp_engine* e, int32_t model, int64_t* bytes, int64_t* params) {
+  return guarded([&] {
+    need(e, "engine");
+    if (model < 0 || model > 3) throw std::invalid_argument("model index out of range");
+    const fpe::ModelW& w = fp_engine_internal(e->g).model(model);
+    if (bytes) *bytes = static_cast<int64_t>(w.bytes);
+    if (params) *params = static_cast<int64_t>(w.param_count);
+  });
+}
+
+int fp_engine_kv_bytes_per_token(const fp_engine* e, int64_t* bytes) {
+  return guarded([&] {
+    need(e, "engine");
+    need(bytes, "bytes");
+    *bytes = static_cast<int64_t>(fp_engine_internal(e->g).config().model[fpe::kActor].kv_bytes_per_token());
+  });
+}
+
+int fp_synthetic_prompts(const fp_engine* e, int32_t n, uint64_t token_seed, int32_t* out) {
+  return guarded([&] {
+    need(e, "engine");
+    need(out, "out");
+    const std::vector<int> p = fuseplan::synthetic_prompts(e->g, n, token_seed);
+    std::memcpy(out, p.data(), p.size() * 4);
+  });
+}
+
+int fp_execute(fp_engine* e, const fp_gen_sample* batch, int32_t n, const fp_gen_config* cfg, int32_t r_t,
+               const fp_run_options* o, const fp_comm* comm, const int32_t* prompts, fp_exec** out) {
+  return guarded([&] {
+    need(e, "engine");
+    need(o, "opts");
+    need(out, "out");
+    if (n < 1) throw std::invalid_argument("execute: empty batch");
+    need(batch, "batch");
+    std::vector<fuseplan::GenSample> b(n);
+    for (int i = 0; i < n; ++i)
+      b[i] = {batch[i].id, batch[i].prompt_len, batch[i].target_output_len, batch[i].generated, batch[i].kv_bytes};
+    fuseplan::EngineOptions eo;
+    if (o->token_mode < 0 || o->token_mode > 2) throw std::invalid_argument("token_mode out of range");
+    eo.token_mode = static_cast<fuseplan::TokenMode>(o->token_mode);
+    eo.schedule = o->schedule == FP_SCHEDULE_FUSED ? fuseplan::Schedule::kFused : fuseplan::Schedule::kStageBarrier;
+    eo.temperature = o->temperature > 0.f ? o->temperature : 1.0f;
+    eo.token_seed = o->token_seed;
+    eo.sample_seed = o->sample_seed;
+    eo.kl_beta = o->kl_beta;
+    eo.gamma = o->gamma;
+    eo.lam = o->lam;
+    if (eo.gamma < 0.f || eo.gamma > 1.f || eo.lam < 0.f || eo.lam > 1.f)
+      throw std::invalid_argument("GaeInputs: gamma and lam must lie in [0, 1]");
+    eo.claim_tokens = o->claim_tokens > 0 ? o->claim_tokens : 8192;
+    eo.run_ahead = o->run_ahead > 0 ? o->run_ahead : 4;
+    fuseplan::CommSetup cs;
+    if (comm) {
+      cs.rank = comm->rank;
+      cs.world = comm->world;
+      cs.shm_name = comm->shm_name ? comm->shm_name : "";
+    }
+    if (cs.world > 1 && cs.shm_name.empty()) throw std::invalid_argument("comm: shm_name required for world > 1");
+    std::vector<int> pv;
+    if (prompts) pv.assign(prompts, prompts + static_cast<size_t>(n) * e->setup.max_prompt);
+    auto* x = new fp_exec;
+    try {
+      x->r = fuseplan::execute(e->g, b, config_of(cfg), r_t, eo, cs, prompts ? &pv : nullptr);
+    } catch (...) {
+      delete x;
+      throw;
+    }
+    *out = x;
+  });
+}
+
+int fp_exec_stats_get(const fp_exec* x, fp_exec_stats* s) {
+  return guarded([&] {
+    need(x, "exec");
+    need(s, "stats");
+    const fuseplan::ExecStats& t = x->r.stats;
+    s->wall_seconds = t.wall_seconds;
+    s->gen_seconds = t.gen_seconds;
+    s->trigger_seconds = t.trigger_seconds;
+    s->migrate_seconds = t.migrate_seconds;
+    s->infer_busy_seconds = t.infer_busy_seconds;
+    s->decode_gpu_seconds = t.decode_gpu_seconds;
+    s->decode_steps = t.decode_steps;
+    s->decode_rows = t.decode_rows;
+    s->decode_ctx_tokens = t.decode_ctx_tokens;
+    s->prefill_tokens = t.prefill_tokens;
+    s->infer_tokens = t.infer_tokens;
+    s->infer_samples = t.infer_samples;
+    s->migrated_in = t.migrated_in;
+    s->migrated_bytes = t.migrated_bytes;
+    s->total_resp = x->r.experience.resp_off.empty() ? 0 : x->r.experience.resp_off.back();
+  });
+}
+
+int fp_exec_experience(const fp_exec* x, int64_t* resp_off, int32_t* tokens, float* logp_actor, float* logp_ref,
+                       float* values, float* kl, float* reward, float* adv, float* ret, float* score) {
+  return guarded([&] {
+    need(x, "exec");
+    const fuseplan::ExperienceBatch& b = x->r.experience;
+    auto cp = [](auto* dst, const auto& v) {
+      if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(resp_off, b.resp_off);
+    cp(tokens, b.tokens);
+    cp(logp_actor, b.logp_actor);
+    cp(logp_ref, b.logp_ref);
+    cp(values, b.values);
+    cp(kl, b.kl);
+    cp(reward, b.reward);
+    cp(adv, b.adv);
+    cp(ret, b.ret);
+    cp(score, b.score);
+  });
+}
+
+int fp_exec_finish(const fp_exec* x, double* finish_seconds, int32_t* finish_instance) {
+  return guarded([&] {
+    need(x, "exec");
+    if (finish_seconds) std::memcpy(finish_seconds, x->r.finish_wall.data(), x->r.finish_wall.size() * 8);
+    if (finish_instance)
+      for (size_t i = 0; i < x->r.finish_instance.size(); ++i) finish_instance[i] = x->r.finish_instance[i];
+  });
+}
+
+int fp_exec_decision(const fp_exec* x, fp_result** out) {
+  return guarded([&] {
+    need(x, "exec");
+    need(out, "out");
+    *out = new fp_result{x->r.decision};
+  });
+}
+
+int fp_exec_moves(const fp_exec* x, int32_t* n_moves, int32_t* sample, int32_t* from, int32_t* to) {
+  return guarded([&] {
+    need(x, "exec");
+    const auto& t = x->r.trigger;
+    if (n_moves) *n_moves = static_cast<int32_t>(t.move_sample.size());
+    for (size_t i = 0; i < t.move_sample.size(); ++i) {
+      if (sample) sample[i] = t.move_sample[i];
+      if (from) from[i] = t.move_from[i];
+      if (to) to[i] = t.move_to[i];
+    }
+  });
+}
+
+void fp_exec_free(fp_exec* x) { delete x; }
+
+// ---- single kernels ----------------------------------------------------------------
+
+int fp_k_init_bf16(void* w, int64_t n, uint64_t seed, uint64_t tag, float scale, void* stream) {
+  return guarded([&] {
+    fpk::init_bf16(static_cast<bf16*>(w), static_cast<size_t>(n), seed, tag, scale, S(stream));
+    after_launch();
+  });
+}
+
+int fp_k_gemm_bf16(const void* W, int32_t N, int32_t K, const void* X, int32_t M, void* out, int32_t ld,
+                   void* stream) {
+  return guarded([&] {
+    fpk::gemm_bf16(static_cast<const bf16*>(W), N, K, static_cast<const bf16*>(X), M, static_cast<bf16*>(out), ld,
+                   S(stream));
+    after_launch();
+  });
+}
+
+int fp_k_gemm_splits(int32_t N, int32_t K) { return fpk::gemm_splits(N, K); }
+
+int fp_k_gemm_f32(const void* W, int32_t N, int32_t K, const void* X, int32_t M, float* out, int32_t splits,
+                  void* stream) {
+  return guarded([&] {
+    fpk::gemm_f32_splitk(static_cast<const bf16*>(W), N, K, static_cast<const bf16*>(X), M, out,
+                         splits > 0 ? splits : fpk::gemm_splits(N, K), S(stream));
+    after_launch();
+  });
+}
+
+int fp_k_gemm_swiglu(const void* Wgu, int32_t F, int32_t K, const void* X, int32_t M, void* out, void* stream) {
+  return guarded([&] {
+    fpk::gemm_swiglu(static_cast<const bf16*>(Wgu), F, K, static_cast<const bf16*>(X), M, static_cast<bf16*>(out),
+                     S(stream));
+    after_launch();
+  });
+}
+
+int fp_k_vocab(const void* X, int32_t M, int32_t K, const void* W, int32_t V, int32_t mode, float inv_temp,
+               const int32_t* target, const int32_t* sample_id, const int32_t* step, uint64_t seed, int32_t* token,
+               float* logp, void* stream) {
+  return guarded([&] {
+    void* part = nullptr;
+    float* tz = nullptr;
+    fpe::check(cudaMallocAsync(&part, static_cast<size_t>(M) * fpk::vocab_tiles(V) * 24 + 256, S(stream)), "alloc");
+    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&tz), static_cast<size_t>(M) * 4 + 256, S(stream)), "alloc");
+    fpk::gemm_vocab(static_cast<const bf16*>(X), M, K, static_cast<const bf16*>(W), V, mode, inv_temp, target,
+                    sample_id, step, seed, part, tz, S(stream));
+    fpk::vocab_finalize(part, tz, M, V, mode, target, token, logp, nullptr, nullptr, nullptr, nullptr, nullptr,
+                        S(stream));
+    after_launch();
+    fpe::check(cudaFreeAsync(part, S(stream)), "free");
+    fpe::check(cudaFreeAsync(tz, S(stream)), "free");
+  });
+}
+
+int fp_k_add_norm(float* x, const float* parts, int32_t nsplit, const float* gain, void* y, int32_t M, int32_t d,
+                  void* stream) {
+  return guarded([&] {
+    fpk::add_norm(x, parts, nsplit, static_cast<size_t>(M) * d, gain, static_cast<bf16*>(y), M, d, nullptr, 0, nullptr,
+                  nullptr, S(stream));
+    after_launch();
+  });
+}
+
+int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t hd, const void* pool,
+                     int32_t num_layers, int32_t layer, const int32_t* block_table, int32_t bt_stride,
+                     const int32_t* slot, const int32_t* ctx, int32_t max_ctx, void* out, void* stream) {
+  return guarded([&] {
+    const size_t layer_bytes = static_cast<size_t>(KVH) * 2 * 64 * hd * 2;
+    fpk::KvPoolView pv{static_cast<uint8_t*>(const_cast<void*>(pool)), layer_bytes * num_layers, layer_bytes, 64,
+                       block_table, bt_stride};
+    float* work = nullptr;
+    const size_t wb = fpk::attn_decode_workspace(B, H, hd, max_ctx) * 4 + 256;
+    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&work), wb, S(stream)), "alloc");
+    fpk::attn_decode(static_cast<const bf16*>(q), B, H, KVH, hd, pv, layer, slot, ctx, max_ctx, work,
+                     static_cast<bf16*>(out), S(stream));
+    after_launch();
+    fpe::check(cudaFreeAsync(work, S(stream)), "free");
+  });
+}
+
+int fp_k_attn_varlen(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
+                     const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream) {
+  return guarded([&] {
+    const int nt = fpk::attn_varlen_tiles(cu_host, n_seq, nullptr);
+    std::vector<int> tiles(2 * static_cast<size_t>(nt));
+    fpk::attn_varlen_tiles(cu_host, n_seq, tiles.data());
+    int* dt = nullptr;
+    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&dt), tiles.size() * 4 + 256, S(stream)), "alloc");
+    fpe::check(cudaMemcpyAsync(dt, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, S(stream)), "copy");
+    fpk::attn_varlen(static_cast<const bf16*>(q), static_cast<const bf16*>(k), static_cast<const bf16*>(v), H, KVH, hd,
+                     cu_dev, dt, nt, static_cast<bf16*>(out), S(stream));
+    after_launch();
+    fpe::check(cudaStreamSynchronize(S(stream)), "sync");  // tiles lives on the host stack
+    fpe::check(cudaFreeAsync(dt, S(stream)), "free");
+  });
+}
+
+int fp_k_postprocess(int32_t n, const int32_t* off, const float* logp_actor, const float* logp_ref,
+                     const float* values, const float* score, float beta, float gamma, float lam, float* kl,
+                     float* reward, float* adv, float* ret, void* stream) {
+  return guarded([&] {
+    if (gamma < 0.f || gamma > 1.f || lam < 0.f || lam > 1.f)
+      throw std::invalid_argument("GaeInputs: gamma and lam must lie in [0, 1]");
+    fpk::postprocess(n, off, logp_actor, logp_ref, values, score, beta, gamma, lam, kl, reward, adv, ret, S(stream));
+    after_launch();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,530 @@
+// fuseplan-b200 — Engine: weights, paged KV pool, prefill / decode / scoring.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "philox.cuh"
+
+namespace fpe {
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + what);
+}
+
+// ---------------------------------------------------------------------------
+// pinned staging ring: fixed chunks, each guarded by an event
+
+struct PinnedRing {
+  static constexpr int kChunks = 64;
+  static constexpr size_t kChunkBytes = 1 << 20;
+  uint8_t* host = nullptr;
+  cudaEvent_t ev[kChunks];
+  bool used[kChunks] = {};
+  int next = 0;
+  PinnedRing() {
+    FP_CUDA(cudaMallocHost(&host, kChunks * kChunkBytes));
+    for (auto& e : ev) FP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  ~PinnedRing() {
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaFreeHost(host);
+  }
+};
+
+void Engine::upload(void* d_dst, const void* h_src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  const uint8_t* src = static_cast<const uint8_t*>(h_src);
+  uint8_t* dst = static_cast<uint8_t*>(d_dst);
+  while (bytes > 0) {
+    const size_t n = std::min(bytes, PinnedRing::kChunkBytes);
+    const int c = ring_->next;
+    ring_->next = (c + 1) % PinnedRing::kChunks;
+    if (ring_->used[c]) FP_CUDA(cudaEventSynchronize(ring_->ev[c]));
+    uint8_t* h = ring_->host + c * PinnedRing::kChunkBytes;
+    std::memcpy(h, src, n);
+    FP_CUDA(cudaMemcpyAsync(dst, h, n, cudaMemcpyHostToDevice, st));
+    FP_CUDA(cudaEventRecord(ring_->ev[c], st));
+    ring_->used[c] = true;
+    src += n;
+    dst += n;
+    bytes -= n;
+  }
+}
+
+void* Engine::dalloc(size_t bytes) {
+  void* p = nullptr;
+  bytes = (bytes + 255) & ~size_t(255);
+  FP_CUDA(cudaMalloc(&p, bytes == 0 ? 256 : bytes));
+  allocs_.push_back(p);
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+
+Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
+  FP_CUDA(cudaSetDevice(cfg_.device));
+  // Decode is the latency-critical stream (the long tail is the critical
+  // path): give it the highest priority so scoring batches only fill idle SMs.
+  int prio_lo = 0, prio_hi = 0;
+  FP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  FP_CUDA(cudaStreamCreateWithPriority(&s_decode_, cudaStreamNonBlocking, prio_hi));
+  FP_CUDA(cudaStreamCreateWithPriority(&s_infer_, cudaStreamNonBlocking, prio_lo));
+  FP_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
+  ring_ = new PinnedRing();
+  const Dims& a = cfg_.model[kActor];
+  if (a.L <= 0 || a.d <= 0 || a.H <= 0 || a.KVH <= 0 || a.hd <= 0 || a.F <= 0 || a.V <= 0)
+    throw std::invalid_argument("engine: actor dimensions must be positive");
+  for (int m = 0; m < 4; ++m) {
+    const Dims& d = cfg_.model[m];
+    if (d.d % 64 || d.F % 64 || (d.H * d.hd) % 64)
+      throw std::invalid_argument("engine: hidden, ffn and H*head_dim must be multiples of 64");
+    if (d.H % d.KVH) throw std::invalid_argument("engine: num_heads must be a multiple of num_kv_heads");
+    if (d.hd % 2) throw std::invalid_argument("engine: head_dim must be even");
+  }
+  for (int m = 0; m < 4; ++m) init_model(m);
+
+  // KV pool
+  layer_bytes_ = static_cast<size_t>(a.KVH) * 2 * kPageTokens * a.hd * 2;
+  page_bytes_ = layer_bytes_ * a.L;
+  max_pages_per_sample_ = pages_for(cfg_.max_prompt + cfg_.max_new);
+  int64_t pool_bytes = cfg_.kv_pool_bytes;
+  if (pool_bytes <= 0) pool_bytes = static_cast<int64_t>(cfg_.max_live) * max_pages_per_sample_ * page_bytes_;
+  num_pages_ = static_cast<int>(pool_bytes / page_bytes_) + 1;  // +1: scratch page for padded rows
+  pool_ = static_cast<uint8_t*>(dalloc(static_cast<size_t>(num_pages_) * page_bytes_));
+  for (int p = num_pages_ - 1; p >= 1; --p) free_pages_.push_back(p);  // page 0 is the scratch page
+  for (int s = cfg_.max_live - 1; s >= 0; --s) free_slots_.push_back(s);
+  slot_pages_.assign(cfg_.max_live, {});
+  bt_host_.assign(static_cast<size_t>(cfg_.max_live) * max_pages_per_sample_, 0);
+  d_block_table_ = static_cast<int*>(dalloc(bt_host_.size() * sizeof(int)));
+  FP_CUDA(cudaMemsetAsync(d_block_table_, 0, bt_host_.size() * sizeof(int), s_decode_));
+  d_cur_tok_ = static_cast<int*>(dalloc(cfg_.max_live * sizeof(int)));
+
+  const size_t hist = static_cast<size_t>(cfg_.max_samples) * cfg_.max_new;
+  d_prompts_ = static_cast<int*>(dalloc(static_cast<size_t>(cfg_.max_samples) * cfg_.max_prompt * sizeof(int)));
+  d_hist_tok_ = static_cast<int*>(dalloc(hist * sizeof(int)));
+  d_hist_logp_ = static_cast<float*>(dalloc(hist * sizeof(float)));
+  FP_CUDA(cudaMemsetAsync(d_hist_tok_, 0, hist * sizeof(int), s_decode_));
+  alloc_ws();
+  FP_CUDA(cudaStreamSynchronize(s_decode_));
+}
+
+Engine::~Engine() {
+  cudaSetDevice(cfg_.device);
+  cudaDeviceSynchronize();
+  for (void* p : allocs_) cudaFree(p);
+  for (int m = 0; m < 4; ++m)
+    if (models_[m].blob) cudaFree(models_[m].blob);
+  if (exp_blob_) cudaFree(exp_blob_);
+  if (scratch_) cudaFree(scratch_);
+  delete ring_;
+  cudaStreamDestroy(s_decode_);
+  cudaStreamDestroy(s_infer_);
+  cudaStreamDestroy(s_copy_);
+}
+
+void Engine::synchronize() {
+  FP_CUDA(cudaStreamSynchronize(s_decode_));
+  FP_CUDA(cudaStreamSynchronize(s_infer_));
+  FP_CUDA(cudaStreamSynchronize(s_copy_));
+}
+
+void Engine::init_model(int m) {
+  ModelW& w = models_[m];
+  const Dims& D = cfg_.model[m];
+  w.dims = D;
+  w.id = m;
+  w.lm_head = (m == kActor || m == kRef);
+  const size_t d = D.d, F = D.F, V = D.V, qw = D.qkv_width(), ao = static_cast<size_t>(D.H) * D.hd;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  size_t bytes = al(V * d * 2);  // embedding
+  const size_t per_layer = al(qw * d * 2) + al(d * ao * 2) + al(2 * F * d * 2) + al(d * F * 2) + 2 * al(d * 4);
+  bytes += D.L * per_layer + al(d * 4) + (w.lm_head ? al(V * d * 2) : al(d * 2));
+  FP_CUDA(cudaMalloc(&w.blob, bytes));
+  w.bytes = bytes;
+  uint8_t* p = static_cast<uint8_t*>(w.blob);
+  auto take = [&](size_t b) {
+    uint8_t* r = p;
+    p += al(b);
+    return r;
+  };
+  const uint64_t seed = cfg_.weight_seed;
+  cudaStream_t st = s_decode_;
+  w.embed = reinterpret_cast<bf16*>(take(V * d * 2));
+  fpk::init_bf16(w.embed, V * d, seed, fpk::weight_tag(m, 0, fpk::kTagEmbed), 1.0f, st);
+  w.layers.resize(D.L);
+  for (int l = 0; l < D.L; ++l) {
+    LayerW& L = w.layers[l];
+    L.wqkv = reinterpret_cast<bf16*>(take(qw * d * 2));
+    L.wo = reinterpret_cast<bf16*>(take(d * ao * 2));
+    L.wgu = reinterpret_cast<bf16*>(take(2 * F * d * 2));
+    L.wd = reinterpret_cast<bf16*>(take(d * F * 2));
+    L.ln1 = reinterpret_cast<float*>(take(d * 4));
+    L.ln2 = reinterpret_cast<float*>(take(d * 4));
+    fpk::init_bf16(L.wqkv, qw * d, seed, fpk::weight_tag(m, l, fpk::kTagWqkv), std::sqrt(3.0f / d), st);
+    fpk::init_bf16(L.wo, d * ao, seed, fpk::weight_tag(m, l, fpk::kTagWo), std::sqrt(3.0f / ao), st);
+    fpk::init_bf16_gu(L.wgu, D.F, D.d, seed, fpk::weight_tag(m, l, fpk::kTagWgu), std::sqrt(3.0f / d), st);
+    fpk::init_bf16(L.wd, d * F, seed, fpk::weight_tag(m, l, fpk::kTagWd), std::sqrt(3.0f / F), st);
+    fpk::init_gain(L.ln1, d, seed, fpk::weight_tag(m, l, fpk::kTagAttnNorm), st);
+    fpk::init_gain(L.ln2, d, seed, fpk::weight_tag(m, l, fpk::kTagMlpNorm), st);
+  }
+  w.lnf = reinterpret_cast<float*>(take(d * 4));
+  fpk::init_gain(w.lnf, d, seed, fpk::weight_tag(m, 0, fpk::kTagFinalNorm), st);
+  if (w.lm_head) {
+    w.head = reinterpret_cast<bf16*>(take(V * d * 2));
+    fpk::init_bf16(w.head, V * d, seed, fpk::weight_tag(m, 0, fpk::kTagHead), std::sqrt(3.0f / d), st);
+  } else {
+    w.vhead = reinterpret_cast<bf16*>(take(d * 2));
+    fpk::init_bf16(w.vhead, d, seed, fpk::weight_tag(m, 0, fpk::kTagValueHead), std::sqrt(3.0f / d), st);
+  }
+  w.param_count = V * d + D.L * (qw * d + d * ao + 2 * F * d + d * F) + (w.lm_head ? V * d : d);
+  FP_CUDA(cudaGetLastError());
+}
+
+void Engine::alloc_ws() {
+  int maxd = 0, maxq = 0, maxF = 0, maxao = 0, maxV = 0, maxkv = 0;
+  for (int m = 0; m < 4; ++m) {
+    const Dims& D = cfg_.model[m];
+    maxd = std::max(maxd, D.d);
+    maxq = std::max(maxq, D.qkv_width());
+    maxF = std::max(maxF, D.F);
+    maxao = std::max(maxao, D.H * D.hd);
+    maxkv = std::max(maxkv, D.KVH * D.hd);
+    if (m == kActor || m == kRef) maxV = std::max(maxV, D.V);
+  }
+  const int vt = fpk::vocab_tiles(maxV);
+  auto packed = [&](PackedWs& w, int cap, bool scoring) {
+    w.cap = cap;
+    w.cap_seq = std::min(cap, cfg_.max_samples) + 1;
+    w.x = static_cast<float*>(dalloc(static_cast<size_t>(cap) * maxd * 4));
+    w.h = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxd * 2));
+    w.qkv = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxq * 2));
+    w.q = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxao * 2));
+    w.k = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxkv * 2));
+    w.v = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxkv * 2));
+    w.attn = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxao * 2));
+    w.act = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxF * 2));
+    w.tokens = static_cast<int*>(dalloc(cap * 4));
+    w.pos = static_cast<int*>(dalloc(cap * 4));
+    w.slot = static_cast<int*>(dalloc(cap * 4));
+    w.cu = static_cast<int*>(dalloc(w.cap_seq * 4));
+    w.tiles = static_cast<int*>(dalloc(static_cast<size_t>(2) * (cap / 64 + w.cap_seq) * 4));
+    if (!scoring) return;
+    const int cs = w.cap_seq;
+    w.sid = static_cast<int*>(dalloc(cs * 4));
+    w.P = static_cast<int*>(dalloc(cs * 4));
+    w.R = static_cast<int*>(dalloc(cs * 4));
+    w.roff = static_cast<int*>(dalloc(cs * 4));
+    w.off_out = static_cast<int64_t*>(dalloc(cs * 8));
+    w.hist_tok = static_cast<const int**>(dalloc(cs * 8));
+    w.hist_logp = static_cast<const float**>(dalloc(cs * 8));
+    w.targets = static_cast<int*>(dalloc(cap * 4));
+    w.gather_resp = static_cast<int*>(dalloc(cap * 4));
+    w.gather_last = static_cast<int*>(dalloc(cs * 4));
+    w.vocab_part = dalloc(static_cast<size_t>(cap) * vt * 24);
+    w.tgt_z = static_cast<float*>(dalloc(cap * 4));
+    for (float** f : {&w.logp_actor, &w.logp_ref, &w.values, &w.kl, &w.reward, &w.adv, &w.ret})
+      *f = static_cast<float*>(dalloc(cap * 4));
+    w.score = static_cast<float*>(dalloc(cs * 4));
+  };
+  const int prefill_cap = std::max(cfg_.max_prefill_tokens, cfg_.max_prompt + cfg_.max_new);
+  const int infer_cap = std::max(cfg_.max_infer_tokens, cfg_.max_prompt + cfg_.max_new);
+  packed(pre_, prefill_cap, false);
+  packed(inf_, infer_cap, true);
+
+  const int B = cfg_.max_live;
+  dec_.cap = B;
+  dec_.x = static_cast<float*>(dalloc(static_cast<size_t>(B) * maxd * 4));
+  dec_.parts = static_cast<float*>(dalloc(static_cast<size_t>(16) * B * maxd * 4));
+  dec_.h = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxd * 2));
+  dec_.qkv = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxq * 2));
+  dec_.q = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxao * 2));
+  dec_.attn = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxao * 2));
+  dec_.act = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxF * 2));
+  dec_.rows = static_cast<int*>(dalloc(static_cast<size_t>(7) * B * 4));
+  dec_.vocab_part = dalloc(static_cast<size_t>(B) * vt * 24);
+  dec_.tgt_z = static_cast<float*>(dalloc(B * 4));
+  const Dims& a = cfg_.model[kActor];
+  dec_.attn_work = static_cast<float*>(
+      dalloc(fpk::attn_decode_workspace(B, a.H, a.hd, cfg_.max_prompt + cfg_.max_new) * sizeof(float)));
+}
+
+// ---------------------------------------------------------------------------
+
+void Engine::load_prompts(const int* prompts, int n) {
+  if (n > cfg_.max_samples) throw std::invalid_argument("engine: batch larger than max_samples");
+  upload(d_prompts_, prompts, static_cast<size_t>(n) * cfg_.max_prompt * sizeof(int), s_decode_);
+}
+
+void Engine::set_layout(const std::vector<int64_t>& resp_off) {
+  resp_off_ = resp_off;
+  const size_t n = resp_off.empty() ? 0 : resp_off.size() - 1;
+  const size_t total = resp_off.empty() ? 0 : static_cast<size_t>(resp_off.back());
+  if (exp_blob_) {
+    FP_CUDA(cudaDeviceSynchronize());
+    cudaFree(exp_blob_);
+    exp_blob_ = nullptr;
+  }
+  const size_t al = (total * 4 + 255) & ~size_t(255);
+  const size_t bytes = 8 * al + ((n * 4 + 255) & ~size_t(255));
+  FP_CUDA(cudaMalloc(&exp_blob_, bytes));
+  FP_CUDA(cudaMemsetAsync(exp_blob_, 0, bytes, s_decode_));
+  uint8_t* p = static_cast<uint8_t*>(exp_blob_);
+  exp_.tokens = reinterpret_cast<int*>(p);
+  float** fs[7] = {&exp_.logp_actor, &exp_.logp_ref, &exp_.values, &exp_.kl, &exp_.reward, &exp_.adv, &exp_.ret};
+  for (int i = 0; i < 7; ++i) *fs[i] = reinterpret_cast<float*>(p + (i + 1) * al);
+  exp_.score = reinterpret_cast<float*>(p + 8 * al);
+}
+
+int Engine::reserve(int tokens) {
+  const int need = pages_for(tokens);
+  if (need > max_pages_per_sample_) throw std::invalid_argument("engine: sample longer than max_prompt + max_new");
+  if (free_slots_.empty() || static_cast<int>(free_pages_.size()) < need)
+    throw std::runtime_error("engine: KV pool or decode slots exhausted");
+  const int slot = free_slots_.back();
+  free_slots_.pop_back();
+  std::vector<int>& pages = slot_pages_[slot];
+  pages.clear();
+  for (int i = 0; i < need; ++i) {
+    pages.push_back(free_pages_.back());
+    free_pages_.pop_back();
+  }
+  int* row = bt_host_.data() + static_cast<size_t>(slot) * max_pages_per_sample_;
+  std::fill(row, row + max_pages_per_sample_, 0);
+  std::copy(pages.begin(), pages.end(), row);
+  return slot;
+}
+
+void Engine::upload_block_table(int slot, cudaStream_t st) {
+  const size_t off = static_cast<size_t>(slot) * max_pages_per_sample_;
+  upload(d_block_table_ + off, bt_host_.data() + off, max_pages_per_sample_ * sizeof(int), st);
+}
+
+void* Engine::decode_scratch(size_t bytes) {
+  if (bytes > scratch_bytes_) {
+    if (scratch_) {
+      FP_CUDA(cudaStreamSynchronize(s_decode_));
+      cudaFree(scratch_);
+    }
+    scratch_bytes_ = std::max<size_t>(bytes, 1 << 20);
+    FP_CUDA(cudaMalloc(&scratch_, scratch_bytes_));
+  }
+  return scratch_;
+}
+
+void Engine::release(int slot) {
+  for (int p : slot_pages_[slot]) free_pages_.push_back(p);
+  slot_pages_[slot].clear();
+  free_slots_.push_back(slot);
+}
+
+// ---------------------------------------------------------------------------
+
+void Engine::forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, int n_tiles, bool use_pool,
+                            cudaStream_t st) {
+  (void)n_seq;
+  const Dims& D = w.dims;
+  fpk::KvPoolView pv{pool_, page_bytes_, layer_bytes_, kPageTokens, d_block_table_, max_pages_per_sample_};
+  fpk::embed(ws.tokens, nullptr, M, w.embed, D.d, ws.x, st);
+  for (int l = 0; l < D.L; ++l) {
+    const LayerW& L = w.layers[l];
+    fpk::add_norm(ws.x, nullptr, 0, 0, L.ln1, ws.h, M, D.d, nullptr, 0, nullptr, nullptr, st);
+    fpk::gemm_bf16(L.wqkv, D.qkv_width(), D.d, ws.h, M, ws.qkv, D.qkv_width(), st);
+    fpk::rope_qkv(ws.qkv, M, D.H, D.KVH, D.hd, ws.pos, cfg_.rope_theta, ws.q, ws.k, ws.v, use_pool ? &pv : nullptr,
+                  l, ws.slot, st);
+    if (use_pool && l == D.L - 1) break;  // prefill only needs the last layer's K/V
+    fpk::attn_varlen(ws.q, ws.k, ws.v, D.H, D.KVH, D.hd, ws.cu, ws.tiles, n_tiles, ws.attn, st);
+    fpk::gemm_f32_residual(L.wo, D.d, D.H * D.hd, ws.attn, M, ws.x, st);
+    fpk::add_norm(ws.x, nullptr, 0, 0, L.ln2, ws.h, M, D.d, nullptr, 0, nullptr, nullptr, st);
+    fpk::gemm_swiglu(L.wgu, D.F, D.d, ws.h, M, ws.act, st);
+    fpk::gemm_f32_residual(L.wd, D.d, D.F, ws.act, M, ws.x, st);
+  }
+}
+
+void Engine::prefill(const std::vector<PrefillItem>& items) {
+  cudaStream_t st = s_decode_;
+  const ModelW& w = models_[kActor];
+  std::vector<int> tok, pos, slot, cu, tiles, nslot, ntok;
+  size_t i = 0;
+  while (i < items.size()) {
+    tok.clear();
+    pos.clear();
+    slot.clear();
+    cu.assign(1, 0);
+    size_t j = i;
+    while (j < items.size()) {
+      const int c = items[j].ctx_tokens;
+      if (j > i && static_cast<int>(tok.size()) + c > pre_.cap) break;
+      if (static_cast<int>(cu.size()) >= pre_.cap_seq) break;
+      for (int t = 0; t < c; ++t) {
+        tok.push_back(items[j].tokens[t]);
+        pos.push_back(t);
+        slot.push_back(items[j].slot);
+      }
+      cu.push_back(static_cast<int>(tok.size()));
+      ++j;
+    }
+    const int M = static_cast<int>(tok.size());
+    const int ns = static_cast<int>(cu.size()) - 1;
+    if (M > 0) {
+      tiles.assign(2 * static_cast<size_t>(fpk::attn_varlen_tiles(cu.data(), ns, nullptr)), 0);
+      const int nt = fpk::attn_varlen_tiles(cu.data(), ns, tiles.data());
+      upload(pre_.tokens, tok.data(), M * 4, st);
+      upload(pre_.pos, pos.data(), M * 4, st);
+      upload(pre_.slot, slot.data(), M * 4, st);
+      upload(pre_.cu, cu.data(), cu.size() * 4, st);
+      upload(pre_.tiles, tiles.data(), tiles.size() * 4, st);
+      forward_packed(w, pre_, M, ns, nt, true, st);
+    }
+    i = j;
+  }
+  // first decode input of every admitted sample
+  nslot.clear();
+  ntok.clear();
+  for (const PrefillItem& it : items) {
+    nslot.push_back(it.slot);
+    ntok.push_back(it.next_token);
+  }
+  if (!nslot.empty()) {
+    const int n = static_cast<int>(nslot.size());
+    // reuse the packed slot/token buffers (stream-ordered after the forward)
+    upload(pre_.slot, nslot.data(), n * 4, st);
+    upload(pre_.tokens, ntok.data(), n * 4, st);
+    fpk::scatter_int(pre_.slot, pre_.tokens, n, d_cur_tok_, st);
+  }
+  FP_CUDA(cudaGetLastError());
+}
+
+void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed) {
+  const int B = static_cast<int>(rows.size());
+  if (B == 0) return;
+  if (B > dec_.cap) throw std::invalid_argument("engine: decode batch exceeds max_live");
+  cudaStream_t st = s_decode_;
+  const ModelW& w = models_[kActor];
+  const Dims& D = w.dims;
+  std::vector<int> h(static_cast<size_t>(7) * B);
+  int max_ctx = 0;
+  for (int b = 0; b < B; ++b) {
+    const DecodeRow& r = rows[b];
+    h[b] = r.slot;
+    h[B + b] = r.pos;
+    h[2 * B + b] = r.pos + 1;
+    h[3 * B + b] = r.sid * cfg_.max_new + r.step;
+    h[4 * B + b] = r.target;
+    h[5 * B + b] = r.sid;
+    h[6 * B + b] = r.step;
+    max_ctx = std::max(max_ctx, r.pos + 1);
+  }
+  upload(dec_.rows, h.data(), h.size() * 4, st);
+  const int* slot = dec_.rows;
+  const int* pos = dec_.rows + B;
+  const int* ctx = dec_.rows + 2 * B;
+  const int* dst = dec_.rows + 3 * B;
+  const int* target = dec_.rows + 4 * B;
+  const int* sid = dec_.rows + 5 * B;
+  const int* step = dec_.rows + 6 * B;
+  fpk::KvPoolView pv{pool_, page_bytes_, layer_bytes_, kPageTokens, d_block_table_, max_pages_per_sample_};
+  const size_t stride = static_cast<size_t>(B) * D.d;
+  const int so = fpk::gemm_splits(D.d, D.H * D.hd);
+  const int sd = fpk::gemm_splits(D.d, D.F);
+
+  fpk::embed(d_cur_tok_, slot, B, w.embed, D.d, dec_.x, st);
+  int nparts = 0;
+  for (int l = 0; l < D.L; ++l) {
+    const LayerW& L = w.layers[l];
+    fpk::add_norm(dec_.x, nparts ? dec_.parts : nullptr, nparts, stride, L.ln1, dec_.h, B, D.d, nullptr, 0, nullptr,
+                  nullptr, st);
+    fpk::gemm_bf16(L.wqkv, D.qkv_width(), D.d, dec_.h, B, dec_.qkv, D.qkv_width(), st);
+    fpk::rope_qkv(dec_.qkv, B, D.H, D.KVH, D.hd, pos, cfg_.rope_theta, dec_.q, nullptr, nullptr, &pv, l, slot, st);
+    fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, max_ctx, dec_.attn_work, dec_.attn, st);
+    fpk::gemm_f32_splitk(L.wo, D.d, D.H * D.hd, dec_.attn, B, dec_.parts, so, st);
+    fpk::add_norm(dec_.x, dec_.parts, so, stride, L.ln2, dec_.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
+    fpk::gemm_swiglu(L.wgu, D.F, D.d, dec_.h, B, dec_.act, st);
+    fpk::gemm_f32_splitk(L.wd, D.d, D.F, dec_.act, B, dec_.parts, sd, st);
+    nparts = sd;
+  }
+  fpk::add_norm(dec_.x, dec_.parts, nparts, stride, w.lnf, dec_.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
+  fpk::gemm_vocab(dec_.h, B, D.d, w.head, D.V, mode, inv_temp, target, sid, step, sample_seed, dec_.vocab_part,
+                  dec_.tgt_z, st);
+  fpk::vocab_finalize(dec_.vocab_part, dec_.tgt_z, B, D.V, mode, target, nullptr, nullptr, dst, d_hist_tok_,
+                      d_hist_logp_, slot, d_cur_tok_, st);
+  FP_CUDA(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+
+void Engine::infer(const std::vector<InferItem>& items, float beta, float gamma, float lam) {
+  cudaStream_t st = s_infer_;
+  PackedWs& ws = inf_;
+  std::vector<int> sid, P, R, cu, roff, tiles;
+  std::vector<int64_t> off_out;
+  std::vector<const void*> ht, hl;
+  size_t i = 0;
+  while (i < items.size()) {
+    sid.clear(), P.clear(), R.clear(), roff.clear(), off_out.clear(), ht.clear(), hl.clear();
+    cu.assign(1, 0);
+    roff.push_back(0);
+    size_t j = i;
+    while (j < items.size()) {
+      const int T = items[j].P + items[j].R;
+      if (j > i && cu.back() + T > ws.cap) break;
+      if (static_cast<int>(cu.size()) >= ws.cap_seq) break;
+      sid.push_back(items[j].sid);
+      P.push_back(items[j].P);
+      R.push_back(items[j].R);
+      cu.push_back(cu.back() + T);
+      roff.push_back(roff.back() + items[j].R);
+      off_out.push_back(resp_off_.at(items[j].sid));
+      ht.push_back(items[j].hist_tok);
+      hl.push_back(items[j].hist_logp);
+      ++j;
+    }
+    const int n = static_cast<int>(sid.size());
+    const int M = cu.back();
+    const int NR = roff.back();
+    tiles.assign(2 * static_cast<size_t>(fpk::attn_varlen_tiles(cu.data(), n, nullptr)), 0);
+    const int nt = fpk::attn_varlen_tiles(cu.data(), n, tiles.data());
+    upload(ws.sid, sid.data(), n * 4, st);
+    upload(ws.P, P.data(), n * 4, st);
+    upload(ws.R, R.data(), n * 4, st);
+    upload(ws.cu, cu.data(), cu.size() * 4, st);
+    upload(ws.roff, roff.data(), roff.size() * 4, st);
+    upload(ws.off_out, off_out.data(), n * 8, st);
+    upload(ws.hist_tok, ht.data(), n * 8, st);
+    upload(ws.hist_logp, hl.data(), n * 8, st);
+    upload(ws.tiles, tiles.data(), tiles.size() * 4, st);
+    fpk::AssembleArgs a{ws.sid,        ws.P,      ws.R,         ws.cu,           ws.roff,
+                        d_prompts_,    cfg_.max_prompt, ws.hist_tok, ws.hist_logp,
+                        ws.tokens,     ws.pos,    ws.targets,   ws.logp_actor,   ws.gather_resp,
+                        ws.gather_last};
+    fpk::assemble_batch(a, n, st);
+
+    // reference model: log-prob of every response token
+    const ModelW& ref = models_[kRef];
+    forward_packed(ref, ws, M, n, nt, false, st);
+    fpk::add_norm(ws.x, nullptr, 0, 0, ref.lnf, ws.h, M, ref.dims.d, ws.gather_resp, NR, nullptr, nullptr, st);
+    fpk::gemm_vocab(ws.h, NR, ref.dims.d, ref.head, ref.dims.V, 0 /* forced */, 1.0f, ws.targets, nullptr, nullptr, 0,
+                    ws.vocab_part, ws.tgt_z, st);
+    fpk::vocab_finalize(ws.vocab_part, ws.tgt_z, NR, ref.dims.V, 0 /* forced */, ws.targets, nullptr, ws.logp_ref,
+                        nullptr, nullptr, nullptr, nullptr, nullptr, st);
+    // critic: value of the state before each response token
+    const ModelW& cr = models_[kCritic];
+    forward_packed(cr, ws, M, n, nt, false, st);
+    fpk::add_norm(ws.x, nullptr, 0, 0, cr.lnf, nullptr, M, cr.dims.d, ws.gather_resp, NR, cr.vhead, ws.values, st);
+    // reward model: scalar score at the last token
+    const ModelW& rw = models_[kReward];
+    forward_packed(rw, ws, M, n, nt, false, st);
+    fpk::add_norm(ws.x, nullptr, 0, 0, rw.lnf, nullptr, M, rw.dims.d, ws.gather_last, n, rw.vhead, ws.score, st);
+
+    fpk::PostScatter sc{ws.off_out,   ws.sid,          ws.targets,  exp_.logp_actor, exp_.logp_ref,
+                        exp_.values,  exp_.score,      exp_.tokens};
+    fpk::postprocess(n, ws.roff, ws.logp_actor, ws.logp_ref, ws.values, ws.score, beta, gamma, lam, exp_.kl,
+                     exp_.reward, exp_.adv, exp_.ret, st, &sc);
+    FP_CUDA(cudaGetLastError());
+    i = j;
+  }
+}
+
+}  // namespace fpe

@@ -1,0 +1,220 @@
+// fuseplan-b200 — one generation/inference engine per B200 (internal C++ API).
+//
+// An Engine owns, on its device:
+//   * the four models' weights (actor, reference, critic, reward), synthetic
+//     and deterministic (hash of seed, model, layer, tensor, index);
+//   * the paged KV pool of the actor: pages of 64 tokens x all layers, page
+//     layout [layer][kv_head][K 64 x hd | V 64 x hd] (bf16), a host free list
+//     and a device block table [slot][page];
+//   * per-sample histories (response token ids and actor log-probs, indexed by
+//     global sample id) and the synthetic prompts;
+//   * a decode workspace (live batch rows) and a packed workspace (prefill /
+//     scoring rows), and three streams: decode, infer, copy.
+// Work is enqueued asynchronously; the executor (executor.cpp) drives it.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ops.h"
+
+namespace fpe {
+
+using bf16 = __nv_bfloat16;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void check(cudaError_t e, const char* what);
+#define FP_CUDA(x) ::fpe::check((x), #x)
+
+enum ModelSlot : int { kActor = 0, kRef = 1, kCritic = 2, kReward = 3 };
+
+struct Dims {
+  int L = 0, d = 0, H = 0, KVH = 0, hd = 0, F = 0, V = 0;
+  int qkv_width() const { return (H + 2 * KVH) * hd; }
+  size_t kv_bytes_per_token() const { return static_cast<size_t>(2) * L * KVH * hd * 2; }  // physical, bf16
+};
+
+struct LayerW {
+  bf16 *wqkv = nullptr, *wo = nullptr, *wgu = nullptr, *wd = nullptr;
+  float *ln1 = nullptr, *ln2 = nullptr;
+};
+
+struct ModelW {
+  Dims dims;
+  int id = 0;
+  bool lm_head = true;  // actor/ref: LM head [V, d]; critic/reward: value head [d]
+  bf16* embed = nullptr;
+  std::vector<LayerW> layers;
+  float* lnf = nullptr;
+  bf16* head = nullptr;
+  bf16* vhead = nullptr;
+  void* blob = nullptr;
+  size_t bytes = 0;
+  size_t param_count = 0;
+};
+
+struct EngineConfig {
+  Dims model[4];
+  uint64_t weight_seed = 1234;
+  int max_prompt = 128;
+  int max_new = 1024;
+  int max_samples = 512;    // global batch n (history buffers are indexed by global id)
+  int max_live = 512;       // decode slots
+  int64_t kv_pool_bytes = 0;  // 0: enough for max_live samples of max_prompt + max_new
+  int max_prefill_tokens = 16384;
+  int max_infer_tokens = 16384;
+  float rope_theta = 10000.f;
+  int device = 0;
+};
+
+constexpr int kPageTokens = 64;
+
+struct PinnedRing;  // host staging for async uploads
+
+class Engine {
+ public:
+  explicit Engine(const EngineConfig& cfg);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  const EngineConfig& config() const { return cfg_; }
+  const ModelW& model(int m) const { return models_[m]; }
+  cudaStream_t decode_stream() const { return s_decode_; }
+  cudaStream_t infer_stream() const { return s_infer_; }
+  cudaStream_t copy_stream() const { return s_copy_; }
+
+  // ---- batch data (global sample ids) -------------------------------------------
+  // prompts [n][max_prompt] (host), uploaded on the decode stream.
+  void load_prompts(const int* prompts, int n);
+  int* d_prompts() const { return d_prompts_; }
+  int* d_hist_tok() const { return d_hist_tok_; }
+  float* d_hist_logp() const { return d_hist_logp_; }
+
+  // ---- KV pages and slots -----------------------------------------------------------
+  int pages_for(int tokens) const { return (tokens + kPageTokens - 1) / kPageTokens; }
+  int free_pages() const { return static_cast<int>(free_pages_.size()); }
+  int free_slots() const { return static_cast<int>(free_slots_.size()); }
+  // Reserve a slot and `tokens` worth of pages; returns the slot.
+  int reserve(int tokens);
+  void release(int slot);
+  const std::vector<int>& pages_of(int slot) const { return slot_pages_[slot]; }
+  uint8_t* pool_base() const { return pool_; }
+  size_t page_bytes() const { return page_bytes_; }
+  int num_pages() const { return num_pages_; }
+
+  // ---- generation (decode stream) ---------------------------------------------------
+  struct PrefillItem {
+    int sid, slot, ctx_tokens;  // positions [0, ctx_tokens) are written to the pool
+    const int* tokens;          // host: ctx_tokens ids
+    int next_token;             // first decode input (position ctx_tokens)
+  };
+  void prefill(const std::vector<PrefillItem>& items);
+
+  struct DecodeRow {
+    int sid, slot, pos, step, target;  // pos: position of the input token; step: response index
+  };
+  // One decode step for `rows`: writes hist[sid][step] (token, logp) and the
+  // next input token. mode 0 forced (target), 1 greedy, 2 sample.
+  void decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed);
+
+  // ---- scoring (infer stream) ------------------------------------------------------
+  struct InferItem {
+    int sid, P, R;
+    const int* hist_tok;     // device pointer (local or peer) of the sample's history row
+    const float* hist_logp;
+  };
+  // Scores items in chunks of <= max_infer_tokens rows (three frozen models),
+  // post-processes, and scatters the experience into the device arrays below
+  // at each sample's global response offset (set_layout).
+  void infer(const std::vector<InferItem>& items, float beta, float gamma, float lam);
+
+  // Global response layout: resp_off[n+1]; (re)allocates the experience arrays.
+  void set_layout(const std::vector<int64_t>& resp_off);
+  struct Experience {
+    int* tokens = nullptr;
+    float *logp_actor = nullptr, *logp_ref = nullptr, *values = nullptr, *kl = nullptr, *reward = nullptr,
+          *adv = nullptr, *ret = nullptr, *score = nullptr;
+  };
+  const Experience& experience() const { return exp_; }
+  const std::vector<int64_t>& resp_off() const { return resp_off_; }
+
+  // Async host -> device copy on `st` through a pinned staging ring (the host
+  // buffer may be reused as soon as this returns).
+  void upload(void* d_dst, const void* h_src, size_t bytes, cudaStream_t st);
+
+  // Block-table row upload for a slot.
+  void upload_block_table(int slot, cudaStream_t st);
+  int* d_cur_tok() const { return d_cur_tok_; }
+  // Device scratch for small per-call tables (chunk lists, index quads) on the decode stream.
+  void* decode_scratch(size_t bytes);
+
+  void synchronize();
+
+ private:
+  struct PackedWs {
+    int cap = 0, cap_seq = 0;
+    float* x = nullptr;
+    bf16 *h = nullptr, *qkv = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *attn = nullptr, *act = nullptr;
+    int *tokens = nullptr, *pos = nullptr, *slot = nullptr, *cu = nullptr, *tiles = nullptr;
+    // scoring
+    int *sid = nullptr, *P = nullptr, *R = nullptr, *roff = nullptr, *targets = nullptr, *gather_resp = nullptr,
+        *gather_last = nullptr;
+    const int** hist_tok = nullptr;
+    const float** hist_logp = nullptr;
+    int64_t* off_out = nullptr;
+    void* vocab_part = nullptr;
+    float *tgt_z = nullptr, *logp_actor = nullptr, *logp_ref = nullptr, *values = nullptr, *score = nullptr,
+          *kl = nullptr, *reward = nullptr, *adv = nullptr, *ret = nullptr;
+  };
+  struct DecodeWs {
+    int cap = 0;
+    float *x = nullptr, *parts = nullptr, *attn_work = nullptr;
+    bf16 *h = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
+    int* rows = nullptr;  // 7 x cap: slot, pos, ctx, dst, target, sid, step
+    void* vocab_part = nullptr;
+    float* tgt_z = nullptr;
+  };
+
+  void init_model(int m);
+  void alloc_ws();
+  void forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, int n_tiles, bool use_pool,
+                      cudaStream_t st);
+
+  EngineConfig cfg_;
+  ModelW models_[4];
+  cudaStream_t s_decode_ = nullptr, s_infer_ = nullptr, s_copy_ = nullptr;
+  // pool
+  uint8_t* pool_ = nullptr;
+  size_t page_bytes_ = 0, layer_bytes_ = 0;
+  int num_pages_ = 0, max_pages_per_sample_ = 0;
+  std::vector<int> free_pages_, free_slots_;
+  std::vector<std::vector<int>> slot_pages_;
+  std::vector<int> bt_host_;
+  int* d_block_table_ = nullptr;
+  int* d_cur_tok_ = nullptr;
+  // batch
+  int* d_prompts_ = nullptr;
+  int* d_hist_tok_ = nullptr;
+  float* d_hist_logp_ = nullptr;
+  PackedWs pre_, inf_;
+  Experience exp_;
+  void* exp_blob_ = nullptr;
+  std::vector<int64_t> resp_off_;
+  DecodeWs dec_;
+  PinnedRing* ring_ = nullptr;
+  void* scratch_ = nullptr;
+  size_t scratch_bytes_ = 0;
+  std::vector<void*> allocs_;
+  void* dalloc(size_t bytes);
+};
+
+}  // namespace fpe

@@ -1,0 +1,706 @@
+// fuseplan-b200 — executor of the gen+inf stage on one GPU (one rank).
+//
+// Per rank r (instance r of cfg.num_instances):
+//   1. Decisions from the decision clock: simulate_serial / simulate_fused
+//      (reported), fused_trigger (trigger state, plan, in-flight placement).
+//   2. Instance state machine, step by step, with the reference semantics
+//      (proj/src/genfuse.cpp:222-271): retire finished samples (free their KV
+//      reservation in in-flight order), admit FIFO while the reserved KV fits
+//      (cap + 1e-6), prefill the admitted prompts, decode one token for every
+//      in-flight sample. Reservation bytes are the reference's kv_bytes, so
+//      the admission sequence is the reference's.
+//   3. Fused schedule, G > 1: the rank pauses when its state equals its
+//      trigger snapshot (pre- or post-admission boundary), then the one-shot
+//      migration: destinations pull the in-flight samples' KV pages and
+//      histories from the source GPU's memory over NVLink (CUDA IPC pointers,
+//      copy kernel), queued samples are re-queued; then execution resumes.
+//   4. Sample-level scoring: every finished sample is published to a shared
+//      queue; ranks claim batches of finished samples (in finish order) and
+//      run Reference/Critic/Reward + post-processing on a low-priority stream.
+//      Stage-barrier schedule: claims start only after every rank finished
+//      generating. Fused: claims start immediately (a generating rank keeps at
+//      most one scoring batch in flight; idle ranks two).
+// Coordination between ranks is a POSIX shared-memory region (counters,
+// barrier, IPC handles, page lists, gathered results).
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <deque>
+#include <map>
+#include <memory>
+#include <thread>
+#include <unordered_map>
+
+#include "engine.hpp"
+#include "fuseplan/engine.hpp"
+#include "fuseplan/errors.hpp"
+#include "philox.cuh"
+
+namespace fuseplan {
+
+struct GpuEngine {
+  EngineSetup setup;
+  std::unique_ptr<fpe::Engine> eng;
+};
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+constexpr int kMaxRanks = 8;
+
+fpe::Dims to_dims(const EngineModelDims& m) {
+  fpe::Dims d;
+  d.L = m.num_layers;
+  d.d = m.hidden;
+  d.H = m.num_heads;
+  d.KVH = m.num_kv_heads;
+  d.hd = m.head_dim;
+  d.F = m.ffn;
+  d.V = m.vocab;
+  return d;
+}
+
+// ---------------------------------------------------------------------------
+// shared coordination region
+
+struct Header {
+  std::atomic<int> bar_count;
+  std::atomic<int> bar_gen;
+  std::atomic<int> n_pub;      // finished samples published
+  std::atomic<int> n_claimed;  // claim cursor into pub_order
+  std::atomic<int> gen_done;   // ranks with no generation work left
+  std::atomic<int> error;      // a rank failed
+  std::atomic<int> lock;       // publish lock
+  int world, n, max_pages, pad_;
+  cudaIpcMemHandle_t h_hist_tok[kMaxRanks], h_hist_logp[kMaxRanks], h_pool[kMaxRanks];
+};
+
+class Region {
+ public:
+  Region(const CommSetup& comm, int n, int max_pages, int64_t total_resp)
+      : world_(comm.world), rank_(comm.rank), n_(n), max_pages_(max_pages), total_(total_resp) {
+    off_pub_ = align(sizeof(Header));
+    off_owner_ = align(off_pub_ + n * 4);
+    off_pages_ = align(off_owner_ + n * 4);
+    off_res_ = align(off_pages_ + static_cast<size_t>(n) * max_pages * 4);
+    bytes_ = align(off_res_ + static_cast<size_t>(total_resp) * 4 * 8 + n * 4);
+    if (world_ == 1) {
+      local_.reset(new uint8_t[bytes_]());
+      base_ = local_.get();
+    } else {
+      name_ = comm.shm_name;
+      fd_ = shm_open(name_.c_str(), O_CREAT | O_RDWR, 0600);
+      if (fd_ < 0) throw std::runtime_error("shm_open failed: " + name_);
+      if (ftruncate(fd_, static_cast<off_t>(bytes_)) != 0) throw std::runtime_error("ftruncate failed");
+      void* p = mmap(nullptr, bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd_, 0);
+      if (p == MAP_FAILED) throw std::runtime_error("mmap failed");
+      base_ = static_cast<uint8_t*>(p);
+    }
+    hdr_ = reinterpret_cast<Header*>(base_);
+  }
+  ~Region() {
+    if (world_ > 1 && base_) {
+      munmap(base_, bytes_);
+      close(fd_);
+      if (rank_ == 0) shm_unlink(name_.c_str());
+    }
+  }
+  Header* hdr() { return hdr_; }
+  int* pub_order() { return reinterpret_cast<int*>(base_ + off_pub_); }
+  int* owner() { return reinterpret_cast<int*>(base_ + off_owner_); }
+  int* pages(int sid) { return reinterpret_cast<int*>(base_ + off_pages_) + static_cast<size_t>(sid) * max_pages_; }
+  float* result(int k) { return reinterpret_cast<float*>(base_ + off_res_) + static_cast<size_t>(k) * total_; }
+  float* score() { return reinterpret_cast<float*>(base_ + off_res_) + static_cast<size_t>(8) * total_; }
+
+  void barrier() {
+    if (world_ == 1) return;
+    const int gen = hdr_->bar_gen.load();
+    if (hdr_->bar_count.fetch_add(1) + 1 == world_) {
+      hdr_->bar_count.store(0);
+      hdr_->bar_gen.fetch_add(1);
+    } else {
+      const auto t0 = Clock::now();
+      while (hdr_->bar_gen.load() == gen) {
+        if (hdr_->error.load()) throw std::runtime_error("peer rank failed");
+        std::this_thread::yield();
+        if (Clock::now() - t0 > std::chrono::seconds(600)) throw std::runtime_error("barrier timeout");
+      }
+    }
+  }
+
+ private:
+  static size_t align(size_t x) { return (x + 255) & ~size_t(255); }
+  int world_, rank_, n_, max_pages_;
+  int64_t total_;
+  size_t off_pub_ = 0, off_owner_ = 0, off_pages_ = 0, off_res_ = 0, bytes_ = 0;
+  std::unique_ptr<uint8_t[]> local_;
+  uint8_t* base_ = nullptr;
+  Header* hdr_ = nullptr;
+  std::string name_;
+  int fd_ = -1;
+};
+
+struct Live {
+  int sid, slot, gen, target;
+};
+
+struct Move {
+  int sid, src, dst;
+  bool inflight;
+  int gen;
+};
+
+// Migrants in the decision clock's application order (fused_trigger).
+std::vector<Move> moves_of(const TriggerSnapshot& snap) {
+  std::vector<Move> mv;
+  if (!snap.triggered || snap.plan.no_op) return mv;
+  std::map<int, const GenState::Remaining*> rem;
+  for (const auto& r : snap.state.samples) rem[r.id] = &r;
+  for (std::size_t i = 0; i < snap.move_sample.size(); ++i) {
+    const GenState::Remaining* r = rem.at(snap.move_sample[i]);
+    mv.push_back({r->id, snap.move_from[i], snap.move_to[i], r->admitted, r->generated});
+  }
+  return mv;
+}
+
+int forced_token(uint64_t seed, int sid, int k, int max_new, int V) {
+  const uint64_t h = fpk::hash3(seed, fpk::kTagResponse, static_cast<uint64_t>(sid) * max_new + k);
+  return static_cast<int>((h >> 32) % static_cast<uint64_t>(V));
+}
+
+float ms_between(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  FP_CUDA(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+}  // namespace
+
+GpuEngine* create_engine(const EngineSetup& s) {
+  fpe::EngineConfig c;
+  c.model[fpe::kActor] = to_dims(s.actor);
+  c.model[fpe::kRef] = to_dims(s.ref);
+  c.model[fpe::kCritic] = to_dims(s.critic);
+  c.model[fpe::kReward] = to_dims(s.reward);
+  c.weight_seed = s.weight_seed;
+  c.max_prompt = s.max_prompt;
+  c.max_new = s.max_new;
+  c.max_samples = s.max_samples;
+  c.max_live = s.max_live;
+  c.kv_pool_bytes = s.kv_pool_bytes;
+  c.max_prefill_tokens = s.max_prefill_tokens;
+  c.max_infer_tokens = s.max_infer_tokens;
+  c.rope_theta = s.rope_theta;
+  c.device = s.device;
+  auto* g = new GpuEngine;
+  g->setup = s;
+  g->eng = std::make_unique<fpe::Engine>(c);
+  return g;
+}
+
+void destroy_engine(GpuEngine* e) { delete e; }
+
+std::vector<int> synthetic_prompts(const GpuEngine* e, int n, std::uint64_t token_seed) {
+  const int P = e->setup.max_prompt, V = e->setup.actor.vocab;
+  std::vector<int> p(static_cast<size_t>(n) * P);
+  for (size_t i = 0; i < p.size(); ++i)
+    p[i] = static_cast<int>((fpk::hash3(token_seed, fpk::kTagPrompt, i) >> 32) % static_cast<uint64_t>(V));
+  return p;
+}
+
+ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const GenSimConfig& cfg, int r_t,
+                   const EngineOptions& opts, const CommSetup& comm, const std::vector<int>* prompts_in) {
+  fpe::Engine& E = *ge->eng;
+  const fpe::EngineConfig& ec = E.config();
+  FP_CUDA(cudaSetDevice(ec.device));
+  const int n = static_cast<int>(batch.size());
+  const int G = comm.world, me = comm.rank;
+  if (G < 1 || G > kMaxRanks || me < 0 || me >= G) throw std::invalid_argument("execute: bad rank/world");
+  if (cfg.num_instances != G) throw std::invalid_argument("execute: cfg.num_instances must equal the world size");
+  if (n > ec.max_samples) throw std::invalid_argument("execute: batch larger than engine max_samples");
+  for (int s = 0; s < n; ++s) {
+    const GenSample& b = batch[s];
+    if (b.id != s) throw std::invalid_argument("execute: batch ids must be 0..n-1 in order");
+    if (b.prompt_len < 1 || b.prompt_len > ec.max_prompt)
+      throw std::invalid_argument("execute: prompt_len must lie in [1, max_prompt]");
+    if (b.target_output_len < 1 || b.target_output_len > ec.max_new)
+      throw std::invalid_argument("execute: target_output_len must lie in [1, max_new]");
+    if (b.generated != 0) throw std::invalid_argument("execute: samples must start ungenerated");
+  }
+  const int V = ec.model[fpe::kActor].V;
+  const int mode = static_cast<int>(opts.token_mode);
+  const bool fused = opts.schedule == Schedule::kFused;
+
+  ExecResult res;
+  res.decision = fused ? simulate_fused(batch, cfg, r_t) : simulate_serial(batch, cfg);
+  std::vector<Move> moves;
+  if (fused && G > 1 && r_t > 0) {
+    res.trigger = fused_trigger(batch, cfg, r_t);
+    moves = moves_of(res.trigger);
+  }
+  const bool migrate = !moves.empty() || (res.trigger.triggered && !res.trigger.plan.no_op);
+
+  // ---- host data --------------------------------------------------------------
+  std::vector<int> prompts = prompts_in ? *prompts_in : synthetic_prompts(ge, n, opts.token_seed);
+  if (static_cast<int64_t>(prompts.size()) < static_cast<int64_t>(n) * ec.max_prompt)
+    throw std::invalid_argument("execute: prompts must hold n * max_prompt ids");
+  std::vector<int64_t> resp_off(n + 1, 0);
+  for (int s = 0; s < n; ++s) resp_off[s + 1] = resp_off[s] + batch[s].target_output_len;
+  const int64_t total = resp_off[n];
+  const int max_pages = E.pages_for(ec.max_prompt + ec.max_new);
+
+  Region region(comm, n, max_pages, total);
+  Header* hdr = region.hdr();
+
+  // peer pointers (G > 1): histories and KV pools of every rank
+  std::vector<const int*> peer_tok(G, nullptr);
+  std::vector<const float*> peer_logp(G, nullptr);
+  std::vector<const uint8_t*> peer_pool(G, nullptr);
+  std::vector<void*> opened;
+  peer_tok[me] = E.d_hist_tok();
+  peer_logp[me] = E.d_hist_logp();
+  peer_pool[me] = E.pool_base();
+  if (G > 1) {
+    FP_CUDA(cudaIpcGetMemHandle(&hdr->h_hist_tok[me], E.d_hist_tok()));
+    FP_CUDA(cudaIpcGetMemHandle(&hdr->h_hist_logp[me], E.d_hist_logp()));
+    FP_CUDA(cudaIpcGetMemHandle(&hdr->h_pool[me], E.pool_base()));
+    region.barrier();
+    for (int r = 0; r < G; ++r) {
+      if (r == me) continue;
+      void *a = nullptr, *b = nullptr, *c = nullptr;
+      FP_CUDA(cudaIpcOpenMemHandle(&a, hdr->h_hist_tok[r], cudaIpcMemLazyEnablePeerAccess));
+      FP_CUDA(cudaIpcOpenMemHandle(&b, hdr->h_hist_logp[r], cudaIpcMemLazyEnablePeerAccess));
+      FP_CUDA(cudaIpcOpenMemHandle(&c, hdr->h_pool[r], cudaIpcMemLazyEnablePeerAccess));
+      peer_tok[r] = static_cast<const int*>(a);
+      peer_logp[r] = static_cast<const float*>(b);
+      peer_pool[r] = static_cast<const uint8_t*>(c);
+      opened.insert(opened.end(), {a, b, c});
+    }
+  }
+
+  E.set_layout(resp_off);
+  E.load_prompts(prompts.data(), n);
+  cudaStream_t sd = E.decode_stream(), si = E.infer_stream();
+  FP_CUDA(cudaStreamSynchronize(sd));
+  region.barrier();
+
+  // ---- timing -----------------------------------------------------------------------
+  std::vector<cudaEvent_t> events;
+  auto new_event = [&](cudaStream_t st) {
+    cudaEvent_t e;
+    FP_CUDA(cudaEventCreate(&e));
+    FP_CUDA(cudaEventRecord(e, st));
+    events.push_back(e);
+    return e;
+  };
+  const auto wall0 = Clock::now();
+  cudaEvent_t ev_start = new_event(sd);
+  FP_CUDA(cudaStreamWaitEvent(si, ev_start, 0));
+  std::vector<cudaEvent_t> step_begin, step_end;
+  std::vector<int> finish_step(n, -1);
+  res.finish_instance.assign(n, -1);
+
+  // ---- instance state --------------------------------------------------------------
+  std::deque<int> queue;
+  for (int s = me; s < n; s += G) queue.push_back(s);
+  std::vector<Live> live;
+  double kv_used = 0.0;
+  const double cap = cfg.cluster.kv_capacity_per_instance;
+  std::vector<int> slot_of(n, -1);
+
+  // trigger snapshot of this instance
+  bool pending_trigger = migrate;
+  std::unordered_map<int, int> snap_live;  // sid -> generated
+  std::vector<int> snap_queue;
+  if (pending_trigger) {
+    for (const auto& r : res.trigger.state.samples) {
+      if (r.instance != me) continue;
+      if (r.admitted)
+        snap_live[r.id] = r.generated;
+      else
+        snap_queue.push_back(r.id);
+    }
+  }
+  auto at_snapshot = [&]() {
+    if (live.size() != snap_live.size() || queue.size() != snap_queue.size()) return false;
+    for (const Live& l : live) {
+      auto it = snap_live.find(l.sid);
+      if (it == snap_live.end() || it->second != l.gen) return false;
+    }
+    std::vector<int> q(queue.begin(), queue.end());
+    std::vector<int> sq = snap_queue;
+    std::sort(q.begin(), q.end());
+    std::sort(sq.begin(), sq.end());
+    return q == sq;
+  };
+
+  // publication of finished samples (G > 1: after the GPU step completed).
+  // Appends to the shared order are serialised by a tiny process-shared lock.
+  std::deque<std::pair<int, int>> to_publish;  // (sid, step index that finished it)
+  std::atomic<int>& n_pub = hdr->n_pub;
+  auto publish_now = [&](int sid) {
+    region.owner()[sid] = me;
+    while (hdr->lock.exchange(1, std::memory_order_acquire)) std::this_thread::yield();
+    const int idx = n_pub.load(std::memory_order_relaxed);
+    region.pub_order()[idx] = sid;
+    n_pub.store(idx + 1, std::memory_order_release);
+    hdr->lock.store(0, std::memory_order_release);
+  };
+
+  auto flush_publish = [&](bool wait_all) {
+    while (!to_publish.empty()) {
+      const int k = to_publish.front().second;
+      if (G > 1 && k >= 0) {
+        if (wait_all) {
+          FP_CUDA(cudaEventSynchronize(step_end[k]));
+        } else if (cudaEventQuery(step_end[k]) != cudaSuccess) {
+          break;
+        }
+      }
+      publish_now(to_publish.front().first);
+      to_publish.pop_front();
+    }
+  };
+
+  // ---- scoring claims --------------------------------------------------------------------
+  struct Batch {
+    cudaEvent_t b, e;
+  };
+  std::deque<Batch> inflight;
+  std::vector<int> my_scored;
+  bool gen_done_me = false;
+  double infer_ms = 0.0;
+  auto retire_batches = [&](bool wait) {
+    while (!inflight.empty()) {
+      if (wait) FP_CUDA(cudaEventSynchronize(inflight.front().e));
+      else if (cudaEventQuery(inflight.front().e) != cudaSuccess) break;
+      infer_ms += ms_between(inflight.front().b, inflight.front().e);
+      inflight.pop_front();
+    }
+  };
+  auto service = [&]() {
+    const bool all_gen_done = hdr->gen_done.load() >= G;
+    if (!fused && !all_gen_done) return;
+    retire_batches(false);
+    const int max_inflight = gen_done_me ? 2 : 1;
+    while (static_cast<int>(inflight.size()) < max_inflight) {
+      int c = hdr->n_claimed.load();
+      const int avail_end = n_pub.load();
+      if (c >= avail_end) return;
+      // take finished samples in publish order up to claim_tokens tokens
+      int end = c;
+      int64_t toks = 0;
+      const int* order = region.pub_order();
+      while (end < avail_end && toks < opts.claim_tokens) {
+        const GenSample& b = batch[order[end]];
+        toks += b.prompt_len + b.target_output_len;
+        ++end;
+      }
+      // Generating ranks take full batches only; an idle rank takes whatever
+      // is there when it has nothing in flight; after every rank finished
+      // generating, the remainder goes in any size.
+      const bool hungry = gen_done_me && inflight.empty();
+      if (toks < opts.claim_tokens && !all_gen_done && !hungry && !(gen_done_me && G == 1)) return;
+      if (!hdr->n_claimed.compare_exchange_strong(c, end)) continue;
+      std::vector<fpe::Engine::InferItem> items;
+      for (int i = c; i < end; ++i) {
+        const int sid = order[i];
+        const int own = region.owner()[sid];
+        items.push_back({sid, batch[sid].prompt_len, batch[sid].target_output_len,
+                         peer_tok[own] + static_cast<size_t>(sid) * ec.max_new,
+                         peer_logp[own] + static_cast<size_t>(sid) * ec.max_new});
+        my_scored.push_back(sid);
+        res.stats.infer_tokens += batch[sid].prompt_len + batch[sid].target_output_len;
+      }
+      res.stats.infer_samples += end - c;
+      // local finishes may still be in flight on the decode stream
+      if (!step_end.empty()) FP_CUDA(cudaStreamWaitEvent(si, step_end.back(), 0));
+      Batch bt;
+      FP_CUDA(cudaEventCreate(&bt.b));
+      FP_CUDA(cudaEventCreate(&bt.e));
+      events.push_back(bt.b);
+      events.push_back(bt.e);
+      FP_CUDA(cudaEventRecord(bt.b, si));
+      E.infer(items, opts.kl_beta, opts.gamma, opts.lam);
+      FP_CUDA(cudaEventRecord(bt.e, si));
+      inflight.push_back(bt);
+    }
+  };
+
+  // ---- generation loop ----------------------------------------------------------------
+  std::vector<fpe::Engine::DecodeRow> rows;
+  auto retire_finished = [&]() {
+    std::vector<Live> keep;
+    keep.reserve(live.size());
+    for (const Live& l : live) {
+      if (l.gen >= l.target) {
+        kv_used -= batch[l.sid].kv_bytes;
+        E.release(l.slot);
+        slot_of[l.sid] = -1;
+        finish_step[l.sid] = static_cast<int>(step_end.size()) - 1;
+        res.finish_instance[l.sid] = me;
+        to_publish.emplace_back(l.sid, static_cast<int>(step_end.size()) - 1);
+      } else {
+        keep.push_back(l);
+      }
+    }
+    live.swap(keep);
+  };
+  auto admit_fitting = [&]() {
+    std::vector<fpe::Engine::PrefillItem> items;
+    while (!queue.empty()) {
+      const int s = queue.front();
+      const double kv = batch[s].kv_bytes;
+      if (cap > 0.0 && kv_used + kv > cap + 1e-6) break;
+      queue.pop_front();
+      kv_used += kv;
+      const int P = batch[s].prompt_len, R = batch[s].target_output_len;
+      const int slot = E.reserve(P - 1 + R);
+      E.upload_block_table(slot, sd);
+      slot_of[s] = slot;
+      const int* pr = prompts.data() + static_cast<size_t>(s) * ec.max_prompt;
+      items.push_back({s, slot, P - 1, pr, pr[P - 1]});
+      live.push_back({s, slot, 0, R});
+      res.stats.prefill_tokens += P - 1;
+    }
+    if (!items.empty()) E.prefill(items);
+  };
+  auto decode_one = [&]() {
+    rows.clear();
+    int64_t ctx = 0;
+    for (const Live& l : live) {
+      const int P = batch[l.sid].prompt_len;
+      const int tgt = mode == 0 ? forced_token(opts.token_seed, l.sid, l.gen, ec.max_new, V) : 0;
+      rows.push_back({l.sid, l.slot, P - 1 + l.gen, l.gen, tgt});
+      ctx += P + l.gen;
+    }
+    cudaEvent_t b, e;
+    FP_CUDA(cudaEventCreate(&b));
+    FP_CUDA(cudaEventCreate(&e));
+    events.push_back(b);
+    events.push_back(e);
+    FP_CUDA(cudaEventRecord(b, sd));
+    E.decode(rows, mode, 1.0f / opts.temperature, opts.sample_seed);
+    FP_CUDA(cudaEventRecord(e, sd));
+    step_begin.push_back(b);
+    step_end.push_back(e);
+    for (Live& l : live) ++l.gen;
+    res.stats.decode_steps += 1;
+    res.stats.decode_rows += static_cast<int64_t>(rows.size());
+    res.stats.decode_ctx_tokens += ctx;
+    // bound host run-ahead
+    const int k = static_cast<int>(step_end.size()) - 1 - opts.run_ahead;
+    if (k >= 0) FP_CUDA(cudaEventSynchronize(step_end[k]));
+  };
+
+  auto generation = [&](bool stop_at_trigger) -> bool {  // returns true when paused at the trigger
+    for (;;) {
+      retire_finished();
+      flush_publish(false);
+      admit_fitting();
+      if (stop_at_trigger && at_snapshot()) return true;
+      if (live.empty()) {
+        if (!queue.empty()) throw InfeasibleError("generation wedged: KV capacity below a single sample");
+        return false;
+      }
+      decode_one();
+      if (stop_at_trigger && at_snapshot()) return true;
+      service();
+    }
+  };
+
+  bool paused = generation(pending_trigger);
+  if (paused) {
+    // ---- one-shot migration --------------------------------------------------------
+    FP_CUDA(cudaStreamSynchronize(sd));
+    cudaEvent_t ev_trig = new_event(sd);
+    FP_CUDA(cudaEventSynchronize(ev_trig));
+    res.stats.trigger_seconds = ms_between(ev_start, ev_trig) * 1e-3;
+    const auto tm0 = Clock::now();
+    // sources publish the page lists of their in-flight migrants
+    for (const Move& m : moves)
+      if (m.src == me && m.inflight) {
+        const auto& pg = E.pages_of(slot_of[m.sid]);
+        std::copy(pg.begin(), pg.end(), region.pages(m.sid));
+      }
+    flush_publish(true);
+    region.barrier();
+    const bool recompute = res.trigger.plan.mechanism == MigrationMechanism::kRecomputePrefill;
+    std::vector<fpk::CopyChunk> chunks;
+    std::vector<int> quad_slot, quad_sid, quad_gen, quad_P;
+    std::vector<fpe::Engine::PrefillItem> redo;
+    std::vector<std::vector<int>> redo_tokens;
+    for (const Move& m : moves) {
+      if (m.dst != me) continue;
+      if (!m.inflight) {
+        queue.push_back(m.sid);
+        continue;
+      }
+      const int P = batch[m.sid].prompt_len, R = batch[m.sid].target_output_len;
+      const int slot = E.reserve(P - 1 + R);
+      E.upload_block_table(slot, sd);
+      slot_of[m.sid] = slot;
+      kv_used += batch[m.sid].kv_bytes;
+      live.push_back({m.sid, slot, m.gen, R});
+      res.stats.migrated_in += 1;
+      // history rows (token ids + actor log-probs)
+      const size_t hoff = static_cast<size_t>(m.sid) * ec.max_new;
+      if (m.gen > 0) {
+        const size_t hb = ((static_cast<size_t>(m.gen) * 4 + 15) / 16) * 16;
+        chunks.push_back({peer_tok[m.src] + hoff, E.d_hist_tok() + hoff, hb});
+        chunks.push_back({peer_logp[m.src] + hoff, E.d_hist_logp() + hoff, hb});
+      }
+      if (!recompute) {
+        const int ctx = P - 1 + m.gen;
+        const int np = E.pages_for(ctx);
+        const auto& dst_pages = E.pages_of(slot);
+        const int* src_pages = region.pages(m.sid);
+        for (int i = 0; i < np; ++i) {
+          chunks.push_back({peer_pool[m.src] + static_cast<size_t>(src_pages[i]) * E.page_bytes(),
+                            E.pool_base() + static_cast<size_t>(dst_pages[i]) * E.page_bytes(), E.page_bytes()});
+          res.stats.migrated_bytes += static_cast<int64_t>(E.page_bytes());
+        }
+        quad_slot.push_back(slot);
+        quad_sid.push_back(m.sid);
+        quad_gen.push_back(m.gen);
+        quad_P.push_back(P);
+      } else {
+        redo.push_back({m.sid, slot, P - 1 + m.gen, nullptr, 0});
+      }
+    }
+    const size_t chunk_bytes = ((chunks.size() * sizeof(fpk::CopyChunk)) + 255) & ~size_t(255);
+    uint8_t* scratch = static_cast<uint8_t*>(E.decode_scratch(chunk_bytes + quad_slot.size() * 16 + 256));
+    if (!chunks.empty()) {
+      // history rows are copied 16-byte padded; the pad stays inside the row
+      auto* d = reinterpret_cast<fpk::CopyChunk*>(scratch);
+      E.upload(d, chunks.data(), chunks.size() * sizeof(fpk::CopyChunk), sd);
+      fpk::copy_chunks(d, static_cast<int>(chunks.size()), sd);
+    }
+    if (!quad_slot.empty()) {
+      const int q = static_cast<int>(quad_slot.size());
+      std::vector<int> quad;
+      quad.insert(quad.end(), quad_slot.begin(), quad_slot.end());
+      quad.insert(quad.end(), quad_sid.begin(), quad_sid.end());
+      quad.insert(quad.end(), quad_gen.begin(), quad_gen.end());
+      quad.insert(quad.end(), quad_P.begin(), quad_P.end());
+      int* d = reinterpret_cast<int*>(scratch + chunk_bytes);
+      E.upload(d, quad.data(), quad.size() * 4, sd);
+      fpk::cur_from_hist(d, q, E.d_hist_tok(), ec.max_new, E.d_prompts(), ec.max_prompt, E.d_cur_tok(), sd);
+    }
+    if (!redo.empty()) {
+      // recompute: prefill prompt + generated prefix on this GPU
+      FP_CUDA(cudaStreamSynchronize(sd));
+      for (auto& it : redo) {
+        const int gen = it.ctx_tokens - (batch[it.sid].prompt_len - 1);
+        std::vector<int> toks(prompts.begin() + static_cast<size_t>(it.sid) * ec.max_prompt,
+                              prompts.begin() + static_cast<size_t>(it.sid) * ec.max_prompt + batch[it.sid].prompt_len);
+        std::vector<int> h(std::max(gen, 1));
+        if (gen > 0)
+          FP_CUDA(cudaMemcpy(h.data(), E.d_hist_tok() + static_cast<size_t>(it.sid) * ec.max_new, gen * 4,
+                             cudaMemcpyDeviceToHost));
+        for (int k = 0; k + 1 < gen; ++k) toks.push_back(h[k]);
+        it.next_token = gen > 0 ? h[gen - 1] : toks[batch[it.sid].prompt_len - 1];
+        redo_tokens.push_back(std::move(toks));
+      }
+      for (size_t i = 0; i < redo.size(); ++i) redo[i].tokens = redo_tokens[i].data();
+      E.prefill(redo);
+    }
+    FP_CUDA(cudaStreamSynchronize(sd));
+    region.barrier();
+    // sources drop what left (reference order: in-flight list order, then FIFO)
+    std::vector<char> gone(n, 0);
+    for (const Move& m : moves)
+      if (m.src == me) gone[m.sid] = 1;
+    std::vector<Live> keep;
+    for (const Live& l : live) {
+      if (gone[l.sid]) {
+        kv_used -= batch[l.sid].kv_bytes;
+        E.release(l.slot);
+        slot_of[l.sid] = -1;
+      } else {
+        keep.push_back(l);
+      }
+    }
+    live.swap(keep);
+    std::deque<int> q2;
+    for (int s : queue)
+      if (!gone[s]) q2.push_back(s);
+    queue.swap(q2);
+    res.stats.migrate_seconds = std::chrono::duration<double>(Clock::now() - tm0).count();
+    generation(false);
+  }
+
+  // ---- generation finished on this rank -----------------------------------------------
+  flush_publish(true);
+  gen_done_me = true;
+  hdr->gen_done.fetch_add(1);
+  while (hdr->n_claimed.load() < n) {
+    flush_publish(false);
+    service();
+    if (hdr->error.load()) throw std::runtime_error("peer rank failed");
+    retire_batches(false);
+    std::this_thread::yield();
+  }
+  retire_batches(true);
+  E.synchronize();
+  cudaEvent_t ev_end = new_event(sd);
+  FP_CUDA(cudaEventSynchronize(ev_end));
+
+  // ---- stats ------------------------------------------------------------------------------
+  res.stats.gen_seconds = step_end.empty() ? 0.0 : ms_between(ev_start, step_end.back()) * 1e-3;
+  double dec_ms = 0.0;
+  for (size_t k = 0; k < step_end.size(); ++k) dec_ms += ms_between(step_begin[k], step_end[k]);
+  res.stats.decode_gpu_seconds = dec_ms * 1e-3;
+  res.stats.infer_busy_seconds = infer_ms * 1e-3;
+  res.finish_wall.assign(n, -1.0);
+  for (int s = 0; s < n; ++s)
+    if (finish_step[s] >= 0) res.finish_wall[s] = ms_between(ev_start, step_end[finish_step[s]]) * 1e-3;
+
+  // ---- gather experience ------------------------------------------------------------------
+  const fpe::Engine::Experience& X = E.experience();
+  ExperienceBatch& xb = res.experience;
+  xb.resp_off = resp_off;
+  const size_t T = static_cast<size_t>(total);
+  xb.tokens.resize(T);
+  std::vector<float>* fv[7] = {&xb.logp_actor, &xb.logp_ref, &xb.values, &xb.kl, &xb.reward, &xb.adv, &xb.ret};
+  const float* dv[7] = {X.logp_actor, X.logp_ref, X.values, X.kl, X.reward, X.adv, X.ret};
+  for (auto* v : fv) v->resize(T);
+  xb.score.resize(n);
+  if (T > 0) {
+    FP_CUDA(cudaMemcpy(xb.tokens.data(), X.tokens, T * 4, cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 7; ++k) FP_CUDA(cudaMemcpy(fv[k]->data(), dv[k], T * 4, cudaMemcpyDeviceToHost));
+  }
+  FP_CUDA(cudaMemcpy(xb.score.data(), X.score, n * 4, cudaMemcpyDeviceToHost));
+  if (G > 1) {
+    // scatter my scored samples into the shared result arrays; rank 0 collects
+    for (int sid : my_scored) {
+      const int64_t b = resp_off[sid], e = resp_off[sid + 1];
+      std::memcpy(reinterpret_cast<int*>(region.result(0)) + b, xb.tokens.data() + b, (e - b) * 4);
+      for (int k = 0; k < 7; ++k) std::memcpy(region.result(k + 1) + b, fv[k]->data() + b, (e - b) * 4);
+      region.score()[sid] = xb.score[sid];
+    }
+    // finish times / instances to rank 0 via the page area is not needed: each
+    // rank reports its own; rank 0 returns the union it can see.
+    region.barrier();
+    if (me == 0) {
+      std::memcpy(xb.tokens.data(), region.result(0), T * 4);
+      for (int k = 0; k < 7; ++k) std::memcpy(fv[k]->data(), region.result(k + 1), T * 4);
+      std::memcpy(xb.score.data(), region.score(), n * 4);
+    }
+    region.barrier();
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+  }
+  res.stats.wall_seconds = std::chrono::duration<double>(Clock::now() - wall0).count();
+  for (cudaEvent_t e : events) cudaEventDestroy(e);
+  return res;
+}
+
+}  // namespace fuseplan
+
+const fpe::Engine& fp_engine_internal(const fuseplan::GpuEngine* g) { return *g->eng; }

@@ -1,0 +1,224 @@
+// fuseplan-b200 — host launchers and instantiations of the tcgen05 GEMM.
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+
+#include "gemm.cuh"
+#include "ops.h"
+#include "vocab.cuh"
+
+namespace fpk {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || p == nullptr)
+      throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  int rows, k, box;
+  bool operator==(const MapKey& o) const { return ptr == o.ptr && rows == o.rows && k == o.k && box == o.box; }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = reinterpret_cast<size_t>(k.ptr);
+    h ^= (static_cast<size_t>(k.rows) * 0x9E3779B97F4A7C15ull) ^ (static_cast<size_t>(k.k) << 20) ^ k.box;
+    return h;
+  }
+};
+
+// bf16 [rows, k] row-major (K innermost), box {64, box_rows}, 128 B swizzle.
+CUtensorMap make_map(const void* ptr, int rows, int k, int box_rows) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  const MapKey key{ptr, rows, k, box_rows};
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  if (cache.size() > 4096) cache.clear();
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(k) * 2};
+  const cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1u, 1u};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  cache.emplace(key, m);
+  return m;
+}
+
+template <int BN, class Epi>
+void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int splits, const Epi& epi,
+            cudaStream_t st) {
+  using C = GemmCfg<BN>;
+  if (K % kBK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
+  if (a_rows <= 0 || b_rows <= 0) return;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr_set = true;
+  }
+  const CUtensorMap ma = make_map(A, a_rows, K, 128);
+  const CUtensorMap mb = make_map(B, b_rows, K, BN);
+  GemmGeom g;
+  g.a_rows = a_rows;
+  g.b_rows = b_rows;
+  g.k_blocks = K / kBK;
+  splits = std::max(1, std::min(splits, g.k_blocks));
+  g.kb_per_split = (g.k_blocks + splits - 1) / splits;
+  const int z = (g.k_blocks + g.kb_per_split - 1) / g.kb_per_split;
+  dim3 grid((a_rows + 127) / 128, (b_rows + BN - 1) / BN, z);
+  tc_gemm_kernel<BN, Epi><<<grid, kGemmThreads, C::kSmem, st>>>(ma, mb, g, epi);
+}
+
+template <class Epi, class F>
+void dispatch_bn(int M, F&& f) {
+  if (M <= 16) f.template operator()<16>();
+  else if (M <= 32) f.template operator()<32>();
+  else if (M <= 64) f.template operator()<64>();
+  else if (M <= 128) f.template operator()<128>();
+  else f.template operator()<256>();
+}
+
+}  // namespace
+
+int gemm_splits(int N, int K) {
+  const int kb = K / kBK;
+  const int tiles = (N + 127) / 128;
+  int s = (2 * 148 + tiles - 1) / tiles;
+  s = std::min(s, 16);
+  s = std::min(s, kb);
+  // Equalise the K range per split so that no split is empty.
+  const int per = (kb + s - 1) / s;
+  return (kb + per - 1) / per;
+}
+
+void gemm_bf16(const bf16* W, int N, int K, const bf16* X, int M, bf16* out, int ld_out, cudaStream_t st) {
+  EpiStoreBF16 e{out, ld_out, N, M};
+  dispatch_bn<EpiStoreBF16>(M, [&]<int BN>() { launch<BN>(W, N, X, M, K, 1, e, st); });
+}
+
+void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* out, int splits, cudaStream_t st) {
+  EpiStoreF32 e{out, static_cast<size_t>(M) * N, N, N, M, 0};
+  dispatch_bn<EpiStoreF32>(M, [&]<int BN>() { launch<BN>(W, N, X, M, K, splits, e, st); });
+}
+
+void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float* resid, cudaStream_t st) {
+  EpiStoreF32 e{resid, 0, N, N, M, 1};
+  dispatch_bn<EpiStoreF32>(M, [&]<int BN>() { launch<BN>(W, N, X, M, K, 1, e, st); });
+}
+
+void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
+  dispatch_bn<int>(M, [&]<int BN>() {
+    EpiSwiGLU<BN> e{out, F, F, M};
+    launch<BN>(Wgu, 2 * F, X, M, K, 1, e, st);
+  });
+}
+
+constexpr int kVocabBN = 256;
+
+int vocab_tiles(int V) { return (V + kVocabBN - 1) / kVocabBN; }
+
+void gemm_vocab(const bf16* X, int M, int K, const bf16* Whead, int V, int mode, float inv_temp, const int* target,
+                const int* sample_id, const int* step, uint64_t seed, void* part, float* tgt_z, cudaStream_t st) {
+  EpiVocab e;
+  e.part = static_cast<VocabPartial*>(part);
+  e.tgt_z = tgt_z;
+  e.info = VocabRowInfo{target, sample_id, step};
+  e.mode = mode;
+  e.inv_temp = inv_temp;
+  e.vocab = V;
+  e.rows = M;
+  e.n_tiles = vocab_tiles(V);
+  e.seed_lo = static_cast<uint32_t>(seed);
+  e.seed_hi = static_cast<uint32_t>(seed >> 32);
+  launch<kVocabBN>(X, M, Whead, V, K, 1, e, st);
+}
+
+// One warp per row: merge the vocab tiles in order.
+__global__ void vocab_finalize_kernel(const VocabPartial* __restrict__ part, const float* __restrict__ tgt_z, int M,
+                                      int n_tiles, int mode, const int* __restrict__ target, int* token, float* logp,
+                                      const int* dst, int* out_tok, float* out_logp, const int* cur_idx,
+                                      int* cur_tok) {
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M) return;
+  const VocabPartial* p = part + static_cast<size_t>(row) * n_tiles;
+  float m = -INFINITY;
+  for (int t = lane; t < n_tiles; t += 32) m = fmaxf(m, p[t].m);
+  m = warp_max(m);
+  float s = 0.f;
+  float bkey = -INFINITY, bz = 0.f;
+  int bidx = 0x7fffffff;
+  for (int t = lane; t < n_tiles; t += 32) {
+    const VocabPartial q = p[t];
+    if (q.m > -INFINITY) s += q.s * expf(q.m - m);
+    if (q.idx >= 0 && (q.key > bkey || (q.key == bkey && q.idx < bidx))) {
+      bkey = q.key;
+      bidx = q.idx;
+      bz = q.z;
+    }
+  }
+  s = warp_sum(s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ok = __shfl_xor_sync(0xffffffffu, bkey, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+    const float oz = __shfl_xor_sync(0xffffffffu, bz, o);
+    if (ok > bkey || (ok == bkey && oi < bidx)) {
+      bkey = ok;
+      bidx = oi;
+      bz = oz;
+    }
+  }
+  if (lane != 0) return;
+  const float lse = m + logf(s);
+  int tok;
+  float lp;
+  if (mode == kForced) {
+    tok = target[row];
+    lp = tgt_z[row] - lse;
+  } else {
+    tok = bidx;
+    lp = bz - lse;
+  }
+  if (token) token[row] = tok;
+  if (logp) logp[row] = lp;
+  if (dst) {
+    const int d = dst[row];
+    if (d >= 0) {
+      if (out_tok) out_tok[d] = tok;
+      if (out_logp) out_logp[d] = lp;
+    }
+  }
+  if (cur_tok) cur_tok[cur_idx[row]] = tok;
+}
+
+void vocab_finalize(const void* part, const float* tgt_z, int M, int V, int mode, const int* target, int* token,
+                    float* logp, const int* dst, int* out_tok, float* out_logp, const int* cur_idx, int* cur_tok,
+                    cudaStream_t st) {
+  if (M <= 0) return;
+  const int warps = 8;
+  vocab_finalize_kernel<<<(M + warps - 1) / warps, warps * 32, 0, st>>>(
+      static_cast<const VocabPartial*>(part), tgt_z, M, vocab_tiles(V), mode, target, token, logp, dst, out_tok,
+      out_logp, cur_idx, cur_tok);
+}
+
+}  // namespace fpk

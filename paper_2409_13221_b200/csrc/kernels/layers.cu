@@ -1,0 +1,274 @@
+// fuseplan-b200 — memory-bound transformer pieces: synthetic weight init,
+// embedding gather, fused residual-add + RMSNorm (+ optional value head),
+// RoPE + KV append into the paged pool.
+#include <math.h>
+
+#include "ops.h"
+#include "philox.cuh"
+#include "ptx.cuh"
+
+namespace fpk {
+
+namespace {
+
+constexpr float kEps = 1e-5f;
+
+__global__ void init_bf16_kernel(bf16* __restrict__ w, size_t n, uint64_t seed, uint64_t tag, float scale) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const float u = unit24(hash3(seed, tag, i));
+    const float t = __fsub_rn(__fmul_rn(u, 2.0f), 1.0f);
+    w[i] = __float2bfloat16_rn(__fmul_rn(t, scale));
+  }
+}
+
+__global__ void init_gain_kernel(float* __restrict__ g, size_t n, uint64_t seed, uint64_t tag) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const float u = unit24(hash3(seed, tag, i));
+    const float t = __fsub_rn(__fmul_rn(u, 2.0f), 1.0f);
+    g[i] = __fadd_rn(1.0f, __fmul_rn(0.1f, t));
+  }
+}
+
+__global__ void init_bf16_gu_kernel(bf16* __restrict__ w, int F, int d, uint64_t seed, uint64_t tag, float scale) {
+  const size_t n = static_cast<size_t>(2) * F * d;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const size_t row = i / d, col = i % d;
+    const size_t grp = row / 128, within = row % 128;
+    const size_t logical = within < 64 ? grp * 64 + within : static_cast<size_t>(F) + grp * 64 + (within - 64);
+    const float u = unit24(hash3(seed, tag, logical * d + col));
+    const float t = __fsub_rn(__fmul_rn(u, 2.0f), 1.0f);
+    w[i] = __float2bfloat16_rn(__fmul_rn(t, scale));
+  }
+}
+
+__global__ void assemble_kernel(AssembleArgs a) {
+  const int j = blockIdx.x;
+  const int sid = a.sid[j], P = a.P[j], R = a.R[j], row0 = a.cu[j], r0 = a.roff[j];
+  const int T = P + R;
+  const int* hist = a.hist_tok[j];
+  const float* hl = a.hist_logp[j];
+  const int* pr = a.prompts + static_cast<size_t>(sid) * a.max_prompt;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    a.tokens[row0 + t] = t < P ? pr[t] : hist[t - P];
+    a.pos[row0 + t] = t;
+  }
+  for (int k = threadIdx.x; k < R; k += blockDim.x) {
+    a.targets[r0 + k] = hist[k];
+    a.logp_actor[r0 + k] = hl[k];
+    a.gather_resp[r0 + k] = row0 + P - 1 + k;
+  }
+  if (threadIdx.x == 0) a.gather_last[j] = row0 + T - 1;
+}
+
+__global__ void embed_kernel(const int* __restrict__ tok, const int* __restrict__ idx, const bf16* __restrict__ E,
+                             int d, float* __restrict__ x) {
+  const int m = blockIdx.x;
+  const bf16* e = E + static_cast<size_t>(tok[idx ? idx[m] : m]) * d;
+  float* o = x + static_cast<size_t>(m) * d;
+  for (int j = threadIdx.x * 2; j < d; j += blockDim.x * 2) {
+    const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(e + j);
+    o[j] = __bfloat162float(v.x);
+    o[j + 1] = __bfloat162float(v.y);
+  }
+}
+
+__device__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  float t = (l < nw) ? red[l] : 0.f;
+  t = warp_sum(t);
+  __syncthreads();
+  return t;
+}
+
+// One block per output row; d <= 8192.
+__global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__ parts, int nsplit,
+                                size_t split_stride, const float* __restrict__ gain, bf16* __restrict__ y, int d,
+                                const int* __restrict__ gather, const bf16* __restrict__ value_w,
+                                float* __restrict__ value) {
+  extern __shared__ float row[];
+  __shared__ float red[32];
+  const int i = blockIdx.x;
+  const int src = gather ? gather[i] : i;
+  float* xr = x + static_cast<size_t>(src) * d;
+  float ss = 0.f;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float v = xr[j];
+    for (int s = 0; s < nsplit; ++s) v += parts[s * split_stride + static_cast<size_t>(src) * d + j];
+    if (!gather && nsplit > 0) xr[j] = v;
+    row[j] = v;
+    ss += v * v;
+  }
+  ss = block_sum(ss, red);
+  const float inv = rsqrtf(ss / d + kEps);
+  if (value_w) {
+    float dot = 0.f;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) dot += row[j] * inv * gain[j] * __bfloat162float(value_w[j]);
+    dot = block_sum(dot, red);
+    if (threadIdx.x == 0) value[i] = dot;
+    return;
+  }
+  bf16* yr = y + static_cast<size_t>(i) * d;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) yr[j] = __float2bfloat16_rn(row[j] * inv * gain[j]);
+}
+
+__device__ __forceinline__ size_t kv_elem_offset(const KvPoolView& p, int page, int layer, int kvh, int hd, int tok,
+                                                 bool is_v) {
+  const size_t head_elems = static_cast<size_t>(2) * p.page_tokens * hd;
+  return (static_cast<size_t>(page) * p.page_bytes + static_cast<size_t>(layer) * p.layer_bytes) / 2 +
+         kvh * head_elems + (is_v ? static_cast<size_t>(p.page_tokens) * hd : 0) + static_cast<size_t>(tok) * hd;
+}
+
+// grid: M rows; block: 128. Rotate-half RoPE (pairs i, i + hd/2).
+__global__ void rope_qkv_kernel(const bf16* __restrict__ qkv, int H, int KVH, int hd, const int* __restrict__ pos,
+                                float log2_theta, bf16* __restrict__ q_out, bf16* __restrict__ k_out,
+                                bf16* __restrict__ v_out, KvPoolView pool, int use_pool, int layer,
+                                const int* __restrict__ slot) {
+  const int m = blockIdx.x;
+  const int p = pos[m];
+  const int width = (H + 2 * KVH) * hd;
+  const bf16* in = qkv + static_cast<size_t>(m) * width;
+  const int half = hd / 2;
+  bf16* pool_base = reinterpret_cast<bf16*>(pool.base);
+  int page = 0, in_page = 0;
+  if (use_pool) {
+    const int sl = slot[m];
+    page = pool.block_table[sl * pool.bt_stride + p / pool.page_tokens];
+    in_page = p % pool.page_tokens;
+  }
+  // rotated heads: H query heads then KVH key heads
+  for (int idx = threadIdx.x; idx < (H + KVH) * half; idx += blockDim.x) {
+    const int h = idx / half, i = idx % half;
+    const float inv_freq = exp2f(-(2.0f * i / hd) * log2_theta);
+    const float ang = static_cast<float>(p) * inv_freq;
+    float sn, cs;
+    sincosf(ang, &sn, &cs);
+    const float x1 = __bfloat162float(in[h * hd + i]);
+    const float x2 = __bfloat162float(in[h * hd + i + half]);
+    const bf16 o1 = __float2bfloat16_rn(x1 * cs - x2 * sn);
+    const bf16 o2 = __float2bfloat16_rn(x2 * cs + x1 * sn);
+    if (h < H) {
+      bf16* q = q_out + (static_cast<size_t>(m) * H + h) * hd;
+      q[i] = o1;
+      q[i + half] = o2;
+    } else {
+      const int kh = h - H;
+      if (k_out) {
+        bf16* k = k_out + (static_cast<size_t>(m) * KVH + kh) * hd;
+        k[i] = o1;
+        k[i + half] = o2;
+      }
+      if (use_pool) {
+        bf16* k = pool_base + kv_elem_offset(pool, page, layer, kh, hd, in_page, false);
+        k[i] = o1;
+        k[i + half] = o2;
+      }
+    }
+  }
+  // values: plain copy
+  for (int idx = threadIdx.x; idx < KVH * hd; idx += blockDim.x) {
+    const int kh = idx / hd, j = idx % hd;
+    const bf16 v = in[(H + KVH) * hd + idx];
+    if (v_out) v_out[(static_cast<size_t>(m) * KVH + kh) * hd + j] = v;
+    if (use_pool) pool_base[kv_elem_offset(pool, page, layer, kh, hd, in_page, true) + j] = v;
+  }
+}
+
+__global__ void scatter_int_kernel(const int* __restrict__ idx, const int* __restrict__ val, int n,
+                                   int* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[idx[i]] = val[i];
+}
+
+__global__ void copy_chunks_kernel(const CopyChunk* __restrict__ list) {
+  const CopyChunk c = list[blockIdx.x];
+  const int4* src = static_cast<const int4*>(c.src);
+  int4* dst = static_cast<int4*>(c.dst);
+  const size_t n = c.bytes / 16;
+  size_t i = threadIdx.x;
+  for (; i + 3 * blockDim.x < n; i += 4 * blockDim.x) {
+    const int4 a = src[i], b = src[i + blockDim.x], cc = src[i + 2 * blockDim.x], d = src[i + 3 * blockDim.x];
+    dst[i] = a;
+    dst[i + blockDim.x] = b;
+    dst[i + 2 * blockDim.x] = cc;
+    dst[i + 3 * blockDim.x] = d;
+  }
+  for (; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+__global__ void cur_from_hist_kernel(const int* __restrict__ q, int n, const int* __restrict__ hist, int max_new,
+                                     const int* __restrict__ prompts, int max_prompt, int* __restrict__ cur) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int slot = q[i], sid = q[n + i], gen = q[2 * n + i], P = q[3 * n + i];
+  cur[slot] = gen > 0 ? hist[static_cast<size_t>(sid) * max_new + gen - 1]
+                      : prompts[static_cast<size_t>(sid) * max_prompt + P - 1];
+}
+
+int grid_for(size_t n) {
+  const size_t b = (n + 255) / 256;
+  return static_cast<int>(b < 148 * 16 ? (b == 0 ? 1 : b) : 148 * 16);
+}
+
+}  // namespace
+
+void init_bf16(bf16* w, size_t n, uint64_t seed, uint64_t tag, float scale, cudaStream_t st) {
+  init_bf16_kernel<<<grid_for(n), 256, 0, st>>>(w, n, seed, tag, scale);
+}
+
+void init_gain(float* g, size_t n, uint64_t seed, uint64_t tag, cudaStream_t st) {
+  init_gain_kernel<<<grid_for(n), 256, 0, st>>>(g, n, seed, tag);
+}
+
+void init_bf16_gu(bf16* w, int F, int d, uint64_t seed, uint64_t tag, float scale, cudaStream_t st) {
+  init_bf16_gu_kernel<<<grid_for(static_cast<size_t>(2) * F * d), 256, 0, st>>>(w, F, d, seed, tag, scale);
+}
+
+void embed(const int* tokens, const int* idx, int M, const bf16* E, int d, float* x, cudaStream_t st) {
+  if (M <= 0) return;
+  embed_kernel<<<M, 128, 0, st>>>(tokens, idx, E, d, x);
+}
+
+void copy_chunks(const CopyChunk* d_list, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  copy_chunks_kernel<<<n, 256, 0, st>>>(d_list);
+}
+
+void cur_from_hist(const int* d_quad, int n, const int* hist_tok, int max_new, const int* prompts, int max_prompt,
+                   int* cur_tok, cudaStream_t st) {
+  if (n <= 0) return;
+  cur_from_hist_kernel<<<(n + 127) / 128, 128, 0, st>>>(d_quad, n, hist_tok, max_new, prompts, max_prompt, cur_tok);
+}
+
+void scatter_int(const int* idx, const int* val, int n, int* dst, cudaStream_t st) {
+  if (n <= 0) return;
+  scatter_int_kernel<<<(n + 255) / 256, 256, 0, st>>>(idx, val, n, dst);
+}
+
+void assemble_batch(const AssembleArgs& a, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  assemble_kernel<<<n, 256, 0, st>>>(a);
+}
+
+void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, const float* gain, bf16* y, int M, int d,
+              const int* gather, int M_out, const bf16* value_w, float* value, cudaStream_t st) {
+  const int rows = gather ? M_out : M;
+  if (rows <= 0) return;
+  const int threads = d >= 2048 ? 256 : 128;
+  add_norm_kernel<<<rows, threads, d * sizeof(float), st>>>(x, parts, parts ? nsplit : 0, split_stride, gain, y, d,
+                                                             gather, value_w, value);
+}
+
+void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, float rope_theta, bf16* q_out,
+              bf16* k_out, bf16* v_out, const KvPoolView* pool, int layer, const int* slot, cudaStream_t st) {
+  if (M <= 0) return;
+  KvPoolView pv{};
+  if (pool) pv = *pool;
+  rope_qkv_kernel<<<M, 128, 0, st>>>(qkv, H, KVH, hd, pos, log2f(rope_theta), q_out, k_out, v_out, pv,
+                                     pool != nullptr ? 1 : 0, layer, slot);
+}
+
+}  // namespace fpk

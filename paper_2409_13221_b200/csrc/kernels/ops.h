@@ -1,0 +1,118 @@
+// fuseplan-b200 — host-callable launchers of the sm_100a kernels.
+// Every function enqueues on `st` and never synchronises.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace fpk {
+
+using bf16 = __nv_bfloat16;
+
+// ---- GEMMs (tcgen05; gemm.cu) --------------------------------------------------
+// swap-AB: out[m][n] = sum_k X[m][k] W[n][k]; W [N, K], X [M, K], K % 64 == 0.
+void gemm_bf16(const bf16* W, int N, int K, const bf16* X, int M, bf16* out, int ld_out, cudaStream_t st);
+// fp32 split-K partials: out[s][m][n] for s < splits (see gemm_splits()).
+void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* out, int splits, cudaStream_t st);
+// resid[m][n] += sum_k X[m][k] W[n][k] (single split; residual add fused).
+void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float* resid, cudaStream_t st);
+// SwiGLU, W_gu [2F, K] interleaved in 64-row gate/up groups: out[m][f], ld = F.
+void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st);
+// Split count used by gemm_f32_splitk for an (N, K) weight; a function of the
+// weight shape only, so each row's result does not depend on the batch.
+int gemm_splits(int N, int K);
+
+struct VocabOut;  // fwd
+// Vocab head: rows X [M, K] against W_head [V, K]; writes per-(row, tile)
+// partials into `part` (M x vocab_tiles(V) VocabPartial = 24 B each) and, in
+// forced mode, tgt_z[M]. mode: 0 forced (target[]), 1 greedy, 2 sample.
+int vocab_tiles(int V);
+void gemm_vocab(const bf16* X, int M, int K, const bf16* Whead, int V, int mode, float inv_temp,
+                const int* target, const int* sample_id, const int* step, uint64_t seed, void* part, float* tgt_z,
+                cudaStream_t st);
+// Merge partials: token[row] (forced -> target), logp[row]; optional scatter
+// into per-sample buffers: out_tok[dst[row]] / out_logp[dst[row]] when dst != nullptr.
+// cur_tok[cur_idx[row]] = token (next decode input) when cur_tok != nullptr.
+void vocab_finalize(const void* part, const float* tgt_z, int M, int V, int mode, const int* target, int* token,
+                    float* logp, const int* dst, int* out_tok, float* out_logp, const int* cur_idx, int* cur_tok,
+                    cudaStream_t st);
+
+// ---- elementwise / norms (layers.cu) ----------------------------------------------
+void init_bf16(bf16* w, size_t n, uint64_t seed, uint64_t tag, float scale, cudaStream_t st);
+void init_gain(float* g, size_t n, uint64_t seed, uint64_t tag, cudaStream_t st);
+// Gate/up weight [2F, d] stored in 64-row interleaved groups (see EpiSwiGLU);
+// the hash index is that of the logical [gate; up] matrix.
+void init_bf16_gu(bf16* w, int F, int d, uint64_t seed, uint64_t tag, float scale, cudaStream_t st);
+// x[m] = E[tokens[idx ? idx[m] : m]] (fp32 residual stream).
+void embed(const int* tokens, const int* idx, int M, const bf16* E, int d, float* x, cudaStream_t st);
+// Packed scoring batch: for sample j (global id sid[j], prompt P[j], response
+// R[j], rows [cu[j], cu[j+1])): tokens = prompt ++ response, pos = 0..T-1;
+// response-aligned outputs at [roff[j], roff[j] + R[j]): targets (response
+// ids), logp_actor (from the generator's history), gather_resp (row of
+// position P-1+k); gather_last[j] = row of position T-1.
+struct AssembleArgs {
+  const int* sid; const int* P; const int* R; const int* cu; const int* roff;
+  const int* prompts; int max_prompt;            // [n_global][max_prompt]
+  const int* const* hist_tok; const float* const* hist_logp;  // per sample j: base of that sample's row
+  int* tokens; int* pos; int* targets; float* logp_actor; int* gather_resp; int* gather_last;
+};
+void assemble_batch(const AssembleArgs& a, int n, cudaStream_t st);
+// For output row i (src = gather ? gather[i] : i): xs = x[src] + sum_s parts[s][src];
+// if !gather, x[src] = xs. y[i] = bf16(rmsnorm(xs) * g). If value_w != nullptr,
+// instead value[i] = dot(rmsnorm(xs) * g, value_w) and y is not written.
+void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, const float* gain, bf16* y, int M,
+              int d, const int* gather, int M_out, const bf16* value_w, float* value, cudaStream_t st);
+
+// RoPE on q, k of a packed qkv [M, (H + 2 KVH) * hd] row block; q -> q_out
+// [M, H, hd]; k, v -> either contiguous k_out/v_out [M, KVH, hd] and/or the
+// paged pool (pool != nullptr): token (slot[i], pos[i]).
+struct KvPoolView {
+  uint8_t* base;          // page 0
+  size_t page_bytes;      // bytes per page (all layers)
+  size_t layer_bytes;     // bytes per layer inside a page
+  int page_tokens;        // tokens per page
+  const int* block_table; // [slots][max_pages]
+  int bt_stride;          // max_pages
+};
+void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, float rope_theta, bf16* q_out,
+              bf16* k_out, bf16* v_out, const KvPoolView* pool, int layer, const int* slot, cudaStream_t st);
+
+// ---- attention (attention.cu) -----------------------------------------------------
+// Decode: q [B, H, hd] (one token per row), paged K/V of `layer`; ctx[b]
+// tokens visible (including the one just appended). out [B, H, hd] bf16.
+// work: float scratch of attn_decode_workspace(B, H, hd, max_ctx) floats.
+size_t attn_decode_workspace(int B, int H, int hd, int max_ctx);
+void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer, const int* slot,
+                 const int* ctx, int max_ctx, float* work, bf16* out, cudaStream_t st);
+// Varlen causal attention over packed q [M, H, hd], k/v [M, KVH, hd];
+// sequences [cu[i], cu[i+1]). tiles: host-built table of (seq, q_tile) pairs
+// (attn_varlen_tiles). out [M, H, hd].
+int attn_varlen_tiles(const int* cu_host, int n_seq, int* tiles_host);
+void attn_varlen(const bf16* q, const bf16* k, const bf16* v, int H, int KVH, int hd, const int* cu, const int* tiles,
+                 int n_tiles, bf16* out, cudaStream_t st);
+
+// ---- post-processing (post.cu) -----------------------------------------------------
+// Per sample i, inputs at tokens [off[i], off[i+1]): kl, reward, advantage,
+// return (fp32). Outputs go to the same packed offsets, or — with `scatter` —
+// to [off_out[i], off_out[i] + R_i) of the global experience arrays, together
+// with copies of logp_actor / logp_ref / values / token ids and score[sid[i]].
+struct PostScatter {
+  const int64_t* off_out; const int* sid; const int* tokens_in;
+  float *logp_actor, *logp_ref, *values, *score_out; int* tokens_out;
+};
+void postprocess(int n, const int* off, const float* logp_actor, const float* logp_ref, const float* values,
+                 const float* score, float beta, float gamma, float lam, float* kl, float* reward, float* adv,
+                 float* ret, cudaStream_t st, const PostScatter* scatter = nullptr);
+// Bulk copies (e.g. KV pages pulled from a peer GPU over NVLink, history
+// rows): one CTA per chunk, 16-byte vector loads; src/dst/bytes 16-aligned.
+struct CopyChunk { const void* src; void* dst; unsigned long long bytes; };
+void copy_chunks(const CopyChunk* d_list, int n, cudaStream_t st);
+// cur_tok[slot[i]] = gen[i] > 0 ? hist[sid[i]][gen[i]-1] : prompts[sid[i]][P[i]-1]
+void cur_from_hist(const int* d_quad, int n, const int* hist_tok, int max_new, const int* prompts, int max_prompt,
+                   int* cur_tok, cudaStream_t st);  // d_quad: [4][n] = slot, sid, gen, P
+// dst[idx[i]] = val[i]
+void scatter_int(const int* idx, const int* val, int n, int* dst, cudaStream_t st);
+
+}  // namespace fpk

@@ -1,0 +1,152 @@
+"""Python host mirror of the engine C ABI (include/fp_engine.h).
+
+`Engine(workload)` creates one B200 engine (weights of the four models, paged
+KV pool, workspaces) on a device; `Engine.execute(...)` runs the gen+inf stage
+(serial = stage barrier, or fused) for a batch, returning the experience
+batch, measured statistics and the decision-clock result — the GPU
+counterpart of Sched.simulate_serial / simulate_fused (genfuse.hpp:113-121).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+from .configs import Dims, Workload
+from .sched import GenSimConfig, Sched, batch_to_c
+
+TOKEN_MODES = {"forced": 0, "greedy": 1, "sample": 2}
+SCHEDULES = {"stage_barrier": 0, "serial": 0, "fused": 1}
+
+
+def _dims(d: Dims) -> _lib.ModelDims:
+    return _lib.ModelDims(d.num_layers, d.hidden, d.num_heads, d.num_kv_heads, d.head_dim, d.ffn, d.vocab)
+
+
+@dataclass
+class Experience:
+    resp_off: np.ndarray
+    tokens: np.ndarray
+    logp_actor: np.ndarray
+    logp_ref: np.ndarray
+    values: np.ndarray
+    kl: np.ndarray
+    reward: np.ndarray
+    adv: np.ndarray
+    ret: np.ndarray
+    score: np.ndarray
+
+    def sample(self, i: int) -> dict:
+        b, e = int(self.resp_off[i]), int(self.resp_off[i + 1])
+        return {k: getattr(self, k)[b:e] for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward",
+                                                   "adv", "ret")} | {"score": float(self.score[i])}
+
+
+@dataclass
+class ExecOutput:
+    stats: dict
+    experience: Experience
+    finish_seconds: np.ndarray
+    finish_instance: np.ndarray
+    decision: object  # sched.GenStageResult
+    moves: list       # (sample, from, to) in application order
+
+
+class Engine:
+    def __init__(self, w: Workload, *, device: int = 0, weight_seed: int = 1234, max_samples: int | None = None,
+                 max_live: int | None = None, kv_pool_bytes: int = 0, max_prefill_tokens: int = 16384,
+                 max_infer_tokens: int = 16384, rope_theta: float = 10000.0):
+        self.lib = _lib.load()
+        self.workload = w
+        n = max_samples or w.n_prompts
+        setup = _lib.EngineSetup(_dims(w.actor), _dims(w.ref), _dims(w.critic), _dims(w.reward), weight_seed,
+                                 w.prompt_len, w.max_new, n, max_live or n, kv_pool_bytes, max_prefill_tokens,
+                                 max_infer_tokens, rope_theta, device)
+        self.setup = setup
+        h = C.c_void_p()
+        check(self.lib, self.lib.fp_engine_create(C.byref(setup), C.byref(h)))
+        self.h = h
+        self.sched = Sched(self.lib)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.fp_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def model_size(self, m: int) -> tuple:
+        b, p = C.c_int64(), C.c_int64()
+        check(self.lib, self.lib.fp_engine_model_size(self.h, m, C.byref(b), C.byref(p)))
+        return b.value, p.value
+
+    def kv_bytes_per_token(self) -> int:
+        v = C.c_int64()
+        check(self.lib, self.lib.fp_engine_kv_bytes_per_token(self.h, C.byref(v)))
+        return v.value
+
+    def synthetic_prompts(self, n: int, token_seed: int) -> np.ndarray:
+        out = np.zeros((n, self.setup.max_prompt), dtype=np.int32)
+        check(self.lib, self.lib.fp_synthetic_prompts(self.h, n, token_seed,
+                                                      out.ctypes.data_as(C.POINTER(C.c_int32))))
+        return out
+
+    def execute(self, batch: list, cfg: GenSimConfig, r_t: int = 0, *, token_mode: str = "forced",
+                schedule: str = "fused", temperature: float = 1.0, token_seed: int = 7, sample_seed: int = 11,
+                kl_beta: float = 0.05, gamma: float = 1.0, lam: float = 0.95, claim_tokens: int = 8192,
+                run_ahead: int = 4, rank: int = 0, world: int = 1, shm_name: str | None = None,
+                prompts: np.ndarray | None = None) -> ExecOutput:
+        keep: list = []
+        n = len(batch)
+        opts = _lib.RunOptions(TOKEN_MODES[token_mode], SCHEDULES[schedule], temperature, token_seed, sample_seed,
+                               kl_beta, gamma, lam, claim_tokens, run_ahead)
+        comm = _lib.Comm(rank, world, shm_name.encode() if shm_name else None)
+        pp = None
+        if prompts is not None:
+            prompts = np.ascontiguousarray(prompts, dtype=np.int32)
+            pp = prompts.ctypes.data_as(C.POINTER(C.c_int32))
+        x = C.c_void_p()
+        check(self.lib, self.lib.fp_execute(self.h, batch_to_c(batch, keep), n, C.byref(cfg.c(keep)), r_t,
+                                            C.byref(opts), C.byref(comm), pp, C.byref(x)))
+        try:
+            st = _lib.ExecStats()
+            check(self.lib, self.lib.fp_exec_stats_get(x, C.byref(st)))
+            stats = {k: getattr(st, k) for k, _ in _lib.ExecStats._fields_}
+            T = st.total_resp
+            f32 = lambda: np.zeros(max(T, 1), dtype=np.float32)  # noqa: E731
+            arrs = {k: f32() for k in ("logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret")}
+            tokens = np.zeros(max(T, 1), dtype=np.int32)
+            off = np.zeros(n + 1, dtype=np.int64)
+            score = np.zeros(n, dtype=np.float32)
+            fp = lambda a: a.ctypes.data_as(C.POINTER(C.c_float))  # noqa: E731
+            check(self.lib, self.lib.fp_exec_experience(
+                x, off.ctypes.data_as(C.POINTER(C.c_int64)), tokens.ctypes.data_as(C.POINTER(C.c_int32)),
+                fp(arrs["logp_actor"]), fp(arrs["logp_ref"]), fp(arrs["values"]), fp(arrs["kl"]),
+                fp(arrs["reward"]), fp(arrs["adv"]), fp(arrs["ret"]), fp(score)))
+            exp = Experience(off, tokens[:T], *(arrs[k][:T] for k in ("logp_actor", "logp_ref", "values", "kl",
+                                                                        "reward", "adv", "ret")), score)
+            fin = np.zeros(n, dtype=np.float64)
+            inst = np.zeros(n, dtype=np.int32)
+            check(self.lib, self.lib.fp_exec_finish(x, fin.ctypes.data_as(C.POINTER(C.c_double)),
+                                                    inst.ctypes.data_as(C.POINTER(C.c_int32))))
+            hres = C.c_void_p()
+            check(self.lib, self.lib.fp_exec_decision(x, C.byref(hres)))
+            try:
+                decision = self.sched.result_from_handle(hres)
+            finally:
+                self.lib.fp_result_free(hres)
+            nm = C.c_int32()
+            check(self.lib, self.lib.fp_exec_moves(x, C.byref(nm), None, None, None))
+            ms, mf, mt = ((C.c_int32 * max(nm.value, 1))() for _ in range(3))
+            check(self.lib, self.lib.fp_exec_moves(x, C.byref(nm), ms, mf, mt))
+            moves = list(zip(ms[:nm.value], mf[:nm.value], mt[:nm.value]))
+            return ExecOutput(stats, exp, fin, inst, decision, moves)
+        finally:
+            self.lib.fp_exec_free(x)
