@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""bench.py — RLHF experience samples/s of the gen+inf stage on B200s.
+
+One step = one full experience collection over a prompt batch: prefill, the
+actor's batched decode with retire-on-finish (sampled tokens, Zipf-skewed
+lengths), Reference/Critic/Reward scoring of every finished sample and
+per-token KL / reward / GAE / returns — through the C ABI (fp_execute).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+N = 1: BASELINE.json configs[1] (GPT-2-small shape, 512 prompts x 128 tokens,
+<= 1024 new). N > 1: weak scaling, 512 prompts per GPU, fused schedule with
+the one-shot long-tail migration at r_t = 20% of the batch.
+
+`value`  — samples/s with prompts resident and the experience left in HBM;
+`e2e`    — the same through host buffers (prompt upload and experience
+           download inside the timed region);
+`stage_barrier` — the unfused schedule on the same GPUs (same K);
+`roofline` — decode attention (the dominant kernel), algorithmic bytes per
+           launch / CUDA-event duration, against MEASURED_PEAKS.json;
+`cpu_baseline` — the CPU oracle (numpy port) on a bounded sample, rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+import uuid
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "RLHF experience samples/sec (gen+inference fused) at 1/2/4/8 B200; % HBM/tensor roofline"
+UNIT = "samples/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = Path(f"/tmp/fp_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=open(self.path, "w"),
+                stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(", ") for r in self.path.read_text().strip().splitlines() if r.strip()]
+        except OSError:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 3 + i and r[3 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][1]),
+                "samples": len(rows), "reasons": reasons}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        pg = dist
+    return world, rank, local, pg
+
+
+def workload_for(n_gpus):
+    from paper_2409_13221_b200.configs import WORKLOADS, scaled
+    w = WORKLOADS["gpt2s"]
+    return scaled(w, n_prompts=w.n_prompts * n_gpus)
+
+
+def cpu_oracle_rate(w, batch, n_samples: int, time_budget: float = 30.0):
+    """Samples/s of the numpy CPU oracle on the first samples of the batch (all host threads)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from model_oracle import Oracle, forced_response, synthetic_prompts
+    orc = Oracle(w)
+    prompts = synthetic_prompts(len(batch), w.prompt_len, w.actor.vocab, 7)
+    t0 = time.perf_counter()
+    done = 0
+    tokens = 0
+    for s in batch[:n_samples]:
+        resp = forced_response(s.id, s.target_output_len, w.max_new, w.actor.vocab, 7)
+        orc.experience(prompts[s.id, :s.prompt_len], resp, 0.05, 1.0, 0.95)
+        done += 1
+        tokens += s.prompt_len + s.target_output_len
+        if time.perf_counter() - t0 > time_budget:
+            break
+    dt = time.perf_counter() - t0
+    return done / dt, done, tokens, dt
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU path. The reference library only
+    simulates this stage (cost formulas, no model math), so the
+    CPU implementation of the path that produces experience is the oracle
+    port; the simulator's own runtime is reported beside it."""
+    if rank != 0:
+        return
+    from paper_2409_13221_b200.configs import batch_for, gen_config
+    from paper_2409_13221_b200.sched import Sched
+    w = workload_for(args.gpus)
+    sched = Sched()
+    batch = batch_for(w, sched)
+    cores = os.cpu_count() or 1
+    rates = []
+    info = None
+    for step in range(args.warmup + args.steps):
+        r, done, toks, dt = cpu_oracle_rate(w, batch, n_samples=2, time_budget=20.0)
+        if step >= args.warmup:
+            rates.append(r)
+            info = (done, toks, dt)
+    value = statistics.median(rates)
+    sim = None
+    ref_lib = ROOT / "oracle" / "_ref" / "libfuseplan_ref.so"
+    if ref_lib.exists():
+        rs = Sched(str(ref_lib))
+        cfg = gen_config(w, args.gpus)
+        t0 = time.perf_counter()
+        rs.simulate_fused(batch, cfg, round(0.2 * len(batch)))
+        sim = time.perf_counter() - t0
+    sample = (f"{info[0]} of {len(batch)} prompts ({info[1]} tokens) teacher-forced through actor/ref/critic/reward "
+              f"+ KL/GAE post-processing, numpy fp32, {info[2]:.1f}s per step")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * len(batch) / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": w.name, "prompts": len(batch), "prompt_len": w.prompt_len,
+                                            "max_new": w.max_new},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_simulator_seconds": sim,
+            "note": "reference path is a discrete-event simulator without model math; CPU arm = oracle port"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--r-ratio", type=float, default=0.2)
+    ap.add_argument("--token-mode", default="sample", choices=["forced", "greedy", "sample"])
+    ap.add_argument("--claim-tokens", type=int, default=8192)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-barrier-arm", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="value pass only (for profiling)")
+    args = ap.parse_args()
+    world, rank, local, dist = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        if dist:
+            dist.barrier()
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    from paper_2409_13221_b200.configs import batch_for, gen_config
+    from paper_2409_13221_b200.engine import Engine
+
+    G = world
+    w = workload_for(G)
+    eng = Engine(w, device=local, max_samples=w.n_prompts, max_live=min(w.n_prompts, 2 * w.n_prompts // G))
+    batch = batch_for(w, eng.sched)
+    cfg = gen_config(w, G)
+    r_t = round(args.r_ratio * len(batch)) if G > 1 else 0
+    shm = None
+    if dist:
+        obj = [f"/fp_bench_{uuid.uuid4().hex[:12]}" if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        shm = obj[0]
+    prompts = eng.synthetic_prompts(len(batch), 7)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def step(schedule, resident, probe=False):
+        return eng.execute(batch, cfg, r_t, token_mode=args.token_mode, schedule=schedule,
+                           claim_tokens=args.claim_tokens, rank=rank, world=G,
+                           shm_name=(shm + f"_{step.k}") if shm else None, prompts=prompts, resident=resident,
+                           probe_attention=probe)
+    step.k = 0
+
+    def timed(schedule, resident, K, probe=False):
+        outs = []
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(K):
+            step.k += 1
+            outs.append(step(schedule, resident, probe))
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, outs
+
+    # warm-up (both schedules, both residency modes)
+    for i in range(args.warmup):
+        step.k += 1
+        step("fused", i % 2 == 0)
+    log(f"[bench] rank {rank}: warm-up done")
+
+    with Clocks(local) as clk:
+        ms_v, outs_v = timed("fused", True, args.steps, probe=True)
+    clocks = clk.summary()
+    n_total = len(batch)
+    value = n_total * args.steps / (ms_v / 1000.0)
+    st = outs_v[-1].stats
+    probe_ms = sum(o.stats["attn_probe_ms"] for o in outs_v)
+    probe_bytes = sum(o.stats["attn_probe_bytes"] for o in outs_v)
+    probe_n = sum(o.stats["attn_probe_launches"] for o in outs_v)
+    launches = sum(o.stats["gpu_launches"] for o in outs_v)
+
+    e2e = sb = None
+    h2d = len(batch) * w.prompt_len * 4 + len(batch) * 4 * 6
+    d2h = int(st["total_resp"]) * 4 * 8 + len(batch) * 4
+    if not args.quick:
+        ms_e, outs_e = timed("fused", False, args.steps)
+        e2e = n_total * args.steps / (ms_e / 1000.0)
+        if not args.no_barrier_arm:
+            ms_s, _ = timed("stage_barrier", True, args.steps)
+            sb = n_total * args.steps / (ms_s / 1000.0)
+
+    cpu = None
+    if rank == 0 and G == 1 and not args.no_cpu_baseline and not args.quick:
+        r, done, toks, dt = cpu_oracle_rate(w, batch, n_samples=2, time_budget=20.0)
+        cpu = {"value": r, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+               "sample": f"{done} of {len(batch)} prompts ({toks} tokens) through the numpy oracle "
+                         f"(teacher-forced actor/ref/critic/reward + post-processing), {dt:.1f}s"}
+
+    if rank != 0:
+        eng.close()
+        return
+    hbm, tflops, src = peaks()
+    achieved = (probe_bytes / (probe_ms / 1000.0)) / 1e9 if probe_ms > 0 else None
+    traffic = None
+    tp = ROOT / "profiles" / "attn_decode_traffic.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_v / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic: hash-seeded random-init weights and prompts, Zipf(s=1.0) output lengths on [16, 1024], "
+                f"{args.token_mode} tokens",
+        "config": {"workload": "GPT-2-small-shape actor/ref/critic/reward (L12 d768 H12 ffn3072 V50257), "
+                               f"{w.n_prompts // G} prompts x {w.prompt_len} tokens per GPU, <= {w.max_new} new",
+                   "prompts": n_total, "schedule": "fused", "r_t": r_t, "token_mode": args.token_mode,
+                   "claim_tokens": args.claim_tokens,
+                   "l2": "inputs larger than L2 (KV pool and weights >> 126 MB)",
+                   "parallelism": f"dp{G} (one engine per B200)"},
+        "roofline": {"kernel": "attn_decode (paged KV flash-decoding)", "bound": "hbm", "achieved": achieved,
+                     "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
+                     "traffic": traffic, "peak_source": src, "launches": probe_n,
+                     "bytes_per_launch": probe_bytes / max(probe_n, 1),
+                     "share_of_step": (probe_ms / ms_v) if ms_v else None},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "stage_barrier": {"value": sb, "unit": UNIT, "speedup_fused": (value / sb) if sb else None},
+        "clocks": clocks,
+        "gpu_launches": launches,
+        "stats": {k: st[k] for k in ("decode_steps", "decode_rows", "decode_ctx_tokens", "prefill_tokens",
+                                     "infer_tokens", "gen_seconds", "decode_gpu_seconds", "infer_busy_seconds",
+                                     "migrated_in", "migrated_bytes")},
+    }
+    print(json.dumps(line), flush=True)
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -54,6 +54,8 @@ typedef struct fp_run_options {
   uint64_t token_seed, sample_seed;
   float kl_beta, gamma, lam;
   int32_t claim_tokens, run_ahead;
+  int32_t resident;        /* 1: prompts already resident (same as previous call), experience kept on device */
+  int32_t probe_attention; /* 1: time each decode-attention launch (stats.attn_probe_*) */
 } fp_run_options;
 
 typedef struct fp_comm {
@@ -66,6 +68,9 @@ typedef struct fp_exec_stats {
   int64_t decode_steps, decode_rows, decode_ctx_tokens, prefill_tokens, infer_tokens, infer_samples;
   int64_t migrated_in, migrated_bytes;
   int64_t total_resp;
+  int64_t gpu_launches;
+  double attn_probe_ms, attn_probe_bytes;
+  int64_t attn_probe_launches;
 } fp_exec_stats;
 
 typedef struct fp_engine fp_engine;

@@ -53,6 +53,8 @@ struct EngineOptions {
   float kl_beta = 0.05f, gamma = 1.0f, lam = 0.95f;
   int claim_tokens = 8192;         // scoring batch granularity (tokens)
   int run_ahead = 4;               // decode steps the host may enqueue ahead of the GPU
+  bool resident = false;           // prompts already on the device (same ids as last call), experience left there
+  bool probe_attention = false;    // time every decode-attention launch (bench roofline)
 };
 
 /// Multi-process coordination (G > 1): every rank passes the same shm name.
@@ -79,6 +81,9 @@ struct ExecStats {
   std::int64_t prefill_tokens = 0, infer_tokens = 0, infer_samples = 0;
   std::int64_t migrated_in = 0, migrated_bytes = 0;
   double decode_gpu_seconds = 0.0;  // sum of decode-step GPU durations
+  std::int64_t gpu_launches = 0;    // kernels this rank launched
+  double attn_probe_ms = 0.0, attn_probe_bytes = 0.0;  // probe_attention totals
+  std::int64_t attn_probe_launches = 0;
 };
 
 struct ExecResult {

@@ -108,7 +108,8 @@ class EngineSetup(C.Structure):
 class RunOptions(C.Structure):
     _fields_ = [("token_mode", C.c_int32), ("schedule", C.c_int32), ("temperature", C.c_float),
                 ("token_seed", C.c_uint64), ("sample_seed", C.c_uint64), ("kl_beta", C.c_float),
-                ("gamma", C.c_float), ("lam", C.c_float), ("claim_tokens", C.c_int32), ("run_ahead", C.c_int32)]
+                ("gamma", C.c_float), ("lam", C.c_float), ("claim_tokens", C.c_int32), ("run_ahead", C.c_int32),
+                ("resident", C.c_int32), ("probe_attention", C.c_int32)]
 
 
 class Comm(C.Structure):
@@ -121,7 +122,8 @@ class ExecStats(C.Structure):
                 ("decode_gpu_seconds", C.c_double), ("decode_steps", C.c_int64), ("decode_rows", C.c_int64),
                 ("decode_ctx_tokens", C.c_int64), ("prefill_tokens", C.c_int64), ("infer_tokens", C.c_int64),
                 ("infer_samples", C.c_int64), ("migrated_in", C.c_int64), ("migrated_bytes", C.c_int64),
-                ("total_resp", C.c_int64)]
+                ("total_resp", C.c_int64), ("gpu_launches", C.c_int64), ("attn_probe_ms", C.c_double),
+                ("attn_probe_bytes", C.c_double), ("attn_probe_launches", C.c_int64)]
 
 
 P = C.POINTER

@@ -199,6 +199,8 @@ int fp_execute(fp_engine* e, const fp_gen_sample* batch, int32_t n, const fp_gen
       throw std::invalid_argument("GaeInputs: gamma and lam must lie in [0, 1]");
     eo.claim_tokens = o->claim_tokens > 0 ? o->claim_tokens : 8192;
     eo.run_ahead = o->run_ahead > 0 ? o->run_ahead : 4;
+    eo.resident = o->resident != 0;
+    eo.probe_attention = o->probe_attention != 0;
     fuseplan::CommSetup cs;
     if (comm) {
       cs.rank = comm->rank;
@@ -239,6 +241,10 @@ int fp_exec_stats_get(const fp_exec* x, fp_exec_stats* s) {
     s->migrated_in = t.migrated_in;
     s->migrated_bytes = t.migrated_bytes;
     s->total_resp = x->r.experience.resp_off.empty() ? 0 : x->r.experience.resp_off.back();
+    s->gpu_launches = t.gpu_launches;
+    s->attn_probe_ms = t.attn_probe_ms;
+    s->attn_probe_bytes = t.attn_probe_bytes;
+    s->attn_probe_launches = t.attn_probe_launches;
   });
 }
 

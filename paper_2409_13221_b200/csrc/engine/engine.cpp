@@ -119,6 +119,8 @@ Engine::~Engine() {
     if (models_[m].blob) cudaFree(models_[m].blob);
   if (exp_blob_) cudaFree(exp_blob_);
   if (scratch_) cudaFree(scratch_);
+  for (auto& p : probes_) probe_pool_.insert(probe_pool_.end(), {p.a, p.b});
+  for (cudaEvent_t e : probe_pool_) cudaEventDestroy(e);
   delete ring_;
   cudaStreamDestroy(s_decode_);
   cudaStreamDestroy(s_infer_);
@@ -253,12 +255,14 @@ void Engine::alloc_ws() {
 
 // ---------------------------------------------------------------------------
 
-void Engine::load_prompts(const int* prompts, int n) {
+void Engine::load_prompts(const int* prompts, int n, uint64_t tag) {
   if (n > cfg_.max_samples) throw std::invalid_argument("engine: batch larger than max_samples");
   upload(d_prompts_, prompts, static_cast<size_t>(n) * cfg_.max_prompt * sizeof(int), s_decode_);
+  prompts_tag_ = tag;
 }
 
 void Engine::set_layout(const std::vector<int64_t>& resp_off) {
+  if (exp_blob_ && resp_off == resp_off_) return;  // same layout: reuse (results are overwritten)
   resp_off_ = resp_off;
   const size_t n = resp_off.empty() ? 0 : resp_off.size() - 1;
   const size_t total = resp_off.empty() ? 0 : static_cast<size_t>(resp_off.back());
@@ -312,6 +316,33 @@ void* Engine::decode_scratch(size_t bytes) {
     FP_CUDA(cudaMalloc(&scratch_, scratch_bytes_));
   }
   return scratch_;
+}
+
+cudaEvent_t Engine::probe_event() {
+  if (probe_pool_.empty()) {
+    cudaEvent_t e;
+    FP_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  cudaEvent_t e = probe_pool_.back();
+  probe_pool_.pop_back();
+  return e;
+}
+
+Engine::ProbeTotals Engine::drain_attn_probe() {
+  ProbeTotals t;
+  FP_CUDA(cudaStreamSynchronize(s_decode_));
+  for (const ProbeRec& p : probes_) {
+    float ms = 0.f;
+    FP_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    t.ms += ms;
+    t.bytes += p.bytes;
+    t.launches += 1;
+    probe_pool_.push_back(p.a);
+    probe_pool_.push_back(p.b);
+  }
+  probes_.clear();
+  return t;
 }
 
 void Engine::release(int slot) {
@@ -438,7 +469,18 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
                   nullptr, st);
     fpk::gemm_bf16(L.wqkv, D.qkv_width(), D.d, dec_.h, B, dec_.qkv, D.qkv_width(), st);
     fpk::rope_qkv(dec_.qkv, B, D.H, D.KVH, D.hd, pos, cfg_.rope_theta, dec_.q, nullptr, nullptr, &pv, l, slot, st);
-    fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, max_ctx, dec_.attn_work, dec_.attn, st);
+    if (probe_on_) {
+      ProbeRec pr{probe_event(), probe_event(), 0.0};
+      const double kv_tok = 2.0 * D.KVH * D.hd * 2.0;  // K + V of one layer, bf16
+      double ctx_sum = 0.0;
+      for (int b = 0; b < B; ++b) ctx_sum += h[2 * B + b];
+      pr.bytes = ctx_sum * kv_tok + static_cast<double>(B) * D.H * D.hd * 2.0;
+      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, max_ctx, dec_.attn_work, dec_.attn, st, pr.a,
+                       pr.b);
+      probes_.push_back(pr);
+    } else {
+      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, max_ctx, dec_.attn_work, dec_.attn, st);
+    }
     fpk::gemm_f32_splitk(L.wo, D.d, D.H * D.hd, dec_.attn, B, dec_.parts, so, st);
     fpk::add_norm(dec_.x, dec_.parts, so, stride, L.ln2, dec_.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
     fpk::gemm_swiglu(L.wgu, D.F, D.d, dec_.h, B, dec_.act, st);

@@ -94,7 +94,8 @@ class Engine {
 
   // ---- batch data (global sample ids) -------------------------------------------
   // prompts [n][max_prompt] (host), uploaded on the decode stream.
-  void load_prompts(const int* prompts, int n);
+  void load_prompts(const int* prompts, int n, uint64_t tag = 0);
+  uint64_t prompts_tag() const { return prompts_tag_; }
   int* d_prompts() const { return d_prompts_; }
   int* d_hist_tok() const { return d_hist_tok_; }
   float* d_hist_logp() const { return d_hist_logp_; }
@@ -159,7 +160,27 @@ class Engine {
 
   void synchronize();
 
+  // Kernel probe: when enabled, every decode-attention launch is bracketed by
+  // CUDA events on the decode stream and its algorithmic bytes recorded
+  // (K/V of the visible context + q), for the roofline of bench.py.
+  void set_attn_probe(bool on) { probe_on_ = on; }
+  struct ProbeTotals {
+    double ms = 0.0;
+    double bytes = 0.0;
+    long long launches = 0;
+  };
+  ProbeTotals drain_attn_probe();  // synchronises the decode stream
+
  private:
+  struct ProbeRec {
+    cudaEvent_t a, b;
+    double bytes;
+  };
+  bool probe_on_ = false;
+  uint64_t prompts_tag_ = 0;
+  std::vector<ProbeRec> probes_;
+  std::vector<cudaEvent_t> probe_pool_;
+  cudaEvent_t probe_event();
   struct PackedWs {
     int cap = 0, cap_seq = 0;
     float* x = nullptr;

@@ -285,7 +285,11 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
   }
 
   E.set_layout(resp_off);
-  E.load_prompts(prompts.data(), n);
+  uint64_t ptag = 1469598103934665603ull;  // FNV-1a of the prompt ids
+  for (int v : prompts) ptag = (ptag ^ static_cast<uint32_t>(v)) * 1099511628211ull;
+  const long long launches0 = fpk::launch_count();
+  if (!(opts.resident && E.prompts_tag() == ptag)) E.load_prompts(prompts.data(), n, ptag);
+  if (opts.probe_attention) E.set_attn_probe(true);
   cudaStream_t sd = E.decode_stream(), si = E.infer_stream();
   FP_CUDA(cudaStreamSynchronize(sd));
   region.barrier();
@@ -662,10 +666,26 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
   for (int s = 0; s < n; ++s)
     if (finish_step[s] >= 0) res.finish_wall[s] = ms_between(ev_start, step_end[finish_step[s]]) * 1e-3;
 
+  res.stats.gpu_launches = fpk::launch_count() - launches0;
+  if (opts.probe_attention) {
+    const fpe::Engine::ProbeTotals pt = E.drain_attn_probe();
+    E.set_attn_probe(false);
+    res.stats.attn_probe_ms = pt.ms;
+    res.stats.attn_probe_bytes = pt.bytes;
+    res.stats.attn_probe_launches = pt.launches;
+  }
+
   // ---- gather experience ------------------------------------------------------------------
   const fpe::Engine::Experience& X = E.experience();
   ExperienceBatch& xb = res.experience;
   xb.resp_off = resp_off;
+  if (opts.resident) {  // experience stays in HBM (engine-owned arrays)
+    region.barrier();
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    res.stats.wall_seconds = std::chrono::duration<double>(Clock::now() - wall0).count();
+    for (cudaEvent_t e : events) cudaEventDestroy(e);
+    return res;
+  }
   const size_t T = static_cast<size_t>(total);
   xb.tokens.resize(T);
   std::vector<float>* fv[7] = {&xb.logp_actor, &xb.logp_ref, &xb.values, &xb.kl, &xb.reward, &xb.adv, &xb.ret};

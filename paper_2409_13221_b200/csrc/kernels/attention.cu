@@ -440,7 +440,7 @@ void launch_decode(const bf16* q, int B, int H, int KVH, const KvPoolView& pool,
   float* part_ml = work + static_cast<size_t>(B) * H * nsplit * HD;
   const float scale = kLog2e / sqrtf(static_cast<float>(HD));
   attn_decode_kernel<HD, G><<<dim3(KVH, B, nsplit), 160, smem, st>>>(q, pool, layer, slot, ctx, H, nsplit, scale,
-                                                                      part_o, part_ml);
+                                                                      part_o, part_ml); fpk::count_launch();
 }
 
 }  // namespace
@@ -451,8 +451,10 @@ size_t attn_decode_workspace(int B, int H, int hd, int max_ctx) {
 }
 
 void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer, const int* slot,
-                 const int* ctx, int max_ctx, float* work, bf16* out, cudaStream_t st) {
+                 const int* ctx, int max_ctx, float* work, bf16* out, cudaStream_t st, cudaEvent_t probe_begin,
+                 cudaEvent_t probe_end) {
   if (B <= 0) return;
+  if (probe_begin) cudaEventRecord(probe_begin, st);
   if (pool.page_tokens != kPT) throw std::invalid_argument("attn_decode: page_tokens must be 64");
   const int ns = std::max(1, (max_ctx + kChunk - 1) / kChunk);
   const int G = H / KVH;
@@ -462,9 +464,10 @@ void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView&
     throw std::invalid_argument("attn_decode: unsupported (head_dim, group) combination");
   }
 #undef FP_DEC
+  if (probe_end) cudaEventRecord(probe_end, st);
   const float* part_o = work;
   const float* part_ml = work + static_cast<size_t>(B) * H * ns * hd;
-  attn_decode_combine_kernel<<<B * H, std::min(hd, 128), 0, st>>>(part_o, part_ml, ctx, H, hd, ns, out);
+  attn_decode_combine_kernel<<<B * H, std::min(hd, 128), 0, st>>>(part_o, part_ml, ctx, H, hd, ns, out); fpk::count_launch();
 }
 
 int attn_varlen_tiles(const int* cu_host, int n_seq, int* tiles_host) {
@@ -497,7 +500,7 @@ void attn_varlen(const bf16* q, const bf16* k, const bf16* v, int H, int KVH, in
       attr = true;                                                                                           \
     }                                                                                                        \
     attn_varlen_kernel<HD_><<<dim3(n_tiles, H), 128, VarlenCfg<HD_>::kSmem, st>>>(q, k, v, H, KVH, cu, tiles, \
-                                                                                  scale, out);               \
+                                                                                  scale, out); fpk::count_launch();               \
   } else
   FP_VL(32) FP_VL(64) FP_VL(128) { throw std::invalid_argument("attn_varlen: unsupported head_dim"); }
 #undef FP_VL

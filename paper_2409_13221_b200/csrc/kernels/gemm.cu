@@ -85,7 +85,7 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
   g.kb_per_split = (g.k_blocks + splits - 1) / splits;
   const int z = (g.k_blocks + g.kb_per_split - 1) / g.kb_per_split;
   dim3 grid((a_rows + 127) / 128, (b_rows + BN - 1) / BN, z);
-  tc_gemm_kernel<BN, Epi><<<grid, kGemmThreads, C::kSmem, st>>>(ma, mb, g, epi);
+  tc_gemm_kernel<BN, Epi><<<grid, kGemmThreads, C::kSmem, st>>>(ma, mb, g, epi); fpk::count_launch();
 }
 
 template <class Epi, class F>
@@ -218,7 +218,7 @@ void vocab_finalize(const void* part, const float* tgt_z, int M, int V, int mode
   const int warps = 8;
   vocab_finalize_kernel<<<(M + warps - 1) / warps, warps * 32, 0, st>>>(
       static_cast<const VocabPartial*>(part), tgt_z, M, vocab_tiles(V), mode, target, token, logp, dst, out_tok,
-      out_logp, cur_idx, cur_tok);
+      out_logp, cur_idx, cur_tok); fpk::count_launch();
 }
 
 }  // namespace fpk

@@ -3,11 +3,17 @@
 // RoPE + KV append into the paged pool.
 #include <math.h>
 
+#include <atomic>
+
 #include "ops.h"
 #include "philox.cuh"
 #include "ptx.cuh"
 
 namespace fpk {
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 namespace {
 
@@ -216,41 +222,41 @@ int grid_for(size_t n) {
 }  // namespace
 
 void init_bf16(bf16* w, size_t n, uint64_t seed, uint64_t tag, float scale, cudaStream_t st) {
-  init_bf16_kernel<<<grid_for(n), 256, 0, st>>>(w, n, seed, tag, scale);
+  init_bf16_kernel<<<grid_for(n), 256, 0, st>>>(w, n, seed, tag, scale); fpk::count_launch();
 }
 
 void init_gain(float* g, size_t n, uint64_t seed, uint64_t tag, cudaStream_t st) {
-  init_gain_kernel<<<grid_for(n), 256, 0, st>>>(g, n, seed, tag);
+  init_gain_kernel<<<grid_for(n), 256, 0, st>>>(g, n, seed, tag); fpk::count_launch();
 }
 
 void init_bf16_gu(bf16* w, int F, int d, uint64_t seed, uint64_t tag, float scale, cudaStream_t st) {
-  init_bf16_gu_kernel<<<grid_for(static_cast<size_t>(2) * F * d), 256, 0, st>>>(w, F, d, seed, tag, scale);
+  init_bf16_gu_kernel<<<grid_for(static_cast<size_t>(2) * F * d), 256, 0, st>>>(w, F, d, seed, tag, scale); fpk::count_launch();
 }
 
 void embed(const int* tokens, const int* idx, int M, const bf16* E, int d, float* x, cudaStream_t st) {
   if (M <= 0) return;
-  embed_kernel<<<M, 128, 0, st>>>(tokens, idx, E, d, x);
+  embed_kernel<<<M, 128, 0, st>>>(tokens, idx, E, d, x); fpk::count_launch();
 }
 
 void copy_chunks(const CopyChunk* d_list, int n, cudaStream_t st) {
   if (n <= 0) return;
-  copy_chunks_kernel<<<n, 256, 0, st>>>(d_list);
+  copy_chunks_kernel<<<n, 256, 0, st>>>(d_list); fpk::count_launch();
 }
 
 void cur_from_hist(const int* d_quad, int n, const int* hist_tok, int max_new, const int* prompts, int max_prompt,
                    int* cur_tok, cudaStream_t st) {
   if (n <= 0) return;
-  cur_from_hist_kernel<<<(n + 127) / 128, 128, 0, st>>>(d_quad, n, hist_tok, max_new, prompts, max_prompt, cur_tok);
+  cur_from_hist_kernel<<<(n + 127) / 128, 128, 0, st>>>(d_quad, n, hist_tok, max_new, prompts, max_prompt, cur_tok); fpk::count_launch();
 }
 
 void scatter_int(const int* idx, const int* val, int n, int* dst, cudaStream_t st) {
   if (n <= 0) return;
-  scatter_int_kernel<<<(n + 255) / 256, 256, 0, st>>>(idx, val, n, dst);
+  scatter_int_kernel<<<(n + 255) / 256, 256, 0, st>>>(idx, val, n, dst); fpk::count_launch();
 }
 
 void assemble_batch(const AssembleArgs& a, int n, cudaStream_t st) {
   if (n <= 0) return;
-  assemble_kernel<<<n, 256, 0, st>>>(a);
+  assemble_kernel<<<n, 256, 0, st>>>(a); fpk::count_launch();
 }
 
 void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, const float* gain, bf16* y, int M, int d,
@@ -259,7 +265,7 @@ void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, con
   if (rows <= 0) return;
   const int threads = d >= 2048 ? 256 : 128;
   add_norm_kernel<<<rows, threads, d * sizeof(float), st>>>(x, parts, parts ? nsplit : 0, split_stride, gain, y, d,
-                                                             gather, value_w, value);
+                                                             gather, value_w, value); fpk::count_launch();
 }
 
 void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, float rope_theta, bf16* q_out,
@@ -268,7 +274,7 @@ void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, fl
   KvPoolView pv{};
   if (pool) pv = *pool;
   rope_qkv_kernel<<<M, 128, 0, st>>>(qkv, H, KVH, hd, pos, log2f(rope_theta), q_out, k_out, v_out, pv,
-                                     pool != nullptr ? 1 : 0, layer, slot);
+                                     pool != nullptr ? 1 : 0, layer, slot); fpk::count_launch();
 }
 
 }  // namespace fpk

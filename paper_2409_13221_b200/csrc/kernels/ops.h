@@ -11,6 +11,10 @@ namespace fpk {
 
 using bf16 = __nv_bfloat16;
 
+// Number of kernels this library has launched (all launchers count).
+void count_launch();
+long long launch_count();
+
 // ---- GEMMs (tcgen05; gemm.cu) --------------------------------------------------
 // swap-AB: out[m][n] = sum_k X[m][k] W[n][k]; W [N, K], X [M, K], K % 64 == 0.
 void gemm_bf16(const bf16* W, int N, int K, const bf16* X, int M, bf16* out, int ld_out, cudaStream_t st);
@@ -84,8 +88,10 @@ void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, fl
 // tokens visible (including the one just appended). out [B, H, hd] bf16.
 // work: float scratch of attn_decode_workspace(B, H, hd, max_ctx) floats.
 size_t attn_decode_workspace(int B, int H, int hd, int max_ctx);
+// probe_begin / probe_end (optional) bracket the main split kernel (not the combine).
 void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer, const int* slot,
-                 const int* ctx, int max_ctx, float* work, bf16* out, cudaStream_t st);
+                 const int* ctx, int max_ctx, float* work, bf16* out, cudaStream_t st,
+                 cudaEvent_t probe_begin = nullptr, cudaEvent_t probe_end = nullptr);
 // Varlen causal attention over packed q [M, H, hd], k/v [M, KVH, hd];
 // sequences [cu[i], cu[i+1]). tiles: host-built table of (seq, q_tile) pairs
 // (attn_varlen_tiles). out [M, H, hd].

@@ -103,7 +103,7 @@ void postprocess(int n, const int* off, const float* logp_actor, const float* lo
   PostScatter sc{};
   if (scatter) sc = *scatter;
   postprocess_kernel<<<(n + warps - 1) / warps, warps * 32, 0, st>>>(n, off, logp_actor, logp_ref, values, score, beta,
-                                                                      gamma, lam, kl, reward, adv, ret, sc);
+                                                                      gamma, lam, kl, reward, adv, ret, sc); fpk::count_launch();
 }
 
 }  // namespace fpk
