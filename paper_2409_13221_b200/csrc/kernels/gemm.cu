@@ -103,7 +103,7 @@ int gemm_splits(int N, int K) {
   const int kb = K / kBK;
   const int tiles = (N + 127) / 128;
   int s = (2 * 148 + tiles - 1) / tiles;
-  s = std::min(s, 16);
+  s = std::min(s, 8);  // partial traffic (splits x M x N x 4 B) is read back by add_norm
   s = std::min(s, kb);
   // Equalise the K range per split so that no split is empty.
   const int per = (kb + s - 1) / s;

@@ -4,6 +4,7 @@
 #include <math.h>
 
 #include <atomic>
+#include <stdexcept>
 
 #include "ops.h"
 #include "philox.cuh"
@@ -90,35 +91,53 @@ __device__ float block_sum(float v, float* red) {
   return t;
 }
 
-// One block per output row; d <= 8192.
+// One warp per output row (4 rows per 128-thread block), float4 traffic.
 __global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__ parts, int nsplit,
                                 size_t split_stride, const float* __restrict__ gain, bf16* __restrict__ y, int d,
-                                const int* __restrict__ gather, const bf16* __restrict__ value_w,
+                                const int* __restrict__ gather, int rows, const bf16* __restrict__ value_w,
                                 float* __restrict__ value) {
-  extern __shared__ float row[];
-  __shared__ float red[32];
-  const int i = blockIdx.x;
+  extern __shared__ float4 row_buf[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 4 + warp;
+  if (i >= rows) return;
   const int src = gather ? gather[i] : i;
-  float* xr = x + static_cast<size_t>(src) * d;
+  const int d4 = d >> 2;
+  float4* row = row_buf + warp * d4;
+  float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(src) * d);
+  const float4* pr = reinterpret_cast<const float4*>(parts + static_cast<size_t>(src) * d);
+  const size_t ps4 = split_stride >> 2;
   float ss = 0.f;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    float v = xr[j];
-    for (int s = 0; s < nsplit; ++s) v += parts[s * split_stride + static_cast<size_t>(src) * d + j];
+  for (int j = lane; j < d4; j += 32) {
+    float4 v = xr[j];
+    for (int s = 0; s < nsplit; ++s) {
+      const float4 p = pr[s * ps4 + j];
+      v.x += p.x, v.y += p.y, v.z += p.z, v.w += p.w;
+    }
     if (!gather && nsplit > 0) xr[j] = v;
     row[j] = v;
-    ss += v * v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
-  ss = block_sum(ss, red);
+  ss = warp_sum(ss);
   const float inv = rsqrtf(ss / d + kEps);
+  const float4* g4 = reinterpret_cast<const float4*>(gain);
   if (value_w) {
     float dot = 0.f;
-    for (int j = threadIdx.x; j < d; j += blockDim.x) dot += row[j] * inv * gain[j] * __bfloat162float(value_w[j]);
-    dot = block_sum(dot, red);
-    if (threadIdx.x == 0) value[i] = dot;
+    for (int j = lane; j < d4; j += 32) {
+      const float4 v = row[j], g = g4[j];
+      const __nv_bfloat162 w01 = reinterpret_cast<const __nv_bfloat162*>(value_w)[2 * j];
+      const __nv_bfloat162 w23 = reinterpret_cast<const __nv_bfloat162*>(value_w)[2 * j + 1];
+      dot += v.x * inv * g.x * __bfloat162float(w01.x) + v.y * inv * g.y * __bfloat162float(w01.y) +
+             v.z * inv * g.z * __bfloat162float(w23.x) + v.w * inv * g.w * __bfloat162float(w23.y);
+    }
+    dot = warp_sum(dot);
+    if (lane == 0) value[i] = dot;
     return;
   }
-  bf16* yr = y + static_cast<size_t>(i) * d;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) yr[j] = __float2bfloat16_rn(row[j] * inv * gain[j]);
+  uint2* yr = reinterpret_cast<uint2*>(y + static_cast<size_t>(i) * d);
+  for (int j = lane; j < d4; j += 32) {
+    const float4 v = row[j], g = g4[j];
+    yr[j] = make_uint2(pack_bf16x2(v.x * inv * g.x, v.y * inv * g.y), pack_bf16x2(v.z * inv * g.z, v.w * inv * g.w));
+  }
 }
 
 __device__ __forceinline__ size_t kv_elem_offset(const KvPoolView& p, int page, int layer, int kvh, int hd, int tok,
@@ -128,58 +147,66 @@ __device__ __forceinline__ size_t kv_elem_offset(const KvPoolView& p, int page, 
          kvh * head_elems + (is_v ? static_cast<size_t>(p.page_tokens) * hd : 0) + static_cast<size_t>(tok) * hd;
 }
 
-// grid: M rows; block: 128. Rotate-half RoPE (pairs i, i + hd/2).
-__global__ void rope_qkv_kernel(const bf16* __restrict__ qkv, int H, int KVH, int hd, const int* __restrict__ pos,
+// grid: M rows; block: 128. Rotate-half RoPE (pairs i, i + HD/2); cos/sin of
+// the row's position are computed once per pair index and shared by all heads.
+template <int HD>
+__global__ void rope_qkv_kernel(const bf16* __restrict__ qkv, int H, int KVH, const int* __restrict__ pos,
                                 float log2_theta, bf16* __restrict__ q_out, bf16* __restrict__ k_out,
                                 bf16* __restrict__ v_out, KvPoolView pool, int use_pool, int layer,
                                 const int* __restrict__ slot) {
+  constexpr int half = HD / 2;
+  __shared__ float cs_s[half], sn_s[half];
   const int m = blockIdx.x;
   const int p = pos[m];
-  const int width = (H + 2 * KVH) * hd;
+  const int width = (H + 2 * KVH) * HD;
   const bf16* in = qkv + static_cast<size_t>(m) * width;
-  const int half = hd / 2;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    const float inv_freq = exp2f(-(2.0f * i / HD) * log2_theta);
+    float sn, cs;
+    sincosf(static_cast<float>(p) * inv_freq, &sn, &cs);
+    cs_s[i] = cs;
+    sn_s[i] = sn;
+  }
+  __syncthreads();
   bf16* pool_base = reinterpret_cast<bf16*>(pool.base);
   int page = 0, in_page = 0;
   if (use_pool) {
-    const int sl = slot[m];
-    page = pool.block_table[sl * pool.bt_stride + p / pool.page_tokens];
+    page = pool.block_table[slot[m] * pool.bt_stride + p / pool.page_tokens];
     in_page = p % pool.page_tokens;
   }
-  // rotated heads: H query heads then KVH key heads
   for (int idx = threadIdx.x; idx < (H + KVH) * half; idx += blockDim.x) {
     const int h = idx / half, i = idx % half;
-    const float inv_freq = exp2f(-(2.0f * i / hd) * log2_theta);
-    const float ang = static_cast<float>(p) * inv_freq;
-    float sn, cs;
-    sincosf(ang, &sn, &cs);
-    const float x1 = __bfloat162float(in[h * hd + i]);
-    const float x2 = __bfloat162float(in[h * hd + i + half]);
+    const float cs = cs_s[i], sn = sn_s[i];
+    const float x1 = __bfloat162float(in[h * HD + i]);
+    const float x2 = __bfloat162float(in[h * HD + i + half]);
     const bf16 o1 = __float2bfloat16_rn(x1 * cs - x2 * sn);
     const bf16 o2 = __float2bfloat16_rn(x2 * cs + x1 * sn);
     if (h < H) {
-      bf16* q = q_out + (static_cast<size_t>(m) * H + h) * hd;
+      bf16* q = q_out + (static_cast<size_t>(m) * H + h) * HD;
       q[i] = o1;
       q[i + half] = o2;
     } else {
       const int kh = h - H;
       if (k_out) {
-        bf16* k = k_out + (static_cast<size_t>(m) * KVH + kh) * hd;
+        bf16* k = k_out + (static_cast<size_t>(m) * KVH + kh) * HD;
         k[i] = o1;
         k[i + half] = o2;
       }
       if (use_pool) {
-        bf16* k = pool_base + kv_elem_offset(pool, page, layer, kh, hd, in_page, false);
+        bf16* k = pool_base + kv_elem_offset(pool, page, layer, kh, HD, in_page, false);
         k[i] = o1;
         k[i + half] = o2;
       }
     }
   }
-  // values: plain copy
-  for (int idx = threadIdx.x; idx < KVH * hd; idx += blockDim.x) {
-    const int kh = idx / hd, j = idx % hd;
-    const bf16 v = in[(H + KVH) * hd + idx];
-    if (v_out) v_out[(static_cast<size_t>(m) * KVH + kh) * hd + j] = v;
-    if (use_pool) pool_base[kv_elem_offset(pool, page, layer, kh, hd, in_page, true) + j] = v;
+  // values: plain copy, 4 bytes per thread
+  const uint32_t* vin = reinterpret_cast<const uint32_t*>(in + (H + KVH) * HD);
+  for (int idx = threadIdx.x; idx < KVH * half; idx += blockDim.x) {
+    const int kh = idx / half, j = (idx % half) * 2;
+    const uint32_t v = vin[idx];
+    if (v_out) *reinterpret_cast<uint32_t*>(v_out + (static_cast<size_t>(m) * KVH + kh) * HD + j) = v;
+    if (use_pool)
+      *reinterpret_cast<uint32_t*>(pool_base + kv_elem_offset(pool, page, layer, kh, HD, in_page, true) + j) = v;
   }
 }
 
@@ -263,9 +290,9 @@ void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, con
               const int* gather, int M_out, const bf16* value_w, float* value, cudaStream_t st) {
   const int rows = gather ? M_out : M;
   if (rows <= 0) return;
-  const int threads = d >= 2048 ? 256 : 128;
-  add_norm_kernel<<<rows, threads, d * sizeof(float), st>>>(x, parts, parts ? nsplit : 0, split_stride, gain, y, d,
-                                                             gather, value_w, value); fpk::count_launch();
+  add_norm_kernel<<<(rows + 3) / 4, 128, 4 * d * sizeof(float), st>>>(x, parts, parts ? nsplit : 0, split_stride, gain,
+                                                                      y, d, gather, rows, value_w, value);
+  fpk::count_launch();
 }
 
 void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, float rope_theta, bf16* q_out,
@@ -273,8 +300,15 @@ void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, fl
   if (M <= 0) return;
   KvPoolView pv{};
   if (pool) pv = *pool;
-  rope_qkv_kernel<<<M, 128, 0, st>>>(qkv, H, KVH, hd, pos, log2f(rope_theta), q_out, k_out, v_out, pv,
-                                     pool != nullptr ? 1 : 0, layer, slot); fpk::count_launch();
+  const float l2 = log2f(rope_theta);
+  const int up = pool != nullptr ? 1 : 0;
+  switch (hd) {
+    case 32: rope_qkv_kernel<32><<<M, 128, 0, st>>>(qkv, H, KVH, pos, l2, q_out, k_out, v_out, pv, up, layer, slot); break;
+    case 64: rope_qkv_kernel<64><<<M, 128, 0, st>>>(qkv, H, KVH, pos, l2, q_out, k_out, v_out, pv, up, layer, slot); break;
+    case 128: rope_qkv_kernel<128><<<M, 128, 0, st>>>(qkv, H, KVH, pos, l2, q_out, k_out, v_out, pv, up, layer, slot); break;
+    default: throw std::invalid_argument("rope_qkv: head_dim must be 32, 64 or 128");
+  }
+  fpk::count_launch();
 }
 
 }  // namespace fpk
