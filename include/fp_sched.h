@@ -153,6 +153,15 @@ int fp_sweep_threshold(const fp_gen_sample* batch, int32_t n, const fp_gen_confi
                        const double* ratios, int32_t n_ratios, fp_sweep_point* curve,
                        int32_t* n_curve, int32_t* best_index, double* serial_total);
 
+/* Extension (product library only; not in the reference API): the fused
+ * trigger as the GPU executor takes it — trigger time, the GenState handed to
+ * plan_migration (genfuse.cpp:492-495), the plan, and the samples
+ * apply_migration (genfuse.cpp:136-208) moves, in application order. Pass
+ * NULL arrays to query n_state / n_moves first. */
+int fp_fused_trigger(const fp_gen_sample* batch, int32_t n, const fp_gen_config* cfg, int32_t r_t,
+                     int32_t* triggered, fp_plan_info* plan, fp_remaining* state, int32_t* n_state,
+                     int32_t* move_sample, int32_t* move_from, int32_t* move_to, int32_t* n_moves);
+
 /* gae_recursive / gae_matrix (numerics.hpp:18-25). values has T+1 entries. */
 int fp_gae_recursive(const double* rewards, const double* values, int32_t T, double gamma,
                      double lam, double* adv_out);

@@ -206,18 +206,25 @@ def gumbel_noise(seed: int, sample_id: int, step: int, vocab: int) -> np.ndarray
 # ---------------------------------------------------------------------------
 # experience
 
+def gae(rewards, values, gamma, lam):
+    """gae_recursive of proj/src/numerics.cpp:11-34: values has T+1 entries."""
+    r, v = np.asarray(rewards, dtype=np.float64), np.asarray(values, dtype=np.float64)
+    if len(r) < 1 or len(v) != len(r) + 1 or not (0 <= gamma <= 1 and 0 <= lam <= 1):
+        raise ValueError("GaeInputs: need T >= 1 rewards, T+1 values, gamma and lam in [0, 1]")
+    adv = r + gamma * v[1:] - v[:-1]
+    c = gamma * lam
+    for t in range(len(r) - 2, -1, -1):
+        adv[t] += c * adv[t + 1]
+    return adv
+
+
 def postprocess(logp_actor, logp_ref, values, score, beta, gamma, lam):
-    """fp64 KL / reward / GAE / returns of one sample (numerics.cpp:27-34 recursion)."""
+    """fp64 KL / reward / GAE (explicit V_R = 0 bootstrap) / returns of one sample."""
     la, lr, v = (np.asarray(a, dtype=np.float64) for a in (logp_actor, logp_ref, values))
-    R = len(la)
     kl = la - lr
     rew = -beta * kl
     rew[-1] += score
-    v_next = np.append(v[1:], 0.0)
-    adv = rew + gamma * v_next - v
-    c = gamma * lam
-    for t in range(R - 2, -1, -1):
-        adv[t] += c * adv[t + 1]
+    adv = gae(rew, np.append(v, 0.0), gamma, lam)
     return {"kl": kl, "reward": rew, "adv": adv, "ret": adv + v}
 
 

@@ -151,6 +151,8 @@ SCHED_SYMBOLS = {
 }
 
 ENGINE_SYMBOLS = {
+    "fp_fused_trigger": (C.c_int, [P(GenSample), C.c_int32, P(GenConfig), C.c_int32, _i32p, P(PlanInfo),
+                                   P(Remaining), _i32p, _i32p, _i32p, _i32p, _i32p]),
     "fp_engine_create": (C.c_int, [P(EngineSetup), P(_vp)]),
     "fp_engine_destroy": (None, [_vp]),
     "fp_engine_model_size": (C.c_int, [_vp, C.c_int32, _i64p, _i64p]),

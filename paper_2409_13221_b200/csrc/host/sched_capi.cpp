@@ -300,6 +300,30 @@ int fp_sweep_threshold(const fp_gen_sample* batch, int32_t n, const fp_gen_confi
   });
 }
 
+#ifdef FUSEPLAN_B200_EXTENSIONS
+int fp_fused_trigger(const fp_gen_sample* batch, int32_t n, const fp_gen_config* cfg, int32_t r_t,
+                     int32_t* triggered, fp_plan_info* plan, fp_remaining* state, int32_t* n_state,
+                     int32_t* move_sample, int32_t* move_from, int32_t* move_to, int32_t* n_moves) {
+  return guarded([&] {
+    const fuseplan::TriggerSnapshot t = fuseplan::fused_trigger(to_batch(batch, n), to_config(cfg), r_t);
+    if (triggered) *triggered = t.triggered ? 1 : 0;
+    if (plan) fill_plan(t.plan, plan);
+    if (n_state) *n_state = static_cast<int32_t>(t.state.samples.size());
+    if (state)
+      for (std::size_t i = 0; i < t.state.samples.size(); ++i) {
+        const auto& r = t.state.samples[i];
+        state[i] = {r.id, r.instance, r.kv_bytes, r.generated, r.prompt_len, r.admitted ? 1 : 0};
+      }
+    if (n_moves) *n_moves = static_cast<int32_t>(t.move_sample.size());
+    for (std::size_t i = 0; i < t.move_sample.size(); ++i) {
+      if (move_sample) move_sample[i] = t.move_sample[i];
+      if (move_from) move_from[i] = t.move_from[i];
+      if (move_to) move_to[i] = t.move_to[i];
+    }
+  });
+}
+#endif
+
 static int gae_common(bool matrix, const double* rewards, const double* values, int32_t T, double gamma,
                       double lam, double* adv_out) {
   return guarded([&] {

@@ -256,6 +256,24 @@ class Sched:
                                                     C.byref(serial)))
         return SweepResult([(p.ratio, p.r_t, p.fused_total) for p in curve[:nc.value]], best.value, serial.value)
 
+    def fused_trigger(self, batch: list, cfg: GenSimConfig, r_t: int) -> dict:
+        """Product-library extension: trigger state, plan and moves the GPU executor takes."""
+        keep: list = []
+        b, c = batch_to_c(batch, keep), C.byref(cfg.c(keep))
+        trig, ns, nm = C.c_int32(), C.c_int32(), C.c_int32()
+        info = _lib.PlanInfo()
+        check(self.lib, self.lib.fp_fused_trigger(b, len(batch), c, r_t, C.byref(trig), C.byref(info), None,
+                                                  C.byref(ns), None, None, None, C.byref(nm)))
+        st = (_lib.Remaining * max(ns.value, 1))()
+        ms, mf, mt = ((C.c_int32 * max(nm.value, 1))() for _ in range(3))
+        check(self.lib, self.lib.fp_fused_trigger(b, len(batch), c, r_t, C.byref(trig), C.byref(info), st,
+                                                  C.byref(ns), ms, mf, mt, C.byref(nm)))
+        return {"triggered": bool(trig.value), "time": info.trigger_time,
+                "state": [Remaining(r.id, r.instance, r.kv_bytes, r.generated, r.prompt_len, bool(r.admitted))
+                          for r in st[:ns.value]],
+                "plan": _plan_from(info, [], []),
+                "moves": list(zip(ms[:nm.value], mf[:nm.value], mt[:nm.value]))}
+
     # --- numerics --------------------------------------------------------------------------
     def _gae(self, fn, rewards, values, gamma, lam) -> np.ndarray:
         r = np.ascontiguousarray(rewards, dtype=np.float64)
