@@ -115,10 +115,12 @@ int fp_k_vocab(const void* X, int32_t M, int32_t K, const void* W, int32_t V, in
                float* logp, void* stream);
 int fp_k_add_norm(float* x, const float* parts, int32_t nsplit, const float* gain, void* y, int32_t M, int32_t d,
                   void* stream);
-/* Paged decode attention. pool: [pages][L][KVH][2][64][hd] bf16; block_table [slots][bt_stride]. */
+/* Paged decode attention. pool: [num_pages][L][KVH][2][64][hd] bf16; block_table [slots][bt_stride].
+ * num_pages > 0 selects the tensor-core TMA kernel (hd 64 / 128); 0 the CUDA-core kernel. */
 int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t hd, const void* pool,
-                     int32_t num_layers, int32_t layer, const int32_t* block_table, int32_t bt_stride,
-                     const int32_t* slot, const int32_t* ctx, int32_t max_ctx, void* out, void* stream);
+                     int32_t num_pages, int32_t num_layers, int32_t layer, const int32_t* block_table,
+                     int32_t bt_stride, const int32_t* slot, const int32_t* ctx, int32_t max_ctx, void* out,
+                     void* stream);
 /* Varlen causal attention; cu_host: n_seq+1 offsets (host), cu_dev the same on device. */
 int fp_k_attn_varlen(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
                      const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream);

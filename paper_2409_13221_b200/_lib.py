@@ -174,8 +174,8 @@ ENGINE_SYMBOLS = {
     "fp_k_vocab": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int32, C.c_float, _vp, _vp, _vp,
                              C.c_uint64, _vp, _vp, _vp]),
     "fp_k_add_norm": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, C.c_int32, C.c_int32, _vp]),
-    "fp_k_attn_decode": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int32, _vp,
-                                   C.c_int32, _vp, _vp, C.c_int32, _vp, _vp]),
+    "fp_k_attn_decode": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int32,
+                                   C.c_int32, _vp, C.c_int32, _vp, _vp, C.c_int32, _vp, _vp]),
     "fp_k_attn_varlen": (C.c_int, [_vp, _vp, _vp, C.c_int32, C.c_int32, C.c_int32, _i32p, _vp, C.c_int32, _vp,
                                    _vp]),
     "fp_k_postprocess": (C.c_int, [C.c_int32, _vp, _vp, _vp, _vp, _vp, C.c_float, C.c_float, C.c_float, _vp, _vp,

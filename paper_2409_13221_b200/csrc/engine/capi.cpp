@@ -366,12 +366,18 @@ int fp_k_add_norm(float* x, const float* parts, int32_t nsplit, const float* gai
 }
 
 int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t hd, const void* pool,
-                     int32_t num_layers, int32_t layer, const int32_t* block_table, int32_t bt_stride,
-                     const int32_t* slot, const int32_t* ctx, int32_t max_ctx, void* out, void* stream) {
+                     int32_t num_pages, int32_t num_layers, int32_t layer, const int32_t* block_table,
+                     int32_t bt_stride, const int32_t* slot, const int32_t* ctx, int32_t max_ctx, void* out,
+                     void* stream) {
   return guarded([&] {
     const size_t layer_bytes = static_cast<size_t>(KVH) * 2 * 64 * hd * 2;
     fpk::KvPoolView pv{static_cast<uint8_t*>(const_cast<void*>(pool)), layer_bytes * num_layers, layer_bytes, 64,
                        block_table, bt_stride};
+    CUtensorMap map;
+    if (num_pages > 0 && (hd == 64 || hd == 128)) {
+      map = fpk::make_kv_map(pool, static_cast<long long>(num_pages) * (layer_bytes * num_layers / (hd * 2)), hd);
+      pv.kv_map = &map;
+    }
     float* work = nullptr;
     const size_t wb = fpk::attn_decode_workspace(B, H, hd, max_ctx) * 4 + 256;
     fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&work), wb, S(stream)), "alloc");

@@ -95,6 +95,11 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
   num_pages_ = static_cast<int>(pool_bytes / page_bytes_) + 1;  // +1: scratch page for padded rows
   pool_ = static_cast<uint8_t*>(dalloc(static_cast<size_t>(num_pages_) * page_bytes_));
   for (int p = num_pages_ - 1; p >= 1; --p) free_pages_.push_back(p);  // page 0 is the scratch page
+  if (a.hd == 64 || a.hd == 128) {  // 2-D TMA view of the pool for tensor-core decode attention
+    const long long rows = static_cast<long long>(num_pages_) * static_cast<long long>(page_bytes_ / (a.hd * 2));
+    kv_map_ = fpk::make_kv_map(pool_, rows, a.hd);
+    has_kv_map_ = true;
+  }
   for (int s = cfg_.max_live - 1; s >= 0; --s) free_slots_.push_back(s);
   slot_pages_.assign(cfg_.max_live, {});
   bt_host_.assign(static_cast<size_t>(cfg_.max_live) * max_pages_per_sample_, 0);
@@ -357,7 +362,7 @@ void Engine::forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, int
                             cudaStream_t st) {
   (void)n_seq;
   const Dims& D = w.dims;
-  fpk::KvPoolView pv{pool_, page_bytes_, layer_bytes_, kPageTokens, d_block_table_, max_pages_per_sample_};
+  const fpk::KvPoolView pv = pool_view();
   fpk::embed(ws.tokens, nullptr, M, w.embed, D.d, ws.x, st);
   for (int l = 0; l < D.L; ++l) {
     const LayerW& L = w.layers[l];
@@ -456,7 +461,7 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
   const int* target = dec_.rows + 4 * B;
   const int* sid = dec_.rows + 5 * B;
   const int* step = dec_.rows + 6 * B;
-  fpk::KvPoolView pv{pool_, page_bytes_, layer_bytes_, kPageTokens, d_block_table_, max_pages_per_sample_};
+  const fpk::KvPoolView pv = pool_view();
   const size_t stride = static_cast<size_t>(B) * D.d;
   const int so = fpk::gemm_splits(D.d, D.H * D.hd);
   const int sd = fpk::gemm_splits(D.d, D.F);

@@ -178,6 +178,13 @@ class Engine {
   };
   bool probe_on_ = false;
   uint64_t prompts_tag_ = 0;
+  CUtensorMap kv_map_{};
+  bool has_kv_map_ = false;
+  fpk::KvPoolView pool_view() const {
+    fpk::KvPoolView pv{pool_, page_bytes_, layer_bytes_, kPageTokens, d_block_table_, max_pages_per_sample_};
+    pv.kv_map = has_kv_map_ ? &kv_map_ : nullptr;
+    return pv;
+  }
   std::vector<ProbeRec> probes_;
   std::vector<cudaEvent_t> probe_pool_;
   cudaEvent_t probe_event();

@@ -25,7 +25,7 @@ namespace fpk {
 namespace {
 
 constexpr int kPT = 64;          // tokens per KV page
-constexpr int kChunk = 256;      // tokens per decode split
+constexpr int kChunk = kDecodeChunk;  // tokens per decode split
 constexpr int kStages = 3;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -460,7 +460,8 @@ void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView&
   const int G = H / KVH;
 #define FP_DEC(HD_, G_) \
   if (hd == HD_ && G == G_) { launch_decode<HD_, G_>(q, B, H, KVH, pool, layer, slot, ctx, ns, work, st); } else
-  FP_DEC(32, 1) FP_DEC(64, 1) FP_DEC(128, 1) FP_DEC(64, 4) FP_DEC(128, 4) FP_DEC(128, 8) FP_DEC(64, 8) {
+  if (attn_decode_mma(q, B, H, KVH, hd, pool, layer, slot, ctx, ns, work, st)) {
+  } else FP_DEC(32, 1) FP_DEC(64, 1) FP_DEC(128, 1) FP_DEC(64, 4) FP_DEC(128, 4) FP_DEC(128, 8) FP_DEC(64, 8) {
     throw std::invalid_argument("attn_decode: unsupported (head_dim, group) combination");
   }
 #undef FP_DEC

@@ -1,0 +1,316 @@
+// fuseplan-b200 — paged decode attention on tensor cores (head_dim 64 / 128).
+//
+// One CTA per (kv head, sample, 512-token context split): 1 producer warp +
+// 4 consumer warps. The producer streams every 64-token page's K and V tiles
+// of (layer, kv head) with 2-D TMA (128-byte swizzle, 64 x 128 B boxes) into
+// an S-stage shared-memory ring signalled on mbarriers. Consumer warp w takes
+// pages w, w+4, ...: S = Q K^T and O += P V with mma.sync m16n8k16 (bf16 in,
+// fp32 accumulate), the G query heads of the GQA group as the MMA rows (K/V
+// read once per group), online softmax in registers; ldmatrix addresses apply
+// the TMA swizzle (16-byte chunk c of row r lives at chunk c ^ (r & 7)), so
+// fragment loads are bank-conflict free. Warps merge through shared memory;
+// splits merge in attn_decode_combine_kernel. Split boundaries depend on the
+// position only (batch-independent results). HBM-bound: every K/V byte of the
+// visible context is read exactly once per launch.
+#include <math.h>
+
+#include <algorithm>
+
+#include "ops.h"
+#include "ptx.cuh"
+
+namespace fpk {
+
+namespace {
+
+constexpr int kPT = 64;
+constexpr int kTileBytes = 32 * 128;  // one 32-row x 64-column bf16 box (a TMA box)
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm4t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// Swizzled address of 16-byte chunk `c16` (along the head dim) of row r.
+template <int HD>
+__device__ __forceinline__ uint32_t swz(uint32_t tile_base, int r, int c16) {
+  const int sub = c16 >> 3, cc = c16 & 7;
+  return tile_base + sub * kTileBytes + r * 128 + ((cc ^ (r & 7)) << 4);
+}
+
+// Persistent warp-per-item design. A work item is (sample, kv head, 512-token
+// split); warp gw of the grid takes items gw, gw + T, ... (T = total warps) and
+// streams their 32-token K|V units through kStages private shared-memory
+// stages: lane 0 issues the 2-D TMA loads (box 64 x 32 rows, 128 B swizzle)
+// for the unit kStages ahead — across item boundaries, so the pipeline never
+// drains — and the warp computes S = Q K^T and O += P V with mma.sync on the
+// resident unit. Stages are private to the warp, so no cross-warp barrier or
+// merge exists; every item writes its (unnormalised O, m, l) split partial.
+template <int HD>
+struct DecCfg {
+  static constexpr int kSub = HD / 64;                  // 64-column boxes per K (or V) unit
+  static constexpr int kBox = 32 * 128;                 // 32 rows x 128 B
+  static constexpr int kStageBytes = 2 * kSub * kBox;   // K + V of one 32-token unit
+  static constexpr int kWarps = HD == 64 ? 8 : 6;
+  static constexpr int kStages = HD == 64 ? 3 : 2;
+  static constexpr int kSmem = kWarps * kStages * kStageBytes + 1024;
+};
+
+struct Cursor {
+  int j;      // item index (grid-strided)
+  int u, ue;  // current / end unit (32-token) index of the item
+};
+
+template <int HD, int G>
+__global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_kernel(
+    const __grid_constant__ CUtensorMap kv_map, const bf16* __restrict__ q, const int* __restrict__ block_table,
+    int bt_stride, int rows_per_page, int layer_rows, int layer, const int* __restrict__ slot,
+    const int* __restrict__ ctx, int B, int H, int KVH, int nsplit_max, float scale_log2,
+    float* __restrict__ part_o, float* __restrict__ part_ml) {
+  using C = DecCfg<HD>;
+  static_assert(G <= 8, "GQA group must fit the first 8 MMA rows");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[C::kWarps][C::kStages];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T = gridDim.x * C::kWarps;
+  const int n_items = nsplit_max * B * KVH;
+  uint64_t* bar = full_bar[warp];
+  uint8_t* my_smem = smem + warp * C::kStages * C::kStageBytes;
+  if (lane == 0) {
+    if (warp == 0) tma_prefetch_desc(&kv_map);
+    for (int s = 0; s < C::kStages; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+
+  // item j -> (split, b, kvh); token range [t0, t1)
+  auto item_range = [&](int j, int& b, int& kvh, int& split, int& t0, int& t1) {
+    kvh = j % KVH;
+    const int rest = j / KVH;
+    b = rest % B;
+    split = rest / B;
+    t0 = split * kDecodeChunk;
+    t1 = min(ctx[b], t0 + kDecodeChunk);
+  };
+  // advance a cursor to the next non-empty unit (u < ue), or j >= n_items
+  auto normalise = [&](Cursor& c) {
+    while (c.j < n_items && c.u >= c.ue) {
+      c.j += T;
+      if (c.j >= n_items) break;
+      int b, kvh, split, t0, t1;
+      item_range(c.j, b, kvh, split, t0, t1);
+      if (t0 < t1) {
+        c.u = t0 >> 5;
+        c.ue = ((t1 - 1) >> 5) + 1;
+      }
+    }
+  };
+  auto issue = [&](const Cursor& c, int k) {  // lane 0 only
+    int b, kvh, split, t0, t1;
+    item_range(c.j, b, kvh, split, t0, t1);
+    const int page = c.u >> 1, half = c.u & 1;
+    const int pid = block_table[slot[b] * bt_stride + page];
+    const int rk = pid * rows_per_page + layer * layer_rows + kvh * 2 * kPT + half * 32;
+    uint8_t* dst = my_smem + k * C::kStageBytes;
+    mbar_arrive_expect_tx(&bar[k], C::kStageBytes);
+#pragma unroll
+    for (int sub = 0; sub < C::kSub; ++sub) {
+      tma_load_2d(dst + sub * C::kBox, &kv_map, &bar[k], sub * 64, rk);
+      tma_load_2d(dst + (C::kSub + sub) * C::kBox, &kv_map, &bar[k], sub * 64, rk + kPT);
+    }
+  };
+
+  Cursor in{warp + blockIdx.x * C::kWarps - T, 0, 0};  // issue cursor
+  normalise(in);
+  Cursor cur = in;                                      // consume cursor
+  // prologue: fill the stages
+  int issued = 0;
+  for (; issued < C::kStages && in.j < n_items; ++issued) {
+    if (lane == 0) issue(in, issued);
+    ++in.u;
+    normalise(in);
+  }
+
+  const int r0 = lane >> 2;
+  const uint32_t base = smem_u32(my_smem);
+  uint32_t qa[HD / 16][4];
+  float o[HD / 8][4];
+  float m_run = -INFINITY, l_run = 0.f;
+  int cur_j = -1, b = 0, kvh = 0, split = 0, t0 = 0, t1 = 0;
+
+  for (int c = 0; cur.j < n_items; ++c) {
+    if (cur.j != cur_j) {  // new item: load Q fragments, reset the running state
+      cur_j = cur.j;
+      item_range(cur_j, b, kvh, split, t0, t1);
+      const bf16* qg = q + (static_cast<size_t>(b) * H + kvh * G) * HD;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        const int col = kk * 16 + 2 * (lane & 3);
+        const bool ok = r0 < G;
+        qa[kk][0] = ok ? *reinterpret_cast<const uint32_t*>(qg + r0 * HD + col) : 0u;
+        qa[kk][1] = 0u;
+        qa[kk][2] = ok ? *reinterpret_cast<const uint32_t*>(qg + r0 * HD + col + 8) : 0u;
+        qa[kk][3] = 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+      m_run = -INFINITY;
+      l_run = 0.f;
+    }
+    const int k = c % C::kStages;
+    mbar_wait(&bar[k], (c / C::kStages) & 1);
+    const uint32_t Kt = base + k * C::kStageBytes;
+    const uint32_t Vt = Kt + C::kSub * C::kBox;
+    const int ut0 = cur.u * 32;
+    const int lo = max(t0, ut0) - ut0, hi = min(t1, ut0 + 32) - ut0;
+
+    // S = Q K^T over 32 tokens (4 n-tiles of 8)
+    float sc[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+    const int mi = lane >> 3;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+#pragma unroll
+      for (int nt = 0; nt < 4; nt += 2) {
+        const int r = (nt + (mi >> 1)) * 8 + (lane & 7);
+        uint32_t b0, b1, b2, b3;
+        ldsm4(swz<HD>(Kt, r, kk * 2 + (mi & 1)), b0, b1, b2, b3);
+        mma16816(sc[nt], qa[kk], b0, b1);
+        mma16816(sc[nt + 1], qa[kk], b2, b3);
+      }
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int tok = nt * 8 + 2 * (lane & 3) + e;
+        const float v = (tok >= lo && tok < hi) ? sc[nt][e] * scale_log2 : -INFINITY;
+        sc[nt][e] = v;
+        mx = fmaxf(mx, v);
+      }
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float nm = fmaxf(m_run, mx);
+    const float corr = (m_run == -INFINITY) ? 0.f : exp2f(m_run - nm);
+    m_run = nm;
+    float rs = 0.f;
+    uint32_t pa[2][4];
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      const float p0 = (sc[nt][0] == -INFINITY) ? 0.f : exp2f(sc[nt][0] - nm);
+      const float p1 = (sc[nt][1] == -INFINITY) ? 0.f : exp2f(sc[nt][1] - nm);
+      rs += p0 + p1;
+      const int kk2 = nt >> 1;
+      if ((nt & 1) == 0) {
+        pa[kk2][0] = pack_bf16x2(p0, p1);
+        pa[kk2][1] = 0u;
+      } else {
+        pa[kk2][2] = pack_bf16x2(p0, p1);
+        pa[kk2][3] = 0u;
+      }
+    }
+    rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+    rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+    l_run = l_run * corr + rs;
+#pragma unroll
+    for (int dn = 0; dn < HD / 8; ++dn) {
+      o[dn][0] *= corr;
+      o[dn][1] *= corr;
+    }
+#pragma unroll
+    for (int kk2 = 0; kk2 < 2; ++kk2) {
+#pragma unroll
+      for (int dn = 0; dn < HD / 8; dn += 2) {
+        const int r = kk2 * 16 + (mi & 1) * 8 + (lane & 7);
+        uint32_t b0, b1, b2, b3;
+        ldsm4t(swz<HD>(Vt, r, dn + (mi >> 1)), b0, b1, b2, b3);
+        mma16816(o[dn], pa[kk2], b0, b1);
+        mma16816(o[dn + 1], pa[kk2], b2, b3);
+      }
+    }
+    // refill this stage with the unit kStages ahead
+    __syncwarp();
+    if (in.j < n_items) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(in, k);
+      }
+      ++in.u;
+      normalise(in);
+    }
+    // advance the consume cursor; flush the item's partial when it ends
+    ++cur.u;
+    if (cur.u >= cur.ue) {
+      if (r0 < G) {
+        const size_t pb = (static_cast<size_t>(b) * H + kvh * G + r0) * nsplit_max + split;
+        float* po = part_o + pb * HD + 2 * (lane & 3);
+#pragma unroll
+        for (int dn = 0; dn < HD / 8; ++dn) *reinterpret_cast<float2*>(po + dn * 8) = make_float2(o[dn][0], o[dn][1]);
+        if ((lane & 3) == 0) {
+          part_ml[pb * 2] = m_run;
+          part_ml[pb * 2 + 1] = l_run;
+        }
+      }
+      normalise(cur);
+    }
+  }
+}
+
+template <int HD, int G>
+void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
+            const int* slot, const int* ctx, int nsplit, float* work, cudaStream_t st) {
+  using C = DecCfg<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_decode_mma_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr = true;
+  }
+  float* part_o = work;
+  float* part_ml = work + static_cast<size_t>(B) * H * nsplit * HD;
+  const int layer_rows = KVH * 2 * kPT;
+  const int rows_per_page = static_cast<int>(pool.page_bytes / (static_cast<size_t>(HD) * 2));
+  const float scale = kLog2e / sqrtf(static_cast<float>(HD));
+  const int items = nsplit * B * KVH;
+  const int grid = std::max(1, std::min(148, (items + C::kWarps - 1) / C::kWarps));
+  attn_decode_mma_kernel<HD, G><<<grid, C::kWarps * 32, C::kSmem, st>>>(
+      map, q, pool.block_table, pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, B, H, KVH, nsplit,
+      scale, part_o, part_ml);
+  count_launch();
+}
+
+}  // namespace
+
+bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer,
+                     const int* slot, const int* ctx, int nsplit, float* work, cudaStream_t st) {
+  if (!pool.kv_map) return false;
+  const int G = H / KVH;
+#define FP_MMA(HD_, G_)                                                                            \
+  if (hd == HD_ && G == G_) {                                                                      \
+    launch<HD_, G_>(*pool.kv_map, q, B, H, KVH, pool, layer, slot, ctx, nsplit, work, st);        \
+    return true;                                                                                   \
+  }
+  FP_MMA(64, 1) FP_MMA(128, 1) FP_MMA(64, 4) FP_MMA(128, 4) FP_MMA(128, 8) FP_MMA(64, 8)
+#undef FP_MMA
+  return false;
+}
+
+}  // namespace fpk

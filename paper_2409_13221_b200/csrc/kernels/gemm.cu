@@ -99,6 +99,19 @@ void dispatch_bn(int M, F&& f) {
 
 }  // namespace
 
+CUtensorMap make_kv_map(const void* pool, long long rows, int hd) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(hd), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(hd) * 2};
+  const cuuint32_t box[2] = {64u, 32u};  // 32-token units
+  const cuuint32_t estr[2] = {1u, 1u};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box,
+                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (kv) failed: " + std::to_string(int(r)));
+  return m;
+}
+
 int gemm_splits(int N, int K) {
   const int kb = K / kBK;
   const int tiles = (N + 127) / 128;

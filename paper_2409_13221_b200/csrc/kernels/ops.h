@@ -2,6 +2,7 @@
 // Every function enqueues on `st` and never synchronises.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stddef.h>
@@ -79,7 +80,16 @@ struct KvPoolView {
   int page_tokens;        // tokens per page
   const int* block_table; // [slots][max_pages]
   int bt_stride;          // max_pages
+  const CUtensorMap* kv_map = nullptr;  // host copy: 2-D TMA view of the pool (make_kv_map), hd 64/128
 };
+// 2-D TMA map over the pool viewed as [rows, hd] bf16 rows (one row = one
+// token's K or V of one (page, layer, kv head)); box {64, 32}, 128 B swizzle.
+CUtensorMap make_kv_map(const void* pool, long long rows, int hd);
+// Tokens per decode-attention split (position-determined).
+constexpr int kDecodeChunk = 512;
+// Tensor-core decode attention (attn_decode.cu); false if (hd, group) unsupported or no map.
+bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer,
+                     const int* slot, const int* ctx, int nsplit, float* work, cudaStream_t st);
 void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, float rope_theta, bf16* q_out,
               bf16* k_out, bf16* v_out, const KvPoolView* pool, int layer, const int* slot, cudaStream_t st);
 

@@ -145,9 +145,10 @@ def test_add_norm(lib):
     assert (y.float() - ref).abs().max().item() < 2e-2 * ref.abs().max().item()
 
 
-@pytest.mark.parametrize("hd,H,KVH", [(64, 12, 12), (128, 32, 8), (32, 8, 8)])
-@pytest.mark.parametrize("ctx_list", [[1, 63, 64, 65, 300], [1000, 7, 257]])
-def test_attn_decode(lib, hd, H, KVH, ctx_list):
+@pytest.mark.parametrize("hd,H,KVH", [(64, 12, 12), (128, 32, 8), (32, 8, 8), (128, 16, 16), (64, 32, 4)])
+@pytest.mark.parametrize("ctx_list", [[1, 63, 64, 65, 300], [1000, 7, 257], [2000, 513, 512, 511]])
+@pytest.mark.parametrize("tma", [True, False])
+def test_attn_decode(lib, hd, H, KVH, ctx_list, tma):
     L, layer, PT = 3, 1, 64
     B = len(ctx_list)
     maxp = (max(ctx_list) + PT - 1) // PT
@@ -160,8 +161,8 @@ def test_attn_decode(lib, hd, H, KVH, ctx_list):
     ctx = torch.tensor(ctx_list, device="cuda", dtype=torch.int32)
     q = (torch.randn(B, H, hd, device="cuda")).to(torch.bfloat16)
     out = torch.zeros(B, H, hd, device="cuda", dtype=torch.bfloat16)
-    ok(lib, lib.fp_k_attn_decode(ptr(q), B, H, KVH, hd, ptr(pool), L, layer, ptr(bt_by_slot), maxp, ptr(slot),
-                                 ptr(ctx), max(ctx_list), ptr(out), stream()))
+    ok(lib, lib.fp_k_attn_decode(ptr(q), B, H, KVH, hd, ptr(pool), npages if tma else 0, L, layer, ptr(bt_by_slot),
+                                 maxp, ptr(slot), ptr(ctx), max(ctx_list), ptr(out), stream()))
     torch.cuda.synchronize()
     g = H // KVH
     for b in range(B):
