@@ -108,6 +108,8 @@ int fp_k_gemm_bf16(const void* W, int32_t N, int32_t K, const void* X, int32_t M
 int fp_k_gemm_f32(const void* W, int32_t N, int32_t K, const void* X, int32_t M, float* out, int32_t splits,
                   void* stream); /* splits <= 0: fp_k_gemm_splits(N, K) */
 int fp_k_gemm_splits(int32_t N, int32_t K);
+/* Debug: record 8 globaltimer stamps per CTA of subsequent GEMMs into buf (device, NULL disables). */
+int fp_k_gemm_trace(void* buf);
 int fp_k_gemm_swiglu(const void* Wgu, int32_t F, int32_t K, const void* X, int32_t M, void* out, void* stream);
 /* LM head + token choice: token[M], logp[M]. mode: FP_TOKENS_*; target/sample_id/step: [M] (device). */
 int fp_k_vocab(const void* X, int32_t M, int32_t K, const void* W, int32_t V, int32_t mode, float inv_temp,

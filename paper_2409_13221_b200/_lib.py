@@ -170,6 +170,7 @@ ENGINE_SYMBOLS = {
     "fp_k_gemm_bf16": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, C.c_int32, _vp]),
     "fp_k_gemm_f32": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, C.c_int32, _vp]),
     "fp_k_gemm_splits": (C.c_int, [C.c_int32, C.c_int32]),
+    "fp_k_gemm_trace": (C.c_int, [_vp]),
     "fp_k_gemm_swiglu": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, _vp]),
     "fp_k_vocab": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int32, C.c_float, _vp, _vp, _vp,
                              C.c_uint64, _vp, _vp, _vp]),

@@ -417,3 +417,8 @@ int fp_k_postprocess(int32_t n, const int32_t* off, const float* logp_actor, con
 }
 
 }  // extern "C"
+
+extern "C" int fp_k_gemm_trace(void* buf) {
+  fpk::set_gemm_trace(static_cast<unsigned long long*>(buf));
+  return FP_OK;
+}

@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(const bf16* __restrict
                                                           const int* __restrict__ slot, const int* __restrict__ ctx,
                                                           int H, int nsplit_max, float scale_log2,
                                                           float* __restrict__ part_o, float* __restrict__ part_ml) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   constexpr int EPL = HD / 32;  // output dims per lane
   constexpr int WH = HD / 4;    // bf16x2 words per half row
   constexpr int kPageElems = 2 * kPT * HD;
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(160) attn_decode_kernel(const bf16* __restrict
 __global__ void attn_decode_combine_kernel(const float* __restrict__ part_o, const float* __restrict__ part_ml,
                                            const int* __restrict__ ctx, int H, int HD, int nsplit_max,
                                            bf16* __restrict__ out) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   const int bh = blockIdx.x;
   const int b = bh / H;
   const int ns = (ctx[b] + kChunk - 1) / kChunk;
@@ -280,6 +282,7 @@ __global__ void __launch_bounds__(128) attn_varlen_kernel(const bf16* __restrict
                                                           const bf16* __restrict__ v, int H, int KVH,
                                                           const int* __restrict__ cu, const int* __restrict__ tiles,
                                                           float scale_log2, bf16* __restrict__ out) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   using C = VarlenCfg<HD>;
   constexpr int LD = C::kLd;
   extern __shared__ __align__(128) uint8_t smem[];

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
     int bt_stride, int rows_per_page, int layer_rows, int layer, const int* __restrict__ slot,
     const int* __restrict__ ctx, int B, int H, int KVH, int nsplit_max, float scale_log2,
     float* __restrict__ part_o, float* __restrict__ part_ml) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   using C = DecCfg<HD>;
   static_assert(G <= 8, "GQA group must fit the first 8 MMA rows");
   extern __shared__ uint8_t smem_raw[];

@@ -1,6 +1,7 @@
 // fuseplan-b200 — host launchers and instantiations of the tcgen05 GEMM.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <mutex>
 #include <stdexcept>
@@ -29,44 +30,73 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// Tensor-map cache keyed by every encode parameter (maps are pure functions
+// of pointer + geometry, so a hit is always valid).
 struct MapKey {
   const void* ptr;
-  int rows, k, box;
-  bool operator==(const MapKey& o) const { return ptr == o.ptr && rows == o.rows && k == o.k && box == o.box; }
+  int dtype, rank, swz;
+  uint64_t dims[3], strides[2];
+  uint32_t box[3];
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && dtype == o.dtype && rank == o.rank && swz == o.swz &&
+           std::equal(dims, dims + 3, o.dims) && std::equal(strides, strides + 2, o.strides) &&
+           std::equal(box, box + 3, o.box);
+  }
 };
 struct MapKeyHash {
   size_t operator()(const MapKey& k) const {
-    size_t h = reinterpret_cast<size_t>(k.ptr);
-    h ^= (static_cast<size_t>(k.rows) * 0x9E3779B97F4A7C15ull) ^ (static_cast<size_t>(k.k) << 20) ^ k.box;
+    size_t h = reinterpret_cast<size_t>(k.ptr) ^ (static_cast<size_t>(k.dtype) << 56) ^ k.swz;
+    for (int i = 0; i < 3; ++i) h = h * 0x9E3779B97F4A7C15ull ^ k.dims[i] ^ (static_cast<size_t>(k.box[i]) << 40);
+    for (int i = 0; i < 2; ++i) h = h * 0x9E3779B97F4A7C15ull ^ k.strides[i];
     return h;
   }
 };
 
-// bf16 [rows, k] row-major (K innermost), box {64, box_rows}, 128 B swizzle.
-CUtensorMap make_map(const void* ptr, int rows, int k, int box_rows) {
+CUtensorMap encode(const void* ptr, CUtensorMapDataType dtype, int rank, const uint64_t* dims,
+                   const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz) {
   static std::mutex mu;
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
-  const MapKey key{ptr, rows, k, box_rows};
+  MapKey key{ptr, static_cast<int>(dtype), rank, static_cast<int>(swz), {0, 0, 0}, {0, 0}, {0, 0, 0}};
+  for (int i = 0; i < rank; ++i) key.dims[i] = dims[i], key.box[i] = box[i];
+  for (int i = 0; i + 1 < rank; ++i) key.strides[i] = strides_bytes[i];
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  if (cache.size() > 4096) cache.clear();
+  if (cache.size() > 8192) cache.clear();
   CUtensorMap m;
-  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(k) * 2};
-  const cuuint32_t box[2] = {64u, static_cast<cuuint32_t>(box_rows)};
-  const cuuint32_t estr[2] = {1u, 1u};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
-                                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint64_t d[3], st[2];
+  cuuint32_t bx[3], es[3] = {1u, 1u, 1u};
+  for (int i = 0; i < rank; ++i) d[i] = dims[i], bx[i] = box[i];
+  for (int i = 0; i + 1 < rank; ++i) st[i] = strides_bytes[i];
+  const CUresult r = encode_fn()(&m, dtype, rank, const_cast<void*>(ptr), d, st, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                 swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
   cache.emplace(key, m);
   return m;
 }
 
+// bf16 [rows, k] row-major (K innermost), box {64, box_rows}, 128 B swizzle: GEMM operands.
+CUtensorMap make_map(const void* ptr, int rows, int k, int box_rows) {
+  const uint64_t dims[2] = {static_cast<uint64_t>(k), static_cast<uint64_t>(rows)};
+  const uint64_t str[1] = {static_cast<uint64_t>(k) * 2};
+  const uint32_t box[2] = {64u, static_cast<uint32_t>(box_rows)};
+  return encode(ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// Output tile maps (no swizzle): [rows][ld] with `cols` valid columns, box {box_cols, box_rows}.
+CUtensorMap out_map_2d(const void* ptr, CUtensorMapDataType dt, int esize, int rows, int cols, int ld, int box_cols,
+                       int box_rows) {
+  const uint64_t dims[2] = {static_cast<uint64_t>(cols), static_cast<uint64_t>(rows)};
+  const uint64_t str[1] = {static_cast<uint64_t>(ld) * esize};
+  const uint32_t box[2] = {static_cast<uint32_t>(box_cols), static_cast<uint32_t>(box_rows)};
+  return encode(ptr, dt, 2, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+unsigned long long* g_trace = nullptr;
+
 template <int BN, class Epi>
 void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int splits, const Epi& epi,
-            cudaStream_t st) {
+            cudaStream_t st, bool weight_is_a = true) {
   using C = GemmCfg<BN>;
   if (K % kBK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
   if (a_rows <= 0 || b_rows <= 0) return;
@@ -83,9 +113,24 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
   g.k_blocks = K / kBK;
   splits = std::max(1, std::min(splits, g.k_blocks));
   g.kb_per_split = (g.k_blocks + splits - 1) / splits;
+  g.weight_is_a = weight_is_a ? 1 : 0;
+  g.trace = g_trace;
   const int z = (g.k_blocks + g.kb_per_split - 1) / g.kb_per_split;
-  dim3 grid((a_rows + 127) / 128, (b_rows + BN - 1) / BN, z);
-  tc_gemm_kernel<BN, Epi><<<grid, kGemmThreads, C::kSmem, st>>>(ma, mb, g, epi); fpk::count_launch();
+  // Programmatic dependent launch: the prologue and the weight prefetch of this
+  // GEMM overlap the tail of the previous kernel (which triggers early).
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((a_rows + 127) / 128, (b_rows + BN - 1) / BN, z);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi>, ma, mb, g, epi);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("gemm launch: ") + cudaGetErrorString(e));
+  fpk::count_launch();
 }
 
 template <class Epi, class F>
@@ -112,6 +157,8 @@ CUtensorMap make_kv_map(const void* pool, long long rows, int hd) {
   return m;
 }
 
+void set_gemm_trace(unsigned long long* buf) { g_trace = buf; }
+
 int gemm_splits(int N, int K) {
   const int kb = K / kBK;
   const int tiles = (N + 127) / 128;
@@ -124,23 +171,40 @@ int gemm_splits(int N, int K) {
 }
 
 void gemm_bf16(const bf16* W, int N, int K, const bf16* X, int M, bf16* out, int ld_out, cudaStream_t st) {
-  EpiStoreBF16 e{out, ld_out, N, M};
-  dispatch_bn<EpiStoreBF16>(M, [&]<int BN>() { launch<BN>(W, N, X, M, K, 1, e, st); });
+  if ((ld_out * 2) % 16) throw std::invalid_argument("gemm_bf16: ld_out must be a multiple of 8");
+  dispatch_bn<EpiStoreBF16>(M, [&]<int BN>() {
+    EpiStoreBF16 e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, ld_out, 128, BN)};
+    launch<BN>(W, N, X, M, K, 1, e, st);
+  });
 }
 
 void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* out, int splits, cudaStream_t st) {
-  EpiStoreF32 e{out, static_cast<size_t>(M) * N, N, N, M, 0};
-  dispatch_bn<EpiStoreF32>(M, [&]<int BN>() { launch<BN>(W, N, X, M, K, splits, e, st); });
+  if (N % 4) throw std::invalid_argument("gemm_f32: N must be a multiple of 4");
+  const int kb = K / kBK;
+  splits = std::max(1, std::min(splits, kb));
+  const int per = (kb + splits - 1) / splits;
+  const int z = (kb + per - 1) / per;
+  dispatch_bn<EpiStoreF32>(M, [&]<int BN>() {
+    const uint64_t dims[3] = {static_cast<uint64_t>(N), static_cast<uint64_t>(M), static_cast<uint64_t>(z)};
+    const uint64_t str[2] = {static_cast<uint64_t>(N) * 4, static_cast<uint64_t>(M) * N * 4};
+    const uint32_t box[3] = {128u, static_cast<uint32_t>(BN), 1u};
+    EpiStoreF32 e{encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE), 0};
+    launch<BN>(W, N, X, M, K, splits, e, st);
+  });
 }
 
 void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float* resid, cudaStream_t st) {
-  EpiStoreF32 e{resid, 0, N, N, M, 1};
-  dispatch_bn<EpiStoreF32>(M, [&]<int BN>() { launch<BN>(W, N, X, M, K, 1, e, st); });
+  if (N % 4) throw std::invalid_argument("gemm_f32: N must be a multiple of 4");
+  dispatch_bn<EpiStoreF32>(M, [&]<int BN>() {
+    EpiStoreF32 e{out_map_2d(resid, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, N, N, 128, BN), 1};
+    launch<BN>(W, N, X, M, K, 1, e, st);
+  });
 }
 
 void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
+  if (F % 64) throw std::invalid_argument("gemm_swiglu: F must be a multiple of 64");
   dispatch_bn<int>(M, [&]<int BN>() {
-    EpiSwiGLU<BN> e{out, F, F, M};
+    EpiSwiGLU<BN> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, BN)};
     launch<BN>(Wgu, 2 * F, X, M, K, 1, e, st);
   });
 }
@@ -162,7 +226,7 @@ void gemm_vocab(const bf16* X, int M, int K, const bf16* Whead, int V, int mode,
   e.n_tiles = vocab_tiles(V);
   e.seed_lo = static_cast<uint32_t>(seed);
   e.seed_hi = static_cast<uint32_t>(seed >> 32);
-  launch<kVocabBN>(X, M, Whead, V, K, 1, e, st);
+  launch<kVocabBN>(X, M, Whead, V, K, 1, e, st, /*weight_is_a=*/false);
 }
 
 // One warp per row: merge the vocab tiles in order.
@@ -170,6 +234,7 @@ __global__ void vocab_finalize_kernel(const VocabPartial* __restrict__ part, con
                                       int n_tiles, int mode, const int* __restrict__ target, int* token, float* logp,
                                       const int* dst, int* out_tok, float* out_logp, const int* cur_idx,
                                       int* cur_tok) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;

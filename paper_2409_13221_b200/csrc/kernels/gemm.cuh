@@ -22,12 +22,14 @@ namespace fpk {
 constexpr int kBK = 64;                  // K elements per stage (128 B)
 constexpr int kTileA = 128 * kBK * 2;    // bytes of one A stage
 constexpr int kGemmThreads = 192;
+constexpr int kSmemBudget = 200 * 1024;
 
 template <int BN>
 struct GemmCfg {
   static constexpr int kTileB = BN * kBK * 2;
   static constexpr int kStageBytes = kTileA + kTileB;
-  static constexpr int kStages = BN >= 256 ? 4 : (BN >= 128 ? 5 : 4);
+  static constexpr int kFit = kSmemBudget / kStageBytes;
+  static constexpr int kStages = kFit > 8 ? 8 : kFit;  // deep ring: the decode mainloop is latency-bound
   static constexpr int kSmem = kStages * kStageBytes + 1024;  // + alignment slack
   static constexpr uint32_t kTmemCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
 };
@@ -37,20 +39,56 @@ struct GemmGeom {
   int b_rows;        // valid rows of B
   int k_blocks;      // total 64-wide K blocks
   int kb_per_split;  // K blocks per gridDim.z slice
+  int weight_is_a;   // 1: A is a weight (may be prefetched before griddepcontrol.wait)
+  unsigned long long* trace;  // optional per-CTA phase stamps (globaltimer ns), 8 per CTA
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_commit_wait() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
 
 // Epilogue protocol (per epilogue thread; `State` lives in registers):
 //   struct State {...};
-//   __device__ void operator()(State&, int a_row0, int b_row0, int split, int r,
-//                              int c0, const float (&v)[32], float* scratch) const;
-//     r  = TMEM lane (A-row within tile), c0 = first of 32 B-columns;
-//     scratch = drained pipeline smem, shared by the 4 epilogue warps, which
-//     may synchronise with named barrier 1 (epi_bar_sync) — uniformly.
+//   __device__ void operator()(State&, uint8_t* smem, int a_row0, int b_row0,
+//                              int split, int r, int c0, const float (&v)[32]) const;
+//     r  = TMEM lane (A-row within tile), c0 = first of 32 B-columns; smem =
+//     the drained pipeline buffers (output tile staging / exchange), shared by
+//     the 4 epilogue warps, which may synchronise with epi_bar_sync (uniformly).
 //   __device__ void finish(State&, int a_row0, int b_row0, int split, int r) const;
+//   static constexpr bool kTmaStore; __device__ void store(const uint8_t* smem,
+//     int a_row0, int b_row0, int split) const;   (one thread, after a barrier)
 template <int BN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                   GemmGeom g, Epi epi) {
+                   const GemmGeom g, const __grid_constant__ Epi epi) {
   using C = GemmCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -66,6 +104,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int kb0 = split * g.kb_per_split;
   const int kb1 = min(g.k_blocks, kb0 + g.kb_per_split);
   const int nkb = kb1 - kb0;
+  unsigned long long* tr = nullptr;
+  if (g.trace) {
+    tr = g.trace + 8ull * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+    if (threadIdx.x == 0) tr[0] = gtime();
+  }
+  pdl_trigger();
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&map_a);
@@ -82,17 +126,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_smem;
+  if (tr && threadIdx.x == 0) tr[1] = gtime();
 
   if (warp == 0) {
     if (elect_one()) {
+      // Weights do not depend on the previous kernel: stream the first stages
+      // of the weight operand before waiting on it (PDL overlap).
+      const int pre = g.weight_is_a ? min(nkb, C::kStages) : 0;
+      for (int i = 0; i < pre; ++i) {
+        uint8_t* sa = smem + i * C::kStageBytes;
+        mbar_arrive_expect_tx(&full_bar[i], C::kStageBytes);
+        tma_load_2d(sa, &map_a, &full_bar[i], (kb0 + i) * kBK, a_row0);
+      }
+      pdl_wait();
       for (int i = 0; i < nkb; ++i) {
         const int s = i % C::kStages;
         const uint32_t ph = (i / C::kStages) & 1;
-        mbar_wait(&empty_bar[s], ph ^ 1);
         uint8_t* sa = smem + s * C::kStageBytes;
         uint8_t* sb = sa + kTileA;
-        mbar_arrive_expect_tx(&full_bar[s], C::kStageBytes);
-        tma_load_2d(sa, &map_a, &full_bar[s], (kb0 + i) * kBK, a_row0);
+        if (i >= pre) {
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full_bar[s], C::kStageBytes);
+          tma_load_2d(sa, &map_a, &full_bar[s], (kb0 + i) * kBK, a_row0);
+        }
         tma_load_2d(sb, &map_b, &full_bar[s], (kb0 + i) * kBK, b_row0);
       }
     }
@@ -102,6 +158,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int s = i % C::kStages;
       const uint32_t ph = (i / C::kStages) & 1;
       mbar_wait(&full_bar[s], ph);
+      if (tr && lane_id() == 0 && (i == 0 || i == nkb - 1)) tr[i == 0 ? 2 : 3] = gtime();
       tc_fence_after();
       if (elect_one()) {
         const uint32_t sa = smem_u32(smem + s * C::kStageBytes);
@@ -117,12 +174,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     // Epilogue warps 2..5 -> TMEM lane quarters (warp % 4).
+    pdl_wait();
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane_id();
-    float* scratch = reinterpret_cast<float*>(smem);  // pipeline buffers are drained by then
     typename Epi::State st;
     if (nkb > 0) {
       mbar_wait(&acc_bar, 0);
+      if (tr && threadIdx.x == 64) tr[4] = gtime();
       tc_fence_after();
     }
 #pragma unroll 1
@@ -134,94 +192,99 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = 0.f;
       }
-      epi(st, a_row0, b_row0, split, r, c0, v, scratch);
+      epi(st, smem, a_row0, b_row0, split, r, c0, v);
     }
     epi.finish(st, a_row0, b_row0, split, r);
+    if constexpr (Epi::kTmaStore) {
+      fence_async_smem();
+      epi_bar_sync();
+      if (threadIdx.x == 64) {
+        epi.store(smem, a_row0, b_row0, split);
+        bulk_commit_wait();
+      }
+    }
+    if (tr && threadIdx.x == 64) tr[5] = gtime();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
 }
 
-__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-
 // ---- epilogues ----------------------------------------------------------------
+// The swap-AB epilogues stage the output tile in shared memory as
+// [BN tokens][128 features] (the row-major layout of the output) and write it
+// with one TMA bulk tensor store (or reduce-add), instead of 2-byte scattered
+// stores: thread r (feature r) writes column r of the tile, so every st.shared
+// of a warp covers 32 consecutive features (conflict-free). Out-of-range rows /
+// columns are clipped by the TMA unit.
 
-// swap-AB: A = weight [N, K] (rows = output features), B = activations [M, K].
-// out[m * ld + n] = D[n][m] as bf16.
+// out[m][n] = D[n][m] as bf16; map: [M rows][ld] bf16, box {128, BN}.
 struct EpiStoreBF16 {
-  __nv_bfloat16* out;
-  int ld, n_valid, m_valid;
+  CUtensorMap map;
+  static constexpr bool kTmaStore = true;
   struct State {};
-  __device__ void operator()(State&, int a0, int b0, int, int r, int c0, const float (&v)[32], float*) const {
-    const int n = a0 + r;
-    if (n >= n_valid) return;
+  __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int c0, const float (&v)[32]) const {
+    __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int m = b0 + c0 + j;
-      if (m < m_valid) out[static_cast<size_t>(m) * ld + n] = f2bf(v[j]);
-    }
+    for (int j = 0; j < 32; ++j) tile[(c0 + j) * 128 + r] = f2bf(v[j]);
   }
   __device__ void finish(State&, int, int, int, int) const {}
+  __device__ void store(const uint8_t* smem, int a0, int b0, int) const { tma_store_2d(&map, smem, a0, b0); }
 };
 
-// swap-AB split-K partials: out[split][m][n] fp32 (summed by the consumer in
-// split order, so each row's result is independent of the batch size).
-// accumulate != 0 (single split only): out[m][n] += D — the residual add of
-// the o / down projections fused into the GEMM.
+// fp32 out: split-K partials out[split][m][n] (3-D map {N, M, splits}; the
+// consumer sums them in split order, so each row is batch-independent), or —
+// accumulate — a TMA reduce-add into the residual stream out[m][n] (2-D map):
+// the residual add of the o / down projections fused into the GEMM.
 struct EpiStoreF32 {
-  float* out;
-  size_t split_stride;
-  int ld, n_valid, m_valid;
+  CUtensorMap map;
   int accumulate;
+  static constexpr bool kTmaStore = true;
   struct State {};
-  __device__ void operator()(State&, int a0, int b0, int split, int r, int c0, const float (&v)[32], float*) const {
-    const int n = a0 + r;
-    if (n >= n_valid) return;
-    float* o = out + split * split_stride;
+  __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int c0, const float (&v)[32]) const {
+    float* tile = reinterpret_cast<float*>(smem);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int m = b0 + c0 + j;
-      if (m < m_valid) {
-        float* dst = o + static_cast<size_t>(m) * ld + n;
-        *dst = accumulate ? *dst + v[j] : v[j];
-      }
-    }
+    for (int j = 0; j < 32; ++j) tile[(c0 + j) * 128 + r] = v[j];
   }
   __device__ void finish(State&, int, int, int, int) const {}
+  __device__ void store(const uint8_t* smem, int a0, int b0, int split) const {
+    if (accumulate)
+      tma_reduce_add_2d(&map, smem, a0, b0);
+    else
+      tma_store_3d(&map, smem, a0, b0, split);
+  }
 };
 
-// swap-AB fused SwiGLU. The gate/up weight is stored interleaved in 64-row
-// groups: tile rows [0,64) are gate rows of features f0..f0+63 and rows
-// [64,128) the matching up rows, f0 = a_row0 / 2. out[m][f] = silu(g) * u.
+// Fused SwiGLU. The gate/up weight is stored interleaved in 64-row groups:
+// tile rows [0,64) are gate rows of features f0..f0+63 and rows [64,128) the
+// matching up rows, f0 = a_row0 / 2. out[m][f] = silu(g) * u; map [M][F] bf16,
+// box {64, BN}. Up values cross the lane quarters through a small exchange
+// buffer behind the output tile.
 template <int BN>
 struct EpiSwiGLU {
-  __nv_bfloat16* out;
-  int ld, f_valid, m_valid;
+  CUtensorMap map;
+  static constexpr bool kTmaStore = true;
   struct State {};
-  __device__ void operator()(State&, int a0, int b0, int, int r, int c0, const float (&v)[32], float* scratch) const {
-    // scratch: [32 cols][64 lanes] of up values
+  __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int c0, const float (&v)[32]) const {
+    __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);                         // [BN][64]
+    float* xch = reinterpret_cast<float*>(smem + BN * 64 * 2);          // [32][64]
     if (r >= 64) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) scratch[j * 64 + (r - 64)] = v[j];
+      for (int j = 0; j < 32; ++j) xch[j * 64 + (r - 64)] = v[j];
     }
     epi_bar_sync();
     if (r < 64) {
-      const int f = a0 / 2 + r;
-      if (f < f_valid) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int m = b0 + c0 + j;
-          const float gte = v[j];
-          const float up = scratch[j * 64 + r];
-          const float act = gte / (1.0f + __expf(-gte)) * up;
-          if (m < m_valid) out[static_cast<size_t>(m) * ld + f] = f2bf(act);
-        }
+      for (int j = 0; j < 32; ++j) {
+        const float gte = v[j];
+        const float up = xch[j * 64 + r];
+        tile[(c0 + j) * 64 + r] = f2bf(gte / (1.0f + __expf(-gte)) * up);
       }
     }
     epi_bar_sync();
   }
   __device__ void finish(State&, int, int, int, int) const {}
+  __device__ void store(const uint8_t* smem, int a0, int b0, int) const { tma_store_2d(&map, smem, a0 / 2, b0); }
 };
 
 }  // namespace fpk

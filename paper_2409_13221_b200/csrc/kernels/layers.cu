@@ -49,6 +49,7 @@ __global__ void init_bf16_gu_kernel(bf16* __restrict__ w, int F, int d, uint64_t
 }
 
 __global__ void assemble_kernel(AssembleArgs a) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   const int j = blockIdx.x;
   const int sid = a.sid[j], P = a.P[j], R = a.R[j], row0 = a.cu[j], r0 = a.roff[j];
   const int T = P + R;
@@ -69,6 +70,7 @@ __global__ void assemble_kernel(AssembleArgs a) {
 
 __global__ void embed_kernel(const int* __restrict__ tok, const int* __restrict__ idx, const bf16* __restrict__ E,
                              int d, float* __restrict__ x) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   const int m = blockIdx.x;
   const bf16* e = E + static_cast<size_t>(tok[idx ? idx[m] : m]) * d;
   float* o = x + static_cast<size_t>(m) * d;
@@ -92,10 +94,11 @@ __device__ float block_sum(float v, float* red) {
 }
 
 // One warp per output row (4 rows per 128-thread block), float4 traffic.
-__global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__ parts, int nsplit,
-                                size_t split_stride, const float* __restrict__ gain, bf16* __restrict__ y, int d,
+template <int NS>  // number of split-K partials (compile time: all loads of a row chunk in flight)
+__global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__ parts, size_t split_stride, const float* __restrict__ gain, bf16* __restrict__ y, int d,
                                 const int* __restrict__ gather, int rows, const bf16* __restrict__ value_w,
                                 float* __restrict__ value) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   extern __shared__ float4 row_buf[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x * 4 + warp;
@@ -109,11 +112,12 @@ __global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__
   float ss = 0.f;
   for (int j = lane; j < d4; j += 32) {
     float4 v = xr[j];
-    for (int s = 0; s < nsplit; ++s) {
-      const float4 p = pr[s * ps4 + j];
-      v.x += p.x, v.y += p.y, v.z += p.z, v.w += p.w;
-    }
-    if (!gather && nsplit > 0) xr[j] = v;
+    float4 p[NS > 0 ? NS : 1];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) p[s] = pr[s * ps4 + j];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) v.x += p[s].x, v.y += p[s].y, v.z += p[s].z, v.w += p[s].w;
+    if (!gather && NS > 0) xr[j] = v;
     row[j] = v;
     ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
@@ -154,6 +158,7 @@ __global__ void rope_qkv_kernel(const bf16* __restrict__ qkv, int H, int KVH, co
                                 float log2_theta, bf16* __restrict__ q_out, bf16* __restrict__ k_out,
                                 bf16* __restrict__ v_out, KvPoolView pool, int use_pool, int layer,
                                 const int* __restrict__ slot) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   constexpr int half = HD / 2;
   __shared__ float cs_s[half], sn_s[half];
   const int m = blockIdx.x;
@@ -290,8 +295,16 @@ void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, con
               const int* gather, int M_out, const bf16* value_w, float* value, cudaStream_t st) {
   const int rows = gather ? M_out : M;
   if (rows <= 0) return;
-  add_norm_kernel<<<(rows + 3) / 4, 128, 4 * d * sizeof(float), st>>>(x, parts, parts ? nsplit : 0, split_stride, gain,
-                                                                      y, d, gather, rows, value_w, value);
+  const int ns = parts ? nsplit : 0;
+  const dim3 grid((rows + 3) / 4), block(128);
+  const size_t sm = 4 * d * sizeof(float);
+#define FP_AN(N_) \
+  case N_: add_norm_kernel<N_><<<grid, block, sm, st>>>(x, parts, split_stride, gain, y, d, gather, rows, value_w, value); break;
+  switch (ns) {
+    FP_AN(0) FP_AN(1) FP_AN(2) FP_AN(3) FP_AN(4) FP_AN(5) FP_AN(6) FP_AN(7) FP_AN(8)
+    default: throw std::invalid_argument("add_norm: at most 8 split-K partials");
+  }
+#undef FP_AN
   fpk::count_launch();
 }
 

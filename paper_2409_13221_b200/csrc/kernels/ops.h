@@ -28,6 +28,8 @@ void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out,
 // Split count used by gemm_f32_splitk for an (N, K) weight; a function of the
 // weight shape only, so each row's result does not depend on the batch.
 int gemm_splits(int N, int K);
+// Debug: per-CTA phase stamps of subsequent GEMM launches (nullptr disables).
+void set_gemm_trace(unsigned long long* buf);
 
 struct VocabOut;  // fwd
 // Vocab head: rows X [M, K] against W_head [V, K]; writes per-(row, tile)

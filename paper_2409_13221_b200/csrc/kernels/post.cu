@@ -23,6 +23,7 @@ __global__ void postprocess_kernel(int n, const int* __restrict__ off, const flo
                                    const float* __restrict__ score, float beta, float gamma, float lam,
                                    float* __restrict__ kl, float* __restrict__ rew, float* __restrict__ adv,
                                    float* __restrict__ ret, PostScatter sc_out) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= n) return;

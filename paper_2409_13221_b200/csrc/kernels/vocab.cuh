@@ -54,8 +54,10 @@ struct EpiVocab {
     float tz;
     int has_t;
   };
+  static constexpr bool kTmaStore = false;
+  __device__ void store(const uint8_t*, int, int, int) const {}
 
-  __device__ void operator()(State& st, int a0, int b0, int, int r, int c0, const float (&v)[32], float*) const {
+  __device__ void operator()(State& st, uint8_t*, int a0, int b0, int, int r, int c0, const float (&v)[32]) const {
     const int row = a0 + r;
     if (c0 == 0) {
       st.m = -INFINITY;
