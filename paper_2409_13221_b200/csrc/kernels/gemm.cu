@@ -211,7 +211,7 @@ void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out,
 
 constexpr int kVocabBN = 256;
 
-int vocab_tiles(int V) { return (V + kVocabBN - 1) / kVocabBN; }
+int vocab_tiles(int V) { return 2 * ((V + kVocabBN - 1) / kVocabBN); }  // partials per row: 2 column halves per tile
 
 void gemm_vocab(const bf16* X, int M, int K, const bf16* Whead, int V, int mode, float inv_temp, const int* target,
                 const int* sample_id, const int* step, uint64_t seed, void* part, float* tgt_z, cudaStream_t st) {

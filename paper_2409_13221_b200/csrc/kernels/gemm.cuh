@@ -21,7 +21,8 @@ namespace fpk {
 
 constexpr int kBK = 64;                  // K elements per stage (128 B)
 constexpr int kTileA = 128 * kBK * 2;    // bytes of one A stage
-constexpr int kGemmThreads = 192;
+constexpr int kEpiWarps = 8;             // two per TMEM lane quarter (interleaved column chunks)
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr int kSmemBudget = 200 * 1024;
 
 template <int BN>
@@ -50,7 +51,9 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 
 
-__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// per-half barrier (128 threads: the 4 epilogue warps sharing column chunks)
+__device__ __forceinline__ void half_bar_sync(int half) { asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void bulk_commit_wait() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -78,11 +81,14 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const 
 // Epilogue protocol (per epilogue thread; `State` lives in registers):
 //   struct State {...};
 //   __device__ void operator()(State&, uint8_t* smem, int a_row0, int b_row0,
-//                              int split, int r, int c0, const float (&v)[32]) const;
-//     r  = TMEM lane (A-row within tile), c0 = first of 32 B-columns; smem =
-//     the drained pipeline buffers (output tile staging / exchange), shared by
-//     the 4 epilogue warps, which may synchronise with epi_bar_sync (uniformly).
-//   __device__ void finish(State&, int a_row0, int b_row0, int split, int r) const;
+//                              int split, int r, int half, int c0, const float (&v)[32]) const;
+//     r = TMEM lane (A-row within tile); the 8 epilogue warps form two halves
+//     (warps 2-5 / 6-9, each covering the 4 lane quarters) that take
+//     alternating 32-column chunks: half h processes c0 = 32 (2k + h). Every
+//     half makes the same number of calls (ceil(BN / 64)); a call with
+//     c0 >= BN carries zeros and must only take part in half_bar_sync(half).
+//     smem = the drained pipeline buffers (tile staging / exchange).
+//   __device__ void finish(State&, int a_row0, int b_row0, int split, int r, int half) const;
 //   static constexpr bool kTmaStore; __device__ void store(const uint8_t* smem,
 //     int a_row0, int b_row0, int split) const;   (one thread, after a barrier)
 template <int BN, class Epi>
@@ -173,9 +179,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
     }
   } else {
-    // Epilogue warps 2..5 -> TMEM lane quarters (warp % 4).
+    // Epilogue warps 2..9 -> TMEM lane quarters (warp % 4), two halves.
     pdl_wait();
     const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = quarter * 32 + lane_id();
     typename Epi::State st;
     if (nkb > 0) {
@@ -184,17 +191,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
     }
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
+    for (int c0 = 32 * half; c0 < ((BN + 63) / 64) * 64; c0 += 64) {
       float v[32];
-      if (nkb > 0) {
+      if (nkb > 0 && c0 < BN) {
         tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
       } else {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = 0.f;
       }
-      epi(st, smem, a_row0, b_row0, split, r, c0, v);
+      epi(st, smem, a_row0, b_row0, split, r, half, c0, v);
     }
-    epi.finish(st, a_row0, b_row0, split, r);
+    epi.finish(st, a_row0, b_row0, split, r, half);
     if constexpr (Epi::kTmaStore) {
       fence_async_smem();
       epi_bar_sync();
@@ -223,12 +230,12 @@ struct EpiStoreBF16 {
   CUtensorMap map;
   static constexpr bool kTmaStore = true;
   struct State {};
-  __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int c0, const float (&v)[32]) const {
+  __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int, int c0, const float (&v)[32]) const {
     __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) tile[(c0 + j) * 128 + r] = f2bf(v[j]);
+    for (int j = 0; j < 32; ++j) tile[(c0 + j) * 128 + r] = f2bf(v[j]);  // c0 < BN + 32: inside the staging area
   }
-  __device__ void finish(State&, int, int, int, int) const {}
+  __device__ void finish(State&, int, int, int, int, int) const {}
   __device__ void store(const uint8_t* smem, int a0, int b0, int) const { tma_store_2d(&map, smem, a0, b0); }
 };
 
@@ -241,12 +248,12 @@ struct EpiStoreF32 {
   int accumulate;
   static constexpr bool kTmaStore = true;
   struct State {};
-  __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int c0, const float (&v)[32]) const {
+  __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int, int c0, const float (&v)[32]) const {
     float* tile = reinterpret_cast<float*>(smem);
 #pragma unroll
     for (int j = 0; j < 32; ++j) tile[(c0 + j) * 128 + r] = v[j];
   }
-  __device__ void finish(State&, int, int, int, int) const {}
+  __device__ void finish(State&, int, int, int, int, int) const {}
   __device__ void store(const uint8_t* smem, int a0, int b0, int split) const {
     if (accumulate)
       tma_reduce_add_2d(&map, smem, a0, b0);
@@ -258,32 +265,35 @@ struct EpiStoreF32 {
 // Fused SwiGLU. The gate/up weight is stored interleaved in 64-row groups:
 // tile rows [0,64) are gate rows of features f0..f0+63 and rows [64,128) the
 // matching up rows, f0 = a_row0 / 2. out[m][f] = silu(g) * u; map [M][F] bf16,
-// box {64, BN}. Up values cross the lane quarters through a small exchange
-// buffer behind the output tile.
+// box {64, BN}. Per chunk, the half's 128 threads park gate and up in a
+// [32][128] fp32 exchange buffer, then each thread computes 16 outputs
+// (feature t % 64, 16 consecutive tokens): all threads share the MUFU work.
 template <int BN>
 struct EpiSwiGLU {
   CUtensorMap map;
   static constexpr bool kTmaStore = true;
+  static constexpr int kTileBytes = (BN < 64 ? 64 : BN) * 64 * 2;
   struct State {};
-  __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int c0, const float (&v)[32]) const {
-    __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);                         // [BN][64]
-    float* xch = reinterpret_cast<float*>(smem + BN * 64 * 2);          // [32][64]
-    if (r >= 64) {
+  __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int half, int c0,
+                             const float (&v)[32]) const {
+    __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);                       // [BN][64]
+    float* xch = reinterpret_cast<float*>(smem + kTileBytes) + half * 32 * 128;          // [32][128]
 #pragma unroll
-      for (int j = 0; j < 32; ++j) xch[j * 64 + (r - 64)] = v[j];
-    }
-    epi_bar_sync();
-    if (r < 64) {
+    for (int j = 0; j < 32; ++j) xch[j * 128 + r] = v[j];
+    half_bar_sync(half);
+    const int t = r;
+    const int f = t & 63, j0 = (t >> 6) * 16;
+    if (c0 < BN) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float gte = v[j];
-        const float up = xch[j * 64 + r];
-        tile[(c0 + j) * 64 + r] = f2bf(gte / (1.0f + __expf(-gte)) * up);
+      for (int j = j0; j < j0 + 16; ++j) {
+        const float gte = xch[j * 128 + f];
+        const float up = xch[j * 128 + 64 + f];
+        tile[(c0 + j) * 64 + f] = f2bf(__fdividef(gte, 1.0f + __expf(-gte)) * up);
       }
     }
-    epi_bar_sync();
+    half_bar_sync(half);
   }
-  __device__ void finish(State&, int, int, int, int) const {}
+  __device__ void finish(State&, int, int, int, int, int) const {}
   __device__ void store(const uint8_t* smem, int a0, int b0, int) const { tma_store_2d(&map, smem, a0 / 2, b0); }
 };
 

@@ -93,53 +93,54 @@ __device__ float block_sum(float v, float* red) {
   return t;
 }
 
-// One warp per output row (4 rows per 128-thread block), float4 traffic.
-template <int NS>  // number of split-K partials (compile time: all loads of a row chunk in flight)
-__global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__ parts, size_t split_stride, const float* __restrict__ gain, bf16* __restrict__ y, int d,
+// One block per output row, one float4 of the row per thread (blockDim =
+// d / 4 rounded up to a warp multiple): the x load and all NS split-K partial
+// loads of a thread are in flight together, so a row costs one memory round
+// trip regardless of d.
+template <int NS>  // number of split-K partials
+__global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__ parts, size_t split_stride,
+                                const float* __restrict__ gain, bf16* __restrict__ y, int d,
                                 const int* __restrict__ gather, int rows, const bf16* __restrict__ value_w,
                                 float* __restrict__ value) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
-  extern __shared__ float4 row_buf[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x * 4 + warp;
-  if (i >= rows) return;
+  __shared__ float red[32];
+  const int i = blockIdx.x;
   const int src = gather ? gather[i] : i;
   const int d4 = d >> 2;
-  float4* row = row_buf + warp * d4;
+  const int j = threadIdx.x;
+  const bool on = j < d4;
   float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(src) * d);
   const float4* pr = reinterpret_cast<const float4*>(parts + static_cast<size_t>(src) * d);
   const size_t ps4 = split_stride >> 2;
-  float ss = 0.f;
-  for (int j = lane; j < d4; j += 32) {
-    float4 v = xr[j];
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (on) {
+    v = xr[j];
     float4 p[NS > 0 ? NS : 1];
 #pragma unroll
     for (int s = 0; s < NS; ++s) p[s] = pr[s * ps4 + j];
 #pragma unroll
     for (int s = 0; s < NS; ++s) v.x += p[s].x, v.y += p[s].y, v.z += p[s].z, v.w += p[s].w;
     if (!gather && NS > 0) xr[j] = v;
-    row[j] = v;
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
-  ss = warp_sum(ss);
+  float ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  ss = block_sum(ss, red);
   const float inv = rsqrtf(ss / d + kEps);
-  const float4* g4 = reinterpret_cast<const float4*>(gain);
+  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (on) g = reinterpret_cast<const float4*>(gain)[j];
   if (value_w) {
     float dot = 0.f;
-    for (int j = lane; j < d4; j += 32) {
-      const float4 v = row[j], g = g4[j];
+    if (on) {
       const __nv_bfloat162 w01 = reinterpret_cast<const __nv_bfloat162*>(value_w)[2 * j];
       const __nv_bfloat162 w23 = reinterpret_cast<const __nv_bfloat162*>(value_w)[2 * j + 1];
-      dot += v.x * inv * g.x * __bfloat162float(w01.x) + v.y * inv * g.y * __bfloat162float(w01.y) +
-             v.z * inv * g.z * __bfloat162float(w23.x) + v.w * inv * g.w * __bfloat162float(w23.y);
+      dot = v.x * inv * g.x * __bfloat162float(w01.x) + v.y * inv * g.y * __bfloat162float(w01.y) +
+            v.z * inv * g.z * __bfloat162float(w23.x) + v.w * inv * g.w * __bfloat162float(w23.y);
     }
-    dot = warp_sum(dot);
-    if (lane == 0) value[i] = dot;
+    dot = block_sum(dot, red);
+    if (threadIdx.x == 0) value[i] = dot;
     return;
   }
-  uint2* yr = reinterpret_cast<uint2*>(y + static_cast<size_t>(i) * d);
-  for (int j = lane; j < d4; j += 32) {
-    const float4 v = row[j], g = g4[j];
+  if (on) {
+    uint2* yr = reinterpret_cast<uint2*>(y + static_cast<size_t>(i) * d);
     yr[j] = make_uint2(pack_bf16x2(v.x * inv * g.x, v.y * inv * g.y), pack_bf16x2(v.z * inv * g.z, v.w * inv * g.w));
   }
 }
@@ -296,8 +297,9 @@ void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, con
   const int rows = gather ? M_out : M;
   if (rows <= 0) return;
   const int ns = parts ? nsplit : 0;
-  const dim3 grid((rows + 3) / 4), block(128);
-  const size_t sm = 4 * d * sizeof(float);
+  if (d % 4 || d > 4096) throw std::invalid_argument("add_norm: d must be a multiple of 4 and <= 4096");
+  const dim3 grid(rows), block(((d / 4 + 31) / 32) * 32);
+  const size_t sm = 0;
 #define FP_AN(N_) \
   case N_: add_norm_kernel<N_><<<grid, block, sm, st>>>(x, parts, split_stride, gain, y, d, gather, rows, value_w, value); break;
   switch (ns) {

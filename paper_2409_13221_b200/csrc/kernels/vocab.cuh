@@ -57,9 +57,10 @@ struct EpiVocab {
   static constexpr bool kTmaStore = false;
   __device__ void store(const uint8_t*, int, int, int) const {}
 
-  __device__ void operator()(State& st, uint8_t*, int a0, int b0, int, int r, int c0, const float (&v)[32]) const {
+  __device__ void operator()(State& st, uint8_t*, int a0, int b0, int, int r, int half, int c0,
+                             const float (&v)[32]) const {
     const int row = a0 + r;
-    if (c0 == 0) {
+    if (c0 == 32 * half) {
       st.m = -INFINITY;
       st.s = 0.f;
       st.key = -INFINITY;
@@ -68,7 +69,7 @@ struct EpiVocab {
       st.has_t = 0;
       st.tz = 0.f;
     }
-    if (row >= rows) return;
+    if (row >= rows || c0 >= 256) return;
     const int base = b0 + c0;
     if (base >= vocab) return;
     const int nvalid = min(32, vocab - base);
@@ -126,17 +127,17 @@ struct EpiVocab {
     }
   }
 
-  __device__ void finish(State& st, int a0, int, int, int r) const {
+  __device__ void finish(State& st, int a0, int, int, int r, int half) const {
     const int row = a0 + r;
     if (row >= rows) return;
-    VocabPartial p;  // one per (row, vocab tile = blockIdx.y)
+    VocabPartial p;  // one per (row, vocab tile = blockIdx.y, column half)
     p.m = st.m;
     p.s = st.s;
     p.key = st.key;
     p.z = st.z;
     p.idx = st.idx;
     p.pad_ = 0;
-    part[static_cast<size_t>(row) * n_tiles + blockIdx.y] = p;
+    part[static_cast<size_t>(row) * n_tiles + 2 * blockIdx.y + half] = p;
     if (mode == kForced && st.has_t) tgt_z[row] = st.tz;
   }
 };

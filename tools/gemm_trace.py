@@ -1,4 +1,7 @@
-"""Phase timeline of tcgen05 GEMM CTAs (globaltimer stamps): where does a decode GEMM spend its time?"""
+"""Phase timeline of tcgen05 GEMM CTAs (globaltimer stamps): where does a GEMM spend its time?
+
+    python tools/gemm_trace.py            # decode-shaped cases of every epilogue
+"""
 import ctypes as C
 import sys
 
@@ -10,27 +13,50 @@ from paper_2409_13221_b200 import _lib  # noqa: E402
 
 lib = _lib.load()
 p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
-tr = torch.zeros(8 * 8192, dtype=torch.int64, device="cuda")
+tr = torch.zeros(8 * 65536, dtype=torch.int64, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 names = ["entry", "setup", "first_full", "last_full", "acc_ready", "epi_done"]
-for M, N, K in ((16, 2304, 768), (256, 2304, 768), (64, 6144, 768), (350, 768, 3072), (4096, 6144, 768)):
-    W = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+
+
+def case(kind, M, N, K):
+    W = torch.randn(N, K, device="cuda").to(torch.bfloat16) * 0.05
     X = torch.randn(M, K, device="cuda").to(torch.bfloat16)
-    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    for rep in range(3):
+    if kind == "bf16":
+        out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        f = lambda: lib.fp_k_gemm_bf16(p(W), N, K, p(X), M, p(out), N, None)  # noqa: E731
+    elif kind == "swiglu":
+        out = torch.empty(M, N // 2, device="cuda", dtype=torch.bfloat16)
+        f = lambda: lib.fp_k_gemm_swiglu(p(W), N // 2, K, p(X), M, p(out), None)  # noqa: E731
+    elif kind == "f32":
+        s = lib.fp_k_gemm_splits(N, K)
+        out = torch.empty(s, M, N, device="cuda")
+        f = lambda: lib.fp_k_gemm_f32(p(W), N, K, p(X), M, p(out), s, None)  # noqa: E731
+    else:  # vocab sampling head: A = X rows, B = W (vocab)
+        sid = torch.arange(M, device="cuda", dtype=torch.int32)
+        stp = torch.zeros(M, device="cuda", dtype=torch.int32)
+        tok = torch.empty(M, device="cuda", dtype=torch.int32)
+        lp = torch.empty(M, device="cuda")
+        f = lambda: lib.fp_k_vocab(p(X), M, K, p(W), N, 2, 1.0, None, p(sid), p(stp), 7, p(tok), p(lp), None)  # noqa
+    for _ in range(3):
         flush.zero_()
         tr.zero_()
         torch.cuda.synchronize()
         lib.fp_k_gemm_trace(p(tr))
-        lib.fp_k_gemm_bf16(p(W), N, K, p(X), M, p(out), N, None)
+        f()
         torch.cuda.synchronize()
         lib.fp_k_gemm_trace(None)
     t = tr.view(-1, 8).cpu().numpy()
     t = t[t[:, 0] > 0][:, :6].astype(np.float64)
-    t0 = t[:, 0].min()
-    rel = (t - t0) / 1000.0
-    print(f"M={M} N={N} K={K} ctas={len(t)}: span {rel[:, 5].max():.2f} us")
-    for i, nm in enumerate(names):
-        print(f"   {nm:11s} min {rel[:, i].min():7.2f}  med {np.median(rel[:, i]):7.2f}  max {rel[:, i].max():7.2f}")
-    d = rel[:, 3] - rel[:, 2]
-    print(f"   mainloop(first->last full) med {np.median(d):.2f}  epi med {np.median(rel[:, 5] - rel[:, 4]):.2f}")
+    rel = (t - t[:, 0].min()) / 1000.0
+    per = rel - rel[:, :1]
+    print(f"{kind:6s} M={M} N={N} K={K} ctas={len(t)}: span {rel[:, 5].max():.2f} us | per-CTA med: "
+          f"setup {np.median(per[:, 1]):.2f} first {np.median(per[:, 2]):.2f} main "
+          f"{np.median(per[:, 3] - per[:, 2]):.2f} acc {np.median(per[:, 4] - per[:, 3]):.2f} "
+          f"epi {np.median(per[:, 5] - per[:, 4]):.2f} total {np.median(per[:, 5]):.2f}", flush=True)
+
+
+for kind, M, N, K in (("bf16", 16, 2304, 768), ("bf16", 350, 2304, 768), ("swiglu", 64, 6144, 768),
+                      ("swiglu", 350, 6144, 768), ("f32", 350, 768, 768), ("f32", 350, 768, 3072),
+                      ("vocab", 350, 50257, 768), ("vocab", 16, 50257, 768), ("bf16", 4096, 6144, 768),
+                      ("bf16", 16384, 2304, 768)):
+    case(kind, M, N, K)
