@@ -191,16 +191,71 @@ def philox4x32_10(ctr: np.ndarray, k0: int, k1: int) -> np.ndarray:
     return c.astype(np.uint32)
 
 
-def gumbel_noise(seed: int, sample_id: int, step: int, vocab: int) -> np.ndarray:
-    nq = (vocab + 3) // 4
-    ctr = np.zeros((nq, 4), dtype=np.uint32)
-    ctr[:, 0] = np.arange(nq, dtype=np.uint32)
-    ctr[:, 1] = step
-    ctr[:, 2] = sample_id
-    ctr[:, 3] = 0xF00D
-    w = philox4x32_10(ctr, seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF).reshape(-1)[:vocab]
-    u = ((w >> np.uint32(8)).astype(np.float32) + np.float32(0.5)) * np.float32(1.0 / 16777216.0)
-    return -np.log(-np.log(u))
+def _unit(w) -> np.float32:
+    return (np.float32(int(w) >> 8) + np.float32(0.5)) * np.float32(1.0 / 16777216.0)
+
+
+def _philox1(seed: int, c0: int, step: int, sid: int) -> int:
+    return int(philox4x32_10(np.array([[c0, step, sid, 0xF00D]], dtype=np.uint32), seed & 0xFFFFFFFF,
+                             (seed >> 32) & 0xFFFFFFFF)[0, 0])
+
+
+def vocab_partials(z: np.ndarray, inv_temp_is_applied: bool = True, c2: np.float32 | None = None):
+    """Per (256-column tile, 128-column half) statistics of one row, in the GPU's
+    column order (half h owns chunks c0 = 32h, 32h + 64, ...): (m2, s, columns)."""
+    V = len(z)
+    out = []
+    for t in range((V + 255) // 256):
+        for h in range(2):
+            cols = [256 * t + c0 + j for c0 in range(32 * h, 256, 64) for j in range(32) if 256 * t + c0 + j < V]
+            out.append(cols)
+    return out
+
+
+def sample_token(logits: np.ndarray, inv_temp: float, seed: int, sid: int, step: int):
+    """Two-level exact sampling of csrc/kernels/vocab.cuh (half-tile by mass, then
+    inverse CDF inside it), replayed in fp32 in the kernel's summation order."""
+    c2 = np.float32(inv_temp) * np.float32(1.4426950408889634)
+    z2 = logits.astype(np.float32) * c2
+    parts = []
+    for pi, cols in enumerate(vocab_partials(logits)):
+        if not cols:
+            parts.append((np.float32(-np.inf), np.float32(0), -1))
+            continue
+        m = np.float32(-np.inf)
+        s = np.float32(0)
+        for k in range(0, len(cols), 32):  # chunk-wise online max / sum, as the epilogue
+            ch = z2[cols[k:k + 32]]
+            nm = max(m, ch.max())
+            acc = np.float32(0) if m == -np.inf else np.float32(s * np.exp2(np.float32(m - nm)))
+            for x in ch:
+                acc = np.float32(acc + np.exp2(np.float32(x - nm)))
+            m, s = nm, acc
+        thr = _unit(_philox1(seed, pi, step, sid)) * s
+        acc = np.float32(0)
+        pick = cols[-1]
+        for c in cols:
+            acc = np.float32(acc + np.exp2(np.float32(z2[c] - m)))
+            pick = c
+            if acc >= thr:
+                break
+        parts.append((m, s, pick))
+    M = max(p[0] for p in parts)
+    tot = np.float32(0)
+    for m, s, _ in parts:
+        if m != -np.inf:
+            tot = np.float32(tot + s * np.exp2(np.float32(m - M)))
+    thr = _unit(_philox1(seed, 0xFFFFFFFF, step, sid)) * tot
+    acc = np.float32(0)
+    tok = -1
+    for m, s, idx in parts:
+        if m == -np.inf:
+            continue
+        acc = np.float32(acc + s * np.exp2(np.float32(m - M)))
+        tok = idx
+        if acc >= thr:
+            break
+    return tok
 
 
 # ---------------------------------------------------------------------------
@@ -306,7 +361,7 @@ class Oracle:
             if mode == "greedy":
                 t = int(np.argmax(z))
             else:
-                t = int(np.argmax(z + gumbel_noise(seed, sample_id, k, len(z))))
+                t = sample_token(h @ W["head"].T, 1.0 / temperature, seed, sample_id, k)
             out_t.append(t)
             out_lp.append(float(lp[t]))
             cur, pos = t, pos + 1

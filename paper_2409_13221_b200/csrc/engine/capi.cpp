@@ -348,7 +348,7 @@ int fp_k_vocab(const void* X, int32_t M, int32_t K, const void* W, int32_t V, in
     fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&tz), static_cast<size_t>(M) * 4 + 256, S(stream)), "alloc");
     fpk::gemm_vocab(static_cast<const bf16*>(X), M, K, static_cast<const bf16*>(W), V, mode, inv_temp, target,
                     sample_id, step, seed, part, tz, S(stream));
-    fpk::vocab_finalize(part, tz, M, V, mode, target, token, logp, nullptr, nullptr, nullptr, nullptr, nullptr,
+    fpk::vocab_finalize(part, tz, M, V, mode, target, sample_id, step, seed, token, logp, nullptr, nullptr, nullptr, nullptr, nullptr,
                         S(stream));
     after_launch();
     fpe::check(cudaFreeAsync(part, S(stream)), "free");

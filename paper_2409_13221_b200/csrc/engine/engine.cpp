@@ -495,7 +495,7 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
   fpk::add_norm(dec_.x, dec_.parts, nparts, stride, w.lnf, dec_.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
   fpk::gemm_vocab(dec_.h, B, D.d, w.head, D.V, mode, inv_temp, target, sid, step, sample_seed, dec_.vocab_part,
                   dec_.tgt_z, st);
-  fpk::vocab_finalize(dec_.vocab_part, dec_.tgt_z, B, D.V, mode, target, nullptr, nullptr, dst, d_hist_tok_,
+  fpk::vocab_finalize(dec_.vocab_part, dec_.tgt_z, B, D.V, mode, target, sid, step, sample_seed, nullptr, nullptr, dst, d_hist_tok_,
                       d_hist_logp_, slot, d_cur_tok_, st);
   FP_CUDA(cudaGetLastError());
 }
@@ -554,7 +554,7 @@ void Engine::infer(const std::vector<InferItem>& items, float beta, float gamma,
     fpk::add_norm(ws.x, nullptr, 0, 0, ref.lnf, ws.h, M, ref.dims.d, ws.gather_resp, NR, nullptr, nullptr, st);
     fpk::gemm_vocab(ws.h, NR, ref.dims.d, ref.head, ref.dims.V, 0 /* forced */, 1.0f, ws.targets, nullptr, nullptr, 0,
                     ws.vocab_part, ws.tgt_z, st);
-    fpk::vocab_finalize(ws.vocab_part, ws.tgt_z, NR, ref.dims.V, 0 /* forced */, ws.targets, nullptr, ws.logp_ref,
+    fpk::vocab_finalize(ws.vocab_part, ws.tgt_z, NR, ref.dims.V, 0 /* forced */, ws.targets, nullptr, nullptr, 0, nullptr, ws.logp_ref,
                         nullptr, nullptr, nullptr, nullptr, nullptr, st);
     // critic: value of the state before each response token
     const ModelW& cr = models_[kCritic];

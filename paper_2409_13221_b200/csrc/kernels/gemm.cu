@@ -215,67 +215,91 @@ int vocab_tiles(int V) { return 2 * ((V + kVocabBN - 1) / kVocabBN); }  // parti
 
 void gemm_vocab(const bf16* X, int M, int K, const bf16* Whead, int V, int mode, float inv_temp, const int* target,
                 const int* sample_id, const int* step, uint64_t seed, void* part, float* tgt_z, cudaStream_t st) {
-  EpiVocab e;
-  e.part = static_cast<VocabPartial*>(part);
-  e.tgt_z = tgt_z;
-  e.info = VocabRowInfo{target, sample_id, step};
-  e.mode = mode;
-  e.inv_temp = inv_temp;
-  e.vocab = V;
-  e.rows = M;
-  e.n_tiles = vocab_tiles(V);
-  e.seed_lo = static_cast<uint32_t>(seed);
-  e.seed_hi = static_cast<uint32_t>(seed >> 32);
-  launch<kVocabBN>(X, M, Whead, V, K, 1, e, st, /*weight_is_a=*/false);
+  auto go = [&](auto e) {
+    e.part = static_cast<VocabPartial*>(part);
+    e.tgt_z = tgt_z;
+    e.info = VocabRowInfo{target, sample_id, step};
+    e.inv_temp = inv_temp;
+    e.vocab = V;
+    e.rows = M;
+    e.n_tiles = vocab_tiles(V);
+    e.seed_lo = static_cast<uint32_t>(seed);
+    e.seed_hi = static_cast<uint32_t>(seed >> 32);
+    launch<kVocabBN>(X, M, Whead, V, K, 1, e, st, /*weight_is_a=*/false);
+  };
+  if (mode == kForced) go(EpiVocab<kForced>{});
+  else if (mode == kGreedy) go(EpiVocab<kGreedy>{});
+  else go(EpiVocab<kSample>{});
 }
 
-// One warp per row: merge the vocab tiles in order.
+// One warp per row: merge the row's partials in partial order. The sampling
+// walk over partials is sequential in lane 0 so that its float order is
+// fixed (the CPU oracle replays it).
 __global__ void vocab_finalize_kernel(const VocabPartial* __restrict__ part, const float* __restrict__ tgt_z, int M,
-                                      int n_tiles, int mode, const int* __restrict__ target, int* token, float* logp,
-                                      const int* dst, int* out_tok, float* out_logp, const int* cur_idx,
-                                      int* cur_tok) {
+                                      int n_tiles, int mode, const int* __restrict__ target,
+                                      const int* __restrict__ sample_id, const int* __restrict__ step,
+                                      uint32_t seed_lo, uint32_t seed_hi, int* token, float* logp, const int* dst,
+                                      int* out_tok, float* out_logp, const int* cur_idx, int* cur_tok) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
   const VocabPartial* p = part + static_cast<size_t>(row) * n_tiles;
   float m = -INFINITY;
-  for (int t = lane; t < n_tiles; t += 32) m = fmaxf(m, p[t].m);
+  for (int t = lane; t < n_tiles; t += 32) m = fmaxf(m, p[t].m2);
   m = warp_max(m);
   float s = 0.f;
-  float bkey = -INFINITY, bz = 0.f;
+  float bz = -INFINITY;
   int bidx = 0x7fffffff;
   for (int t = lane; t < n_tiles; t += 32) {
     const VocabPartial q = p[t];
-    if (q.m > -INFINITY) s += q.s * expf(q.m - m);
-    if (q.idx >= 0 && (q.key > bkey || (q.key == bkey && q.idx < bidx))) {
-      bkey = q.key;
+    if (q.m2 > -INFINITY) s += q.s * exp2f(q.m2 - m);
+    if (mode == kGreedy && q.idx >= 0 && (q.zsel > bz || (q.zsel == bz && q.idx < bidx))) {
+      bz = q.zsel;
       bidx = q.idx;
-      bz = q.z;
     }
   }
   s = warp_sum(s);
+  if (mode == kGreedy) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float ok = __shfl_xor_sync(0xffffffffu, bkey, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
-    const float oz = __shfl_xor_sync(0xffffffffu, bz, o);
-    if (ok > bkey || (ok == bkey && oi < bidx)) {
-      bkey = ok;
-      bidx = oi;
-      bz = oz;
+    for (int o = 16; o > 0; o >>= 1) {
+      const float oz = __shfl_xor_sync(0xffffffffu, bz, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, o);
+      if (oz > bz || (oz == bz && oi < bidx)) {
+        bz = oz;
+        bidx = oi;
+      }
     }
   }
   if (lane != 0) return;
-  const float lse = m + logf(s);
+  const float lse = m * kLn2 + logf(s);  // natural-log logsumexp of z
   int tok;
   float lp;
   if (mode == kForced) {
     tok = target[row];
     lp = tgt_z[row] - lse;
-  } else {
+  } else if (mode == kGreedy) {
     tok = bidx;
     lp = bz - lse;
+  } else {
+    // half-tile choice: inverse CDF of s_t 2^(m2_t - M2), sequential in t
+    float tot = 0.f;
+    for (int t = 0; t < n_tiles; ++t)
+      if (p[t].m2 > -INFINITY) tot += p[t].s * exp2f(p[t].m2 - m);
+    const U4 w = philox4x32_10(U4{kRowDraw, static_cast<uint32_t>(step[row]), static_cast<uint32_t>(sample_id[row]),
+                                  0xF00Du},
+                               seed_lo, seed_hi);
+    const float thr = unit_open(w.x) * tot;
+    float acc = 0.f;
+    int pick = -1;
+    for (int t = 0; t < n_tiles; ++t) {
+      if (p[t].m2 == -INFINITY) continue;
+      acc += p[t].s * exp2f(p[t].m2 - m);
+      pick = t;
+      if (acc >= thr) break;
+    }
+    tok = p[pick].idx;
+    lp = p[pick].zsel - lse;
   }
   if (token) token[row] = tok;
   if (logp) logp[row] = lp;
@@ -289,14 +313,16 @@ __global__ void vocab_finalize_kernel(const VocabPartial* __restrict__ part, con
   if (cur_tok) cur_tok[cur_idx[row]] = tok;
 }
 
-void vocab_finalize(const void* part, const float* tgt_z, int M, int V, int mode, const int* target, int* token,
-                    float* logp, const int* dst, int* out_tok, float* out_logp, const int* cur_idx, int* cur_tok,
-                    cudaStream_t st) {
+void vocab_finalize(const void* part, const float* tgt_z, int M, int V, int mode, const int* target,
+                    const int* sample_id, const int* step, uint64_t seed, int* token, float* logp, const int* dst,
+                    int* out_tok, float* out_logp, const int* cur_idx, int* cur_tok, cudaStream_t st) {
   if (M <= 0) return;
   const int warps = 8;
   vocab_finalize_kernel<<<(M + warps - 1) / warps, warps * 32, 0, st>>>(
-      static_cast<const VocabPartial*>(part), tgt_z, M, vocab_tiles(V), mode, target, token, logp, dst, out_tok,
-      out_logp, cur_idx, cur_tok); fpk::count_launch();
+      static_cast<const VocabPartial*>(part), tgt_z, M, vocab_tiles(V), mode, target, sample_id, step,
+      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), token, logp, dst, out_tok, out_logp, cur_idx,
+      cur_tok);
+  fpk::count_launch();
 }
 
 }  // namespace fpk

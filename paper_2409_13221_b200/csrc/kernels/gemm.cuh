@@ -184,22 +184,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     const int r = quarter * 32 + lane_id();
-    typename Epi::State st;
+    typename Epi::State st{};
     if (nkb > 0) {
       mbar_wait(&acc_bar, 0);
       if (tr && threadIdx.x == 64) tr[4] = gtime();
       tc_fence_after();
     }
 #pragma unroll 1
-    for (int c0 = 32 * half; c0 < ((BN + 63) / 64) * 64; c0 += 64) {
-      float v[32];
-      if (nkb > 0 && c0 < BN) {
-        tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
-      } else {
+    for (int pass = 0; pass < Epi::kPasses; ++pass) {  // two-pass epilogues re-read TMEM (cheap)
+      if (pass) epi.next_pass(st, a_row0, b_row0, r, half);
+#pragma unroll 1
+      for (int c0 = 32 * half; c0 < ((BN + 63) / 64) * 64; c0 += 64) {
+        float v[32];
+        if (nkb > 0 && c0 < BN) {
+          tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        }
+        epi(st, smem, a_row0, b_row0, split, r, half, c0, v);
       }
-      epi(st, smem, a_row0, b_row0, split, r, half, c0, v);
     }
     epi.finish(st, a_row0, b_row0, split, r, half);
     if constexpr (Epi::kTmaStore) {
@@ -229,6 +233,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 struct EpiStoreBF16 {
   CUtensorMap map;
   static constexpr bool kTmaStore = true;
+  static constexpr int kPasses = 1;
+  template <class S> __device__ void next_pass(S&, int, int, int, int) const {}
   struct State {};
   __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int, int c0, const float (&v)[32]) const {
     __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);
@@ -247,6 +253,8 @@ struct EpiStoreF32 {
   CUtensorMap map;
   int accumulate;
   static constexpr bool kTmaStore = true;
+  static constexpr int kPasses = 1;
+  template <class S> __device__ void next_pass(S&, int, int, int, int) const {}
   struct State {};
   __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int, int c0, const float (&v)[32]) const {
     float* tile = reinterpret_cast<float*>(smem);
@@ -272,6 +280,8 @@ template <int BN>
 struct EpiSwiGLU {
   CUtensorMap map;
   static constexpr bool kTmaStore = true;
+  static constexpr int kPasses = 1;
+  template <class S> __device__ void next_pass(S&, int, int, int, int) const {}
   static constexpr int kTileBytes = (BN < 64 ? 64 : BN) * 64 * 2;
   struct State {};
   __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int half, int c0,

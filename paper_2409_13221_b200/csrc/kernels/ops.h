@@ -33,7 +33,8 @@ void set_gemm_trace(unsigned long long* buf);
 
 struct VocabOut;  // fwd
 // Vocab head: rows X [M, K] against W_head [V, K]; writes per-(row, tile)
-// partials into `part` (M x vocab_tiles(V) VocabPartial = 24 B each) and, in
+// partials into `part` (M x vocab_tiles(V) VocabPartial = 24 B each, two
+// 128-column halves per 256-wide vocab tile) and, in
 // forced mode, tgt_z[M]. mode: 0 forced (target[]), 1 greedy, 2 sample.
 int vocab_tiles(int V);
 void gemm_vocab(const bf16* X, int M, int K, const bf16* Whead, int V, int mode, float inv_temp,
@@ -42,9 +43,10 @@ void gemm_vocab(const bf16* X, int M, int K, const bf16* Whead, int V, int mode,
 // Merge partials: token[row] (forced -> target), logp[row]; optional scatter
 // into per-sample buffers: out_tok[dst[row]] / out_logp[dst[row]] when dst != nullptr.
 // cur_tok[cur_idx[row]] = token (next decode input) when cur_tok != nullptr.
-void vocab_finalize(const void* part, const float* tgt_z, int M, int V, int mode, const int* target, int* token,
-                    float* logp, const int* dst, int* out_tok, float* out_logp, const int* cur_idx, int* cur_tok,
-                    cudaStream_t st);
+// Sampling (mode 2) draws the half-tile with Philox(seed, sample_id[row], step[row], 0xFFFFFFFF).
+void vocab_finalize(const void* part, const float* tgt_z, int M, int V, int mode, const int* target,
+                    const int* sample_id, const int* step, uint64_t seed, int* token, float* logp, const int* dst,
+                    int* out_tok, float* out_logp, const int* cur_idx, int* cur_tok, cudaStream_t st);
 
 // ---- elementwise / norms (layers.cu) ----------------------------------------------
 void init_bf16(bf16* w, size_t n, uint64_t seed, uint64_t tag, float scale, cudaStream_t st);

@@ -1,14 +1,23 @@
 // fuseplan-b200 — LM-head epilogue: log-softmax statistics, target gather,
-// greedy argmax and Gumbel-max temperature sampling, fused into the tcgen05
-// head GEMM so the [rows, V] logits never reach HBM.
+// greedy argmax and exact temperature sampling, fused into the tcgen05 head
+// GEMM so the [rows, V] logits never reach HBM.
 //
-// Orientation: A = hidden rows (one token per TMEM lane / epilogue thread),
-// B = head weight rows (vocab ids on the BN columns). Each CTA emits, per row
-// and per vocab tile, a VocabPartial {max z, sum exp(z - max), best key,
-// best id, z of best}; z = logit / temperature. vocab_finalize() merges the
-// tiles of a row in tile order (deterministic), picks the token (forced
-// target | argmax z | argmax z + Gumbel(Philox(seed, sample, step, v))) and
-// its log-probability z_token - logsumexp(z).
+// Orientation: A = hidden rows (one token per TMEM lane), B = head weight rows
+// (vocab ids on the BN = 256 columns). Each epilogue thread owns one row and
+// one half of the tile's columns (the interleaved 32-column chunks of its
+// warp half), and emits one VocabPartial per (row, tile, half): with
+// z = logit / T and z2 = z log2(e),
+//   m2 = max z2,  s = sum 2^(z2 - m2)  (exp2 on the MUFU),
+//   (idx, zsel) = the half-tile's candidate token:
+//       greedy: argmax z (ties: lower id);
+//       sample: inverse CDF of 2^(z2 - m2) at u s, u = Philox(seed, sample,
+//               step, partial index) — a second pass re-reads TMEM;
+//   forced targets write their z to tgt_z.
+// vocab_finalize() merges a row's partials in partial order (deterministic):
+// logsumexp, and for sampling picks the half-tile by inverse CDF of
+// s_t 2^(m2_t - M2) at u' (Philox counter 0xFFFFFFFF). Exact sampling from
+// softmax(z): P(v) = P(tile) P(v | tile). One Philox draw per 128 vocab
+// entries instead of a Gumbel variate per entry.
 #pragma once
 
 #include <math.h>
@@ -19,10 +28,14 @@
 namespace fpk {
 
 enum TokenMode : int { kForced = 0, kGreedy = 1, kSample = 2 };
+constexpr float kLog2E = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+constexpr uint32_t kRowDraw = 0xFFFFFFFFu;  // Philox counter word of the tile choice
 
 struct VocabPartial {
-  float m, s, key, z;
-  int idx, pad_;
+  float m2, s, zsel;
+  int idx;
+  float pad0, pad1;
 };
 
 struct VocabRowInfo {
@@ -31,114 +44,121 @@ struct VocabRowInfo {
   const int* step;       // [rows] response position (kSample)
 };
 
-// Gumbel noise of vocab id v in the stream (sample, step).
-__device__ __forceinline__ float gumbel_of(uint32_t w) {
-  const float u = (static_cast<float>(w >> 8) + 0.5f) * (1.0f / 16777216.0f);  // (0, 1)
-  return -logf(-logf(u));
+// u in (0, 1) from the top 24 bits of a Philox word.
+__host__ __device__ __forceinline__ float unit_open(uint32_t w) {
+  return (static_cast<float>(w >> 8) + 0.5f) * (1.0f / 16777216.0f);
 }
 
+template <int MODE>
 struct EpiVocab {
   VocabPartial* part;   // [rows][n_tiles]
   float* tgt_z;         // [rows] z of the forced target (written by its tile)
   VocabRowInfo info;
-  int mode;
   float inv_temp;
   int vocab;
   int rows;
   int n_tiles;
   uint32_t seed_lo, seed_hi;
 
-  struct State {
-    float m, s, key, z;
-    int idx;
-    float tz;
-    int has_t;
-  };
   static constexpr bool kTmaStore = false;
+  static constexpr int kPasses = MODE == kSample ? 2 : 1;
   __device__ void store(const uint8_t*, int, int, int) const {}
+
+  struct State {
+    float m, s;      // running max of z2, sum of 2^(z2 - m)
+    float zsel;      // z of the candidate
+    int idx;         // candidate id
+    float thr, acc;  // sampling walk (pass 1)
+    float tz;
+    int has_t, pass;
+  };
+
+  __device__ void next_pass(State& st, int a0, int b0, int r, int half) const {
+    st.pass = 1;
+    st.acc = 0.f;
+    const int row = a0 + r;
+    if (row >= rows || st.m == -INFINITY) {
+      st.thr = INFINITY;
+      return;
+    }
+    const uint32_t pidx = static_cast<uint32_t>(2 * (b0 / 256) + half);
+    const U4 w = philox4x32_10(U4{pidx, static_cast<uint32_t>(info.step[row]),
+                                  static_cast<uint32_t>(info.sample_id[row]), 0xF00Du},
+                               seed_lo, seed_hi);
+    st.thr = unit_open(w.x) * st.s;
+  }
 
   __device__ void operator()(State& st, uint8_t*, int a0, int b0, int, int r, int half, int c0,
                              const float (&v)[32]) const {
     const int row = a0 + r;
-    if (c0 == 32 * half) {
+    if (c0 == 32 * half && st.pass == 0) {
       st.m = -INFINITY;
       st.s = 0.f;
-      st.key = -INFINITY;
-      st.z = -INFINITY;
+      st.zsel = -INFINITY;
       st.idx = -1;
       st.has_t = 0;
       st.tz = 0.f;
+      st.pass = 0;
     }
     if (row >= rows || c0 >= 256) return;
     const int base = b0 + c0;
     if (base >= vocab) return;
     const int nvalid = min(32, vocab - base);
-    float z[32];
+    const float c2 = inv_temp * kLog2E;
+    if (st.pass == 1) {  // sampling walk: first column whose running mass reaches thr
+      if (st.acc >= st.thr) return;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (j < nvalid && st.acc < st.thr) {
+          st.acc += exp2f(v[j] * c2 - st.m);
+          st.idx = base + j;
+          st.zsel = v[j] * inv_temp;
+        }
+      }
+      return;
+    }
     float cmax = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      z[j] = v[j] * inv_temp;
-      if (j < nvalid) cmax = fmaxf(cmax, z[j]);
-    }
+    for (int j = 0; j < 32; ++j)
+      if (j < nvalid) cmax = fmaxf(cmax, v[j] * c2);
     const float nm = fmaxf(st.m, cmax);
-    float acc = (st.m == -INFINITY) ? 0.f : st.s * expf(st.m - nm);
+    float acc = (st.m == -INFINITY) ? 0.f : st.s * exp2f(st.m - nm);
 #pragma unroll
     for (int j = 0; j < 32; ++j)
-      if (j < nvalid) acc += expf(z[j] - nm);
+      if (j < nvalid) acc += exp2f(v[j] * c2 - nm);
     st.m = nm;
     st.s = acc;
-
-    if (mode == kForced) {
+    if constexpr (MODE == kForced) {
       const int t = info.target[row];
       if (t >= base && t < base + nvalid) {
 #pragma unroll
         for (int j = 0; j < 32; ++j)
-          if (base + j == t) st.tz = z[j];
+          if (base + j == t) st.tz = v[j] * inv_temp;
         st.has_t = 1;
       }
-    } else if (mode == kGreedy) {
+    } else if constexpr (MODE == kGreedy) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nvalid && z[j] > st.key) {
-          st.key = z[j];
-          st.z = z[j];
+      for (int j = 0; j < 32; ++j) {
+        const float z = v[j] * inv_temp;
+        if (j < nvalid && z > st.zsel) {
+          st.zsel = z;
           st.idx = base + j;
-        }
-    } else {
-      const uint32_t sid = static_cast<uint32_t>(info.sample_id[row]);
-      const uint32_t stp = static_cast<uint32_t>(info.step[row]);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const U4 w = philox4x32_10(U4{static_cast<uint32_t>((base >> 2) + q), stp, sid, 0xF00Du}, seed_lo, seed_hi);
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int j = q * 4 + e;
-          if (j < nvalid) {
-            const float k = z[j] + gumbel_of(ws[e]);
-            if (k > st.key) {
-              st.key = k;
-              st.z = z[j];
-              st.idx = base + j;
-            }
-          }
         }
       }
     }
   }
 
-  __device__ void finish(State& st, int a0, int, int, int r, int half) const {
+  __device__ void finish(State& st, int a0, int b0, int, int r, int half) const {
     const int row = a0 + r;
     if (row >= rows) return;
     VocabPartial p;  // one per (row, vocab tile = blockIdx.y, column half)
-    p.m = st.m;
+    p.m2 = st.m;
     p.s = st.s;
-    p.key = st.key;
-    p.z = st.z;
+    p.zsel = st.zsel;
     p.idx = st.idx;
-    p.pad_ = 0;
-    part[static_cast<size_t>(row) * n_tiles + 2 * blockIdx.y + half] = p;
-    if (mode == kForced && st.has_t) tgt_z[row] = st.tz;
+    p.pad0 = p.pad1 = 0.f;
+    part[static_cast<size_t>(row) * n_tiles + 2 * (b0 / 256) + half] = p;
+    if (MODE == kForced && st.has_t) tgt_z[row] = st.tz;
   }
 };
 

@@ -107,9 +107,10 @@ def test_vocab_forced_and_greedy(lib, M, V, K):
     assert (lp - lsm.gather(1, tok.long()[:, None])[:, 0]).abs().max().item() < 2e-3
 
 
-def test_vocab_sample_matches_philox_oracle(lib):
-    from model_oracle import gumbel_noise
-    M, V, K = 6, 3000, 256
+def test_vocab_sample_matches_two_level_oracle(lib):
+    """Exact two-level sampling: same Philox draws, same fp32 walk order as the oracle."""
+    from model_oracle import sample_token
+    M, V, K = 12, 3000, 256
     X = rand_bf16(M, K, seed=10)
     W = rand_bf16(V, K, scale=3 * K ** -0.5, seed=11)
     sid = torch.arange(M, device="cuda", dtype=torch.int32) * 7 + 3
@@ -121,14 +122,36 @@ def test_vocab_sample_matches_philox_oracle(lib):
     ok(lib, lib.fp_k_vocab(ptr(X), M, K, ptr(W), V, 2, inv_t, None, ptr(sid), ptr(stp), seed, ptr(tok), ptr(lp),
                            stream()))
     torch.cuda.synchronize()
-    z = ((X.float() @ W.float().T) * inv_t).cpu().numpy()
+    logits = (X.float() @ W.float().T)
+    lsm = torch.log_softmax(logits * inv_t, -1)
+    logits = logits.cpu().numpy()
+    agree = 0
     for i in range(M):
-        key = z[i] + gumbel_noise(seed, int(sid[i]), int(stp[i]), V)
-        order = np.argsort(-key)
-        # GPU accumulates logits in a different order: accept the oracle's
-        # choice unless the top-2 keys are within fp32 GEMM noise.
-        if key[order[0]] - key[order[1]] > 1e-3:
-            assert int(tok[i]) == int(order[0])
+        want = sample_token(logits[i], inv_t, seed, int(sid[i]), int(stp[i]))
+        agree += int(want == int(tok[i]))
+        # the reported log-prob is that of the chosen token
+        assert abs(float(lp[i]) - float(lsm[i, int(tok[i])])) < 2e-3
+    # GEMM summation order differs from torch's by fp32 rounding: a boundary
+    # case may flip, nothing more
+    assert agree >= M - 1, agree
+
+
+def test_vocab_sampling_distribution(lib):
+    """Empirical frequencies over many Philox streams follow softmax(z / T)."""
+    M, V, K = 4096, 300, 64
+    X = rand_bf16(1, K, seed=12).repeat(M, 1).contiguous()
+    W = rand_bf16(V, K, scale=6 * K ** -0.5, seed=13)
+    sid = torch.arange(M, device="cuda", dtype=torch.int32)
+    stp = torch.zeros(M, device="cuda", dtype=torch.int32)
+    tok = torch.zeros(M, device="cuda", dtype=torch.int32)
+    lp = torch.zeros(M, device="cuda", dtype=torch.float32)
+    ok(lib, lib.fp_k_vocab(ptr(X), M, K, ptr(W), V, 2, 1.0, None, ptr(sid), ptr(stp), 99, ptr(tok), ptr(lp), stream()))
+    torch.cuda.synchronize()
+    p = torch.softmax(X[0].float() @ W.float().T, -1)
+    freq = torch.bincount(tok.long(), minlength=V).float() / M
+    top = p.topk(5).indices
+    assert (freq[top] - p[top]).abs().max().item() < 0.03
+    assert (freq - p).abs().sum().item() < 0.25
 
 
 def test_add_norm(lib):
