@@ -248,15 +248,18 @@ def main():
     log(f"[bench] rank {rank}: warm-up done")
 
     with Clocks(local) as clk:
-        ms_v, outs_v = timed("fused", True, args.steps, probe=True)
+        ms_v, outs_v = timed("fused", True, args.steps)
     clocks = clk.summary()
     n_total = len(batch)
     value = n_total * args.steps / (ms_v / 1000.0)
     st = outs_v[-1].stats
-    probe_ms = sum(o.stats["attn_probe_ms"] for o in outs_v)
-    probe_bytes = sum(o.stats["attn_probe_bytes"] for o in outs_v)
-    probe_n = sum(o.stats["attn_probe_launches"] for o in outs_v)
     launches = sum(o.stats["gpu_launches"] for o in outs_v)
+    # roofline probe: one more (untimed) step with CUDA events around every
+    # decode-attention launch (eager: the probe disables the step graphs)
+    ms_p, outs_p = timed("fused", True, 1, probe=True)
+    probe_ms = sum(o.stats["attn_probe_ms"] for o in outs_p)
+    probe_bytes = sum(o.stats["attn_probe_bytes"] for o in outs_p)
+    probe_n = sum(o.stats["attn_probe_launches"] for o in outs_p)
 
     e2e = sb = None
     h2d = len(batch) * w.prompt_len * 4 + len(batch) * 4 * 6
@@ -300,7 +303,7 @@ def main():
                      "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
                      "traffic": traffic, "peak_source": src, "launches": probe_n,
                      "bytes_per_launch": probe_bytes / max(probe_n, 1),
-                     "share_of_step": (probe_ms / ms_v) if ms_v else None},
+                     "share_of_step": (probe_ms / ms_p) if ms_p else None},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "stage_barrier": {"value": sb, "unit": UNIT, "speedup_fused": (value / sb) if sb else None},

@@ -99,6 +99,8 @@ int fp_exec_finish(const fp_exec* x, double* finish_seconds, int32_t* finish_ins
 int fp_exec_decision(const fp_exec* x, fp_result** out);
 /* Trigger / plan actually executed (fused, world > 1); moves in application order. */
 int fp_exec_moves(const fp_exec* x, int32_t* n_moves, int32_t* sample, int32_t* from, int32_t* to);
+/* Per decode step of this rank: batch rows and GPU milliseconds (n_steps entries; NULL to query). */
+int fp_exec_steps(const fp_exec* x, int32_t* n_steps, int32_t* rows, float* ms);
 void fp_exec_free(fp_exec* x);
 
 /* ---- single-kernel entry points (device pointers) ---- */
@@ -111,6 +113,14 @@ int fp_k_gemm_splits(int32_t N, int32_t K);
 /* Debug: record 8 globaltimer stamps per CTA of subsequent GEMMs into buf (device, NULL disables). */
 int fp_k_gemm_trace(void* buf);
 int fp_k_gemm_swiglu(const void* Wgu, int32_t F, int32_t K, const void* X, int32_t M, void* out, void* stream);
+/* Decode QKV projection with RoPE and the KV append fused (one kernel):
+ * q_out [M, H, hd] = rope(bf16(X Wqkv^T))[q heads]; K, V of row m -> pool
+ * (layout of fp_k_attn_decode) at token (slot[m], pos[m]) of `layer`.
+ * max_pos: bound on pos (size of the cos/sin table). */
+int fp_k_qkv_rope(const void* Wqkv, int32_t K, const void* X, int32_t M, int32_t H, int32_t KVH, int32_t hd,
+                  const int32_t* pos, int32_t max_pos, float rope_theta, void* pool, int32_t num_layers,
+                  int32_t layer, const int32_t* block_table, int32_t bt_stride, const int32_t* slot, void* q_out,
+                  void* stream);
 /* LM head + token choice: token[M], logp[M]. mode: FP_TOKENS_*; target/sample_id/step: [M] (device). */
 int fp_k_vocab(const void* X, int32_t M, int32_t K, const void* W, int32_t V, int32_t mode, float inv_temp,
                const int32_t* target, const int32_t* sample_id, const int32_t* step, uint64_t seed, int32_t* token,

@@ -93,6 +93,8 @@ struct ExecResult {
   std::vector<int> finish_instance;
   ExperienceBatch experience;       // complete on rank 0 (gathered), local part elsewhere
   ExecStats stats;
+  std::vector<int> step_rows;       // per decode step: batch rows
+  std::vector<float> step_ms;       // per decode step: GPU duration (ms)
 };
 
 class GpuEngine;  // opaque

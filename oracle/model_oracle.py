@@ -240,19 +240,44 @@ def sample_token(logits: np.ndarray, inv_temp: float, seed: int, sid: int, step:
             if acc >= thr:
                 break
         parts.append((m, s, pick))
+    # finalize (gemm.cu vocab_finalize_kernel): lane l of a warp owns the
+    # contiguous half-tiles [l*C, (l+1)*C); lane sums, then lanes in order
     M = max(p[0] for p in parts)
+    n = len(parts)
+    C = (n + 31) // 32
+    chunks = [range(min(n, l * C), min(n, l * C + C)) for l in range(32)]
+
+    def w(t):
+        return np.float32(parts[t][1] * np.exp2(np.float32(parts[t][0] - M)))
+
+    lane_sum = []
+    for ch in chunks:
+        c = np.float32(0)
+        for t in ch:
+            if parts[t][0] != -np.inf:
+                c = np.float32(c + w(t))
+        lane_sum.append(c)
     tot = np.float32(0)
-    for m, s, _ in parts:
-        if m != -np.inf:
-            tot = np.float32(tot + s * np.exp2(np.float32(m - M)))
-    thr = _unit(_philox1(seed, 0xFFFFFFFF, step, sid)) * tot
-    acc = np.float32(0)
+    for c in lane_sum:
+        tot = np.float32(tot + c)
+    thr = np.float32(_unit(_philox1(seed, 0xFFFFFFFF, step, sid)) * tot)
+    acc = base = np.float32(0)
+    pl = -1
+    for l, c in enumerate(lane_sum):
+        base = acc
+        acc = np.float32(acc + c)
+        if acc >= thr and c > 0:
+            pl = l
+            break
+    if pl < 0:
+        pl = 31
+    acc = base
     tok = -1
-    for m, s, idx in parts:
-        if m == -np.inf:
+    for t in chunks[pl]:
+        if parts[t][0] == -np.inf:
             continue
-        acc = np.float32(acc + s * np.exp2(np.float32(m - M)))
-        tok = idx
+        acc = np.float32(acc + w(t))
+        tok = parts[t][2]
         if acc >= thr:
             break
     return tok

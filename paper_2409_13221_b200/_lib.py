@@ -165,6 +165,7 @@ ENGINE_SYMBOLS = {
     "fp_exec_finish": (C.c_int, [_vp, _f64p, _i32p]),
     "fp_exec_decision": (C.c_int, [_vp, P(_vp)]),
     "fp_exec_moves": (C.c_int, [_vp, _i32p, _i32p, _i32p, _i32p]),
+    "fp_exec_steps": (C.c_int, [_vp, _i32p, _i32p, _f32p]),
     "fp_exec_free": (None, [_vp]),
     "fp_k_init_bf16": (C.c_int, [_vp, C.c_int64, C.c_uint64, C.c_uint64, C.c_float, _vp]),
     "fp_k_gemm_bf16": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, C.c_int32, _vp]),
@@ -172,6 +173,8 @@ ENGINE_SYMBOLS = {
     "fp_k_gemm_splits": (C.c_int, [C.c_int32, C.c_int32]),
     "fp_k_gemm_trace": (C.c_int, [_vp]),
     "fp_k_gemm_swiglu": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, _vp]),
+    "fp_k_qkv_rope": (C.c_int, [_vp, C.c_int32, _vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int32,
+                                C.c_float, _vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, _vp, _vp]),
     "fp_k_vocab": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int32, C.c_float, _vp, _vp, _vp,
                              C.c_uint64, _vp, _vp, _vp]),
     "fp_k_add_norm": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, C.c_int32, C.c_int32, _vp]),

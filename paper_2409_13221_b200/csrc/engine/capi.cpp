@@ -299,6 +299,17 @@ int fp_exec_moves(const fp_exec* x, int32_t* n_moves, int32_t* sample, int32_t* 
   });
 }
 
+int fp_exec_steps(const fp_exec* x, int32_t* n_steps, int32_t* rows, float* ms) {
+  return guarded([&] {
+    need(x, "exec");
+    if (n_steps) *n_steps = static_cast<int32_t>(x->r.step_rows.size());
+    for (size_t i = 0; i < x->r.step_rows.size(); ++i) {
+      if (rows) rows[i] = x->r.step_rows[i];
+      if (ms) ms[i] = i < x->r.step_ms.size() ? x->r.step_ms[i] : 0.f;
+    }
+  });
+}
+
 void fp_exec_free(fp_exec* x) { delete x; }
 
 // ---- single kernels ----------------------------------------------------------------
@@ -335,6 +346,25 @@ int fp_k_gemm_swiglu(const void* Wgu, int32_t F, int32_t K, const void* X, int32
     fpk::gemm_swiglu(static_cast<const bf16*>(Wgu), F, K, static_cast<const bf16*>(X), M, static_cast<bf16*>(out),
                      S(stream));
     after_launch();
+  });
+}
+
+int fp_k_qkv_rope(const void* Wqkv, int32_t K, const void* X, int32_t M, int32_t H, int32_t KVH, int32_t hd,
+                  const int32_t* pos, int32_t max_pos, float rope_theta, void* pool, int32_t num_layers,
+                  int32_t layer, const int32_t* block_table, int32_t bt_stride, const int32_t* slot, void* q_out,
+                  void* stream) {
+  return guarded([&] {
+    const size_t layer_bytes = static_cast<size_t>(KVH) * 2 * 64 * hd * 2;
+    fpk::KvPoolView pv{static_cast<uint8_t*>(pool), layer_bytes * num_layers, layer_bytes, 64, block_table,
+                       bt_stride};
+    float2* cs = nullptr;
+    const size_t cb = static_cast<size_t>(max_pos) * (hd / 2) * sizeof(float2);
+    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&cs), cb, S(stream)), "alloc");
+    fpk::rope_table(cs, max_pos, hd, rope_theta, S(stream));
+    fpk::gemm_qkv_rope(static_cast<const bf16*>(Wqkv), K, static_cast<const bf16*>(X), M, H, KVH, hd, pos, cs, pv,
+                       layer, slot, static_cast<bf16*>(q_out), S(stream));
+    after_launch();
+    fpe::check(cudaFreeAsync(cs, S(stream)), "free");
   });
 }
 
@@ -380,9 +410,12 @@ int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t h
     }
     float* work = nullptr;
     const size_t wb = fpk::attn_decode_workspace(B, H, hd, max_ctx) * 4 + 256;
-    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&work), wb, S(stream)), "alloc");
+    const size_t cb = static_cast<size_t>(B) * KVH * 4;
+    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&work), wb + cb, S(stream)), "alloc");
+    int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(work) + wb);
+    fpe::check(cudaMemsetAsync(counters, 0, cb, S(stream)), "memset");
     fpk::attn_decode(static_cast<const bf16*>(q), B, H, KVH, hd, pv, layer, slot, ctx, max_ctx, work,
-                     static_cast<bf16*>(out), S(stream));
+                     static_cast<bf16*>(out), counters, S(stream));
     after_launch();
     fpe::check(cudaFreeAsync(work, S(stream)), "free");
   });

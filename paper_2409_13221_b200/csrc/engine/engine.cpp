@@ -2,6 +2,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -101,13 +102,22 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
     has_kv_map_ = true;
   }
   for (int s = cfg_.max_live - 1; s >= 0; --s) free_slots_.push_back(s);
-  slot_pages_.assign(cfg_.max_live, {});
-  bt_host_.assign(static_cast<size_t>(cfg_.max_live) * max_pages_per_sample_, 0);
+  if (const char* g = std::getenv("FUSEPLAN_DECODE_GRAPHS")) use_graphs_ = std::atoi(g) != 0;  // A/B switch
+  pad_slot_ = cfg_.max_live;  // decode padding rows: block-table row of zeros -> scratch page 0
+  slot_pages_.assign(cfg_.max_live + 1, {});
+  bt_host_.assign(static_cast<size_t>(cfg_.max_live + 1) * max_pages_per_sample_, 0);
   d_block_table_ = static_cast<int*>(dalloc(bt_host_.size() * sizeof(int)));
   FP_CUDA(cudaMemsetAsync(d_block_table_, 0, bt_host_.size() * sizeof(int), s_decode_));
-  d_cur_tok_ = static_cast<int*>(dalloc(cfg_.max_live * sizeof(int)));
+  d_cur_tok_ = static_cast<int*>(dalloc((cfg_.max_live + 1) * sizeof(int)));
+  {  // RoPE (cos, sin) table of the actor for every position the decode step can see
+    const int max_pos = cfg_.max_prompt + cfg_.max_new;
+    const int hd = cfg_.model[kActor].hd;
+    rope_cs_ = static_cast<float2*>(dalloc(static_cast<size_t>(max_pos) * (hd / 2) * sizeof(float2)));
+    fpk::rope_table(rope_cs_, max_pos, hd, cfg_.rope_theta, s_decode_);
+  }
 
-  const size_t hist = static_cast<size_t>(cfg_.max_samples) * cfg_.max_new;
+  // one extra history row: the destination of decode padding rows
+  const size_t hist = static_cast<size_t>(cfg_.max_samples + 1) * cfg_.max_new;
   d_prompts_ = static_cast<int*>(dalloc(static_cast<size_t>(cfg_.max_samples) * cfg_.max_prompt * sizeof(int)));
   d_hist_tok_ = static_cast<int*>(dalloc(hist * sizeof(int)));
   d_hist_logp_ = static_cast<float*>(dalloc(hist * sizeof(float)));
@@ -124,6 +134,7 @@ Engine::~Engine() {
     if (models_[m].blob) cudaFree(models_[m].blob);
   if (exp_blob_) cudaFree(exp_blob_);
   if (scratch_) cudaFree(scratch_);
+  for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
   for (auto& p : probes_) probe_pool_.insert(probe_pool_.end(), {p.a, p.b});
   for (cudaEvent_t e : probe_pool_) cudaEventDestroy(e);
   delete ring_;
@@ -241,7 +252,7 @@ void Engine::alloc_ws() {
   packed(pre_, prefill_cap, false);
   packed(inf_, infer_cap, true);
 
-  const int B = cfg_.max_live;
+  const int B = bucket_of(cfg_.max_live);
   dec_.cap = B;
   dec_.x = static_cast<float*>(dalloc(static_cast<size_t>(B) * maxd * 4));
   dec_.parts = static_cast<float*>(dalloc(static_cast<size_t>(16) * B * maxd * 4));
@@ -256,6 +267,8 @@ void Engine::alloc_ws() {
   const Dims& a = cfg_.model[kActor];
   dec_.attn_work = static_cast<float*>(
       dalloc(fpk::attn_decode_workspace(B, a.H, a.hd, cfg_.max_prompt + cfg_.max_new) * sizeof(float)));
+  dec_.attn_cnt = static_cast<int*>(dalloc(static_cast<size_t>(B) * a.KVH * sizeof(int)));
+  FP_CUDA(cudaMemsetAsync(dec_.attn_cnt, 0, static_cast<size_t>(B) * a.KVH * sizeof(int), s_decode_));
 }
 
 // ---------------------------------------------------------------------------
@@ -433,27 +446,78 @@ void Engine::prefill(const std::vector<PrefillItem>& items) {
   FP_CUDA(cudaGetLastError());
 }
 
+int Engine::bucket_of(int B) {
+  static const int kBuckets[] = {1,  2,  4,  8,   12,  16,  24,  32,  40,  48,  56,  64,
+                                 80, 96, 112, 128, 160, 192, 224, 256, 320, 384, 448, 512};
+  for (int b : kBuckets)
+    if (B <= b) return b;
+  return ((B + 127) / 128) * 128;
+}
+
+// One decode step. Rows are padded to a batch-size bucket (padding rows decode
+// a dummy token into the scratch slot / page / history row) so that the whole
+// step — ~10 kernels per layer with PDL edges — replays as one CUDA graph per
+// (bucket, mode, temperature, seed): host launch cost and inter-kernel gaps
+// vanish. The probe mode (per-launch CUDA events) runs the step eagerly.
 void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed) {
   const int B = static_cast<int>(rows.size());
   if (B == 0) return;
-  if (B > dec_.cap) throw std::invalid_argument("engine: decode batch exceeds max_live");
+  const bool graph = use_graphs_ && !probe_on_;
+  const int Bb = graph ? bucket_of(B) : B;
+  if (Bb > dec_.cap) throw std::invalid_argument("engine: decode batch exceeds max_live");
+  cudaStream_t st = s_decode_;
+  std::vector<int> h(static_cast<size_t>(7) * Bb);
+  int max_ctx = 0;
+  double ctx_sum = 0.0;
+  for (int b = 0; b < Bb; ++b) {
+    const bool pad = b >= B;
+    const DecodeRow r = pad ? DecodeRow{cfg_.max_samples, pad_slot_, 0, 0, 0} : rows[b];
+    h[b] = r.slot;
+    h[Bb + b] = r.pos;
+    h[2 * Bb + b] = r.pos + 1;
+    h[3 * Bb + b] = r.sid * cfg_.max_new + r.step;
+    h[4 * Bb + b] = r.target;
+    h[5 * Bb + b] = r.sid;
+    h[6 * Bb + b] = r.step;
+    max_ctx = std::max(max_ctx, r.pos + 1);
+    if (!pad) ctx_sum += r.pos + 1;
+  }
+  upload(dec_.rows, h.data(), h.size() * 4, st);
+  if (!graph) {
+    decode_kernels(Bb, max_ctx, mode, inv_temp, sample_seed, ctx_sum);
+    return;
+  }
+  const int ctx_cap = cfg_.max_prompt + cfg_.max_new;
+  const GraphKey key{Bb, mode, inv_temp, sample_seed};
+  auto it = graphs_.find(key);
+  if (it == graphs_.end()) {
+    // first sight of this key: run eagerly (sets kernel attributes, builds the
+    // tensor-map cache), capture from the second occurrence on
+    if (!graph_seen_.count(key)) {
+      graph_seen_.insert(key);
+      decode_kernels(Bb, ctx_cap, mode, inv_temp, sample_seed, 0.0);
+      return;
+    }
+    cudaGraph_t g = nullptr;
+    const long long n0 = fpk::launch_count();
+    FP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    decode_kernels(Bb, ctx_cap, mode, inv_temp, sample_seed, 0.0);
+    FP_CUDA(cudaStreamEndCapture(st, &g));
+    const long long nk = fpk::launch_count() - n0;
+    fpk::count_launches(-nk);  // captured, not launched: counted at each replay
+    cudaGraphExec_t ex = nullptr;
+    FP_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    it = graphs_.emplace(key, StepGraph{ex, nk}).first;
+  }
+  FP_CUDA(cudaGraphLaunch(it->second.exec, st));
+  fpk::count_launches(it->second.kernels);
+}
+
+void Engine::decode_kernels(int B, int max_ctx, int mode, float inv_temp, uint64_t sample_seed, double ctx_sum) {
   cudaStream_t st = s_decode_;
   const ModelW& w = models_[kActor];
   const Dims& D = w.dims;
-  std::vector<int> h(static_cast<size_t>(7) * B);
-  int max_ctx = 0;
-  for (int b = 0; b < B; ++b) {
-    const DecodeRow& r = rows[b];
-    h[b] = r.slot;
-    h[B + b] = r.pos;
-    h[2 * B + b] = r.pos + 1;
-    h[3 * B + b] = r.sid * cfg_.max_new + r.step;
-    h[4 * B + b] = r.target;
-    h[5 * B + b] = r.sid;
-    h[6 * B + b] = r.step;
-    max_ctx = std::max(max_ctx, r.pos + 1);
-  }
-  upload(dec_.rows, h.data(), h.size() * 4, st);
   const int* slot = dec_.rows;
   const int* pos = dec_.rows + B;
   const int* ctx = dec_.rows + 2 * B;
@@ -472,19 +536,16 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
     const LayerW& L = w.layers[l];
     fpk::add_norm(dec_.x, nparts ? dec_.parts : nullptr, nparts, stride, L.ln1, dec_.h, B, D.d, nullptr, 0, nullptr,
                   nullptr, st);
-    fpk::gemm_bf16(L.wqkv, D.qkv_width(), D.d, dec_.h, B, dec_.qkv, D.qkv_width(), st);
-    fpk::rope_qkv(dec_.qkv, B, D.H, D.KVH, D.hd, pos, cfg_.rope_theta, dec_.q, nullptr, nullptr, &pv, l, slot, st);
+    fpk::gemm_qkv_rope(L.wqkv, D.d, dec_.h, B, D.H, D.KVH, D.hd, pos, rope_cs_, pv, l, slot, dec_.q, st);
     if (probe_on_) {
       ProbeRec pr{probe_event(), probe_event(), 0.0};
       const double kv_tok = 2.0 * D.KVH * D.hd * 2.0;  // K + V of one layer, bf16
-      double ctx_sum = 0.0;
-      for (int b = 0; b < B; ++b) ctx_sum += h[2 * B + b];
       pr.bytes = ctx_sum * kv_tok + static_cast<double>(B) * D.H * D.hd * 2.0;
-      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, max_ctx, dec_.attn_work, dec_.attn, st, pr.a,
+      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, max_ctx, dec_.attn_work, dec_.attn, dec_.attn_cnt, st, pr.a,
                        pr.b);
       probes_.push_back(pr);
     } else {
-      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, max_ctx, dec_.attn_work, dec_.attn, st);
+      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, max_ctx, dec_.attn_work, dec_.attn, dec_.attn_cnt, st);
     }
     fpk::gemm_f32_splitk(L.wo, D.d, D.H * D.hd, dec_.attn, B, dec_.parts, so, st);
     fpk::add_norm(dec_.x, dec_.parts, so, stride, L.ln2, dec_.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
@@ -495,8 +556,8 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
   fpk::add_norm(dec_.x, dec_.parts, nparts, stride, w.lnf, dec_.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
   fpk::gemm_vocab(dec_.h, B, D.d, w.head, D.V, mode, inv_temp, target, sid, step, sample_seed, dec_.vocab_part,
                   dec_.tgt_z, st);
-  fpk::vocab_finalize(dec_.vocab_part, dec_.tgt_z, B, D.V, mode, target, sid, step, sample_seed, nullptr, nullptr, dst, d_hist_tok_,
-                      d_hist_logp_, slot, d_cur_tok_, st);
+  fpk::vocab_finalize(dec_.vocab_part, dec_.tgt_z, B, D.V, mode, target, sid, step, sample_seed, nullptr, nullptr, dst,
+                      d_hist_tok_, d_hist_logp_, slot, d_cur_tok_, st);
   FP_CUDA(cudaGetLastError());
 }
 

@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -126,6 +128,8 @@ class Engine {
   // One decode step for `rows`: writes hist[sid][step] (token, logp) and the
   // next input token. mode 0 forced (target), 1 greedy, 2 sample.
   void decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed);
+  void set_use_graphs(bool on) { use_graphs_ = on; }
+  static int bucket_of(int B);
 
   // ---- scoring (infer stream) ------------------------------------------------------
   struct InferItem {
@@ -177,6 +181,26 @@ class Engine {
     double bytes;
   };
   bool probe_on_ = false;
+  bool use_graphs_ = true;
+  int pad_slot_ = 0;
+  struct GraphKey {
+    int B, mode;
+    float inv_temp;
+    uint64_t seed;
+    bool operator<(const GraphKey& o) const {
+      if (B != o.B) return B < o.B;
+      if (mode != o.mode) return mode < o.mode;
+      if (inv_temp != o.inv_temp) return inv_temp < o.inv_temp;
+      return seed < o.seed;
+    }
+  };
+  struct StepGraph {
+    cudaGraphExec_t exec;
+    long long kernels;  // launches the graph replays (gpu_launches accounting)
+  };
+  std::map<GraphKey, StepGraph> graphs_;
+  std::set<GraphKey> graph_seen_;
+  void decode_kernels(int B, int max_ctx, int mode, float inv_temp, uint64_t sample_seed, double ctx_sum);
   uint64_t prompts_tag_ = 0;
   CUtensorMap kv_map_{};
   bool has_kv_map_ = false;
@@ -206,6 +230,7 @@ class Engine {
   struct DecodeWs {
     int cap = 0;
     float *x = nullptr, *parts = nullptr, *attn_work = nullptr;
+    int* attn_cnt = nullptr;  // split-merge tickets of the decode attention (B x KVH, kept zero)
     bf16 *h = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
     int* rows = nullptr;  // 7 x cap: slot, pos, ctx, dst, target, sid, step
     void* vocab_part = nullptr;
@@ -229,6 +254,7 @@ class Engine {
   std::vector<int> bt_host_;
   int* d_block_table_ = nullptr;
   int* d_cur_tok_ = nullptr;
+  float2* rope_cs_ = nullptr;
   // batch
   int* d_prompts_ = nullptr;
   int* d_hist_tok_ = nullptr;

@@ -497,6 +497,7 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
     for (Live& l : live) ++l.gen;
     res.stats.decode_steps += 1;
     res.stats.decode_rows += static_cast<int64_t>(rows.size());
+    res.step_rows.push_back(static_cast<int>(rows.size()));
     res.stats.decode_ctx_tokens += ctx;
     // bound host run-ahead
     const int k = static_cast<int>(step_end.size()) - 1 - opts.run_ahead;
@@ -659,7 +660,11 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
   // ---- stats ------------------------------------------------------------------------------
   res.stats.gen_seconds = step_end.empty() ? 0.0 : ms_between(ev_start, step_end.back()) * 1e-3;
   double dec_ms = 0.0;
-  for (size_t k = 0; k < step_end.size(); ++k) dec_ms += ms_between(step_begin[k], step_end[k]);
+  res.step_ms.resize(step_end.size());
+  for (size_t k = 0; k < step_end.size(); ++k) {
+    res.step_ms[k] = ms_between(step_begin[k], step_end[k]);
+    dec_ms += res.step_ms[k];
+  }
   res.stats.decode_gpu_seconds = dec_ms * 1e-3;
   res.stats.infer_busy_seconds = infer_ms * 1e-3;
   res.finish_wall.assign(n, -1.0);

@@ -214,18 +214,8 @@ __global__ void attn_decode_combine_kernel(const float* __restrict__ part_o, con
   const int bh = blockIdx.x;
   const int b = bh / H;
   const int ns = (ctx[b] + kChunk - 1) / kChunk;
-  const size_t base = static_cast<size_t>(bh) * nsplit_max;
-  float M = -INFINITY;
-  for (int s = 0; s < ns; ++s) M = fmaxf(M, part_ml[(base + s) * 2]);
-  for (int d = threadIdx.x; d < HD; d += blockDim.x) {
-    float L = 0.f, O = 0.f;
-    for (int s = 0; s < ns; ++s) {
-      const float f = exp2f(part_ml[(base + s) * 2] - M);
-      L += part_ml[(base + s) * 2 + 1] * f;
-      O += part_o[(base + s) * HD + d] * f;
-    }
-    out[static_cast<size_t>(bh) * HD + d] = __float2bfloat16_rn(O / L);
-  }
+  combine_row(part_o, part_ml, static_cast<size_t>(bh) * nsplit_max, ns, HD, threadIdx.x, blockDim.x,
+              out + static_cast<size_t>(bh) * HD);
 }
 
 // ---------------------------------------------------------------------------
@@ -454,7 +444,8 @@ size_t attn_decode_workspace(int B, int H, int hd, int max_ctx) {
 }
 
 void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer, const int* slot,
-                 const int* ctx, int max_ctx, float* work, bf16* out, cudaStream_t st, cudaEvent_t probe_begin,
+                 const int* ctx, int max_ctx, float* work, bf16* out, int* counters, cudaStream_t st,
+                 cudaEvent_t probe_begin,
                  cudaEvent_t probe_end) {
   if (B <= 0) return;
   if (probe_begin) cudaEventRecord(probe_begin, st);
@@ -463,7 +454,9 @@ void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView&
   const int G = H / KVH;
 #define FP_DEC(HD_, G_) \
   if (hd == HD_ && G == G_) { launch_decode<HD_, G_>(q, B, H, KVH, pool, layer, slot, ctx, ns, work, st); } else
-  if (attn_decode_mma(q, B, H, KVH, hd, pool, layer, slot, ctx, ns, work, st)) {
+  if (attn_decode_mma(q, B, H, KVH, hd, pool, layer, slot, ctx, ns, work, out, counters, st)) {
+    if (probe_end) cudaEventRecord(probe_end, st);
+    return;  // splits merged in-kernel
   } else FP_DEC(32, 1) FP_DEC(64, 1) FP_DEC(128, 1) FP_DEC(64, 4) FP_DEC(128, 4) FP_DEC(128, 8) FP_DEC(64, 8) {
     throw std::invalid_argument("attn_decode: unsupported (head_dim, group) combination");
   }

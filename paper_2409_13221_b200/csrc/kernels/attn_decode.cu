@@ -9,7 +9,8 @@
 // read once per group), online softmax in registers; ldmatrix addresses apply
 // the TMA swizzle (16-byte chunk c of row r lives at chunk c ^ (r & 7)), so
 // fragment loads are bank-conflict free. Warps merge through shared memory;
-// splits merge in attn_decode_combine_kernel. Split boundaries depend on the
+// the last split of a (sample, kv head) to finish merges the splits (an atomic
+// ticket per pair; single-split items normalise in place). Split boundaries depend on the
 // position only (batch-independent results). HBM-bound: every K/V byte of the
 // visible context is read exactly once per launch.
 #include <math.h>
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
     const __grid_constant__ CUtensorMap kv_map, const bf16* __restrict__ q, const int* __restrict__ block_table,
     int bt_stride, int rows_per_page, int layer_rows, int layer, const int* __restrict__ slot,
     const int* __restrict__ ctx, int B, int H, int KVH, int nsplit_max, float scale_log2,
-    float* __restrict__ part_o, float* __restrict__ part_ml) {
+    float* __restrict__ part_o, float* __restrict__ part_ml, bf16* __restrict__ out, int* __restrict__ counters) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   using C = DecCfg<HD>;
   static_assert(G <= 8, "GQA group must fit the first 8 MMA rows");
@@ -261,14 +262,40 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
     // advance the consume cursor; flush the item's partial when it ends
     ++cur.u;
     if (cur.u >= cur.ue) {
-      if (r0 < G) {
-        const size_t pb = (static_cast<size_t>(b) * H + kvh * G + r0) * nsplit_max + split;
-        float* po = part_o + pb * HD + 2 * (lane & 3);
+      const int nsb = (ctx[b] + kDecodeChunk - 1) / kDecodeChunk;  // non-empty splits of this sample
+      const size_t row0 = static_cast<size_t>(b) * H + kvh * G;
+      if (nsb == 1) {
+        // single split: the combine is the identity (f = 1), normalise here
+        if (r0 < G) {
+          bf16* og = out + (row0 + r0) * HD + 2 * (lane & 3);
 #pragma unroll
-        for (int dn = 0; dn < HD / 8; ++dn) *reinterpret_cast<float2*>(po + dn * 8) = make_float2(o[dn][0], o[dn][1]);
-        if ((lane & 3) == 0) {
-          part_ml[pb * 2] = m_run;
-          part_ml[pb * 2 + 1] = l_run;
+          for (int dn = 0; dn < HD / 8; ++dn)
+            *reinterpret_cast<__nv_bfloat162*>(og + dn * 8) =
+                __floats2bfloat162_rn(__fdiv_rn(o[dn][0], l_run), __fdiv_rn(o[dn][1], l_run));
+        }
+      } else {
+        if (r0 < G) {
+          const size_t pb = (row0 + r0) * nsplit_max + split;
+          float* po = part_o + pb * HD + 2 * (lane & 3);
+#pragma unroll
+          for (int dn = 0; dn < HD / 8; ++dn)
+            *reinterpret_cast<float2*>(po + dn * 8) = make_float2(o[dn][0], o[dn][1]);
+          if ((lane & 3) == 0) {
+            part_ml[pb * 2] = m_run;
+            part_ml[pb * 2 + 1] = l_run;
+          }
+        }
+        // the last split of (sample, kv head) to finish merges all of them
+        __threadfence();
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) last = atomicAdd(&counters[b * KVH + kvh], 1) == nsb - 1;
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          if (lane == 0) counters[b * KVH + kvh] = 0;  // ready for the next launch
+          __threadfence();
+          for (int g = 0; g < G; ++g) combine_row(part_o, part_ml, (row0 + g) * nsplit_max, nsb, HD, lane, 32,
+                                                  out + (row0 + g) * HD);
         }
       }
       normalise(cur);
@@ -278,7 +305,7 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
 
 template <int HD, int G>
 void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
-            const int* slot, const int* ctx, int nsplit, float* work, cudaStream_t st) {
+            const int* slot, const int* ctx, int nsplit, float* work, bf16* out, int* counters, cudaStream_t st) {
   using C = DecCfg<HD>;
   static bool attr = false;
   if (!attr) {
@@ -294,19 +321,20 @@ void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const 
   const int grid = std::max(1, std::min(148, (items + C::kWarps - 1) / C::kWarps));
   attn_decode_mma_kernel<HD, G><<<grid, C::kWarps * 32, C::kSmem, st>>>(
       map, q, pool.block_table, pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, B, H, KVH, nsplit,
-      scale, part_o, part_ml);
+      scale, part_o, part_ml, out, counters);
   count_launch();
 }
 
 }  // namespace
 
 bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer,
-                     const int* slot, const int* ctx, int nsplit, float* work, cudaStream_t st) {
-  if (!pool.kv_map) return false;
+                     const int* slot, const int* ctx, int nsplit, float* work, bf16* out, int* counters,
+                     cudaStream_t st) {
+  if (!pool.kv_map || !counters) return false;
   const int G = H / KVH;
 #define FP_MMA(HD_, G_)                                                                            \
   if (hd == HD_ && G == G_) {                                                                      \
-    launch<HD_, G_>(*pool.kv_map, q, B, H, KVH, pool, layer, slot, ctx, nsplit, work, st);        \
+    launch<HD_, G_>(*pool.kv_map, q, B, H, KVH, pool, layer, slot, ctx, nsplit, work, out, counters, st);      \
     return true;                                                                                   \
   }
   FP_MMA(64, 1) FP_MMA(128, 1) FP_MMA(64, 4) FP_MMA(128, 4) FP_MMA(128, 8) FP_MMA(64, 8)

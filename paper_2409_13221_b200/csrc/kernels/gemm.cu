@@ -97,7 +97,7 @@ unsigned long long* g_trace = nullptr;
 template <int BN, class Epi>
 void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int splits, const Epi& epi,
             cudaStream_t st, bool weight_is_a = true) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, EpiStages<Epi>::value>;
   if (K % kBK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
   if (a_rows <= 0 || b_rows <= 0) return;
   static bool attr_set = false;
@@ -133,13 +133,27 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
   fpk::count_launch();
 }
 
+// Batch-tile width of a swap-AB GEMM with `a_ctas` weight tiles (x splits):
+// the widest BN that still yields >= 128 CTAs, else the narrowest that covers
+// the rows. Decode GEMMs stream weights, so filling the SMs matters more than
+// the L2 re-reads of narrower tiles; a row's bits do not depend on BN (each
+// output element is one tensor-core dot product in the same K order).
+int pick_bn(int M, int a_ctas) {
+  static const int kBN[] = {256, 128, 64, 32, 16};
+  for (int bn : kBN)
+    if (a_ctas * ((M + bn - 1) / bn) >= 128) return bn;
+  return 16;
+}
+
 template <class Epi, class F>
-void dispatch_bn(int M, F&& f) {
-  if (M <= 16) f.template operator()<16>();
-  else if (M <= 32) f.template operator()<32>();
-  else if (M <= 64) f.template operator()<64>();
-  else if (M <= 128) f.template operator()<128>();
-  else f.template operator()<256>();
+void dispatch_bn(int M, int a_ctas, F&& f) {
+  switch (pick_bn(M, a_ctas)) {
+    case 16: f.template operator()<16>(); break;
+    case 32: f.template operator()<32>(); break;
+    case 64: f.template operator()<64>(); break;
+    case 128: f.template operator()<128>(); break;
+    default: f.template operator()<256>(); break;
+  }
 }
 
 }  // namespace
@@ -172,7 +186,7 @@ int gemm_splits(int N, int K) {
 
 void gemm_bf16(const bf16* W, int N, int K, const bf16* X, int M, bf16* out, int ld_out, cudaStream_t st) {
   if ((ld_out * 2) % 16) throw std::invalid_argument("gemm_bf16: ld_out must be a multiple of 8");
-  dispatch_bn<EpiStoreBF16>(M, [&]<int BN>() {
+  dispatch_bn<EpiStoreBF16>(M, (N + 127) / 128, [&]<int BN>() {
     EpiStoreBF16 e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, ld_out, 128, BN)};
     launch<BN>(W, N, X, M, K, 1, e, st);
   });
@@ -184,7 +198,7 @@ void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* o
   splits = std::max(1, std::min(splits, kb));
   const int per = (kb + splits - 1) / splits;
   const int z = (kb + per - 1) / per;
-  dispatch_bn<EpiStoreF32>(M, [&]<int BN>() {
+  dispatch_bn<EpiStoreF32>(M, (N + 127) / 128 * z, [&]<int BN>() {
     const uint64_t dims[3] = {static_cast<uint64_t>(N), static_cast<uint64_t>(M), static_cast<uint64_t>(z)};
     const uint64_t str[2] = {static_cast<uint64_t>(N) * 4, static_cast<uint64_t>(M) * N * 4};
     const uint32_t box[3] = {128u, static_cast<uint32_t>(BN), 1u};
@@ -195,7 +209,7 @@ void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* o
 
 void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float* resid, cudaStream_t st) {
   if (N % 4) throw std::invalid_argument("gemm_f32: N must be a multiple of 4");
-  dispatch_bn<EpiStoreF32>(M, [&]<int BN>() {
+  dispatch_bn<EpiStoreF32>(M, (N + 127) / 128, [&]<int BN>() {
     EpiStoreF32 e{out_map_2d(resid, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, N, N, 128, BN), 1};
     launch<BN>(W, N, X, M, K, 1, e, st);
   });
@@ -203,9 +217,21 @@ void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float*
 
 void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
   if (F % 64) throw std::invalid_argument("gemm_swiglu: F must be a multiple of 64");
-  dispatch_bn<int>(M, [&]<int BN>() {
+  dispatch_bn<int>(M, (2 * F + 127) / 128, [&]<int BN>() {
     EpiSwiGLU<BN> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, BN)};
     launch<BN>(Wgu, 2 * F, X, M, K, 1, e, st);
+  });
+}
+
+void gemm_qkv_rope(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH, int hd, const int* pos,
+                   const float2* cs, const KvPoolView& pool, int layer, const int* slot, bf16* q_out,
+                   cudaStream_t st) {
+  if (128 % hd != 0) throw std::invalid_argument("gemm_qkv_rope: head_dim must divide 128");
+  const int N = (H + 2 * KVH) * hd;
+  dispatch_bn<int>(M, (N + 127) / 128, [&]<int BN>() {
+    EpiRopeKV<BN> e{q_out, pool, slot, pos, cs, layer, H, KVH, hd, M};
+    e.pool.kv_map = nullptr;  // host pointer: not dereferenced on the device
+    launch<BN>(Wqkv, N, X, M, K, 1, e, st);
   });
 }
 
@@ -245,21 +271,25 @@ __global__ void vocab_finalize_kernel(const VocabPartial* __restrict__ part, con
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
   const VocabPartial* p = part + static_cast<size_t>(row) * n_tiles;
+  // lane l owns the contiguous half-tiles [t0, t1); the mass is summed in
+  // that fixed order (per lane, then lane 0..31 sequentially) so the oracle
+  // (model_oracle.sample_token) replays it bit-for-bit
+  const int chunk = (n_tiles + 31) / 32;
+  const int t0 = min(n_tiles, lane * chunk), t1 = min(n_tiles, t0 + chunk);
   float m = -INFINITY;
-  for (int t = lane; t < n_tiles; t += 32) m = fmaxf(m, p[t].m2);
+  for (int t = t0; t < t1; ++t) m = fmaxf(m, p[t].m2);
   m = warp_max(m);
-  float s = 0.f;
+  float c = 0.f;
   float bz = -INFINITY;
   int bidx = 0x7fffffff;
-  for (int t = lane; t < n_tiles; t += 32) {
+  for (int t = t0; t < t1; ++t) {
     const VocabPartial q = p[t];
-    if (q.m2 > -INFINITY) s += q.s * exp2f(q.m2 - m);
+    if (q.m2 > -INFINITY) c += __fmul_rn(q.s, exp2f(q.m2 - m));  // no FMA contraction: oracle order
     if (mode == kGreedy && q.idx >= 0 && (q.zsel > bz || (q.zsel == bz && q.idx < bidx))) {
       bz = q.zsel;
       bidx = q.idx;
     }
   }
-  s = warp_sum(s);
   if (mode == kGreedy) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -271,10 +301,21 @@ __global__ void vocab_finalize_kernel(const VocabPartial* __restrict__ part, con
       }
     }
   }
-  if (lane != 0) return;
-  const float lse = m * kLn2 + logf(s);  // natural-log logsumexp of z
-  int tok;
-  float lp;
+  float thr = 0.f;
+  if (mode == kSample) {
+    const U4 w = philox4x32_10(U4{kRowDraw, static_cast<uint32_t>(step[row]), static_cast<uint32_t>(sample_id[row]),
+                                  0xF00Du},
+                               seed_lo, seed_hi);
+    thr = unit_open(w.x);
+  }
+  // tot = sum of the lane sums in lane order; the picked lane is the first
+  // whose running sum reaches thr * tot (same in every lane)
+  float tot = 0.f;
+#pragma unroll
+  for (int l = 0; l < 32; ++l) tot += __shfl_sync(0xffffffffu, c, l);
+  const float lse = m * kLn2 + logf(tot);  // natural-log logsumexp of z
+  int tok = 0;
+  float lp = 0.f;
   if (mode == kForced) {
     tok = target[row];
     lp = tgt_z[row] - lse;
@@ -282,25 +323,32 @@ __global__ void vocab_finalize_kernel(const VocabPartial* __restrict__ part, con
     tok = bidx;
     lp = bz - lse;
   } else {
-    // half-tile choice: inverse CDF of s_t 2^(m2_t - M2), sequential in t
-    float tot = 0.f;
-    for (int t = 0; t < n_tiles; ++t)
-      if (p[t].m2 > -INFINITY) tot += p[t].s * exp2f(p[t].m2 - m);
-    const U4 w = philox4x32_10(U4{kRowDraw, static_cast<uint32_t>(step[row]), static_cast<uint32_t>(sample_id[row]),
-                                  0xF00Du},
-                               seed_lo, seed_hi);
-    const float thr = unit_open(w.x) * tot;
-    float acc = 0.f;
+    thr *= tot;
+    float acc = 0.f, base = 0.f;
+    int pl = -1;
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      const float cl = __shfl_sync(0xffffffffu, c, l);
+      if (pl < 0) {
+        base = acc;
+        acc += cl;
+        if (acc >= thr && cl > 0.f) pl = l;
+      }
+    }
+    if (pl < 0) pl = 31;  // unreachable: acc == tot >= thr
+    if (lane != pl) return;
     int pick = -1;
-    for (int t = 0; t < n_tiles; ++t) {
+    acc = base;
+    for (int t = t0; t < t1; ++t) {
       if (p[t].m2 == -INFINITY) continue;
-      acc += p[t].s * exp2f(p[t].m2 - m);
+      acc += __fmul_rn(p[t].s, exp2f(p[t].m2 - m));
       pick = t;
       if (acc >= thr) break;
     }
     tok = p[pick].idx;
     lp = p[pick].zsel - lse;
   }
+  if (mode != kSample && lane != 0) return;
   if (token) token[row] = tok;
   if (logp) logp[row] = lp;
   if (dst) {

@@ -5,16 +5,20 @@
 // One CTA owns a 128 x BN tile of D (UMMA M=128, N=BN), loops over a K range
 // of 64-element blocks (one 128-byte swizzle atom) through an S-stage
 // TMA -> shared-memory ring, and hands the TMEM accumulator to an epilogue
-// functor. Warp roles (192 threads):
+// functor. Warp roles (320 threads):
 //   warp 0      TMA producer (one elected lane)
 //   warp 1      TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> registers -> Epi
+//   warps 2..9  epilogue: tcgen05.ld 32x32b.x32 -> registers -> Epi; warp w
+//               reads TMEM lane quarter w & 3, column half (w - 2) >> 2
 // Which operand is the weight is the caller's choice: "swap-AB" (A = weight,
 // B = activations) puts output features on TMEM lanes, which is what the
 // decode GEMMs (batch on N <= 256) and the SwiGLU epilogue want; the vocab
 // epilogue uses A = activations so that one thread owns one token row.
 #pragma once
 
+#include <type_traits>
+
+#include "ops.h"
 #include "ptx.cuh"
 
 namespace fpk {
@@ -25,14 +29,26 @@ constexpr int kEpiWarps = 8;             // two per TMEM lane quarter (interleav
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr int kSmemBudget = 200 * 1024;
 
-template <int BN>
+// STAGES = 0: as deep as the budget allows (the decode mainloop is latency-
+// bound); an epilogue may pin a shallower ring (Epi::kStages) so that two CTAs
+// share an SM and one's epilogue overlaps the other's mainloop.
+template <int BN, int STAGES = 0>
 struct GemmCfg {
   static constexpr int kTileB = BN * kBK * 2;
   static constexpr int kStageBytes = kTileA + kTileB;
   static constexpr int kFit = kSmemBudget / kStageBytes;
-  static constexpr int kStages = kFit > 8 ? 8 : kFit;  // deep ring: the decode mainloop is latency-bound
+  static constexpr int kStages = STAGES > 0 ? STAGES : (kFit > 8 ? 8 : kFit);
   static constexpr int kSmem = kStages * kStageBytes + 1024;  // + alignment slack
   static constexpr uint32_t kTmemCols = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+};
+
+template <class E, class = void>
+struct EpiStages {
+  static constexpr int value = 0;
+};
+template <class E>
+struct EpiStages<E, std::void_t<decltype(E::kStages)>> {
+  static constexpr int value = E::kStages;
 };
 
 struct GemmGeom {
@@ -95,7 +111,7 @@ template <int BN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const GemmGeom g, const __grid_constant__ Epi epi) {
-  using C = GemmCfg<BN>;
+  using C = GemmCfg<BN, EpiStages<Epi>::value>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full_bar[C::kStages];
@@ -305,6 +321,87 @@ struct EpiSwiGLU {
   }
   __device__ void finish(State&, int, int, int, int, int) const {}
   __device__ void store(const uint8_t* smem, int a0, int b0, int) const { tma_store_2d(&map, smem, a0 / 2, b0); }
+};
+
+// Decode QKV projection with RoPE + KV-cache append (swap-AB: tile rows = 128
+// qkv features a0.., columns = batch rows b0..). The tile is staged as bf16 —
+// the rounding of the unfused qkv output — then, after one barrier, the 256
+// epilogue threads rotate pairs (i, i + hd/2) of every head in the tile with
+// the position's (cos, sin) from the rope table and write q rows to q_out and
+// the new token's K / V straight into its pool page. A warp covers the i of
+// one (row, head), so every global store is a contiguous 64-byte run.
+template <int BN>
+struct EpiRopeKV {
+  __nv_bfloat16* q_out;
+  KvPoolView pool;
+  const int* slot;
+  const int* pos;
+  const float2* cs;
+  int layer, H, KVH, hd, M;
+  static constexpr bool kTmaStore = false;
+  static constexpr int kPasses = 1;
+  template <class S> __device__ void next_pass(S&, int, int, int, int) const {}
+  struct State {
+    uint8_t* smem;
+  };
+  __device__ void operator()(State& st, uint8_t* smem, int, int, int, int r, int, int c0,
+                             const float (&v)[32]) const {
+    st.smem = smem;
+    __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) tile[(c0 + j) * 128 + r] = f2bf(v[j]);
+  }
+  __device__ void finish(State& st, int a0, int b0, int, int, int) const {
+    epi_bar_sync();
+    const __nv_bfloat16* tile = reinterpret_cast<const __nv_bfloat16*>(st.smem);
+    const int ew = (threadIdx.x >> 5) - 2;  // epilogue warp 0..7: columns ew, ew + 8, ...
+    const int lane = threadIdx.x & 31;
+    const int hh = hd >> 1;
+    const int nb = min(BN, M - b0);
+    __nv_bfloat16* pool_base = reinterpret_cast<__nv_bfloat16*>(pool.base);
+    // lane j fetches position and page of the warp's j-th column once
+    int pj = 0, pagej = 0;
+    {
+      const int bl = ew + 8 * lane;
+      if (bl < nb) {
+        pj = pos[b0 + bl];
+        pagej = pool.block_table[slot[b0 + bl] * pool.bt_stride + pj / pool.page_tokens];
+      }
+    }
+    const int ncol = (nb - ew + 7) >> 3;  // columns of this warp
+    for (int k = 0; k < ncol; ++k) {
+      const int bl = ew + 8 * k;
+      const int b = b0 + bl;
+      const int p = __shfl_sync(0xffffffffu, pj, k);
+      const int page = __shfl_sync(0xffffffffu, pagej, k);
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2) {  // 64 pairs per column: lane, lane + 32
+        const int pr = lane + 32 * k2;
+        const int i = pr % hh;
+        const int fl = (pr / hh) * hd + i;  // tile-local feature of the pair's low element
+        const int head = (a0 + fl) / hd;    // [0, H) q, [H, H + KVH) k, then v
+        __nv_bfloat16 o1 = tile[bl * 128 + fl], o2 = tile[bl * 128 + fl + hh];
+        if (head < H + KVH) {
+          const float2 c = cs[p * hh + i];
+          float r1, r2;
+          rope_pair(__bfloat162float(o1), __bfloat162float(o2), c.x, c.y, r1, r2);
+          o1 = f2bf(r1);
+          o2 = f2bf(r2);
+        }
+        __nv_bfloat16* dst;
+        if (head < H) {
+          dst = q_out + (static_cast<size_t>(b) * H + head) * hd;
+        } else {
+          const bool is_v = head >= H + KVH;
+          const int kh = head - H - (is_v ? KVH : 0);
+          dst = pool_base + kv_elem_offset(pool, page, layer, kh, hd, p % pool.page_tokens, is_v);
+        }
+        dst[i] = o1;
+        dst[i + hh] = o2;
+      }
+    }
+  }
+  __device__ void store(const uint8_t*, int, int, int) const {}
 };
 
 }  // namespace fpk

@@ -14,6 +14,7 @@ namespace fpk {
 
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 namespace {
@@ -145,13 +146,6 @@ __global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__
   }
 }
 
-__device__ __forceinline__ size_t kv_elem_offset(const KvPoolView& p, int page, int layer, int kvh, int hd, int tok,
-                                                 bool is_v) {
-  const size_t head_elems = static_cast<size_t>(2) * p.page_tokens * hd;
-  return (static_cast<size_t>(page) * p.page_bytes + static_cast<size_t>(layer) * p.layer_bytes) / 2 +
-         kvh * head_elems + (is_v ? static_cast<size_t>(p.page_tokens) * hd : 0) + static_cast<size_t>(tok) * hd;
-}
-
 // grid: M rows; block: 128. Rotate-half RoPE (pairs i, i + HD/2); cos/sin of
 // the row's position are computed once per pair index and shared by all heads.
 template <int HD>
@@ -185,8 +179,10 @@ __global__ void rope_qkv_kernel(const bf16* __restrict__ qkv, int H, int KVH, co
     const float cs = cs_s[i], sn = sn_s[i];
     const float x1 = __bfloat162float(in[h * HD + i]);
     const float x2 = __bfloat162float(in[h * HD + i + half]);
-    const bf16 o1 = __float2bfloat16_rn(x1 * cs - x2 * sn);
-    const bf16 o2 = __float2bfloat16_rn(x2 * cs + x1 * sn);
+    float r1, r2;
+    rope_pair(x1, x2, cs, sn, r1, r2);
+    const bf16 o1 = __float2bfloat16_rn(r1);
+    const bf16 o2 = __float2bfloat16_rn(r2);
     if (h < H) {
       bf16* q = q_out + (static_cast<size_t>(m) * H + h) * HD;
       q[i] = o1;
@@ -214,6 +210,18 @@ __global__ void rope_qkv_kernel(const bf16* __restrict__ qkv, int H, int KVH, co
     if (use_pool)
       *reinterpret_cast<uint32_t*>(pool_base + kv_elem_offset(pool, page, layer, kh, HD, in_page, true) + j) = v;
   }
+}
+
+template <int HD>
+__global__ void rope_table_kernel(float2* tab, int max_pos, float log2_theta) {
+  constexpr int half = HD / 2;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= max_pos * half) return;
+  const int p = idx / half, i = idx % half;
+  const float inv_freq = exp2f(-(2.0f * i / HD) * log2_theta);  // the expression of rope_qkv_kernel
+  float sn, cs;
+  sincosf(static_cast<float>(p) * inv_freq, &sn, &cs);
+  tab[idx] = make_float2(cs, sn);
 }
 
 __global__ void scatter_int_kernel(const int* __restrict__ idx, const int* __restrict__ val, int n,
@@ -322,6 +330,18 @@ void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, fl
     case 64: rope_qkv_kernel<64><<<M, 128, 0, st>>>(qkv, H, KVH, pos, l2, q_out, k_out, v_out, pv, up, layer, slot); break;
     case 128: rope_qkv_kernel<128><<<M, 128, 0, st>>>(qkv, H, KVH, pos, l2, q_out, k_out, v_out, pv, up, layer, slot); break;
     default: throw std::invalid_argument("rope_qkv: head_dim must be 32, 64 or 128");
+  }
+  fpk::count_launch();
+}
+
+void rope_table(float2* tab, int max_pos, int hd, float rope_theta, cudaStream_t st) {
+  const float l2 = log2f(rope_theta);
+  const int n = max_pos * hd / 2;
+  switch (hd) {
+    case 32: rope_table_kernel<32><<<(n + 255) / 256, 256, 0, st>>>(tab, max_pos, l2); break;
+    case 64: rope_table_kernel<64><<<(n + 255) / 256, 256, 0, st>>>(tab, max_pos, l2); break;
+    case 128: rope_table_kernel<128><<<(n + 255) / 256, 256, 0, st>>>(tab, max_pos, l2); break;
+    default: throw std::invalid_argument("rope_table: head_dim must be 32, 64 or 128");
   }
   fpk::count_launch();
 }

@@ -14,6 +14,7 @@ using bf16 = __nv_bfloat16;
 
 // Number of kernels this library has launched (all launchers count).
 void count_launch();
+void count_launches(long long n);  // graph replays: the kernels the graph holds
 long long launch_count();
 
 // ---- GEMMs (tcgen05; gemm.cu) --------------------------------------------------
@@ -86,14 +87,62 @@ struct KvPoolView {
   int bt_stride;          // max_pages
   const CUtensorMap* kv_map = nullptr;  // host copy: 2-D TMA view of the pool (make_kv_map), hd 64/128
 };
+#ifdef __CUDACC__
+#include <math.h>
+// Merge ns context splits of one (sample, head) row: partial o [ns][HD]
+// (unnormalised) and (m, l) pairs at part_*[base ..]; threads t, t + nt, ...
+// of the caller write out[d]. Shared by the combine kernel and the fused
+// last-split merge, with explicit roundings, so both give the same bits
+// (one split: f = 1 and out = o / l exactly). L2 loads: the partials were
+// written by other SMs.
+__device__ __forceinline__ void combine_row(const float* part_o, const float* part_ml, size_t base, int ns, int HD,
+                                            int t, int nt, __nv_bfloat16* out) {
+  float M = -INFINITY;
+  for (int s = 0; s < ns; ++s) M = fmaxf(M, __ldcg(part_ml + (base + s) * 2));
+  for (int d = t; d < HD; d += nt) {
+    float L = 0.f, O = 0.f;
+    for (int s = 0; s < ns; ++s) {
+      const float f = exp2f(__ldcg(part_ml + (base + s) * 2) - M);
+      L = __fmaf_rn(__ldcg(part_ml + (base + s) * 2 + 1), f, L);
+      O = __fmaf_rn(__ldcg(part_o + (base + s) * HD + d), f, O);
+    }
+    out[d] = __float2bfloat16_rn(__fdiv_rn(O, L));
+  }
+}
+// Element offset of token `tok` of (page, layer, kv head) K (or V) in the pool.
+__device__ __forceinline__ size_t kv_elem_offset(const KvPoolView& p, int page, int layer, int kvh, int hd, int tok,
+                                                 bool is_v) {
+  const size_t head_elems = static_cast<size_t>(2) * p.page_tokens * hd;
+  return (static_cast<size_t>(page) * p.page_bytes + static_cast<size_t>(layer) * p.layer_bytes) / 2 +
+         kvh * head_elems + (is_v ? static_cast<size_t>(p.page_tokens) * hd : 0) + static_cast<size_t>(tok) * hd;
+}
+// Rotate-half RoPE of the pair (x1, x2) = (x[i], x[i + hd/2}) with (cos, sin);
+// explicit roundings (no FMA contraction) so every kernel that rotates agrees
+// bit-for-bit with the others and with the oracle.
+__device__ __forceinline__ void rope_pair(float x1, float x2, float cs, float sn, float& o1, float& o2) {
+  o1 = __fsub_rn(__fmul_rn(x1, cs), __fmul_rn(x2, sn));
+  o2 = __fadd_rn(__fmul_rn(x2, cs), __fmul_rn(x1, sn));
+}
+#endif
+// RoPE table: tab[p * hd/2 + i] = (cos, sin)(p * theta^(-2i/hd)) for p < max_pos.
+void rope_table(float2* tab, int max_pos, int hd, float rope_theta, cudaStream_t st);
+// Decode QKV projection with RoPE and the KV-cache append fused into the
+// epilogue: qkv = X W^T (never stored); q -> q_out [M, H, hd]; the new
+// token's K / V -> the pool at (slot[m], pos[m]) of `layer`. cs: rope_table.
+void gemm_qkv_rope(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH, int hd, const int* pos,
+                   const float2* cs, const KvPoolView& pool, int layer, const int* slot, bf16* q_out,
+                   cudaStream_t st);
 // 2-D TMA map over the pool viewed as [rows, hd] bf16 rows (one row = one
 // token's K or V of one (page, layer, kv head)); box {64, 32}, 128 B swizzle.
 CUtensorMap make_kv_map(const void* pool, long long rows, int hd);
 // Tokens per decode-attention split (position-determined).
 constexpr int kDecodeChunk = 512;
 // Tensor-core decode attention (attn_decode.cu); false if (hd, group) unsupported or no map.
+// The splits of a (sample, kv head) merge inside the kernel (the last to finish
+// merges; counters: B * KVH ints, zero, left zero) and out [B, H, hd] is written.
 bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer,
-                     const int* slot, const int* ctx, int nsplit, float* work, cudaStream_t st);
+                     const int* slot, const int* ctx, int nsplit, float* work, bf16* out, int* counters,
+                     cudaStream_t st);
 void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, float rope_theta, bf16* q_out,
               bf16* k_out, bf16* v_out, const KvPoolView* pool, int layer, const int* slot, cudaStream_t st);
 
@@ -102,9 +151,11 @@ void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, fl
 // tokens visible (including the one just appended). out [B, H, hd] bf16.
 // work: float scratch of attn_decode_workspace(B, H, hd, max_ctx) floats.
 size_t attn_decode_workspace(int B, int H, int hd, int max_ctx);
+// counters: B * KVH zero ints (left zero) enabling the fused split merge of
+// the tensor-core kernel; nullptr runs the separate combine kernel.
 // probe_begin / probe_end (optional) bracket the main split kernel (not the combine).
 void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer, const int* slot,
-                 const int* ctx, int max_ctx, float* work, bf16* out, cudaStream_t st,
+                 const int* ctx, int max_ctx, float* work, bf16* out, int* counters, cudaStream_t st,
                  cudaEvent_t probe_begin = nullptr, cudaEvent_t probe_end = nullptr);
 // Varlen causal attention over packed q [M, H, hd], k/v [M, KVH, hd];
 // sequences [cu[i], cu[i+1]). tiles: host-built table of (seq, q_tile) pairs

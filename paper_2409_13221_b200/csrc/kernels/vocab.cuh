@@ -62,6 +62,10 @@ struct EpiVocab {
 
   static constexpr bool kTmaStore = false;
   static constexpr int kPasses = MODE == kSample ? 2 : 1;
+  // 2 x 48 KB ring: two CTAs per SM, so a vocab sweep of 197 column tiles at
+  // small M is one wave and each CTA's (heavy) epilogue overlaps the other's
+  // mainloop
+  static constexpr int kStages = 2;
   __device__ void store(const uint8_t*, int, int, int) const {}
 
   struct State {

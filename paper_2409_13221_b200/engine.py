@@ -53,6 +53,8 @@ class ExecOutput:
     finish_instance: np.ndarray
     decision: object  # sched.GenStageResult
     moves: list       # (sample, from, to) in application order
+    step_rows: np.ndarray = None  # per decode step of this rank: batch rows
+    step_ms: np.ndarray = None    # per decode step: GPU ms
 
 
 class Engine:
@@ -148,6 +150,12 @@ class Engine:
             ms, mf, mt = ((C.c_int32 * max(nm.value, 1))() for _ in range(3))
             check(self.lib, self.lib.fp_exec_moves(x, C.byref(nm), ms, mf, mt))
             moves = list(zip(ms[:nm.value], mf[:nm.value], mt[:nm.value]))
-            return ExecOutput(stats, exp, fin, inst, decision, moves)
+            ns = C.c_int32()
+            check(self.lib, self.lib.fp_exec_steps(x, C.byref(ns), None, None))
+            srows = np.zeros(max(ns.value, 1), dtype=np.int32)
+            sms = np.zeros(max(ns.value, 1), dtype=np.float32)
+            check(self.lib, self.lib.fp_exec_steps(x, C.byref(ns), srows.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                   sms.ctypes.data_as(C.POINTER(C.c_float))))
+            return ExecOutput(stats, exp, fin, inst, decision, moves, srows[:ns.value], sms[:ns.value])
         finally:
             self.lib.fp_exec_free(x)

@@ -259,3 +259,44 @@ def test_postprocess_matches_c_oracle(lib):
         g = got.cpu().numpy().astype(np.float64)
         # fp32 reverse scan vs fp64 recursion: |d| <= 1e-4 * max(1, max|A|) (T <= 4096)
         assert np.max(np.abs(g - want)) <= 1e-4 * max(1.0, np.max(np.abs(want)))
+
+
+@pytest.mark.parametrize("H,KVH,hd", [(12, 12, 64), (8, 8, 32), (16, 4, 128)])
+@pytest.mark.parametrize("M", [1, 7, 40, 300])
+def test_qkv_rope_fused(lib, H, KVH, hd, M):
+    """Decode QKV GEMM with RoPE + KV append in the epilogue vs torch: bf16(X W^T),
+    rotate-half RoPE in fp32, K/V written at (slot, pos) of the paged pool."""
+    K, L, layer, PT, max_pos, theta = 256, 2, 1, 64, 320, 10000.0
+    N = (H + 2 * KVH) * hd
+    W = rand_bf16(N, K, scale=0.1, seed=1)
+    X = rand_bf16(M, K, seed=2)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    pos = torch.randint(0, max_pos, (M,), device="cuda", generator=g, dtype=torch.int32)
+    maxp = (max_pos + PT - 1) // PT
+    npages = M * maxp + 1
+    pool = torch.zeros(npages, L, KVH, 2, PT, hd, device="cuda", dtype=torch.bfloat16)
+    bt = (torch.randperm(npages - 1, device="cuda", generator=g)[: M * maxp] + 1).to(torch.int32).view(M, maxp)
+    slot = torch.randperm(M, device="cuda", generator=g).to(torch.int32)
+    q = torch.zeros(M, H, hd, device="cuda", dtype=torch.bfloat16)
+    ok(lib, lib.fp_k_qkv_rope(ptr(W), K, ptr(X), M, H, KVH, hd, ptr(pos), max_pos, theta, ptr(pool), L, layer,
+                              ptr(bt.contiguous()), maxp, ptr(slot), ptr(q), stream()))
+    torch.cuda.synchronize()
+    qkv = (X.float() @ W.float().T).to(torch.bfloat16).float().view(M, H + 2 * KVH, hd)
+    half = hd // 2
+    inv = torch.exp2(-(2.0 * torch.arange(half, device="cuda") / hd) * np.log2(theta))
+    ang = pos.float()[:, None] * inv[None]
+    c, s = ang.cos()[:, None], ang.sin()[:, None]
+    x1, x2 = qkv[..., :half], qkv[..., half:]
+    rot = torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1)
+    tol = 2e-2 * qkv.abs().max().item()
+    assert (q.float() - rot[:, :H]).abs().max().item() < tol
+    written = torch.zeros_like(pool, dtype=torch.bool)
+    for m in range(M):
+        p = int(pos[m])
+        page = int(bt[int(slot[m]), p // PT])
+        kk = pool[page, layer, :, 0, p % PT].float()
+        vv = pool[page, layer, :, 1, p % PT].float()
+        assert (kk - rot[m, H:H + KVH]).abs().max().item() < tol, m
+        assert (vv - qkv[m, H + KVH:]).abs().max().item() < tol, m
+        written[page, layer, :, :, p % PT] = True
+    assert not pool[~written].any()  # nothing else touched
