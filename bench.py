@@ -222,15 +222,25 @@ def main():
                            probe_attention=probe)
     step.k = 0
 
+    # ncu --profile-from-start off: profile only the first timed region
+    prof_range = os.environ.get("FUSEPLAN_PROFILE_TIMED") == "1"
+
     def timed(schedule, resident, K, probe=False):
+        nonlocal prof_range
         outs = []
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if prof_range:
+            torch.cuda.profiler.start()
         e0.record()
         for _ in range(K):
             step.k += 1
             outs.append(step(schedule, resident, probe))
+        if prof_range:
+            torch.cuda.synchronize()
+            torch.cuda.profiler.stop()
+            prof_range = False
         e1.record()
         torch.cuda.synchronize()
         barrier()

@@ -133,6 +133,16 @@ int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t h
                      int32_t num_pages, int32_t num_layers, int32_t layer, const int32_t* block_table,
                      int32_t bt_stride, const int32_t* slot, const int32_t* ctx, int32_t max_ctx, void* out,
                      void* stream);
+/* The same with caller-owned buffers and no host synchronisation (graph-
+ * capturable; tooling / roofline): items_dev from fp_k_attn_items (host ctx),
+ * workspace of fp_k_attn_workspace_bytes, zero-filled before its first use
+ * (the kernel leaves its counters zero). */
+int64_t fp_k_attn_workspace_bytes(int32_t B, int32_t H, int32_t KVH, int32_t hd, int32_t max_ctx);
+int fp_k_attn_items(const int32_t* ctx_host, int32_t B, int32_t max_ctx, int32_t* items_host);
+int fp_k_attn_decode_ws(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t hd, const void* pool,
+                        int32_t num_pages, int32_t num_layers, int32_t layer, const int32_t* block_table,
+                        int32_t bt_stride, const int32_t* slot, const int32_t* ctx, const int32_t* items_dev,
+                        int32_t max_ctx, void* workspace, void* out, void* stream);
 /* Varlen causal attention; cu_host: n_seq+1 offsets (host), cu_dev the same on device. */
 int fp_k_attn_varlen(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
                      const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream);

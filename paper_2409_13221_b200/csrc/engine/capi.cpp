@@ -410,14 +410,60 @@ int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t h
     }
     float* work = nullptr;
     const size_t wb = fpk::attn_decode_workspace(B, H, hd, max_ctx) * 4 + 256;
-    const size_t cb = static_cast<size_t>(B) * KVH * 4;
-    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&work), wb + cb, S(stream)), "alloc");
+    const size_t cb = static_cast<size_t>(fpk::attn_decode_counters(B, KVH)) * 4;
+    const size_t ob = (1 + static_cast<size_t>(B) * ((max_ctx + fpk::kDecodeChunk - 1) / fpk::kDecodeChunk)) * 4;
+    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&work), wb + cb + ob, S(stream)), "alloc");
     int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(work) + wb);
+    int* items = counters + fpk::attn_decode_counters(B, KVH);
     fpe::check(cudaMemsetAsync(counters, 0, cb, S(stream)), "memset");
-    fpk::attn_decode(static_cast<const bf16*>(q), B, H, KVH, hd, pv, layer, slot, ctx, max_ctx, work,
+    std::vector<int> hc(B), hi(ob / 4);
+    {  // work-item table from the contexts (host; this entry is a test / tooling path)
+      fpe::check(cudaMemcpyAsync(hc.data(), ctx, B * 4, cudaMemcpyDeviceToHost, S(stream)), "ctx d2h");
+      fpe::check(cudaStreamSynchronize(S(stream)), "sync");
+      for (int b = 0; b < B; ++b)
+        if (hc[b] < 1 || hc[b] > max_ctx) throw std::invalid_argument("attn_decode: ctx out of [1, max_ctx]");
+      fpk::attn_decode_items(hc.data(), B, hi.data());
+      fpe::check(cudaMemcpyAsync(items, hi.data(), ob, cudaMemcpyHostToDevice, S(stream)), "items h2d");
+    }
+    fpk::attn_decode(static_cast<const bf16*>(q), B, H, KVH, hd, pv, layer, slot, ctx, items, max_ctx, work,
                      static_cast<bf16*>(out), counters, S(stream));
     after_launch();
     fpe::check(cudaFreeAsync(work, S(stream)), "free");
+  });
+}
+
+int64_t fp_k_attn_workspace_bytes(int32_t B, int32_t H, int32_t KVH, int32_t hd, int32_t max_ctx) {
+  return static_cast<int64_t>(fpk::attn_decode_workspace(B, H, hd, max_ctx)) * 4 + 256 +
+         static_cast<int64_t>(fpk::attn_decode_counters(B, KVH)) * 4;
+}
+
+int fp_k_attn_items(const int32_t* ctx_host, int32_t B, int32_t max_ctx, int32_t* items_host) {
+  return guarded([&] {
+    for (int b = 0; b < B; ++b)
+      if (ctx_host[b] < 1 || ctx_host[b] > max_ctx) throw std::invalid_argument("attn_items: ctx out of [1, max_ctx]");
+    fpk::attn_decode_items(ctx_host, B, items_host);
+  });
+}
+
+int fp_k_attn_decode_ws(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t hd, const void* pool,
+                        int32_t num_pages, int32_t num_layers, int32_t layer, const int32_t* block_table,
+                        int32_t bt_stride, const int32_t* slot, const int32_t* ctx, const int32_t* items_dev,
+                        int32_t max_ctx, void* workspace, void* out, void* stream) {
+  return guarded([&] {
+    const size_t layer_bytes = static_cast<size_t>(KVH) * 2 * 64 * hd * 2;
+    fpk::KvPoolView pv{static_cast<uint8_t*>(const_cast<void*>(pool)), layer_bytes * num_layers, layer_bytes, 64,
+                       block_table, bt_stride};
+    CUtensorMap map;
+    if (num_pages > 0 && (hd == 64 || hd == 128)) {
+      map = fpk::make_kv_map(pool, static_cast<long long>(num_pages) * (layer_bytes * num_layers / (hd * 2)), hd);
+      pv.kv_map = &map;
+    }
+    float* work = static_cast<float*>(workspace);
+    int* counters = reinterpret_cast<int*>(static_cast<uint8_t*>(workspace) +
+                                           fpk::attn_decode_workspace(B, H, hd, max_ctx) * 4 + 256);
+    fpk::attn_decode(static_cast<const bf16*>(q), B, H, KVH, hd, pv, layer, slot, ctx, items_dev, max_ctx, work,
+                     static_cast<bf16*>(out), counters, S(stream));
+    after_launch();
   });
 }
 

@@ -261,14 +261,16 @@ void Engine::alloc_ws() {
   dec_.q = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxao * 2));
   dec_.attn = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxao * 2));
   dec_.act = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxF * 2));
-  dec_.rows = static_cast<int*>(dalloc(static_cast<size_t>(7) * B * 4));
+  const int ns_cap = (cfg_.max_prompt + cfg_.max_new + fpk::kDecodeChunk - 1) / fpk::kDecodeChunk;
+  dec_.rows = static_cast<int*>(dalloc((static_cast<size_t>(7 + ns_cap) * B + 1) * 4));
   dec_.vocab_part = dalloc(static_cast<size_t>(B) * vt * 24);
   dec_.tgt_z = static_cast<float*>(dalloc(B * 4));
   const Dims& a = cfg_.model[kActor];
   dec_.attn_work = static_cast<float*>(
       dalloc(fpk::attn_decode_workspace(B, a.H, a.hd, cfg_.max_prompt + cfg_.max_new) * sizeof(float)));
-  dec_.attn_cnt = static_cast<int*>(dalloc(static_cast<size_t>(B) * a.KVH * sizeof(int)));
-  FP_CUDA(cudaMemsetAsync(dec_.attn_cnt, 0, static_cast<size_t>(B) * a.KVH * sizeof(int), s_decode_));
+  const size_t cnt = static_cast<size_t>(fpk::attn_decode_counters(B, a.KVH)) * sizeof(int);
+  dec_.attn_cnt = static_cast<int*>(dalloc(cnt));
+  FP_CUDA(cudaMemsetAsync(dec_.attn_cnt, 0, cnt, s_decode_));
 }
 
 // ---------------------------------------------------------------------------
@@ -466,7 +468,8 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
   const int Bb = graph ? bucket_of(B) : B;
   if (Bb > dec_.cap) throw std::invalid_argument("engine: decode batch exceeds max_live");
   cudaStream_t st = s_decode_;
-  std::vector<int> h(static_cast<size_t>(7) * Bb);
+  const int ns_cap = (cfg_.max_prompt + cfg_.max_new + fpk::kDecodeChunk - 1) / fpk::kDecodeChunk;
+  std::vector<int> h(static_cast<size_t>(7 + ns_cap) * Bb + 1);
   int max_ctx = 0;
   double ctx_sum = 0.0;
   for (int b = 0; b < Bb; ++b) {
@@ -482,7 +485,8 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
     max_ctx = std::max(max_ctx, r.pos + 1);
     if (!pad) ctx_sum += r.pos + 1;
   }
-  upload(dec_.rows, h.data(), h.size() * 4, st);
+  const int n_pairs = fpk::attn_decode_items(h.data() + 2 * Bb, Bb, h.data() + 7 * Bb);
+  upload(dec_.rows, h.data(), (static_cast<size_t>(7) * Bb + 1 + n_pairs) * 4, st);
   if (!graph) {
     decode_kernels(Bb, max_ctx, mode, inv_temp, sample_seed, ctx_sum);
     return;
@@ -525,6 +529,7 @@ void Engine::decode_kernels(int B, int max_ctx, int mode, float inv_temp, uint64
   const int* target = dec_.rows + 4 * B;
   const int* sid = dec_.rows + 5 * B;
   const int* step = dec_.rows + 6 * B;
+  const int* items = dec_.rows + 7 * B;
   const fpk::KvPoolView pv = pool_view();
   const size_t stride = static_cast<size_t>(B) * D.d;
   const int so = fpk::gemm_splits(D.d, D.H * D.hd);
@@ -541,15 +546,15 @@ void Engine::decode_kernels(int B, int max_ctx, int mode, float inv_temp, uint64
       ProbeRec pr{probe_event(), probe_event(), 0.0};
       const double kv_tok = 2.0 * D.KVH * D.hd * 2.0;  // K + V of one layer, bf16
       pr.bytes = ctx_sum * kv_tok + static_cast<double>(B) * D.H * D.hd * 2.0;
-      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, max_ctx, dec_.attn_work, dec_.attn, dec_.attn_cnt, st, pr.a,
+      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, items, max_ctx, dec_.attn_work, dec_.attn, dec_.attn_cnt, st, pr.a,
                        pr.b);
       probes_.push_back(pr);
     } else {
-      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, max_ctx, dec_.attn_work, dec_.attn, dec_.attn_cnt, st);
+      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, items, max_ctx, dec_.attn_work, dec_.attn, dec_.attn_cnt, st);
     }
     fpk::gemm_f32_splitk(L.wo, D.d, D.H * D.hd, dec_.attn, B, dec_.parts, so, st);
     fpk::add_norm(dec_.x, dec_.parts, so, stride, L.ln2, dec_.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
-    fpk::gemm_swiglu(L.wgu, D.F, D.d, dec_.h, B, dec_.act, st);
+    fpk::gemm_swiglu_decode(L.wgu, D.F, D.d, dec_.h, B, dec_.act, st);
     fpk::gemm_f32_splitk(L.wd, D.d, D.F, dec_.act, B, dec_.parts, sd, st);
     nparts = sd;
   }

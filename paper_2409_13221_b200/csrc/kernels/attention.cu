@@ -438,13 +438,30 @@ void launch_decode(const bf16* q, int B, int H, int KVH, const KvPoolView& pool,
 
 }  // namespace
 
+int attn_decode_items(const int* ctx, int B, int* items) {
+  // counting sort by units (32-token) descending: buckets 0..kDecodeChunk/32
+  constexpr int kU = kDecodeChunk / 32;
+  int n = 0;
+  for (int u = kU; u >= 1; --u)
+    for (int b = 0; b < B; ++b) {
+      const int ns = (ctx[b] + kDecodeChunk - 1) / kDecodeChunk;
+      for (int s = 0; s < ns; ++s) {
+        const int len = std::min(ctx[b], (s + 1) * kDecodeChunk) - s * kDecodeChunk;
+        if ((len + 31) / 32 == u) items[1 + n++] = b << 8 | s;
+      }
+    }
+  items[0] = n;
+  return n;
+}
+
 size_t attn_decode_workspace(int B, int H, int hd, int max_ctx) {
   const int ns = (max_ctx + kChunk - 1) / kChunk;
   return static_cast<size_t>(B) * H * ns * (hd + 2);
 }
 
 void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer, const int* slot,
-                 const int* ctx, int max_ctx, float* work, bf16* out, int* counters, cudaStream_t st,
+                 const int* ctx, const int* items, int max_ctx, float* work, bf16* out, int* counters,
+                 cudaStream_t st,
                  cudaEvent_t probe_begin,
                  cudaEvent_t probe_end) {
   if (B <= 0) return;
@@ -454,7 +471,7 @@ void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView&
   const int G = H / KVH;
 #define FP_DEC(HD_, G_) \
   if (hd == HD_ && G == G_) { launch_decode<HD_, G_>(q, B, H, KVH, pool, layer, slot, ctx, ns, work, st); } else
-  if (attn_decode_mma(q, B, H, KVH, hd, pool, layer, slot, ctx, ns, work, out, counters, st)) {
+  if (attn_decode_mma(q, B, H, KVH, hd, pool, layer, slot, ctx, items, ns, work, out, counters, st)) {
     if (probe_end) cudaEventRecord(probe_end, st);
     return;  // splits merged in-kernel
   } else FP_DEC(32, 1) FP_DEC(64, 1) FP_DEC(128, 1) FP_DEC(64, 4) FP_DEC(128, 4) FP_DEC(128, 8) FP_DEC(64, 8) {

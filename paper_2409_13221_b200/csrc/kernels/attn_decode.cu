@@ -1,22 +1,25 @@
 // fuseplan-b200 — paged decode attention on tensor cores (head_dim 64 / 128).
 //
-// One CTA per (kv head, sample, 512-token context split): 1 producer warp +
-// 4 consumer warps. The producer streams every 64-token page's K and V tiles
-// of (layer, kv head) with 2-D TMA (128-byte swizzle, 64 x 128 B boxes) into
-// an S-stage shared-memory ring signalled on mbarriers. Consumer warp w takes
-// pages w, w+4, ...: S = Q K^T and O += P V with mma.sync m16n8k16 (bf16 in,
-// fp32 accumulate), the G query heads of the GQA group as the MMA rows (K/V
-// read once per group), online softmax in registers; ldmatrix addresses apply
-// the TMA swizzle (16-byte chunk c of row r lives at chunk c ^ (r & 7)), so
-// fragment loads are bank-conflict free. Warps merge through shared memory;
-// the last split of a (sample, kv head) to finish merges the splits (an atomic
-// ticket per pair; single-split items normalise in place). Split boundaries depend on the
-// position only (batch-independent results). HBM-bound: every K/V byte of the
-// visible context is read exactly once per launch.
+// Persistent kernel, one CTA per SM (<= 148), 6-8 independent warps. A work
+// item is (sample, 256-token context split, kv head); warps take items from a
+// launch-wide atomic counter in the host's longest-first order (dynamic load
+// balance). Each warp streams its items' 32-token K|V units with 2-D TMA
+// (box 64 x 32 rows, 128-byte swizzle) into a private 2-3 stage ring on
+// mbarriers, issuing kStages units ahead across item boundaries so the pipe
+// never drains, and computes S = Q K^T and O += P V with mma.sync m16n8k16
+// (bf16 in, fp32 accumulate), the G query heads of a GQA group as MMA rows
+// (K/V read once per group) and the online softmax in registers; ldmatrix
+// addresses apply the TMA swizzle (16-byte chunk c of row r lives at chunk
+// c ^ (r & 7)), so fragment loads are bank-conflict free. A single-split item
+// normalises in place; otherwise the last split of a (sample, kv head) to
+// finish merges the (o, m, l) partials (atomic ticket), so no combine kernel
+// runs. Split boundaries depend on the position only (batch-independent
+// results). HBM-bound: every K/V byte of the visible context is read once.
 #include <math.h>
 
 #include <algorithm>
 
+#include "launch.cuh"
 #include "ops.h"
 #include "ptx.cuh"
 
@@ -53,19 +56,17 @@ __device__ __forceinline__ uint32_t swz(uint32_t tile_base, int r, int c16) {
   return tile_base + sub * kTileBytes + r * 128 + ((cc ^ (r & 7)) << 4);
 }
 
-// Persistent warp-per-item design. A work item is (sample, kv head, 512-token
-// split); warp gw of the grid takes items gw, gw + T, ... (T = total warps) and
-// streams their 32-token K|V units through kStages private shared-memory
-// stages: lane 0 issues the 2-D TMA loads (box 64 x 32 rows, 128 B swizzle)
-// for the unit kStages ahead — across item boundaries, so the pipeline never
-// drains — and the warp computes S = Q K^T and O += P V with mma.sync on the
-// resident unit. Stages are private to the warp, so no cross-warp barrier or
-// merge exists; every item writes its (unnormalised O, m, l) split partial.
+// Stages are private to the warp, so no cross-warp barrier exists.
+// A stage holds K and V of one 32-token unit and, for the first unit of an
+// item, the item's G query rows (bulk-copied with it, so starting an item
+// never waits on a global load of q).
 template <int HD>
 struct DecCfg {
   static constexpr int kSub = HD / 64;                  // 64-column boxes per K (or V) unit
   static constexpr int kBox = 32 * 128;                 // 32 rows x 128 B
-  static constexpr int kStageBytes = 2 * kSub * kBox;   // K + V of one 32-token unit
+  static constexpr int kKV = 2 * kSub * kBox;           // K + V of one 32-token unit
+  static constexpr int kQSlot = HD == 64 ? 1024 : 2048; // >= 8 q rows x HD x 2 B, keeps 1 KB alignment
+  static constexpr int kStageBytes = kKV + kQSlot;
   static constexpr int kWarps = HD == 64 ? 8 : 6;
   static constexpr int kStages = HD == 64 ? 3 : 2;
   static constexpr int kSmem = kWarps * kStages * kStageBytes + 1024;
@@ -80,7 +81,8 @@ template <int HD, int G>
 __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_kernel(
     const __grid_constant__ CUtensorMap kv_map, const bf16* __restrict__ q, const int* __restrict__ block_table,
     int bt_stride, int rows_per_page, int layer_rows, int layer, const int* __restrict__ slot,
-    const int* __restrict__ ctx, int B, int H, int KVH, int nsplit_max, float scale_log2,
+    const int* __restrict__ ctx, const int* __restrict__ items, int B, int H, int KVH, int nsplit_max,
+    float scale_log2,
     float* __restrict__ part_o, float* __restrict__ part_ml, bf16* __restrict__ out, int* __restrict__ counters) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   using C = DecCfg<HD>;
@@ -89,39 +91,50 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full_bar[C::kWarps][C::kStages];
 
+  __shared__ int ring_s[C::kWarps][8];  // items grabbed by the issue cursor, in order, for the consumer
+
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int T = gridDim.x * C::kWarps;
-  const int n_items = nsplit_max * B * KVH;
   uint64_t* bar = full_bar[warp];
   uint8_t* my_smem = smem + warp * C::kStages * C::kStageBytes;
+  int* ring = ring_s[warp];
   if (lane == 0) {
     if (warp == 0) tma_prefetch_desc(&kv_map);
     for (int s = 0; s < C::kStages; ++s) mbar_init(&bar[s], 1);
     fence_barrier_init();
   }
   __syncwarp();
+  pdl_wait();  // PDL-launched: q, the new K/V and the work counters come from earlier kernels
+  const int n_items = items[0] * KVH;
 
-  // item j -> (split, b, kvh); token range [t0, t1)
+  // item j -> (sample b, split, kv head): pair items[1 + j / KVH] = b << 8 |
+  // split (the host lists pairs longest first), kv head j % KVH; tokens [t0, t1)
   auto item_range = [&](int j, int& b, int& kvh, int& split, int& t0, int& t1) {
-    kvh = j % KVH;
-    const int rest = j / KVH;
-    b = rest % B;
-    split = rest / B;
+    const int pr = j / KVH;
+    kvh = j - pr * KVH;
+    const int e = items[1 + pr];
+    b = e >> 8;
+    split = e & 255;
     t0 = split * kDecodeChunk;
     t1 = min(ctx[b], t0 + kDecodeChunk);
   };
-  // advance a cursor to the next non-empty unit (u < ue), or j >= n_items
-  auto normalise = [&](Cursor& c) {
-    while (c.j < n_items && c.u >= c.ue) {
-      c.j += T;
-      if (c.j >= n_items) break;
+  // dynamic schedule: the next item from the launch-wide work counter
+  int wr = 0, rd = 0;
+  auto grab = [&](Cursor& c) {
+    int j = 0;
+    if (lane == 0) j = atomicAdd(&counters[0], 1);
+    c.j = __shfl_sync(0xffffffffu, j, 0);
+    if (lane == 0) ring[wr & 7] = c.j;
+    ++wr;
+    __syncwarp();
+    if (c.j < n_items) {
       int b, kvh, split, t0, t1;
       item_range(c.j, b, kvh, split, t0, t1);
-      if (t0 < t1) {
-        c.u = t0 >> 5;
-        c.ue = ((t1 - 1) >> 5) + 1;
-      }
+      c.u = t0 >> 5;
+      c.ue = ((t1 - 1) >> 5) + 1;
     }
+  };
+  auto next_issue = [&](Cursor& c) {  // advance the issue cursor by one unit
+    if (++c.u >= c.ue) grab(c);
   };
   auto issue = [&](const Cursor& c, int k) {  // lane 0 only
     int b, kvh, split, t0, t1;
@@ -130,23 +143,32 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
     const int pid = block_table[slot[b] * bt_stride + page];
     const int rk = pid * rows_per_page + layer * layer_rows + kvh * 2 * kPT + half * 32;
     uint8_t* dst = my_smem + k * C::kStageBytes;
-    mbar_arrive_expect_tx(&bar[k], C::kStageBytes);
+    const bool first = c.u == (t0 >> 5);
+    constexpr uint32_t kQBytes = G * HD * 2;
+    mbar_arrive_expect_tx(&bar[k], C::kKV + (first ? kQBytes : 0u));
 #pragma unroll
     for (int sub = 0; sub < C::kSub; ++sub) {
       tma_load_2d(dst + sub * C::kBox, &kv_map, &bar[k], sub * 64, rk);
       tma_load_2d(dst + (C::kSub + sub) * C::kBox, &kv_map, &bar[k], sub * 64, rk + kPT);
     }
+    if (first) bulk_load(dst + C::kKV, q + (static_cast<size_t>(b) * H + kvh * G) * HD, kQBytes, &bar[k]);
   };
 
-  Cursor in{warp + blockIdx.x * C::kWarps - T, 0, 0};  // issue cursor
-  normalise(in);
-  Cursor cur = in;                                      // consume cursor
+  Cursor in{0, 0, 0};  // issue cursor
+  grab(in);
   // prologue: fill the stages
   int issued = 0;
   for (; issued < C::kStages && in.j < n_items; ++issued) {
     if (lane == 0) issue(in, issued);
-    ++in.u;
-    normalise(in);
+    next_issue(in);
+  }
+  Cursor cur{ring[rd & 7], 0, 0};  // consume cursor: the issue cursor's items, in order
+  ++rd;
+  if (cur.j < n_items) {
+    int b, kvh, split, t0, t1;
+    item_range(cur.j, b, kvh, split, t0, t1);
+    cur.u = t0 >> 5;
+    cur.ue = ((t1 - 1) >> 5) + 1;
   }
 
   const int r0 = lane >> 2;
@@ -157,17 +179,19 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
   int cur_j = -1, b = 0, kvh = 0, split = 0, t0 = 0, t1 = 0;
 
   for (int c = 0; cur.j < n_items; ++c) {
-    if (cur.j != cur_j) {  // new item: load Q fragments, reset the running state
+    const int k = c % C::kStages;
+    mbar_wait(&bar[k], (c / C::kStages) & 1);
+    if (cur.j != cur_j) {  // new item: Q fragments from the stage's q slot, reset the running state
       cur_j = cur.j;
       item_range(cur_j, b, kvh, split, t0, t1);
-      const bf16* qg = q + (static_cast<size_t>(b) * H + kvh * G) * HD;
+      const bf16* qs = reinterpret_cast<const bf16*>(my_smem + k * C::kStageBytes + C::kKV);
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
         const int col = kk * 16 + 2 * (lane & 3);
         const bool ok = r0 < G;
-        qa[kk][0] = ok ? *reinterpret_cast<const uint32_t*>(qg + r0 * HD + col) : 0u;
+        qa[kk][0] = ok ? *reinterpret_cast<const uint32_t*>(qs + r0 * HD + col) : 0u;
         qa[kk][1] = 0u;
-        qa[kk][2] = ok ? *reinterpret_cast<const uint32_t*>(qg + r0 * HD + col + 8) : 0u;
+        qa[kk][2] = ok ? *reinterpret_cast<const uint32_t*>(qs + r0 * HD + col + 8) : 0u;
         qa[kk][3] = 0u;
       }
 #pragma unroll
@@ -175,8 +199,6 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
       m_run = -INFINITY;
       l_run = 0.f;
     }
-    const int k = c % C::kStages;
-    mbar_wait(&bar[k], (c / C::kStages) & 1);
     const uint32_t Kt = base + k * C::kStageBytes;
     const uint32_t Vt = Kt + C::kSub * C::kBox;
     const int ut0 = cur.u * 32;
@@ -256,8 +278,7 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(in, k);
       }
-      ++in.u;
-      normalise(in);
+      next_issue(in);
     }
     // advance the consume cursor; flush the item's partial when it ends
     ++cur.u;
@@ -289,23 +310,36 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
         __threadfence();
         __syncwarp();
         int last = 0;
-        if (lane == 0) last = atomicAdd(&counters[b * KVH + kvh], 1) == nsb - 1;
+        if (lane == 0) last = atomicAdd(&counters[2 + b * KVH + kvh], 1) == nsb - 1;
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
-          if (lane == 0) counters[b * KVH + kvh] = 0;  // ready for the next launch
+          if (lane == 0) counters[2 + b * KVH + kvh] = 0;  // ready for the next launch
           __threadfence();
           for (int g = 0; g < G; ++g) combine_row(part_o, part_ml, (row0 + g) * nsplit_max, nsb, HD, lane, 32,
                                                   out + (row0 + g) * HD);
         }
       }
-      normalise(cur);
+      cur.j = ring[rd & 7];
+      ++rd;
+      if (cur.j < n_items) {
+        int bb, kk, ss, a0, a1;
+        item_range(cur.j, bb, kk, ss, a0, a1);
+        cur.u = a0 >> 5;
+        cur.ue = ((a1 - 1) >> 5) + 1;
+      }
     }
+  }
+  // the last warp out resets the work counter for the next launch
+  if (lane == 0 && atomicAdd(&counters[1], 1) == static_cast<int>(gridDim.x) * C::kWarps - 1) {
+    counters[0] = 0;
+    counters[1] = 0;
   }
 }
 
 template <int HD, int G>
 void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
-            const int* slot, const int* ctx, int nsplit, float* work, bf16* out, int* counters, cudaStream_t st) {
+            const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out, int* counters,
+            cudaStream_t st) {
   using C = DecCfg<HD>;
   static bool attr = false;
   if (!attr) {
@@ -317,24 +351,24 @@ void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const 
   const int layer_rows = KVH * 2 * kPT;
   const int rows_per_page = static_cast<int>(pool.page_bytes / (static_cast<size_t>(HD) * 2));
   const float scale = kLog2e / sqrtf(static_cast<float>(HD));
-  const int items = nsplit * B * KVH;
-  const int grid = std::max(1, std::min(148, (items + C::kWarps - 1) / C::kWarps));
-  attn_decode_mma_kernel<HD, G><<<grid, C::kWarps * 32, C::kSmem, st>>>(
-      map, q, pool.block_table, pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, B, H, KVH, nsplit,
-      scale, part_o, part_ml, out, counters);
+  const int max_items = nsplit * B * KVH;  // upper bound of the non-empty items
+  const int grid = std::max(1, std::min(148, (max_items + C::kWarps - 1) / C::kWarps));
+  launch_pdl(attn_decode_mma_kernel<HD, G>, dim3(grid), dim3(C::kWarps * 32), C::kSmem, st, map, q,
+             pool.block_table, pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, items, B, H, KVH, nsplit,
+             scale, part_o, part_ml, out, counters);
   count_launch();
 }
 
 }  // namespace
 
 bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer,
-                     const int* slot, const int* ctx, int nsplit, float* work, bf16* out, int* counters,
-                     cudaStream_t st) {
-  if (!pool.kv_map || !counters) return false;
+                     const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out,
+                     int* counters, cudaStream_t st) {
+  if (!pool.kv_map || !counters || !items) return false;
   const int G = H / KVH;
 #define FP_MMA(HD_, G_)                                                                            \
   if (hd == HD_ && G == G_) {                                                                      \
-    launch<HD_, G_>(*pool.kv_map, q, B, H, KVH, pool, layer, slot, ctx, nsplit, work, out, counters, st);      \
+    launch<HD_, G_>(*pool.kv_map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);      \
     return true;                                                                                   \
   }
   FP_MMA(64, 1) FP_MMA(128, 1) FP_MMA(64, 4) FP_MMA(128, 4) FP_MMA(128, 8) FP_MMA(64, 8)

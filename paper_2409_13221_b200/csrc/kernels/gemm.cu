@@ -3,12 +3,14 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
 
 #include "gemm.cuh"
+#include "launch.cuh"
 #include "ops.h"
 #include "vocab.cuh"
 
@@ -96,7 +98,7 @@ unsigned long long* g_trace = nullptr;
 
 template <int BN, class Epi>
 void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int splits, const Epi& epi,
-            cudaStream_t st, bool weight_is_a = true) {
+            cudaStream_t st, bool weight_is_a = true, bool cluster_split = false) {
   using C = GemmCfg<BN, EpiStages<Epi>::value>;
   if (K % kBK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
   if (a_rows <= 0 || b_rows <= 0) return;
@@ -116,6 +118,8 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
   g.weight_is_a = weight_is_a ? 1 : 0;
   g.trace = g_trace;
   const int z = (g.k_blocks + g.kb_per_split - 1) / g.kb_per_split;
+  if (cluster_split && (BN > 64 || z > 8)) throw std::invalid_argument("gemm: cluster split needs BN <= 64, z <= 8");
+  g.cz = cluster_split ? z : 1;
   // Programmatic dependent launch: the prologue and the weight prefetch of this
   // GEMM overlap the tail of the previous kernel (which triggers early).
   cudaLaunchConfig_t cfg{};
@@ -123,11 +127,15 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = g.cz;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g.cz > 1 ? 2 : 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi>, ma, mb, g, epi);
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm launch: ") + cudaGetErrorString(e));
   fpk::count_launch();
@@ -141,8 +149,41 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
 int pick_bn(int M, int a_ctas) {
   static const int kBN[] = {256, 128, 64, 32, 16};
   for (int bn : kBN)
-    if (a_ctas * ((M + bn - 1) / bn) >= 128) return bn;
+    if ((bn / 2 < M || bn == 16) && a_ctas * ((M + bn - 1) / bn) >= 128) return bn;  // never wider than needed
   return 16;
+}
+
+// Cluster split of a decode GEMM: a function of the weight shape only (so a
+// row's bits do not depend on the batch): the largest z <= 8 dividing the K
+// blocks with tiles x z <= 148.
+int cluster_splits(int N, int K) {
+  static const int enabled = [] {
+    const char* e = std::getenv("FUSEPLAN_CLUSTER_SPLIT");  // A/B switch
+    return e ? std::atoi(e) : 0;  // off by default: measured slower
+  }();
+  if (!enabled) return 1;
+  const int tiles = (N + 127) / 128, kb = K / kBK;
+  int best = 1;
+  for (int z = 2; z <= 8; ++z)
+    if (kb % z == 0 && tiles * z <= 148) best = z;
+  return best;
+}
+
+// Decode GEMMs with a cluster split use BN <= 64 (the parked partial must fit).
+int pick_bn_small(int M, int a_ctas) {
+  static const int kBN[] = {64, 32, 16};
+  for (int bn : kBN)
+    if ((bn / 2 < M || bn == 16) && a_ctas * ((M + bn - 1) / bn) >= 128) return bn;  // never wider than needed
+  return 16;
+}
+
+template <class F>
+void dispatch_bn_small(int M, int a_ctas, F&& f) {
+  switch (pick_bn_small(M, a_ctas)) {
+    case 16: f.template operator()<16>(); break;
+    case 32: f.template operator()<32>(); break;
+    default: f.template operator()<64>(); break;
+  }
 }
 
 template <class Epi, class F>
@@ -215,6 +256,15 @@ void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float*
   });
 }
 
+void gemm_swiglu_decode(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
+  if (F % 64) throw std::invalid_argument("gemm_swiglu: F must be a multiple of 64");
+  const int z = cluster_splits(2 * F, K);
+  dispatch_bn_small(M, (2 * F + 127) / 128 * z, [&]<int BN>() {
+    EpiSwiGLU<BN> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, BN)};
+    launch<BN>(Wgu, 2 * F, X, M, K, z, e, st, true, z > 1);
+  });
+}
+
 void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
   if (F % 64) throw std::invalid_argument("gemm_swiglu: F must be a multiple of 64");
   dispatch_bn<int>(M, (2 * F + 127) / 128, [&]<int BN>() {
@@ -228,10 +278,11 @@ void gemm_qkv_rope(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH
                    cudaStream_t st) {
   if (128 % hd != 0) throw std::invalid_argument("gemm_qkv_rope: head_dim must divide 128");
   const int N = (H + 2 * KVH) * hd;
-  dispatch_bn<int>(M, (N + 127) / 128, [&]<int BN>() {
+  const int z = cluster_splits(N, K);
+  dispatch_bn_small(M, (N + 127) / 128 * z, [&]<int BN>() {
     EpiRopeKV<BN> e{q_out, pool, slot, pos, cs, layer, H, KVH, hd, M};
     e.pool.kv_map = nullptr;  // host pointer: not dereferenced on the device
-    launch<BN>(Wqkv, N, X, M, K, 1, e, st);
+    launch<BN>(Wqkv, N, X, M, K, z, e, st, true, z > 1);
   });
 }
 
@@ -267,6 +318,7 @@ __global__ void vocab_finalize_kernel(const VocabPartial* __restrict__ part, con
                                       uint32_t seed_lo, uint32_t seed_hi, int* token, float* logp, const int* dst,
                                       int* out_tok, float* out_logp, const int* cur_idx, int* cur_tok) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
+  pdl_wait();     // PDL-launched: the partials come from the vocab GEMM
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
@@ -366,10 +418,10 @@ void vocab_finalize(const void* part, const float* tgt_z, int M, int V, int mode
                     int* out_tok, float* out_logp, const int* cur_idx, int* cur_tok, cudaStream_t st) {
   if (M <= 0) return;
   const int warps = 8;
-  vocab_finalize_kernel<<<(M + warps - 1) / warps, warps * 32, 0, st>>>(
-      static_cast<const VocabPartial*>(part), tgt_z, M, vocab_tiles(V), mode, target, sample_id, step,
-      static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), token, logp, dst, out_tok, out_logp, cur_idx,
-      cur_tok);
+  launch_pdl(vocab_finalize_kernel, dim3((M + warps - 1) / warps), dim3(warps * 32), 0, st,
+             static_cast<const VocabPartial*>(part), tgt_z, M, vocab_tiles(V), mode, target, sample_id, step,
+             static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), token, logp, dst, out_tok, out_logp,
+             cur_idx, cur_tok);
   fpk::count_launch();
 }
 

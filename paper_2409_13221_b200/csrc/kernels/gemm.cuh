@@ -57,6 +57,7 @@ struct GemmGeom {
   int k_blocks;      // total 64-wide K blocks
   int kb_per_split;  // K blocks per gridDim.z slice
   int weight_is_a;   // 1: A is a weight (may be prefetched before griddepcontrol.wait)
+  int cz;            // > 1: the gridDim.z splits form one cluster, reduced through DSMEM (BN <= 64)
   unsigned long long* trace;  // optional per-CTA phase stamps (globaltimer ns), 8 per CTA
 };
 
@@ -194,43 +195,96 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       __syncwarp();
     }
-  } else {
-    // Epilogue warps 2..9 -> TMEM lane quarters (warp % 4), two halves.
-    pdl_wait();
-    const int quarter = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const int r = quarter * 32 + lane_id();
+  }
+  // Epilogue warps 2..9 -> TMEM lane quarters (warp % 4), two halves. Without
+  // a cluster split, each reads its accumulator chunks from TMEM. With one
+  // (g.cz > 1: the K splits of a tile are the CTAs of a cluster along z),
+  // every CTA parks its fp32 partial in shared memory, and rank 0 runs the
+  // epilogue on the sum over ranks 0..cz-1 in rank order, read through DSMEM —
+  // a deterministic split-K reduction without a global round trip.
+  const int quarter = warp & 3;
+  const int half = (static_cast<int>(warp) - 2) >> 2;
+  const int r = quarter * 32 + lane_id();
+  constexpr int kPStride = (BN < 32 ? 32 : BN) + 4;  // padded fp32 row of the parked partial (32-column chunks)
+  constexpr int kPOff = 64 * 1024;                // parked partial: after any epilogue staging
+  static_assert(BN > 64 || kPOff + 128 * kPStride * 4 <= C::kStages * C::kStageBytes, "partial does not fit");
+  auto run_epi = [&](auto&& load) {
     typename Epi::State st{};
-    if (nkb > 0) {
-      mbar_wait(&acc_bar, 0);
-      if (tr && threadIdx.x == 64) tr[4] = gtime();
-      tc_fence_after();
-    }
 #pragma unroll 1
     for (int pass = 0; pass < Epi::kPasses; ++pass) {  // two-pass epilogues re-read TMEM (cheap)
       if (pass) epi.next_pass(st, a_row0, b_row0, r, half);
 #pragma unroll 1
       for (int c0 = 32 * half; c0 < ((BN + 63) / 64) * 64; c0 += 64) {
         float v[32];
-        if (nkb > 0 && c0 < BN) {
-          tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.f;
-        }
-        epi(st, smem, a_row0, b_row0, split, r, half, c0, v);
+        load(c0, v);
+        epi(st, smem, a_row0, b_row0, g.cz > 1 ? 0 : split, r, half, c0, v);
       }
     }
-    epi.finish(st, a_row0, b_row0, split, r, half);
+    epi.finish(st, a_row0, b_row0, g.cz > 1 ? 0 : split, r, half);
     if constexpr (Epi::kTmaStore) {
       fence_async_smem();
       epi_bar_sync();
       if (threadIdx.x == 64) {
-        epi.store(smem, a_row0, b_row0, split);
+        epi.store(smem, a_row0, b_row0, g.cz > 1 ? 0 : split);
         bulk_commit_wait();
       }
     }
-    if (tr && threadIdx.x == 64) tr[5] = gtime();
+  };
+  auto tmem_load = [&](int c0, float (&v)[32]) {
+    if (nkb > 0 && c0 < BN) {
+      tmem_ld32(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = 0.f;
+    }
+  };
+  if (warp >= 2) {
+    pdl_wait();
+    if (nkb > 0) {
+      mbar_wait(&acc_bar, 0);
+      if (tr && threadIdx.x == 64) tr[4] = gtime();
+      tc_fence_after();
+    }
+    if (g.cz > 1) {
+      if constexpr (BN <= 64) {
+        float* P = reinterpret_cast<float*>(smem + kPOff) + r * kPStride;
+        for (int c0 = 32 * half; c0 < BN; c0 += 64) {
+          float v[32];
+          tmem_load(c0, v);
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(P + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        }
+      }
+    } else {
+      run_epi(tmem_load);
+      if (tr && threadIdx.x == 64) tr[5] = gtime();
+    }
+  }
+  if constexpr (BN <= 64) {
+    if (g.cz > 1) {
+      cluster_sync();
+      if (warp >= 2 && cluster_ctarank() == 0) {
+        const uint32_t prow = smem_u32(smem + kPOff) + r * kPStride * 4;
+        run_epi([&](int c0, float (&v)[32]) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          if (c0 >= BN) return;
+          for (int q = 0; q < g.cz; ++q) {
+            const uint32_t a = mapa_shared(prow + c0 * 4, q);
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 x = ld_dsmem_v4(a + j * 4);
+              v[j] += x.x;
+              v[j + 1] += x.y;
+              v[j + 2] += x.z;
+              v[j + 3] += x.w;
+            }
+          }
+        });
+        if (tr && threadIdx.x == 64) tr[5] = gtime();
+      }
+      cluster_sync();  // peers keep their partials until rank 0 has read them
+    }
   }
   tc_fence_before();
   __syncthreads();

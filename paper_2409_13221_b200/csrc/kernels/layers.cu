@@ -6,6 +6,7 @@
 #include <atomic>
 #include <stdexcept>
 
+#include "launch.cuh"
 #include "ops.h"
 #include "philox.cuh"
 #include "ptx.cuh"
@@ -72,6 +73,7 @@ __global__ void assemble_kernel(AssembleArgs a) {
 __global__ void embed_kernel(const int* __restrict__ tok, const int* __restrict__ idx, const bf16* __restrict__ E,
                              int d, float* __restrict__ x) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
+  pdl_wait();     // PDL-launched: the input tokens come from the previous kernel
   const int m = blockIdx.x;
   const bf16* e = E + static_cast<size_t>(tok[idx ? idx[m] : m]) * d;
   float* o = x + static_cast<size_t>(m) * d;
@@ -104,6 +106,7 @@ __global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__
                                 const int* __restrict__ gather, int rows, const bf16* __restrict__ value_w,
                                 float* __restrict__ value) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
+  pdl_wait();     // PDL-launched: x and the partials come from the previous kernels
   __shared__ float red[32];
   const int i = blockIdx.x;
   const int src = gather ? gather[i] : i;
@@ -276,7 +279,8 @@ void init_bf16_gu(bf16* w, int F, int d, uint64_t seed, uint64_t tag, float scal
 
 void embed(const int* tokens, const int* idx, int M, const bf16* E, int d, float* x, cudaStream_t st) {
   if (M <= 0) return;
-  embed_kernel<<<M, 128, 0, st>>>(tokens, idx, E, d, x); fpk::count_launch();
+  launch_pdl(embed_kernel, dim3(M), dim3(128), 0, st, tokens, idx, E, d, x);
+  fpk::count_launch();
 }
 
 void copy_chunks(const CopyChunk* d_list, int n, cudaStream_t st) {
@@ -309,7 +313,7 @@ void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, con
   const dim3 grid(rows), block(((d / 4 + 31) / 32) * 32);
   const size_t sm = 0;
 #define FP_AN(N_) \
-  case N_: add_norm_kernel<N_><<<grid, block, sm, st>>>(x, parts, split_stride, gain, y, d, gather, rows, value_w, value); break;
+  case N_: launch_pdl(add_norm_kernel<N_>, dim3(grid), dim3(block), sm, st, x, parts, split_stride, gain, y, d, gather, rows, value_w, value); break;
   switch (ns) {
     FP_AN(0) FP_AN(1) FP_AN(2) FP_AN(3) FP_AN(4) FP_AN(5) FP_AN(6) FP_AN(7) FP_AN(8)
     default: throw std::invalid_argument("add_norm: at most 8 split-K partials");

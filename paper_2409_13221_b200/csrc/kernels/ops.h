@@ -26,6 +26,9 @@ void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* o
 void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float* resid, cudaStream_t st);
 // SwiGLU, W_gu [2F, K] interleaved in 64-row gate/up groups: out[m][f], ld = F.
 void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st);
+// Decode variant: the K range split over a thread-block cluster (z CTAs, a
+// function of the weight shape) and reduced through DSMEM in rank order.
+void gemm_swiglu_decode(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st);
 // Split count used by gemm_f32_splitk for an (N, K) weight; a function of the
 // weight shape only, so each row's result does not depend on the batch.
 int gemm_splits(int N, int K);
@@ -138,11 +141,20 @@ CUtensorMap make_kv_map(const void* pool, long long rows, int hd);
 // Tokens per decode-attention split (position-determined).
 constexpr int kDecodeChunk = 512;
 // Tensor-core decode attention (attn_decode.cu); false if (hd, group) unsupported or no map.
-// The splits of a (sample, kv head) merge inside the kernel (the last to finish
-// merges; counters: B * KVH ints, zero, left zero) and out [B, H, hd] is written.
+// Work items are (sample, non-empty split, kv head), handed out dynamically
+// through counters[0..1] in the order of `items` (attn_decode_items: the
+// (sample, split) pairs, longest first); the splits of a (sample, kv head)
+// merge inside the kernel (the last to finish merges; tickets counters[2 + b *
+// KVH + kvh]). counters: attn_decode_counters(B, KVH) ints, zero, left zero.
 bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer,
-                     const int* slot, const int* ctx, int nsplit, float* work, bf16* out, int* counters,
-                     cudaStream_t st);
+                     const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out,
+                     int* counters, cudaStream_t st);
+inline int attn_decode_counters(int B, int KVH) { return 2 + B * KVH; }
+// Host: the item table of attn_decode_mma from the contexts: items[0] = n,
+// items[1..n] = b << 8 | split over the non-empty splits, longest first (a
+// longest-processing-time order for the dynamic schedule); ties by (b, split).
+// Capacity: 1 + B * ceil(max_ctx / kDecodeChunk) ints.
+int attn_decode_items(const int* ctx, int B, int* items);
 void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, float rope_theta, bf16* q_out,
               bf16* k_out, bf16* v_out, const KvPoolView* pool, int layer, const int* slot, cudaStream_t st);
 
@@ -151,11 +163,12 @@ void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, fl
 // tokens visible (including the one just appended). out [B, H, hd] bf16.
 // work: float scratch of attn_decode_workspace(B, H, hd, max_ctx) floats.
 size_t attn_decode_workspace(int B, int H, int hd, int max_ctx);
-// counters: B * KVH zero ints (left zero) enabling the fused split merge of
-// the tensor-core kernel; nullptr runs the separate combine kernel.
+// counters / items (see attn_decode_mma) enable the tensor-core kernel with
+// its fused split merge; nullptr runs the CUDA-core kernel + combine kernel.
 // probe_begin / probe_end (optional) bracket the main split kernel (not the combine).
 void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer, const int* slot,
-                 const int* ctx, int max_ctx, float* work, bf16* out, int* counters, cudaStream_t st,
+                 const int* ctx, const int* items, int max_ctx, float* work, bf16* out, int* counters,
+                 cudaStream_t st,
                  cudaEvent_t probe_begin = nullptr, cudaEvent_t probe_end = nullptr);
 // Varlen causal attention over packed q [M, H, hd], k/v [M, KVH, hd];
 // sequences [cu[i], cu[i+1]). tiles: host-built table of (seq, q_tile) pairs

@@ -1,0 +1,74 @@
+"""Decode-attention roofline on a bench-shaped launch (gpt2s: H = KVH = 12, hd 64).
+
+    python tools/attn_roofline.py [B] [mean_ctx]        # CUDA-event timing, L2 flushed per launch
+    ncu --set full -k regex:attn_decode_mma -s 5 -c 1 python tools/attn_roofline.py ...
+
+Algorithmic bytes per launch = K and V of every visible token of the layer
+(2 x KVH x hd x 2 B per token) + q (B x H x hd x 2 B) — the same count bench.py's
+probe uses. Prints one JSON line.
+"""
+import ctypes as C
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2409_13221_b200 import _lib  # noqa: E402
+
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+mean_ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 380
+H, KVH, hd, L, layer, PT = 12, 12, 64, 12, 5, 64
+lib = _lib.load()
+g = torch.Generator().manual_seed(5)
+ctx = (torch.rand(B, generator=g) * 2 * mean_ctx).clamp(min=1).to(torch.int32)  # uniform on [1, 2 mean)
+maxp = (int(ctx.max()) + PT - 1) // PT
+npages = B * maxp + 1
+pool = torch.empty(npages, L, KVH, 2, PT, hd, device="cuda", dtype=torch.bfloat16).normal_()
+bt = (torch.randperm(npages - 1)[: B * maxp] + 1).to(torch.int32).view(B, maxp).cuda()
+slot = torch.arange(B, dtype=torch.int32, device="cuda")
+ctx_d = ctx.cuda()
+q = torch.randn(B, H, hd, device="cuda").to(torch.bfloat16)
+out = torch.empty(B, H, hd, device="cuda", dtype=torch.bfloat16)
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+max_ctx = int(ctx.max())
+ws = torch.zeros(int(lib.fp_k_attn_workspace_bytes(B, H, KVH, hd, max_ctx)), dtype=torch.uint8, device="cuda")
+ns = (max_ctx + 63) // 64  # >= splits at any chunk >= 64
+items_h = (C.c_int32 * (1 + B * ns))()
+ctx_h = (C.c_int32 * B)(*[int(c) for c in ctx])
+assert lib.fp_k_attn_items(ctx_h, B, max_ctx, items_h) == 0
+items = torch.tensor(list(items_h), dtype=torch.int32, device="cuda")
+
+
+def run(st):
+    r = lib.fp_k_attn_decode_ws(p(q), B, H, KVH, hd, p(pool), npages, L, layer, p(bt), maxp, p(slot), p(ctx_d),
+                                p(items), max_ctx, p(ws), p(out), C.c_void_p(st))
+    assert r == 0, r
+
+
+s = torch.cuda.Stream()
+with torch.cuda.stream(s):
+    for _ in range(3):
+        run(s.cuda_stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        run(s.cuda_stream)
+torch.cuda.synchronize()
+times = []
+for _ in range(20):
+    flush.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    times.append(e0.elapsed_time(e1))
+times.sort()
+ms = times[len(times) // 2]
+alg = float(ctx.sum()) * 2 * KVH * hd * 2 + B * H * hd * 2
+print(json.dumps({"kernel": "attn_decode_mma_kernel<64,1>", "B": B, "ctx_sum": int(ctx.sum()),
+                  "algorithmic_bytes": alg, "median_ms": ms, "achieved_GBps": alg / (ms / 1e3) / 1e9,
+                  "note": "one graph-replayed launch (fp_k_attn_decode_ws), CUDA events, L2 flushed "
+                          "(512 MiB write) before each of 20 timed launches; median"}))
