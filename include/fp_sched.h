@@ -163,6 +163,14 @@ int fp_fused_trigger(const fp_gen_sample* batch, int32_t n, const fp_gen_config*
                      int32_t* move_sample, int32_t* move_from, int32_t* move_to, int32_t* n_moves);
 
 /* gae_recursive / gae_matrix (numerics.hpp:18-25). values has T+1 entries. */
+/* balance_minibatch (workflow.hpp:63-66; workflow.cpp:160-182): LPT packing
+ * of n sample lengths into dp groups. Outputs: group_of[n] (group of each
+ * sample), order[n] (sample indices group-major, insertion order within a
+ * group) and group_off[dp+1] (group g = order[group_off[g] .. group_off[g+1])).
+ * FP_EINVAL for dp < 1 or n < dp. */
+int fp_balance_minibatch(const int32_t* lengths, int32_t n, int32_t dp, int32_t* group_of, int32_t* order,
+                         int32_t* group_off);
+
 int fp_gae_recursive(const double* rewards, const double* values, int32_t T, double gamma,
                      double lam, double* adv_out);
 int fp_gae_matrix(const double* rewards, const double* values, int32_t T, double gamma,

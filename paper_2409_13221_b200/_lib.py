@@ -146,6 +146,7 @@ SCHED_SYMBOLS = {
     "fp_result_free": (None, [_vp]),
     "fp_sweep_threshold": (C.c_int, [P(GenSample), C.c_int32, P(GenConfig), _f64p, C.c_int32, P(SweepPoint), _i32p,
                                      _i32p, _f64p]),
+    "fp_balance_minibatch": (C.c_int, [_i32p, C.c_int32, C.c_int32, _i32p, _i32p, _i32p]),
     "fp_gae_recursive": (C.c_int, [_f64p, _f64p, C.c_int32, C.c_double, C.c_double, _f64p]),
     "fp_gae_matrix": (C.c_int, [_f64p, _f64p, C.c_int32, C.c_double, C.c_double, _f64p]),
 }

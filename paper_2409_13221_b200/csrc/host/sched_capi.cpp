@@ -14,6 +14,7 @@
 #include "fp_sched.h"
 #include "fuseplan/errors.hpp"
 #include "fuseplan/genfuse.hpp"
+#include "fuseplan/minibatch.hpp"
 #include "fuseplan/numerics.hpp"
 
 struct fp_result {
@@ -340,6 +341,26 @@ static int gae_common(bool matrix, const double* rewards, const double* values, 
     in.lam = lam;
     const std::vector<double> a = matrix ? fuseplan::gae_matrix(in) : fuseplan::gae_recursive(in);
     std::memcpy(adv_out, a.data(), a.size() * sizeof(double));
+  });
+}
+
+int fp_balance_minibatch(const int32_t* lengths, int32_t n, int32_t dp, int32_t* group_of, int32_t* order,
+                         int32_t* group_off) {
+  return guarded([&] {
+    if (n < 0) throw std::invalid_argument("balance_minibatch: n must be >= 0");
+    if (n > 0) need(lengths, "lengths");
+    const std::vector<int> len(lengths, lengths + n);
+    const auto groups = fuseplan::balance_minibatch(len, dp);
+    int k = 0;
+    for (int g = 0; g < static_cast<int>(groups.size()); ++g) {
+      if (group_off) group_off[g] = k;
+      for (const int s : groups[g]) {
+        if (group_of) group_of[s] = g;
+        if (order) order[k] = s;
+        ++k;
+      }
+    }
+    if (group_off) group_off[groups.size()] = k;
   });
 }
 

@@ -103,8 +103,11 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
     fence_barrier_init();
   }
   __syncwarp();
-  pdl_wait();  // PDL-launched: q, the new K/V and the work counters come from earlier kernels
+  // items / ctx / slot / block table were uploaded before the step's first
+  // kernel: readable before griddepcontrol.wait. q, the new token's K/V and
+  // the work counters are not (they come from the kernels before this one).
   const int n_items = items[0] * KVH;
+  const int T = gridDim.x * C::kWarps;
 
   // item j -> (sample b, split, kv head): pair items[1 + j / KVH] = b << 8 |
   // split (the host lists pairs longest first), kv head j % KVH; tokens [t0, t1)
@@ -119,9 +122,9 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
   };
   // dynamic schedule: the next item from the launch-wide work counter
   int wr = 0, rd = 0;
-  auto grab = [&](Cursor& c) {
+  auto grab = [&](Cursor& c) {  // (the first T items are assigned statically)
     int j = 0;
-    if (lane == 0) j = atomicAdd(&counters[0], 1);
+    if (lane == 0) j = T + atomicAdd(&counters[0], 1);
     c.j = __shfl_sync(0xffffffffu, j, 0);
     if (lane == 0) ring[wr & 7] = c.j;
     ++wr;
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
   auto next_issue = [&](Cursor& c) {  // advance the issue cursor by one unit
     if (++c.u >= c.ue) grab(c);
   };
-  auto issue = [&](const Cursor& c, int k) {  // lane 0 only
+  auto issue = [&](const Cursor& c, int k, bool with_q = true) {  // lane 0 only
     int b, kvh, split, t0, t1;
     item_range(c.j, b, kvh, split, t0, t1);
     const int page = c.u >> 1, half = c.u & 1;
@@ -151,13 +154,38 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
       tma_load_2d(dst + sub * C::kBox, &kv_map, &bar[k], sub * 64, rk);
       tma_load_2d(dst + (C::kSub + sub) * C::kBox, &kv_map, &bar[k], sub * 64, rk + kPT);
     }
-    if (first) bulk_load(dst + C::kKV, q + (static_cast<size_t>(b) * H + kvh * G) * HD, kQBytes, &bar[k]);
+    if (first && with_q) bulk_load(dst + C::kKV, q + (static_cast<size_t>(b) * H + kvh * G) * HD, kQBytes, &bar[k]);
   };
 
-  Cursor in{0, 0, 0};  // issue cursor
-  grab(in);
-  // prologue: fill the stages
+  // issue cursor: the first item is static (warp index in the grid)
+  Cursor in{warp + static_cast<int>(blockIdx.x) * C::kWarps, 0, 0};
+  if (lane == 0) ring[wr & 7] = in.j;
+  ++wr;
+  __syncwarp();
   int issued = 0;
+  bool q_pending = false;
+  if (in.j < n_items) {
+    int b, kvh, split, t0, t1;
+    item_range(in.j, b, kvh, split, t0, t1);
+    in.u = t0 >> 5;
+    in.ue = ((t1 - 1) >> 5) + 1;
+    // Before waiting on the previous kernel: stream the units of the first
+    // item that hold only cached tokens (positions < ctx - 1, written by
+    // earlier steps); the q rows follow after the wait.
+    const int u_new = (ctx[b] - 1) >> 5;  // unit of the token appended this step
+    q_pending = true;
+    for (; issued < C::kStages && in.u < in.ue && in.u < u_new; ++issued, ++in.u)
+      if (lane == 0) issue(in, issued, false);
+  }
+  pdl_wait();
+  if (q_pending && lane == 0) {
+    int b, kvh, split, t0, t1;
+    item_range(in.j, b, kvh, split, t0, t1);
+    if (issued > 0)  // stage 0 expects the q bytes already
+      bulk_load(my_smem + C::kKV, q + (static_cast<size_t>(b) * H + kvh * G) * HD, G * HD * 2, &bar[0]);
+  }
+  if (in.j < n_items && in.u >= in.ue) grab(in);
+  // prologue: fill the remaining stages
   for (; issued < C::kStages && in.j < n_items; ++issued) {
     if (lane == 0) issue(in, issued);
     next_issue(in);

@@ -279,7 +279,9 @@ void init_bf16_gu(bf16* w, int F, int d, uint64_t seed, uint64_t tag, float scal
 
 void embed(const int* tokens, const int* idx, int M, const bf16* E, int d, float* x, cudaStream_t st) {
   if (M <= 0) return;
-  launch_pdl(embed_kernel, dim3(M), dim3(128), 0, st, tokens, idx, E, d, x);
+  // a plain launch: the step's first kernel fully orders the step after the
+  // previous one (the decode attention reads cached K/V before its PDL wait)
+  embed_kernel<<<M, 128, 0, st>>>(tokens, idx, E, d, x);
   fpk::count_launch();
 }
 

@@ -285,6 +285,15 @@ class Sched:
         check(self.lib, fn(r.ctypes.data_as(dp), v.ctypes.data_as(dp), len(r), gamma, lam, out.ctypes.data_as(dp)))
         return out[:len(r)]
 
+    def balance_minibatch(self, lengths, dp: int) -> list:
+        """balance_minibatch (workflow.hpp:63-66): sample indices per DP group."""
+        n = len(lengths)
+        ln = (C.c_int32 * max(n, 1))(*[int(x) for x in lengths])
+        order = (C.c_int32 * max(n, 1))()
+        off = (C.c_int32 * (max(dp, 0) + 1))()
+        check(self.lib, self.lib.fp_balance_minibatch(ln, n, dp, None, order, off))
+        return [list(order[off[g]:off[g + 1]]) for g in range(dp)]
+
     def gae_recursive(self, rewards, values, gamma=0.99, lam=0.95) -> np.ndarray:
         return self._gae(self.lib.fp_gae_recursive, rewards, values, gamma, lam)
 
