@@ -56,6 +56,7 @@ typedef struct fp_run_options {
   int32_t claim_tokens, run_ahead;
   int32_t resident;        /* 1: prompts already resident (same as previous call), experience kept on device */
   int32_t probe_attention; /* 1: time each decode-attention launch (stats.attn_probe_*) */
+  int32_t handoff_dp;      /* > 0: pack the experience into length-balanced DP mini-batches (fp_exec_handoff) */
 } fp_run_options;
 
 typedef struct fp_comm {
@@ -71,6 +72,7 @@ typedef struct fp_exec_stats {
   int64_t gpu_launches;
   double attn_probe_ms, attn_probe_bytes;
   int64_t attn_probe_launches;
+  double ipc_seconds;
 } fp_exec_stats;
 
 typedef struct fp_engine fp_engine;
@@ -99,6 +101,20 @@ int fp_exec_finish(const fp_exec* x, double* finish_seconds, int32_t* finish_ins
 int fp_exec_decision(const fp_exec* x, fp_result** out);
 /* Trigger / plan actually executed (fused, world > 1); moves in application order. */
 int fp_exec_moves(const fp_exec* x, int32_t* n_moves, int32_t* sample, int32_t* from, int32_t* to);
+/* Experience hand-off (handoff_dp > 0; balance_minibatch, workflow.hpp:63-66):
+ * order[n], group_off[dp+1], packed_off[n+1] (response-token offsets in
+ * order); this rank's groups [*group_begin, *group_end) and device pointers
+ * dev[9] = tokens, logp_actor, logp_ref, values, kl, reward, adv, ret, score of
+ * its packed range (engine-owned, valid until the next fp_execute). Any
+ * pointer may be NULL. */
+int fp_exec_handoff(const fp_exec* x, int32_t* dp, int32_t* group_begin, int32_t* group_end, int32_t* order,
+                    int32_t* group_off, int64_t* packed_off, void** dev, double* seconds, int64_t* bytes,
+                    int64_t* peer_bytes);
+/* Copy this rank's packed hand-off range to host buffers (sizes from
+ * fp_exec_handoff: tokens / arrays hold packed_off[group_off[end]] -
+ * packed_off[group_off[begin]] entries, score group_off[end] - group_off[begin]).
+ * host[9] in the order of dev[]; NULL entries are skipped. */
+int fp_exec_handoff_download(const fp_exec* x, void** host);
 /* Per decode step of this rank: batch rows and GPU milliseconds (n_steps entries; NULL to query). */
 int fp_exec_steps(const fp_exec* x, int32_t* n_steps, int32_t* rows, float* ms);
 void fp_exec_free(fp_exec* x);

@@ -55,6 +55,11 @@ struct EngineOptions {
   int run_ahead = 4;               // decode steps the host may enqueue ahead of the GPU
   bool resident = false;           // prompts already on the device (same ids as last call), experience left there
   bool probe_attention = false;    // time every decode-attention launch (bench roofline)
+  // > 0: hand the experience off as `handoff_dp` length-balanced data-parallel
+  // mini-batches (balance_minibatch over prompt + response lengths): rank r
+  // packs groups [r dp / world, (r + 1) dp / world) contiguously on its GPU,
+  // pulling samples scored on other GPUs over NVLink. dp % world == 0.
+  int handoff_dp = 0;
 };
 
 /// Multi-process coordination (G > 1): every rank passes the same shm name.
@@ -76,6 +81,7 @@ struct ExecStats {
   double gen_seconds = 0.0;         // this rank's last decode step end (GPU clock from start)
   double trigger_seconds = -1.0;    // trigger reached (GPU clock), -1 if none
   double migrate_seconds = 0.0;     // migration exchange (host clock)
+  double ipc_seconds = 0.0;         // opening peer mappings (host clock; cached after the first call)
   double infer_busy_seconds = 0.0;  // GPU time of this rank's scoring batches
   std::int64_t decode_steps = 0, decode_rows = 0, decode_ctx_tokens = 0;
   std::int64_t prefill_tokens = 0, infer_tokens = 0, infer_samples = 0;
@@ -84,6 +90,24 @@ struct ExecStats {
   std::int64_t gpu_launches = 0;    // kernels this rank launched
   double attn_probe_ms = 0.0, attn_probe_bytes = 0.0;  // probe_attention totals
   std::int64_t attn_probe_launches = 0;
+};
+
+// Experience hand-off (EngineOptions::handoff_dp > 0).
+struct Handoff {
+  int dp = 0;
+  std::vector<int> order;                // n sample ids, group-major (balance_minibatch)
+  std::vector<int> group_off;            // dp + 1: group g = order[group_off[g] .. group_off[g + 1])
+  std::vector<std::int64_t> packed_off;  // n + 1: response-token offsets in `order`
+  int group_begin = 0, group_end = 0;    // this rank's groups
+  // This rank's device buffers (engine-owned, valid until the next execute):
+  // response tokens [packed_off[group_off[group_begin]], packed_off[group_off[group_end]])
+  // of tokens / logp_actor, logp_ref, values, kl, reward, adv, ret, and the
+  // score of samples order[group_off[group_begin] ..], all in `order`.
+  const int* tokens = nullptr;
+  const float* arrays[7] = {};
+  const float* score = nullptr;
+  double seconds = 0.0;                   // GPU time of the pack
+  std::int64_t bytes = 0, peer_bytes = 0;  // bytes packed; of which pulled from other GPUs
 };
 
 struct ExecResult {
@@ -95,6 +119,7 @@ struct ExecResult {
   ExecStats stats;
   std::vector<int> step_rows;       // per decode step: batch rows
   std::vector<float> step_ms;       // per decode step: GPU duration (ms)
+  Handoff handoff;
 };
 
 class GpuEngine;  // opaque

@@ -109,7 +109,7 @@ class RunOptions(C.Structure):
     _fields_ = [("token_mode", C.c_int32), ("schedule", C.c_int32), ("temperature", C.c_float),
                 ("token_seed", C.c_uint64), ("sample_seed", C.c_uint64), ("kl_beta", C.c_float),
                 ("gamma", C.c_float), ("lam", C.c_float), ("claim_tokens", C.c_int32), ("run_ahead", C.c_int32),
-                ("resident", C.c_int32), ("probe_attention", C.c_int32)]
+                ("resident", C.c_int32), ("probe_attention", C.c_int32), ("handoff_dp", C.c_int32)]
 
 
 class Comm(C.Structure):
@@ -123,7 +123,7 @@ class ExecStats(C.Structure):
                 ("decode_ctx_tokens", C.c_int64), ("prefill_tokens", C.c_int64), ("infer_tokens", C.c_int64),
                 ("infer_samples", C.c_int64), ("migrated_in", C.c_int64), ("migrated_bytes", C.c_int64),
                 ("total_resp", C.c_int64), ("gpu_launches", C.c_int64), ("attn_probe_ms", C.c_double),
-                ("attn_probe_bytes", C.c_double), ("attn_probe_launches", C.c_int64)]
+                ("attn_probe_bytes", C.c_double), ("attn_probe_launches", C.c_int64), ("ipc_seconds", C.c_double)]
 
 
 P = C.POINTER
@@ -166,6 +166,9 @@ ENGINE_SYMBOLS = {
     "fp_exec_finish": (C.c_int, [_vp, _f64p, _i32p]),
     "fp_exec_decision": (C.c_int, [_vp, P(_vp)]),
     "fp_exec_moves": (C.c_int, [_vp, _i32p, _i32p, _i32p, _i32p]),
+    "fp_exec_handoff": (C.c_int, [_vp, _i32p, _i32p, _i32p, _i32p, _i32p, _i64p, P(C.c_void_p), _f64p, _i64p,
+                                  _i64p]),
+    "fp_exec_handoff_download": (C.c_int, [_vp, P(C.c_void_p)]),
     "fp_exec_steps": (C.c_int, [_vp, _i32p, _i32p, _f32p]),
     "fp_exec_free": (None, [_vp]),
     "fp_k_init_bf16": (C.c_int, [_vp, C.c_int64, C.c_uint64, C.c_uint64, C.c_float, _vp]),

@@ -201,6 +201,7 @@ int fp_execute(fp_engine* e, const fp_gen_sample* batch, int32_t n, const fp_gen
     eo.run_ahead = o->run_ahead > 0 ? o->run_ahead : 4;
     eo.resident = o->resident != 0;
     eo.probe_attention = o->probe_attention != 0;
+    eo.handoff_dp = o->handoff_dp;
     fuseplan::CommSetup cs;
     if (comm) {
       cs.rank = comm->rank;
@@ -245,6 +246,7 @@ int fp_exec_stats_get(const fp_exec* x, fp_exec_stats* s) {
     s->attn_probe_ms = t.attn_probe_ms;
     s->attn_probe_bytes = t.attn_probe_bytes;
     s->attn_probe_launches = t.attn_probe_launches;
+    s->ipc_seconds = t.ipc_seconds;
   });
 }
 
@@ -295,6 +297,46 @@ int fp_exec_moves(const fp_exec* x, int32_t* n_moves, int32_t* sample, int32_t* 
       if (sample) sample[i] = t.move_sample[i];
       if (from) from[i] = t.move_from[i];
       if (to) to[i] = t.move_to[i];
+    }
+  });
+}
+
+int fp_exec_handoff(const fp_exec* x, int32_t* dp, int32_t* group_begin, int32_t* group_end, int32_t* order,
+                    int32_t* group_off, int64_t* packed_off, void** dev, double* seconds, int64_t* bytes,
+                    int64_t* peer_bytes) {
+  return guarded([&] {
+    need(x, "exec");
+    const fuseplan::Handoff& h = x->r.handoff;
+    if (dp) *dp = h.dp;
+    if (group_begin) *group_begin = h.group_begin;
+    if (group_end) *group_end = h.group_end;
+    if (order) std::copy(h.order.begin(), h.order.end(), order);
+    if (group_off) std::copy(h.group_off.begin(), h.group_off.end(), group_off);
+    if (packed_off) std::copy(h.packed_off.begin(), h.packed_off.end(), packed_off);
+    if (dev) {
+      dev[0] = const_cast<int*>(h.tokens);
+      for (int k = 0; k < 7; ++k) dev[1 + k] = const_cast<float*>(h.arrays[k]);
+      dev[8] = const_cast<float*>(h.score);
+    }
+    if (seconds) *seconds = h.seconds;
+    if (bytes) *bytes = h.bytes;
+    if (peer_bytes) *peer_bytes = h.peer_bytes;
+  });
+}
+
+int fp_exec_handoff_download(const fp_exec* x, void** host) {
+  return guarded([&] {
+    need(x, "exec");
+    need(host, "host");
+    const fuseplan::Handoff& h = x->r.handoff;
+    if (h.dp == 0) throw std::invalid_argument("handoff: the run had handoff_dp = 0");
+    const int k0 = h.group_off[h.group_begin], k1 = h.group_off[h.group_end];
+    const size_t toks = static_cast<size_t>(h.packed_off[k1] - h.packed_off[k0]);
+    const void* src[9] = {h.tokens, h.arrays[0], h.arrays[1], h.arrays[2], h.arrays[3],
+                          h.arrays[4], h.arrays[5], h.arrays[6], h.score};
+    for (int a = 0; a < 9; ++a) {
+      const size_t bytes = (a == 8 ? static_cast<size_t>(k1 - k0) : toks) * 4;
+      if (host[a] && bytes) fpe::check(cudaMemcpy(host[a], src[a], bytes, cudaMemcpyDeviceToHost), "handoff d2h");
     }
   });
 }

@@ -126,13 +126,25 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
   FP_CUDA(cudaStreamSynchronize(s_decode_));
 }
 
+void* Engine::open_ipc(const cudaIpcMemHandle_t& h) {
+  const std::string key(reinterpret_cast<const char*>(&h), sizeof(h));
+  auto it = ipc_cache_.find(key);
+  if (it != ipc_cache_.end()) return it->second;
+  void* p = nullptr;
+  FP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  ipc_cache_.emplace(key, p);
+  return p;
+}
+
 Engine::~Engine() {
   cudaSetDevice(cfg_.device);
   cudaDeviceSynchronize();
+  for (auto& kv : ipc_cache_) cudaIpcCloseMemHandle(kv.second);
   for (void* p : allocs_) cudaFree(p);
   for (int m = 0; m < 4; ++m)
     if (models_[m].blob) cudaFree(models_[m].blob);
   if (exp_blob_) cudaFree(exp_blob_);
+  if (handoff_blob_) cudaFree(handoff_blob_);
   if (scratch_) cudaFree(scratch_);
   for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second.exec);
   for (auto& p : probes_) probe_pool_.insert(probe_pool_.end(), {p.a, p.b});
@@ -300,6 +312,26 @@ void Engine::set_layout(const std::vector<int64_t>& resp_off) {
   float** fs[7] = {&exp_.logp_actor, &exp_.logp_ref, &exp_.values, &exp_.kl, &exp_.reward, &exp_.adv, &exp_.ret};
   for (int i = 0; i < 7; ++i) *fs[i] = reinterpret_cast<float*>(p + (i + 1) * al);
   exp_.score = reinterpret_cast<float*>(p + 8 * al);
+}
+
+const Engine::Experience& Engine::handoff_buffers(int64_t tokens, int n) {
+  const size_t al = (static_cast<size_t>(std::max<int64_t>(tokens, 1)) * 4 + 255) & ~size_t(255);
+  const size_t bytes = 8 * al + ((static_cast<size_t>(std::max(n, 1)) * 4 + 255) & ~size_t(255));
+  if (bytes > handoff_bytes_) {
+    if (handoff_blob_) {
+      FP_CUDA(cudaDeviceSynchronize());
+      cudaFree(handoff_blob_);
+    }
+    FP_CUDA(cudaMalloc(&handoff_blob_, bytes));
+    handoff_bytes_ = bytes;
+  }
+  uint8_t* p = static_cast<uint8_t*>(handoff_blob_);
+  hand_.tokens = reinterpret_cast<int*>(p);
+  float** fs[7] = {&hand_.logp_actor, &hand_.logp_ref, &hand_.values, &hand_.kl, &hand_.reward, &hand_.adv,
+                   &hand_.ret};
+  for (int i = 0; i < 7; ++i) *fs[i] = reinterpret_cast<float*>(p + (i + 1) * al);
+  hand_.score = reinterpret_cast<float*>(p + 8 * al);
+  return hand_;
 }
 
 int Engine::reserve(int tokens) {

@@ -150,6 +150,10 @@ class Engine {
           *adv = nullptr, *ret = nullptr, *score = nullptr;
   };
   const Experience& experience() const { return exp_; }
+  void* exp_blob() const { return exp_blob_; }  // one cudaMalloc holding the arrays above (IPC-exportable)
+  // Hand-off destination: `tokens` response entries of the 8 arrays + `n` scores
+  // (reallocated when too small; same member layout as Experience).
+  const Experience& handoff_buffers(int64_t tokens, int n);
   const std::vector<int64_t>& resp_off() const { return resp_off_; }
 
   // Async host -> device copy on `st` through a pinned staging ring (the host
@@ -163,6 +167,11 @@ class Engine {
   void* decode_scratch(size_t bytes);
 
   void synchronize();
+
+  // Peer mapping of another process's allocation (CUDA IPC). Mappings are cached
+  // for the engine's lifetime: the peers' KV pools / histories are persistent,
+  // and opening a multi-GB pool costs milliseconds per call.
+  void* open_ipc(const cudaIpcMemHandle_t& h);
 
   // Kernel probe: when enabled, every decode-attention launch is bracketed by
   // CUDA events on the decode stream and its algorithmic bytes recorded
@@ -262,12 +271,16 @@ class Engine {
   PackedWs pre_, inf_;
   Experience exp_;
   void* exp_blob_ = nullptr;
+  void* handoff_blob_ = nullptr;
+  size_t handoff_bytes_ = 0;
+  Experience hand_;
   std::vector<int64_t> resp_off_;
   DecodeWs dec_;
   PinnedRing* ring_ = nullptr;
   void* scratch_ = nullptr;
   size_t scratch_bytes_ = 0;
   std::vector<void*> allocs_;
+  std::map<std::string, void*> ipc_cache_;
   void* dalloc(size_t bytes);
 };
 

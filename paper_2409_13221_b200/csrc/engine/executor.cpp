@@ -38,6 +38,7 @@
 #include <unordered_map>
 
 #include "engine.hpp"
+#include "fuseplan/minibatch.hpp"
 #include "fuseplan/engine.hpp"
 #include "fuseplan/errors.hpp"
 #include "philox.cuh"
@@ -79,6 +80,7 @@ struct Header {
   std::atomic<int> lock;       // publish lock
   int world, n, max_pages, pad_;
   cudaIpcMemHandle_t h_hist_tok[kMaxRanks], h_hist_logp[kMaxRanks], h_pool[kMaxRanks];
+  cudaIpcMemHandle_t h_exp[kMaxRanks];  // experience arrays (hand-off)
 };
 
 class Region {
@@ -87,7 +89,8 @@ class Region {
       : world_(comm.world), rank_(comm.rank), n_(n), max_pages_(max_pages), total_(total_resp) {
     off_pub_ = align(sizeof(Header));
     off_owner_ = align(off_pub_ + n * 4);
-    off_pages_ = align(off_owner_ + n * 4);
+    off_scorer_ = align(off_owner_ + n * 4);
+    off_pages_ = align(off_scorer_ + n * 4);
     off_res_ = align(off_pages_ + static_cast<size_t>(n) * max_pages * 4);
     bytes_ = align(off_res_ + static_cast<size_t>(total_resp) * 4 * 8 + n * 4);
     if (world_ == 1) {
@@ -114,6 +117,7 @@ class Region {
   Header* hdr() { return hdr_; }
   int* pub_order() { return reinterpret_cast<int*>(base_ + off_pub_); }
   int* owner() { return reinterpret_cast<int*>(base_ + off_owner_); }
+  int* scorer() { return reinterpret_cast<int*>(base_ + off_scorer_); }  // rank holding the sample's experience
   int* pages(int sid) { return reinterpret_cast<int*>(base_ + off_pages_) + static_cast<size_t>(sid) * max_pages_; }
   float* result(int k) { return reinterpret_cast<float*>(base_ + off_res_) + static_cast<size_t>(k) * total_; }
   float* score() { return reinterpret_cast<float*>(base_ + off_res_) + static_cast<size_t>(8) * total_; }
@@ -138,7 +142,7 @@ class Region {
   static size_t align(size_t x) { return (x + 255) & ~size_t(255); }
   int world_, rank_, n_, max_pages_;
   int64_t total_;
-  size_t off_pub_ = 0, off_owner_ = 0, off_pages_ = 0, off_res_ = 0, bytes_ = 0;
+  size_t off_pub_ = 0, off_owner_ = 0, off_scorer_ = 0, off_pages_ = 0, off_res_ = 0, bytes_ = 0;
   std::unique_ptr<uint8_t[]> local_;
   uint8_t* base_ = nullptr;
   Header* hdr_ = nullptr;
@@ -271,17 +275,14 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
     FP_CUDA(cudaIpcGetMemHandle(&hdr->h_hist_logp[me], E.d_hist_logp()));
     FP_CUDA(cudaIpcGetMemHandle(&hdr->h_pool[me], E.pool_base()));
     region.barrier();
+    const auto ti = Clock::now();
     for (int r = 0; r < G; ++r) {
       if (r == me) continue;
-      void *a = nullptr, *b = nullptr, *c = nullptr;
-      FP_CUDA(cudaIpcOpenMemHandle(&a, hdr->h_hist_tok[r], cudaIpcMemLazyEnablePeerAccess));
-      FP_CUDA(cudaIpcOpenMemHandle(&b, hdr->h_hist_logp[r], cudaIpcMemLazyEnablePeerAccess));
-      FP_CUDA(cudaIpcOpenMemHandle(&c, hdr->h_pool[r], cudaIpcMemLazyEnablePeerAccess));
-      peer_tok[r] = static_cast<const int*>(a);
-      peer_logp[r] = static_cast<const float*>(b);
-      peer_pool[r] = static_cast<const uint8_t*>(c);
-      opened.insert(opened.end(), {a, b, c});
+      peer_tok[r] = static_cast<const int*>(E.open_ipc(hdr->h_hist_tok[r]));
+      peer_logp[r] = static_cast<const float*>(E.open_ipc(hdr->h_hist_logp[r]));
+      peer_pool[r] = static_cast<const uint8_t*>(E.open_ipc(hdr->h_pool[r]));
     }
+    res.stats.ipc_seconds += std::chrono::duration<double>(Clock::now() - ti).count();
   }
 
   E.set_layout(resp_off);
@@ -656,6 +657,97 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
   E.synchronize();
   cudaEvent_t ev_end = new_event(sd);
   FP_CUDA(cudaEventSynchronize(ev_end));
+
+  // ---- experience hand-off (length-balanced DP mini-batches) ----------------------------
+  if (opts.handoff_dp > 0) {
+    const int dp = opts.handoff_dp;
+    if (dp % G != 0) throw std::invalid_argument("handoff_dp must be a multiple of the world size");
+    Handoff& h = res.handoff;
+    std::vector<int> lens(n);
+    for (int s = 0; s < n; ++s) lens[s] = batch[s].prompt_len + batch[s].target_output_len;
+    const auto groups = fuseplan::balance_minibatch(lens, dp);
+    h.dp = dp;
+    h.group_off.assign(1, 0);
+    for (const auto& g : groups) {
+      h.order.insert(h.order.end(), g.begin(), g.end());
+      h.group_off.push_back(static_cast<int>(h.order.size()));
+    }
+    h.packed_off.assign(n + 1, 0);
+    for (int k = 0; k < n; ++k) h.packed_off[k + 1] = h.packed_off[k] + batch[h.order[k]].target_output_len;
+    h.group_begin = me * dp / G;
+    h.group_end = (me + 1) * dp / G;
+    // where each sample's experience lives (the rank that scored it)
+    for (int sid : my_scored) region.scorer()[sid] = me;
+    std::vector<uint8_t*> exp_base(G, nullptr);
+    exp_base[me] = static_cast<uint8_t*>(E.exp_blob());
+    if (G > 1) {
+      FP_CUDA(cudaIpcGetMemHandle(&hdr->h_exp[me], E.exp_blob()));
+      region.barrier();
+      // not cached: the experience blob is reallocated when the batch layout changes
+      const auto ti = Clock::now();
+      for (int r = 0; r < G; ++r) {
+        if (r == me) continue;
+        void* p = nullptr;
+        FP_CUDA(cudaIpcOpenMemHandle(&p, hdr->h_exp[r], cudaIpcMemLazyEnablePeerAccess));
+        exp_base[r] = static_cast<uint8_t*>(p);
+        opened.push_back(p);
+      }
+      res.stats.ipc_seconds += std::chrono::duration<double>(Clock::now() - ti).count();
+    }
+    // array offsets inside an experience blob (identical layout on every rank)
+    const fpe::Engine::Experience& X0 = E.experience();
+    const uint8_t* b0 = exp_base[me];
+    const size_t aoff[9] = {
+        static_cast<size_t>(reinterpret_cast<const uint8_t*>(X0.tokens) - b0),
+        static_cast<size_t>(reinterpret_cast<const uint8_t*>(X0.logp_actor) - b0),
+        static_cast<size_t>(reinterpret_cast<const uint8_t*>(X0.logp_ref) - b0),
+        static_cast<size_t>(reinterpret_cast<const uint8_t*>(X0.values) - b0),
+        static_cast<size_t>(reinterpret_cast<const uint8_t*>(X0.kl) - b0),
+        static_cast<size_t>(reinterpret_cast<const uint8_t*>(X0.reward) - b0),
+        static_cast<size_t>(reinterpret_cast<const uint8_t*>(X0.adv) - b0),
+        static_cast<size_t>(reinterpret_cast<const uint8_t*>(X0.ret) - b0),
+        static_cast<size_t>(reinterpret_cast<const uint8_t*>(X0.score) - b0)};
+    const int k0 = h.group_off[h.group_begin], k1 = h.group_off[h.group_end];
+    const int64_t t0 = h.packed_off[k0];
+    const fpe::Engine::Experience& D = E.handoff_buffers(h.packed_off[k1] - t0, k1 - k0);
+    uint8_t* dbase[9] = {reinterpret_cast<uint8_t*>(D.tokens), reinterpret_cast<uint8_t*>(D.logp_actor),
+                         reinterpret_cast<uint8_t*>(D.logp_ref), reinterpret_cast<uint8_t*>(D.values),
+                         reinterpret_cast<uint8_t*>(D.kl), reinterpret_cast<uint8_t*>(D.reward),
+                         reinterpret_cast<uint8_t*>(D.adv), reinterpret_cast<uint8_t*>(D.ret),
+                         reinterpret_cast<uint8_t*>(D.score)};
+    std::vector<fpk::CopyChunk> chunks;
+    for (int k = k0; k < k1; ++k) {
+      const int sid = h.order[k];
+      const int src = region.scorer()[sid];
+      const int64_t R = batch[sid].target_output_len;
+      for (int a = 0; a < 9; ++a) {
+        const bool per_sample = a == 8;
+        const uint8_t* sp = exp_base[src] + aoff[a] + (per_sample ? static_cast<size_t>(sid) : resp_off[sid]) * 4;
+        uint8_t* dpp = dbase[a] + (per_sample ? static_cast<size_t>(k - k0) : h.packed_off[k] - t0) * 4;
+        const uint64_t bytes = static_cast<uint64_t>(per_sample ? 1 : R) * 4;
+        if (bytes == 0) continue;
+        chunks.push_back({sp, dpp, bytes});
+        h.bytes += static_cast<int64_t>(bytes);
+        if (src != me) h.peer_bytes += static_cast<int64_t>(bytes);
+      }
+    }
+    cudaEvent_t hb = new_event(sd);
+    if (!chunks.empty()) {
+      void* dl = E.decode_scratch(chunks.size() * sizeof(fpk::CopyChunk));
+      E.upload(dl, chunks.data(), chunks.size() * sizeof(fpk::CopyChunk), sd);
+      fpk::copy_words(static_cast<const fpk::CopyChunk*>(dl), static_cast<int>(chunks.size()), sd);
+    }
+    cudaEvent_t he = new_event(sd);
+    FP_CUDA(cudaEventSynchronize(he));
+    h.seconds = ms_between(hb, he) * 1e-3;
+    h.tokens = D.tokens;
+    const float* fa[7] = {D.logp_actor, D.logp_ref, D.values, D.kl, D.reward, D.adv, D.ret};
+    for (int a = 0; a < 7; ++a) h.arrays[a] = fa[a];
+    h.score = D.score;
+    region.barrier();  // every rank has pulled before any blob may change
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    opened.clear();
+  }
 
   // ---- stats ------------------------------------------------------------------------------
   res.stats.gen_seconds = step_end.empty() ? 0.0 : ms_between(ev_start, step_end.back()) * 1e-3;

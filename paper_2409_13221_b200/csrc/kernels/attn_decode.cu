@@ -72,10 +72,20 @@ struct DecCfg {
   static constexpr int kSmem = kWarps * kStages * kStageBytes + 1024;
 };
 
-struct Cursor {
-  int j;      // item index (grid-strided)
-  int u, ue;  // current / end unit (32-token) index of the item
+// A decoded work item: (sample b, split, kv head), its token range [t0, t1),
+// the sample's context cx and number of non-empty splits nsb.
+struct DecItem {
+  int j, b, kvh, split, t0, t1, cx, nsb;
 };
+// Issue cursor: the item, its current / end 32-token unit, and (lane l) the
+// pool page id of the item's l-th 64-token page — fetched once per item, so
+// issuing a unit needs no dependent global load.
+struct Cursor {
+  DecItem it;
+  int u, ue;
+  int pg;
+};
+static_assert(kDecodeChunk / 64 <= 32, "an item's pages must fit one per lane");
 
 template <int HD, int G>
 __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_kernel(
@@ -91,12 +101,12 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full_bar[C::kWarps][C::kStages];
 
-  __shared__ int ring_s[C::kWarps][8];  // items grabbed by the issue cursor, in order, for the consumer
+  __shared__ int4 ring_s[C::kWarps][8][2];  // items decoded by the issue cursor, in order, for the consumer
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* bar = full_bar[warp];
   uint8_t* my_smem = smem + warp * C::kStages * C::kStageBytes;
-  int* ring = ring_s[warp];
+  int4(*ring)[2] = ring_s[warp];
   if (lane == 0) {
     if (warp == 0) tma_prefetch_desc(&kv_map);
     for (int s = 0; s < C::kStages; ++s) mbar_init(&bar[s], 1);
@@ -110,43 +120,51 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
   const int T = gridDim.x * C::kWarps;
 
   // item j -> (sample b, split, kv head): pair items[1 + j / KVH] = b << 8 |
-  // split (the host lists pairs longest first), kv head j % KVH; tokens [t0, t1)
-  auto item_range = [&](int j, int& b, int& kvh, int& split, int& t0, int& t1) {
+  // split (the host lists pairs longest first), kv head j % KVH
+  auto decode = [&](int j, DecItem& it) {
+    it.j = j;
+    if (j >= n_items) return;
     const int pr = j / KVH;
-    kvh = j - pr * KVH;
+    it.kvh = j - pr * KVH;
     const int e = items[1 + pr];
-    b = e >> 8;
-    split = e & 255;
-    t0 = split * kDecodeChunk;
-    t1 = min(ctx[b], t0 + kDecodeChunk);
+    it.b = e >> 8;
+    it.split = e & 255;
+    it.cx = ctx[it.b];
+    it.t0 = it.split * kDecodeChunk;
+    it.t1 = min(it.cx, it.t0 + kDecodeChunk);
+    it.nsb = (it.cx + kDecodeChunk - 1) / kDecodeChunk;
   };
-  // dynamic schedule: the next item from the launch-wide work counter
   int wr = 0, rd = 0;
-  auto grab = [&](Cursor& c) {  // (the first T items are assigned statically)
+  auto begin_item = [&](Cursor& c) {  // all lanes: page ids, hand the item to the consumer
+    if (lane == 0) {
+      ring[wr & 7][0] = make_int4(c.it.j, c.it.b, c.it.kvh, c.it.split);
+      ring[wr & 7][1] = make_int4(c.it.t0, c.it.t1, c.it.cx, c.it.nsb);
+    }
+    ++wr;
+    if (c.it.j < n_items) {
+      c.u = c.it.t0 >> 5;
+      c.ue = ((c.it.t1 - 1) >> 5) + 1;
+      const int p0 = c.it.t0 >> 6, np = ((c.it.t1 - 1) >> 6) - p0 + 1;
+      c.pg = lane < np ? block_table[slot[c.it.b] * bt_stride + p0 + lane] : 0;
+    }
+    __syncwarp();
+  };
+  // dynamic schedule: the first T items are static, then a launch-wide counter
+  auto grab = [&](Cursor& c) {
     int j = 0;
     if (lane == 0) j = T + atomicAdd(&counters[0], 1);
-    c.j = __shfl_sync(0xffffffffu, j, 0);
-    if (lane == 0) ring[wr & 7] = c.j;
-    ++wr;
-    __syncwarp();
-    if (c.j < n_items) {
-      int b, kvh, split, t0, t1;
-      item_range(c.j, b, kvh, split, t0, t1);
-      c.u = t0 >> 5;
-      c.ue = ((t1 - 1) >> 5) + 1;
-    }
+    decode(__shfl_sync(0xffffffffu, j, 0), c.it);
+    begin_item(c);
   };
   auto next_issue = [&](Cursor& c) {  // advance the issue cursor by one unit
     if (++c.u >= c.ue) grab(c);
   };
-  auto issue = [&](const Cursor& c, int k, bool with_q = true) {  // lane 0 only
-    int b, kvh, split, t0, t1;
-    item_range(c.j, b, kvh, split, t0, t1);
-    const int page = c.u >> 1, half = c.u & 1;
-    const int pid = block_table[slot[b] * bt_stride + page];
-    const int rk = pid * rows_per_page + layer * layer_rows + kvh * 2 * kPT + half * 32;
+  auto issue = [&](const Cursor& c, int k, bool with_q = true) {  // all lanes (lane 0 issues)
+    const int pid = __shfl_sync(0xffffffffu, c.pg, (c.u >> 1) - (c.it.t0 >> 6));
+    if (lane != 0) return;
+    const int rk = pid * rows_per_page + layer * layer_rows + c.it.kvh * 2 * kPT + (c.u & 1) * 32;
     uint8_t* dst = my_smem + k * C::kStageBytes;
-    const bool first = c.u == (t0 >> 5);
+    const bool first = c.u == (c.it.t0 >> 5);
     constexpr uint32_t kQBytes = G * HD * 2;
     mbar_arrive_expect_tx(&bar[k], C::kKV + (first ? kQBytes : 0u));
 #pragma unroll
@@ -154,64 +172,53 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
       tma_load_2d(dst + sub * C::kBox, &kv_map, &bar[k], sub * 64, rk);
       tma_load_2d(dst + (C::kSub + sub) * C::kBox, &kv_map, &bar[k], sub * 64, rk + kPT);
     }
-    if (first && with_q) bulk_load(dst + C::kKV, q + (static_cast<size_t>(b) * H + kvh * G) * HD, kQBytes, &bar[k]);
+    if (first && with_q)
+      bulk_load(dst + C::kKV, q + (static_cast<size_t>(c.it.b) * H + c.it.kvh * G) * HD, kQBytes, &bar[k]);
   };
 
   // issue cursor: the first item is static (warp index in the grid)
-  Cursor in{warp + static_cast<int>(blockIdx.x) * C::kWarps, 0, 0};
-  if (lane == 0) ring[wr & 7] = in.j;
-  ++wr;
-  __syncwarp();
+  Cursor in;
+  decode(warp + static_cast<int>(blockIdx.x) * C::kWarps, in.it);
+  begin_item(in);
   int issued = 0;
-  bool q_pending = false;
-  if (in.j < n_items) {
-    int b, kvh, split, t0, t1;
-    item_range(in.j, b, kvh, split, t0, t1);
-    in.u = t0 >> 5;
-    in.ue = ((t1 - 1) >> 5) + 1;
+  if (in.it.j < n_items) {
     // Before waiting on the previous kernel: stream the units of the first
     // item that hold only cached tokens (positions < ctx - 1, written by
     // earlier steps); the q rows follow after the wait.
-    const int u_new = (ctx[b] - 1) >> 5;  // unit of the token appended this step
-    q_pending = true;
-    for (; issued < C::kStages && in.u < in.ue && in.u < u_new; ++issued, ++in.u)
-      if (lane == 0) issue(in, issued, false);
+    const int u_new = (in.it.cx - 1) >> 5;  // unit of the token appended this step
+    for (; issued < C::kStages && in.u < in.ue && in.u < u_new; ++issued, ++in.u) issue(in, issued, false);
   }
   pdl_wait();
-  if (q_pending && lane == 0) {
-    int b, kvh, split, t0, t1;
-    item_range(in.j, b, kvh, split, t0, t1);
-    if (issued > 0)  // stage 0 expects the q bytes already
-      bulk_load(my_smem + C::kKV, q + (static_cast<size_t>(b) * H + kvh * G) * HD, G * HD * 2, &bar[0]);
-  }
-  if (in.j < n_items && in.u >= in.ue) grab(in);
+  if (issued > 0 && lane == 0)  // stage 0 (the item's first unit) already expects the q bytes
+    bulk_load(my_smem + C::kKV, q + (static_cast<size_t>(in.it.b) * H + in.it.kvh * G) * HD, G * HD * 2, &bar[0]);
+  if (in.it.j < n_items && in.u >= in.ue) grab(in);
   // prologue: fill the remaining stages
-  for (; issued < C::kStages && in.j < n_items; ++issued) {
-    if (lane == 0) issue(in, issued);
+  for (; issued < C::kStages && in.it.j < n_items; ++issued) {
+    issue(in, issued);
     next_issue(in);
   }
-  Cursor cur{ring[rd & 7], 0, 0};  // consume cursor: the issue cursor's items, in order
-  ++rd;
-  if (cur.j < n_items) {
-    int b, kvh, split, t0, t1;
-    item_range(cur.j, b, kvh, split, t0, t1);
-    cur.u = t0 >> 5;
-    cur.ue = ((t1 - 1) >> 5) + 1;
-  }
+  // consume cursor: the issue cursor's items, in order
+  DecItem cur;
+  auto pop = [&]() {
+    const int4 x = ring[rd & 7][0], y = ring[rd & 7][1];
+    ++rd;
+    cur = DecItem{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+  };
+  pop();
+  int cu = cur.t0 >> 5, cue = ((cur.t1 - 1) >> 5) + 1;
 
   const int r0 = lane >> 2;
   const uint32_t base = smem_u32(my_smem);
   uint32_t qa[HD / 16][4];
   float o[HD / 8][4];
   float m_run = -INFINITY, l_run = 0.f;
-  int cur_j = -1, b = 0, kvh = 0, split = 0, t0 = 0, t1 = 0;
+  bool fresh = true;
 
   for (int c = 0; cur.j < n_items; ++c) {
     const int k = c % C::kStages;
     mbar_wait(&bar[k], (c / C::kStages) & 1);
-    if (cur.j != cur_j) {  // new item: Q fragments from the stage's q slot, reset the running state
-      cur_j = cur.j;
-      item_range(cur_j, b, kvh, split, t0, t1);
+    if (fresh) {  // new item: Q fragments from the stage's q slot, reset the running state
+      fresh = false;
       const bf16* qs = reinterpret_cast<const bf16*>(my_smem + k * C::kStageBytes + C::kKV);
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk) {
@@ -229,8 +236,8 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
     }
     const uint32_t Kt = base + k * C::kStageBytes;
     const uint32_t Vt = Kt + C::kSub * C::kBox;
-    const int ut0 = cur.u * 32;
-    const int lo = max(t0, ut0) - ut0, hi = min(t1, ut0 + 32) - ut0;
+    const int ut0 = cu * 32;
+    const int lo = max(cur.t0, ut0) - ut0, hi = min(cur.t1, ut0 + 32) - ut0;
 
     // S = Q K^T over 32 tokens (4 n-tiles of 8)
     float sc[4][4];
@@ -301,17 +308,14 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
     }
     // refill this stage with the unit kStages ahead
     __syncwarp();
-    if (in.j < n_items) {
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(in, k);
-      }
+    if (in.it.j < n_items) {
+      if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(in, k);
       next_issue(in);
     }
     // advance the consume cursor; flush the item's partial when it ends
-    ++cur.u;
-    if (cur.u >= cur.ue) {
-      const int nsb = (ctx[b] + kDecodeChunk - 1) / kDecodeChunk;  // non-empty splits of this sample
+    if (++cu >= cue) {
+      const int nsb = cur.nsb, b = cur.b, kvh = cur.kvh, split = cur.split;
       const size_t row0 = static_cast<size_t>(b) * H + kvh * G;
       if (nsb == 1) {
         // single split: the combine is the identity (f = 1), normalise here
@@ -347,14 +351,10 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
                                                   out + (row0 + g) * HD);
         }
       }
-      cur.j = ring[rd & 7];
-      ++rd;
-      if (cur.j < n_items) {
-        int bb, kk, ss, a0, a1;
-        item_range(cur.j, bb, kk, ss, a0, a1);
-        cur.u = a0 >> 5;
-        cur.ue = ((a1 - 1) >> 5) + 1;
-      }
+      pop();
+      cu = cur.t0 >> 5;
+      cue = ((cur.t1 - 1) >> 5) + 1;
+      fresh = true;
     }
   }
   // the last warp out resets the work counter for the next launch

@@ -285,6 +285,29 @@ void embed(const int* tokens, const int* idx, int M, const bf16* E, int d, float
   fpk::count_launch();
 }
 
+// 4-byte granular gather (experience hand-off: response segments start at
+// arbitrary token offsets); 16-byte vectors when both ends are aligned.
+__global__ void copy_words_kernel(const CopyChunk* __restrict__ list) {
+  const CopyChunk c = list[blockIdx.x];
+  const size_t n = c.bytes / 4;
+  const uint32_t* src = static_cast<const uint32_t*>(c.src);
+  uint32_t* dst = static_cast<uint32_t*>(c.dst);
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+    const size_t n4 = n / 4;
+    for (size_t i = threadIdx.x; i < n4; i += blockDim.x)
+      reinterpret_cast<int4*>(dst)[i] = reinterpret_cast<const int4*>(src)[i];
+    for (size_t i = n4 * 4 + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  } else {
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+void copy_words(const CopyChunk* d_list, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  copy_words_kernel<<<n, 128, 0, st>>>(d_list);
+  fpk::count_launch();
+}
+
 void copy_chunks(const CopyChunk* d_list, int n, cudaStream_t st) {
   if (n <= 0) return;
   copy_chunks_kernel<<<n, 256, 0, st>>>(d_list); fpk::count_launch();

@@ -193,6 +193,8 @@ void postprocess(int n, const int* off, const float* logp_actor, const float* lo
 // rows): one CTA per chunk, 16-byte vector loads; src/dst/bytes 16-aligned.
 struct CopyChunk { const void* src; void* dst; unsigned long long bytes; };
 void copy_chunks(const CopyChunk* d_list, int n, cudaStream_t st);
+// The same at 4-byte granularity (src/dst/bytes multiples of 4).
+void copy_words(const CopyChunk* d_list, int n, cudaStream_t st);
 // cur_tok[slot[i]] = gen[i] > 0 ? hist[sid[i]][gen[i]-1] : prompts[sid[i]][P[i]-1]
 void cur_from_hist(const int* d_quad, int n, const int* hist_tok, int max_new, const int* prompts, int max_prompt,
                    int* cur_tok, cudaStream_t st);  // d_quad: [4][n] = slot, sid, gen, P

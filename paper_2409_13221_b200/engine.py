@@ -55,6 +55,7 @@ class ExecOutput:
     moves: list       # (sample, from, to) in application order
     step_rows: np.ndarray = None  # per decode step of this rank: batch rows
     step_ms: np.ndarray = None    # per decode step: GPU ms
+    handoff: dict = None          # handoff_dp > 0: order, group_off, packed_off, this rank's packed arrays
 
 
 class Engine:
@@ -94,6 +95,31 @@ class Engine:
         check(self.lib, self.lib.fp_engine_kv_bytes_per_token(self.h, C.byref(v)))
         return v.value
 
+    def _handoff(self, x, n: int) -> dict:
+        dp, gb, ge = C.c_int32(), C.c_int32(), C.c_int32()
+        check(self.lib, self.lib.fp_exec_handoff(x, C.byref(dp), None, None, None, None, None, None, None, None,
+                                                 None))
+        order = np.zeros(n, dtype=np.int32)
+        goff = np.zeros(dp.value + 1, dtype=np.int32)
+        poff = np.zeros(n + 1, dtype=np.int64)
+        sec, nb, pb = C.c_double(), C.c_int64(), C.c_int64()
+        i32 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))  # noqa: E731
+        check(self.lib, self.lib.fp_exec_handoff(x, C.byref(dp), C.byref(gb), C.byref(ge), i32(order), i32(goff),
+                                                 poff.ctypes.data_as(C.POINTER(C.c_int64)), None, C.byref(sec),
+                                                 C.byref(nb), C.byref(pb)))
+        k0, k1 = goff[gb.value], goff[ge.value]
+        T = int(poff[k1] - poff[k0])
+        arrays = [np.zeros(max(T, 1), dtype=np.int32)] + [np.zeros(max(T, 1), dtype=np.float32) for _ in range(7)]
+        score = np.zeros(max(k1 - k0, 1), dtype=np.float32)
+        host = (C.c_void_p * 9)(*[a.ctypes.data for a in arrays], score.ctypes.data)
+        check(self.lib, self.lib.fp_exec_handoff_download(x, host))
+        names = ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret")
+        out = {"dp": dp.value, "order": order, "group_off": goff, "packed_off": poff, "group_begin": gb.value,
+               "group_end": ge.value, "seconds": sec.value, "bytes": nb.value, "peer_bytes": pb.value,
+               "score": score[:k1 - k0]}
+        out.update({k: a[:T] for k, a in zip(names, arrays)})
+        return out
+
     def synthetic_prompts(self, n: int, token_seed: int) -> np.ndarray:
         out = np.zeros((n, self.setup.max_prompt), dtype=np.int32)
         check(self.lib, self.lib.fp_synthetic_prompts(self.h, n, token_seed,
@@ -105,11 +131,12 @@ class Engine:
                 kl_beta: float = 0.05, gamma: float = 1.0, lam: float = 0.95, claim_tokens: int = 8192,
                 run_ahead: int = 4, rank: int = 0, world: int = 1, shm_name: str | None = None,
                 prompts: np.ndarray | None = None, resident: bool = False,
-                probe_attention: bool = False) -> ExecOutput:
+                probe_attention: bool = False, handoff_dp: int = 0) -> ExecOutput:
         keep: list = []
         n = len(batch)
         opts = _lib.RunOptions(TOKEN_MODES[token_mode], SCHEDULES[schedule], temperature, token_seed, sample_seed,
-                               kl_beta, gamma, lam, claim_tokens, run_ahead, int(resident), int(probe_attention))
+                               kl_beta, gamma, lam, claim_tokens, run_ahead, int(resident), int(probe_attention),
+                               handoff_dp)
         comm = _lib.Comm(rank, world, shm_name.encode() if shm_name else None)
         pp = None
         if prompts is not None:
@@ -156,6 +183,7 @@ class Engine:
             sms = np.zeros(max(ns.value, 1), dtype=np.float32)
             check(self.lib, self.lib.fp_exec_steps(x, C.byref(ns), srows.ctypes.data_as(C.POINTER(C.c_int32)),
                                                    sms.ctypes.data_as(C.POINTER(C.c_float))))
-            return ExecOutput(stats, exp, fin, inst, decision, moves, srows[:ns.value], sms[:ns.value])
+            handoff = self._handoff(x, n) if handoff_dp > 0 else None
+            return ExecOutput(stats, exp, fin, inst, decision, moves, srows[:ns.value], sms[:ns.value], handoff)
         finally:
             self.lib.fp_exec_free(x)

@@ -47,7 +47,9 @@ def main():
     res = {}
     for rep in range(2):
         out = eng.execute(batch, cfg, r_t, token_mode=mode, schedule="fused", claim_tokens=2048, rank=rank,
-                          world=world, shm_name=name[0] + f"_{rep}")
+                          world=world, shm_name=name[0] + f"_{rep}", handoff_dp=2 * world if rep else 0)
+    h = out.handoff
+    np.savez(f"{out_path}.rank{rank}.npz", **{k: np.asarray(v) for k, v in h.items()})
     res["stats"] = out.stats
     res["moves"] = out.moves
     ref_moves = None
@@ -71,6 +73,21 @@ def main():
         res["max_abs"] = {k: float(np.max(np.abs(getattr(a, k).astype(np.float64) - getattr(b, k))))
                           for k in ("logp_actor", "logp_ref", "values", "adv", "ret")}
         res["n"] = len(batch)
+        # hand-off: every rank's packed DP groups == the gathered experience in
+        # balance_minibatch order (pulled over NVLink from the scoring ranks)
+        x = out.experience
+        ho_ok, peer = True, 0
+        for r in range(world):
+            hr = np.load(f"{out_path}.rank{r}.npz")
+            k0, k1 = hr["group_off"][int(hr["group_begin"])], hr["group_off"][int(hr["group_end"])]
+            ids = hr["order"][k0:k1]
+            idx = np.concatenate([np.arange(x.resp_off[s], x.resp_off[s + 1]) for s in ids])
+            for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret"):
+                ho_ok &= bool(np.array_equal(hr[k], getattr(x, k)[idx]))
+            ho_ok &= bool(np.array_equal(hr["score"], x.score[ids]))
+            peer += int(hr["peer_bytes"])
+        res["handoff_ok"] = ho_ok
+        res["handoff_peer_bytes"] = peer
         eng1.close()
         Path(out_path).write_text(json.dumps(res, default=lambda o: o if not hasattr(o, "__dict__") else o.__dict__))
     dist.barrier()

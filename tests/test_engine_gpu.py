@@ -84,3 +84,24 @@ def test_greedy_agreement_rate(toy):
     rate = agree / total
     print(f"greedy prefix agreement rate vs fp32 oracle: {rate:.4f} ({agree}/{total})")
     assert rate >= 0.5
+
+
+@pytest.mark.parametrize("dp", [1, 3, 4])
+def test_handoff_packs_balanced_minibatches(toy, dp):
+    """Experience hand-off: the packed DP mini-batches are the
+    experience gathered in balance_minibatch order, bit for bit."""
+    from paper_2409_13221_b200.configs import gen_config
+    w, eng, batch, _ = toy
+    out = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="fused", claim_tokens=512,
+                      handoff_dp=dp)
+    h = out.handoff
+    lens = [b.prompt_len + b.target_output_len for b in batch]
+    groups = eng.sched.balance_minibatch(lens, dp)
+    assert [list(h["order"][h["group_off"][g]:h["group_off"][g + 1]]) for g in range(dp)] == groups
+    assert (h["group_begin"], h["group_end"]) == (0, dp)
+    x = out.experience
+    idx = np.concatenate([np.arange(x.resp_off[s], x.resp_off[s + 1]) for s in h["order"]])
+    for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret"):
+        assert np.array_equal(h[k], getattr(x, k)[idx]), k
+    assert np.array_equal(h["score"], x.score[h["order"]])
+    assert h["bytes"] == 4 * (8 * len(idx) + len(batch)) and h["peer_bytes"] == 0
