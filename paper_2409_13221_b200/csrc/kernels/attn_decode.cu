@@ -18,6 +18,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "launch.cuh"
 #include "ops.h"
@@ -60,15 +61,19 @@ __device__ __forceinline__ uint32_t swz(uint32_t tile_base, int r, int c16) {
 // A stage holds K and V of one 32-token unit and, for the first unit of an
 // item, the item's G query rows (bulk-copied with it, so starting an item
 // never waits on a global load of q).
-template <int HD>
+// Two shapes of the same per-item computation (identical numerics): WIDE —
+// many warps, 2 stages each — for large batches, where warps per SM hide the
+// per-unit latency; DEEP — few warps, a deep ring each — for small batches,
+// where each warp streams a long item alone and needs many units in flight.
+template <int HD, bool DEEP = false>
 struct DecCfg {
   static constexpr int kSub = HD / 64;                  // 64-column boxes per K (or V) unit
   static constexpr int kBox = 32 * 128;                 // 32 rows x 128 B
   static constexpr int kKV = 2 * kSub * kBox;           // K + V of one 32-token unit
   static constexpr int kQSlot = HD == 64 ? 1024 : 2048; // >= 8 q rows x HD x 2 B, keeps 1 KB alignment
   static constexpr int kStageBytes = kKV + kQSlot;
-  static constexpr int kWarps = HD == 64 ? 8 : 6;
-  static constexpr int kStages = HD == 64 ? 3 : 2;
+  static constexpr int kWarps = DEEP ? (HD == 64 ? 4 : 3) : (HD == 64 ? 12 : 6);
+  static constexpr int kStages = DEEP ? (HD == 64 ? 6 : 4) : 2;
   static constexpr int kSmem = kWarps * kStages * kStageBytes + 1024;
 };
 
@@ -87,15 +92,15 @@ struct Cursor {
 };
 static_assert(kDecodeChunk / 64 <= 32, "an item's pages must fit one per lane");
 
-template <int HD, int G>
-__global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_kernel(
+template <int HD, int G, bool DEEP>
+__global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_mma_kernel(
     const __grid_constant__ CUtensorMap kv_map, const bf16* __restrict__ q, const int* __restrict__ block_table,
     int bt_stride, int rows_per_page, int layer_rows, int layer, const int* __restrict__ slot,
     const int* __restrict__ ctx, const int* __restrict__ items, int B, int H, int KVH, int nsplit_max,
     float scale_log2,
     float* __restrict__ part_o, float* __restrict__ part_ml, bf16* __restrict__ out, int* __restrict__ counters) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
-  using C = DecCfg<HD>;
+  using C = DecCfg<HD, DEEP>;
   static_assert(G <= 8, "GQA group must fit the first 8 MMA rows");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -338,15 +343,24 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
             part_ml[pb * 2 + 1] = l_run;
           }
         }
-        // the last split of (sample, kv head) to finish merges all of them
-        __threadfence();
+        // the last split of (sample, kv head) to finish merges all of them:
+        // a release-ordered ticket (the warp's partial stores are ordered
+        // before it by __syncwarp) instead of a full __threadfence, whose L1
+        // invalidation would evict every warp's cached tables; the merge
+        // reads the partials through L2 (ld.global.cg).
         __syncwarp();
         int last = 0;
-        if (lane == 0) last = atomicAdd(&counters[2 + b * KVH + kvh], 1) == nsb - 1;
+        if (lane == 0) {
+          int old;
+          asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;"
+                       : "=r"(old)
+                       : "l"(counters + 2 + b * KVH + kvh)
+                       : "memory");
+          last = old == nsb - 1;
+        }
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {
           if (lane == 0) counters[2 + b * KVH + kvh] = 0;  // ready for the next launch
-          __threadfence();
           for (int g = 0; g < G; ++g) combine_row(part_o, part_ml, (row0 + g) * nsplit_max, nsb, HD, lane, 32,
                                                   out + (row0 + g) * HD);
         }
@@ -364,14 +378,14 @@ __global__ void __launch_bounds__(DecCfg<HD>::kWarps * 32, 1) attn_decode_mma_ke
   }
 }
 
-template <int HD, int G>
-void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
+template <int HD, int G, bool DEEP>
+void launch_cfg(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
             const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out, int* counters,
             cudaStream_t st) {
-  using C = DecCfg<HD>;
+  using C = DecCfg<HD, DEEP>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_decode_mma_kernel<HD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(attn_decode_mma_kernel<HD, G, DEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr = true;
   }
   float* part_o = work;
@@ -381,10 +395,27 @@ void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const 
   const float scale = kLog2e / sqrtf(static_cast<float>(HD));
   const int max_items = nsplit * B * KVH;  // upper bound of the non-empty items
   const int grid = std::max(1, std::min(148, (max_items + C::kWarps - 1) / C::kWarps));
-  launch_pdl(attn_decode_mma_kernel<HD, G>, dim3(grid), dim3(C::kWarps * 32), C::kSmem, st, map, q,
+  launch_pdl(attn_decode_mma_kernel<HD, G, DEEP>, dim3(grid), dim3(C::kWarps * 32), C::kSmem, st, map, q,
              pool.block_table, pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, items, B, H, KVH, nsplit,
              scale, part_o, part_ml, out, counters);
   count_launch();
+}
+
+template <int HD, int G>
+void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
+            const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out, int* counters,
+            cudaStream_t st) {
+  // DEEP when the (sample, kv head) pairs cannot fill the WIDE grid's warps
+  // four times over; FUSEPLAN_ATTN_DEEP=0/1 forces a shape (A/B runs)
+  static const int force = [] {
+    const char* e = std::getenv("FUSEPLAN_ATTN_DEEP");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool deep = force >= 0 ? force == 1 : B * KVH * 4 <= 148 * DecCfg<HD, false>::kWarps;
+  if (deep)
+    launch_cfg<HD, G, true>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);
+  else
+    launch_cfg<HD, G, false>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);
 }
 
 }  // namespace
