@@ -293,10 +293,15 @@ def main():
         return
     hbm, tflops, src = peaks()
     achieved = (probe_bytes / (probe_ms / 1000.0)) / 1e9 if probe_ms > 0 else None
-    traffic = None
+    # traffic: DRAM bytes per launch from the committed ncu --set full capture
+    # of this kernel (profiles/attn_decode_traffic.json), as its DRAM /
+    # algorithmic ratio applied to this run's mean launch
+    traffic = traffic_src = None
     tp = ROOT / "profiles" / "attn_decode_traffic.json"
-    if tp.exists():
-        traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+    if tp.exists() and probe_n:
+        tj = json.loads(tp.read_text())
+        traffic = tj["dram_over_algorithmic"] * probe_bytes / probe_n
+        traffic_src = f"{tj['source']} on {tj['config']}: dram/algorithmic = {tj['dram_over_algorithmic']:.3f}"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_v / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -311,7 +316,7 @@ def main():
                    "parallelism": f"dp{G} (one engine per B200)"},
         "roofline": {"kernel": "attn_decode (paged KV flash-decoding)", "bound": "hbm", "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
-                     "traffic": traffic, "peak_source": src, "launches": probe_n,
+                     "traffic": traffic, "traffic_source": traffic_src, "peak_source": src, "launches": probe_n,
                      "bytes_per_launch": probe_bytes / max(probe_n, 1),
                      "share_of_step": (probe_ms / ms_p) if ms_p else None},
         "cpu_baseline": cpu,
