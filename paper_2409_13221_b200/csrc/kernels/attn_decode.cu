@@ -50,6 +50,22 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// Attention numerics: inside a 512-token split item, the online softmax runs
+// over 128-token sub-chunks (4 units) and the sub-chunk partials are folded
+// left to right with this update (explicit roundings), so the warp-per-item
+// and the team kernels give the same bits for every batch size.
+constexpr int kSubUnits = 4;
+__device__ __forceinline__ void sub_fold(float& M, float& L, float m, float l, float& fa, float& fb) {
+  const float Mn = fmaxf(M, m);
+  fa = exp2f(M - Mn);
+  fb = exp2f(m - Mn);
+  L = __fadd_rn(__fmul_rn(L, fa), __fmul_rn(l, fb));
+  M = Mn;
+}
+__device__ __forceinline__ float sub_fold_o(float O, float o, float fa, float fb) {
+  return __fadd_rn(__fmul_rn(O, fa), __fmul_rn(o, fb));
+}
+
 // Swizzled address of 16-byte chunk `c16` (along the head dim) of row r.
 template <int HD>
 __device__ __forceinline__ uint32_t swz(uint32_t tile_base, int r, int c16) {
@@ -217,6 +233,8 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
   uint32_t qa[HD / 16][4];
   float o[HD / 8][4];
   float m_run = -INFINITY, l_run = 0.f;
+  float acc_m = -INFINITY, acc_l = 0.f, acc_o[HD / 8][2];  // folded sub-chunks of the current item
+  bool acc_has = false;
   bool fresh = true;
 
   for (int c = 0; cur.j < n_items; ++c) {
@@ -318,8 +336,35 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
       issue(in, k);
       next_issue(in);
     }
-    // advance the consume cursor; flush the item's partial when it ends
-    if (++cu >= cue) {
+    // sub-chunk boundary: fold the running softmax into the item accumulator
+    ++cu;
+    if (cu >= cue || ((cu - (cur.t0 >> 5)) % kSubUnits) == 0) {
+      if (!acc_has) {
+        acc_m = m_run;
+        acc_l = l_run;
+#pragma unroll
+        for (int dn = 0; dn < HD / 8; ++dn) {
+          acc_o[dn][0] = o[dn][0];
+          acc_o[dn][1] = o[dn][1];
+        }
+        acc_has = true;
+      } else {
+        float fa, fb;
+        sub_fold(acc_m, acc_l, m_run, l_run, fa, fb);
+#pragma unroll
+        for (int dn = 0; dn < HD / 8; ++dn) {
+          acc_o[dn][0] = sub_fold_o(acc_o[dn][0], o[dn][0], fa, fb);
+          acc_o[dn][1] = sub_fold_o(acc_o[dn][1], o[dn][1], fa, fb);
+        }
+      }
+      m_run = -INFINITY;
+      l_run = 0.f;
+#pragma unroll
+      for (int dn = 0; dn < HD / 8; ++dn) o[dn][0] = o[dn][1] = o[dn][2] = o[dn][3] = 0.f;
+    }
+    // flush the item's partial when it ends
+    if (cu >= cue) {
+      acc_has = false;
       const int nsb = cur.nsb, b = cur.b, kvh = cur.kvh, split = cur.split;
       const size_t row0 = static_cast<size_t>(b) * H + kvh * G;
       if (nsb == 1) {
@@ -329,7 +374,7 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
 #pragma unroll
           for (int dn = 0; dn < HD / 8; ++dn)
             *reinterpret_cast<__nv_bfloat162*>(og + dn * 8) =
-                __floats2bfloat162_rn(__fdiv_rn(o[dn][0], l_run), __fdiv_rn(o[dn][1], l_run));
+                __floats2bfloat162_rn(__fdiv_rn(acc_o[dn][0], acc_l), __fdiv_rn(acc_o[dn][1], acc_l));
         }
       } else {
         if (r0 < G) {
@@ -337,10 +382,10 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
           float* po = part_o + pb * HD + 2 * (lane & 3);
 #pragma unroll
           for (int dn = 0; dn < HD / 8; ++dn)
-            *reinterpret_cast<float2*>(po + dn * 8) = make_float2(o[dn][0], o[dn][1]);
+            *reinterpret_cast<float2*>(po + dn * 8) = make_float2(acc_o[dn][0], acc_o[dn][1]);
           if ((lane & 3) == 0) {
-            part_ml[pb * 2] = m_run;
-            part_ml[pb * 2 + 1] = l_run;
+            part_ml[pb * 2] = acc_m;
+            part_ml[pb * 2 + 1] = acc_l;
           }
         }
         // the last split of (sample, kv head) to finish merges all of them:
@@ -401,10 +446,347 @@ void launch_cfg(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, co
   count_launch();
 }
 
+
+// ---------------------------------------------------------------------------
+// Team kernel (head_dim 64, no GQA grouping). The work item is the same
+// (sample, 512-token split, kv head), but a team of 4 warps shares it: warp w
+// streams the item's sub-chunk w (128 tokens = 4 units) through its own
+// 2-stage ring and runs the online softmax over it; the team leader then folds
+// the 4 sub-partials in order (the combine_row formula) and flushes the item
+// (normalised output, or a split partial + ticket as above). A warp's stream is
+// 4 units per item instead of 16, so long items no longer serialise on one
+// warp and the dynamic queue balances at a 4x finer grain. The sub-chunk fold
+// is part of the numerics for every batch size (batch-independent results).
+struct TeamCfg {
+  static constexpr int kTeamWarps = 4;
+  static constexpr int kTeams = 3;
+  static constexpr int kWarps = kTeams * kTeamWarps;
+  static constexpr int kStages = 2;
+  static constexpr int kSubUnits = fpk::kSubUnits;                      // units per sub-chunk
+  static constexpr int kSubs = kDecodeChunk / (32 * kSubUnits);         // sub-chunks per item
+  static constexpr int kKV = 2 * 32 * 128;                              // K + V of one unit (hd 64)
+  static constexpr int kStageBytes = kKV + 1024;                        // + q slot
+  static constexpr int kSmem = kWarps * kStages * kStageBytes + 1024;
+};
+static_assert(TeamCfg::kSubs == TeamCfg::kTeamWarps, "one sub-chunk per team warp");
+
+__device__ __forceinline__ void team_bar(int team) {
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + team) : "memory");
+}
+
+__global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kernel(
+    const __grid_constant__ CUtensorMap kv_map, const bf16* __restrict__ q, const int* __restrict__ block_table,
+    int bt_stride, int rows_per_page, int layer_rows, int layer, const int* __restrict__ slot,
+    const int* __restrict__ ctx, const int* __restrict__ items, int H, int KVH, int nsplit_max, float scale_log2,
+    float* __restrict__ part_o, float* __restrict__ part_ml, bf16* __restrict__ out, int* __restrict__ counters) {
+  constexpr int HD = 64;
+  using C = TeamCfg;
+  pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ __align__(8) uint64_t full_bar[C::kWarps][C::kStages];
+  __shared__ int4 ring_s[C::kTeams][4][2];                 // team item infos (decoded), items i .. i+2
+  __shared__ float sub_o[C::kTeams][2][C::kSubs][HD];      // sub-chunk partials, double-buffered by item
+  __shared__ float sub_ml[C::kTeams][2][C::kSubs][2];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int team = warp / C::kTeamWarps, tw = warp % C::kTeamWarps;
+  uint64_t* bar = full_bar[warp];
+  uint8_t* my_smem = smem + warp * C::kStages * C::kStageBytes;
+  int4(*ring)[2] = ring_s[team];
+  if (lane == 0) {
+    if (warp == 0) tma_prefetch_desc(&kv_map);
+    for (int s2 = 0; s2 < C::kStages; ++s2) mbar_init(&bar[s2], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+  const int n_items = items[0] * KVH;
+  const int n_teams = gridDim.x * C::kTeams;
+
+  auto decode = [&](int j, DecItem& it) {
+    it.j = j;
+    it.b = it.kvh = it.split = it.t0 = it.t1 = it.cx = it.nsb = 0;
+    if (j >= n_items) return;
+    const int pr = j / KVH;
+    it.kvh = j - pr * KVH;
+    const int e = items[1 + pr];
+    it.b = e >> 8;
+    it.split = e & 255;
+    it.cx = ctx[it.b];
+    it.t0 = it.split * kDecodeChunk;
+    it.t1 = min(it.cx, it.t0 + kDecodeChunk);
+    it.nsb = (it.cx + kDecodeChunk - 1) / kDecodeChunk;
+  };
+  auto put = [&](int idx, int j) {  // leader lane only
+    DecItem it;
+    decode(j, it);
+    ring[idx & 3][0] = make_int4(it.j, it.b, it.kvh, it.split);
+    ring[idx & 3][1] = make_int4(it.t0, it.t1, it.cx, it.nsb);
+  };
+  auto get = [&](int idx) {
+    const int4 x = ring[idx & 3][0], y = ring[idx & 3][1];
+    return DecItem{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+  };
+  // this warp's units of an item: sub-chunk tw
+  auto my_units = [&](const DecItem& it, int& ua, int& ub) {
+    ua = (it.t0 >> 5) + tw * C::kSubUnits;
+    ub = min(((it.t1 - 1) >> 5) + 1, ua + C::kSubUnits);
+    if (it.j >= n_items || ub < ua) ub = ua;
+  };
+
+  pdl_wait();  // q, the new K/V and the counters come from earlier kernels
+  if (tw == 0 && lane == 0) {
+    const int first = static_cast<int>(blockIdx.x) * C::kTeams + team;  // static first item
+    put(0, first * 1);
+    put(1, n_teams + atomicAdd(&counters[0], 1));
+  }
+  team_bar(team);
+  int known = 1;  // highest item index whose info is in the ring
+
+  // issue cursor over (item index, unit) of this warp's sub-chunks
+  int in_i = 0, in_u = 0, in_ue = 0, in_ua = 0, in_pg = 0;
+  DecItem in_it = get(0);
+  bool in_ok = in_it.j < n_items;
+  auto load_item = [&]() {  // all lanes: unit range and page ids of item in_i
+    my_units(in_it, in_ua, in_ue);
+    in_u = in_ua;
+    const int p0 = in_ua >> 1;
+    in_pg = (in_ue > in_ua && lane < 2) ? block_table[slot[in_it.b] * bt_stride + p0 + lane] : 0;
+  };
+  if (in_ok) load_item();
+  auto advance_item = [&]() {  // move past empty / finished items while their infos are known
+    while (in_ok && in_u >= in_ue) {
+      if (in_i + 1 > known) return;  // wait for the next team barrier
+      ++in_i;
+      in_it = get(in_i);
+      in_ok = in_it.j < n_items;
+      if (in_ok) load_item();
+    }
+  };
+  int n_iss = 0, n_con = 0;
+  auto pump = [&]() {  // all lanes
+    advance_item();
+    while (in_ok && in_u < in_ue && n_iss - n_con < C::kStages) {
+      const int k = n_iss % C::kStages;
+      const int pid = __shfl_sync(0xffffffffu, in_pg, (in_u >> 1) - (in_ua >> 1));
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const int rk = pid * rows_per_page + layer * layer_rows + in_it.kvh * 2 * kPT + (in_u & 1) * 32;
+        uint8_t* dst = my_smem + k * C::kStageBytes;
+        const bool first = in_u == in_ua;
+        mbar_arrive_expect_tx(&bar[k], C::kKV + (first ? HD * 2 : 0));
+        tma_load_2d(dst, &kv_map, &bar[k], 0, rk);
+        tma_load_2d(dst + 32 * 128, &kv_map, &bar[k], 0, rk + kPT);
+        if (first) bulk_load(dst + C::kKV, q + (static_cast<size_t>(in_it.b) * H + in_it.kvh) * HD, HD * 2, &bar[k]);
+      }
+      ++n_iss;
+      ++in_u;
+      advance_item();
+    }
+  };
+  pump();
+
+  const int r0 = lane >> 2;
+  const uint32_t base = smem_u32(my_smem);
+  const int mi = lane >> 3;
+  for (int i = 0;; ++i) {
+    const DecItem it = get(i);
+    if (it.j >= n_items) break;
+    int ua, ub;
+    my_units(it, ua, ub);
+    float o[HD / 8][4];
+    float m_run = -INFINITY, l_run = 0.f;
+#pragma unroll
+    for (int d = 0; d < HD / 8; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
+    uint32_t qa[HD / 16][4];
+    for (int u = ua; u < ub; ++u) {
+      const int k = n_con % C::kStages;
+      mbar_wait(&bar[k], (n_con / C::kStages) & 1);
+      if (u == ua) {
+        const bf16* qs = reinterpret_cast<const bf16*>(my_smem + k * C::kStageBytes + C::kKV);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const int col = kk * 16 + 2 * (lane & 3);
+          qa[kk][0] = r0 == 0 ? *reinterpret_cast<const uint32_t*>(qs + col) : 0u;
+          qa[kk][1] = 0u;
+          qa[kk][2] = r0 == 0 ? *reinterpret_cast<const uint32_t*>(qs + col + 8) : 0u;
+          qa[kk][3] = 0u;
+        }
+      }
+      const uint32_t Kt = base + k * C::kStageBytes;
+      const uint32_t Vt = Kt + 32 * 128;
+      const int ut0 = u * 32;
+      const int lo = max(it.t0, ut0) - ut0, hi = min(it.t1, ut0 + 32) - ut0;
+      float sc[4][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+#pragma unroll
+        for (int nt = 0; nt < 4; nt += 2) {
+          const int r = (nt + (mi >> 1)) * 8 + (lane & 7);
+          uint32_t b0, b1, b2, b3;
+          ldsm4(swz<HD>(Kt, r, kk * 2 + (mi & 1)), b0, b1, b2, b3);
+          mma16816(sc[nt], qa[kk], b0, b1);
+          mma16816(sc[nt + 1], qa[kk], b2, b3);
+        }
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int tok = nt * 8 + 2 * (lane & 3) + e;
+          const float v = (tok >= lo && tok < hi) ? sc[nt][e] * scale_log2 : -INFINITY;
+          sc[nt][e] = v;
+          mx = fmaxf(mx, v);
+        }
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float nm = fmaxf(m_run, mx);
+      const float corr = (m_run == -INFINITY) ? 0.f : exp2f(m_run - nm);
+      m_run = nm;
+      float rs = 0.f;
+      uint32_t pa[2][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const float p0 = (sc[nt][0] == -INFINITY) ? 0.f : exp2f(sc[nt][0] - nm);
+        const float p1 = (sc[nt][1] == -INFINITY) ? 0.f : exp2f(sc[nt][1] - nm);
+        rs += p0 + p1;
+        const int kk2 = nt >> 1;
+        if ((nt & 1) == 0) {
+          pa[kk2][0] = pack_bf16x2(p0, p1);
+          pa[kk2][1] = 0u;
+        } else {
+          pa[kk2][2] = pack_bf16x2(p0, p1);
+          pa[kk2][3] = 0u;
+        }
+      }
+      rs += __shfl_xor_sync(0xffffffffu, rs, 1);
+      rs += __shfl_xor_sync(0xffffffffu, rs, 2);
+      l_run = l_run * corr + rs;
+#pragma unroll
+      for (int dn = 0; dn < HD / 8; ++dn) {
+        o[dn][0] *= corr;
+        o[dn][1] *= corr;
+      }
+#pragma unroll
+      for (int kk2 = 0; kk2 < 2; ++kk2) {
+#pragma unroll
+        for (int dn = 0; dn < HD / 8; dn += 2) {
+          const int r = kk2 * 16 + (mi & 1) * 8 + (lane & 7);
+          uint32_t b0, b1, b2, b3;
+          ldsm4t(swz<HD>(Vt, r, dn + (mi >> 1)), b0, b1, b2, b3);
+          mma16816(o[dn], pa[kk2], b0, b1);
+          mma16816(o[dn + 1], pa[kk2], b2, b3);
+        }
+      }
+      __syncwarp();
+      ++n_con;
+      pump();
+    }
+    // park this warp's sub-partial (row 0 lives in lanes 0..3)
+    const int sl = i & 1;
+    if (lane < 4) {
+#pragma unroll
+      for (int dn = 0; dn < HD / 8; ++dn) {
+        sub_o[team][sl][tw][dn * 8 + 2 * lane] = o[dn][0];
+        sub_o[team][sl][tw][dn * 8 + 2 * lane + 1] = o[dn][1];
+      }
+      if (lane == 0) {
+        sub_ml[team][sl][tw][0] = m_run;
+        sub_ml[team][sl][tw][1] = l_run;
+      }
+    }
+    if (tw == 0 && lane == 0) put(i + 2, n_teams + atomicAdd(&counters[0], 1));
+    team_bar(team);
+    known = i + 2;
+    pump();
+    if (tw != 0) continue;
+    // leader: fold the sub-chunks in order, then flush the item
+    const int nsub = (it.t1 - it.t0 + 32 * C::kSubUnits - 1) / (32 * C::kSubUnits);
+    float M = sub_ml[team][sl][0][0], L = sub_ml[team][sl][0][1];
+    float O0 = sub_o[team][sl][0][lane], O1 = sub_o[team][sl][0][lane + 32];
+    for (int s2 = 1; s2 < nsub; ++s2) {
+      float fa, fb;
+      sub_fold(M, L, sub_ml[team][sl][s2][0], sub_ml[team][sl][s2][1], fa, fb);
+      O0 = sub_fold_o(O0, sub_o[team][sl][s2][lane], fa, fb);
+      O1 = sub_fold_o(O1, sub_o[team][sl][s2][lane + 32], fa, fb);
+    }
+    const size_t row0 = static_cast<size_t>(it.b) * H + it.kvh;
+    if (it.nsb == 1) {
+      bf16* og = out + row0 * HD;
+      og[lane] = __float2bfloat16_rn(__fdiv_rn(O0, L));
+      og[lane + 32] = __float2bfloat16_rn(__fdiv_rn(O1, L));
+    } else {
+      const size_t pb = row0 * nsplit_max + it.split;
+      part_o[pb * HD + lane] = O0;
+      part_o[pb * HD + lane + 32] = O1;
+      if (lane == 0) {
+        part_ml[pb * 2] = M;
+        part_ml[pb * 2 + 1] = L;
+      }
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        int old;
+        asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;"
+                     : "=r"(old)
+                     : "l"(counters + 2 + it.b * KVH + it.kvh)
+                     : "memory");
+        last = old == it.nsb - 1;
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last) {
+        if (lane == 0) counters[2 + it.b * KVH + it.kvh] = 0;
+        combine_row(part_o, part_ml, row0 * nsplit_max, it.nsb, HD, lane, 32, out + row0 * HD);
+      }
+    }
+  }
+  // the last team out resets the work counter for the next launch
+  if (tw == 0 && lane == 0 && atomicAdd(&counters[1], 1) == n_teams - 1) {
+    counters[0] = 0;
+    counters[1] = 0;
+  }
+}
+
+void launch_team(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
+                 const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out, int* counters,
+                 cudaStream_t st) {
+  using C = TeamCfg;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(attn_decode_team_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr = true;
+  }
+  float* part_o = work;
+  float* part_ml = work + static_cast<size_t>(B) * H * nsplit * 64;
+  const int layer_rows = KVH * 2 * kPT;
+  const int rows_per_page = static_cast<int>(pool.page_bytes / (static_cast<size_t>(64) * 2));
+  const float scale = kLog2e / sqrtf(64.f);
+  const int max_items = nsplit * B * KVH;
+  const int grid = std::max(1, std::min(148, (max_items + C::kTeams - 1) / C::kTeams));
+  launch_pdl(attn_decode_team_kernel, dim3(grid), dim3(C::kWarps * 32), C::kSmem, st, map, q, pool.block_table,
+             pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, items, H, KVH, nsplit, scale, part_o,
+             part_ml, out, counters);
+  count_launch();
+}
+
 template <int HD, int G>
 void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
             const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out, int* counters,
             cudaStream_t st) {
+  static const int team_mode = [] {  // FUSEPLAN_ATTN_TEAM=0 selects the warp-per-item kernels (A/B runs)
+    const char* e = std::getenv("FUSEPLAN_ATTN_TEAM");
+    return e ? std::atoi(e) : 1;
+  }();
+  // the team kernel wins while the (sample, kv head) pairs cannot fill the
+  // warp-per-item grid (small batches); identical numerics either way
+  if (HD == 64 && G == 1 && team_mode && (team_mode == 2 || B * KVH * 4 <= 148 * DecCfg<HD, false>::kWarps)) {
+    launch_team(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);
+    return;
+  }
   // DEEP when the (sample, kv head) pairs cannot fill the WIDE grid's warps
   // four times over; FUSEPLAN_ATTN_DEEP=0/1 forces a shape (A/B runs)
   static const int force = [] {

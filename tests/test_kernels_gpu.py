@@ -300,3 +300,28 @@ def test_qkv_rope_fused(lib, H, KVH, hd, M):
         assert (vv - qkv[m, H + KVH:]).abs().max().item() < tol, m
         written[page, layer, :, :, p % PT] = True
     assert not pool[~written].any()  # nothing else touched
+
+
+@pytest.mark.parametrize("hd,H,KVH", [(64, 12, 12), (128, 32, 8)])
+def test_attn_decode_batch_independent(lib, hd, H, KVH):
+    """A row's decode-attention bits do not depend on the batch it runs in, although
+    small batches take the team / deep kernel and large ones the wide kernel."""
+    L, layer, PT = 2, 1, 64
+    g = torch.Generator(device="cuda").manual_seed(11)
+    Bs, Bl = 6, 80
+    ctx_l = torch.randint(1, 1500, (Bl,), generator=g, device="cuda").to(torch.int32)
+    maxp = (int(ctx_l.max()) + PT - 1) // PT
+    npages = Bl * maxp + 1
+    pool = (torch.randn(npages, L, KVH, 2, PT, hd, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    bt = (torch.randperm(npages - 1, device="cuda", generator=g)[: Bl * maxp] + 1).to(torch.int32).view(Bl, maxp)
+    q = torch.randn(Bl, H, hd, device="cuda", generator=g).to(torch.bfloat16)
+    slot = torch.arange(Bl, device="cuda", dtype=torch.int32)
+    outs = []
+    for B in (Bs, Bl):
+        out = torch.zeros(B, H, hd, device="cuda", dtype=torch.bfloat16)
+        ok(lib, lib.fp_k_attn_decode(ptr(q[:B].contiguous()), B, H, KVH, hd, ptr(pool), npages, L, layer,
+                                     ptr(bt.contiguous()), maxp, ptr(slot[:B].contiguous()),
+                                     ptr(ctx_l[:B].contiguous()), int(ctx_l[:B].max()), ptr(out), stream()))
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1][:Bs])
