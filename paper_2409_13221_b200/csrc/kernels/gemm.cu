@@ -142,15 +142,24 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
 }
 
 // Batch-tile width of a swap-AB GEMM with `a_ctas` weight tiles (x splits):
-// the widest BN that still yields >= 128 CTAs, else the narrowest that covers
-// the rows. Decode GEMMs stream weights, so filling the SMs matters more than
-// the L2 re-reads of narrower tiles; a row's bits do not depend on BN (each
-// output element is one tensor-core dot product in the same K order).
+// the fewest waves over the 148 SMs, then the narrowest tile (most CTAs
+// streaming weights in that wave), never wider than the rows need. A CTA's
+// time is dominated by streaming its 128-row weight tile, which does not
+// depend on BN, so a second wave costs about as much as the first; a row's
+// bits do not depend on BN (each output element is one tensor-core dot
+// product in the same K order).
 int pick_bn(int M, int a_ctas) {
-  static const int kBN[] = {256, 128, 64, 32, 16};
-  for (int bn : kBN)
-    if ((bn / 2 < M || bn == 16) && a_ctas * ((M + bn - 1) / bn) >= 128) return bn;  // never wider than needed
-  return 16;
+  static const int kBN[] = {16, 32, 64, 128, 256};
+  int best = 16, best_waves = 1 << 30;
+  for (int bn : kBN) {
+    if (bn != 16 && bn / 2 >= M) break;  // wider than the rows need
+    const int waves = (a_ctas * ((M + bn - 1) / bn) + 147) / 148;
+    if (waves < best_waves) {
+      best = bn;
+      best_waves = waves;
+    }
+  }
+  return best;
 }
 
 // Cluster split of a decode GEMM: a function of the weight shape only (so a
@@ -170,11 +179,18 @@ int cluster_splits(int N, int K) {
 }
 
 // Decode GEMMs with a cluster split use BN <= 64 (the parked partial must fit).
-int pick_bn_small(int M, int a_ctas) {
-  static const int kBN[] = {64, 32, 16};
-  for (int bn : kBN)
-    if ((bn / 2 < M || bn == 16) && a_ctas * ((M + bn - 1) / bn) >= 128) return bn;  // never wider than needed
-  return 16;
+int pick_bn_small(int M, int a_ctas) {  // pick_bn restricted to BN <= 64
+  static const int kBN[] = {16, 32, 64};
+  int best = 16, best_waves = 1 << 30;
+  for (int bn : kBN) {
+    if (bn != 16 && bn / 2 >= M) break;
+    const int waves = (a_ctas * ((M + bn - 1) / bn) + 147) / 148;
+    if (waves < best_waves) {
+      best = bn;
+      best_waves = waves;
+    }
+  }
+  return best;
 }
 
 template <class F>
@@ -259,10 +275,14 @@ void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float*
 void gemm_swiglu_decode(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
   if (F % 64) throw std::invalid_argument("gemm_swiglu: F must be a multiple of 64");
   const int z = cluster_splits(2 * F, K);
-  dispatch_bn_small(M, (2 * F + 127) / 128 * z, [&]<int BN>() {
+  auto go = [&]<int BN>() {
     EpiSwiGLU<BN> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, BN)};
     launch<BN>(Wgu, 2 * F, X, M, K, z, e, st, true, z > 1);
-  });
+  };
+  if (z > 1)
+    dispatch_bn_small(M, (2 * F + 127) / 128 * z, go);
+  else
+    dispatch_bn<int>(M, (2 * F + 127) / 128, go);
 }
 
 void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
@@ -279,11 +299,15 @@ void gemm_qkv_rope(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH
   if (128 % hd != 0) throw std::invalid_argument("gemm_qkv_rope: head_dim must divide 128");
   const int N = (H + 2 * KVH) * hd;
   const int z = cluster_splits(N, K);
-  dispatch_bn_small(M, (N + 127) / 128 * z, [&]<int BN>() {
+  auto go = [&]<int BN>() {
     EpiRopeKV<BN> e{q_out, pool, slot, pos, cs, layer, H, KVH, hd, M};
     e.pool.kv_map = nullptr;  // host pointer: not dereferenced on the device
     launch<BN>(Wqkv, N, X, M, K, z, e, st, true, z > 1);
-  });
+  };
+  if (z > 1)
+    dispatch_bn_small(M, (N + 127) / 128 * z, go);
+  else
+    dispatch_bn<int>(M, (N + 127) / 128, go);
 }
 
 constexpr int kVocabBN = 256;
