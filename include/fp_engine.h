@@ -154,7 +154,8 @@ int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t h
  * workspace of fp_k_attn_workspace_bytes, zero-filled before its first use
  * (the kernel leaves its counters zero). */
 int64_t fp_k_attn_workspace_bytes(int32_t B, int32_t H, int32_t KVH, int32_t hd, int32_t max_ctx);
-int fp_k_attn_items(const int32_t* ctx_host, int32_t B, int32_t max_ctx, int32_t* items_host);
+int fp_k_attn_items(const int32_t* ctx_host, int32_t B, int32_t H, int32_t KVH, int32_t hd, int32_t max_ctx,
+                    int32_t* items_host); /* items_host: 1 + B * ceil(max_ctx / 128) ints */
 int fp_k_attn_decode_ws(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t hd, const void* pool,
                         int32_t num_pages, int32_t num_layers, int32_t layer, const int32_t* block_table,
                         int32_t bt_stride, const int32_t* slot, const int32_t* ctx, const int32_t* items_dev,

@@ -452,11 +452,11 @@ int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t h
     }
     float* work = nullptr;
     const size_t wb = fpk::attn_decode_workspace(B, H, hd, max_ctx) * 4 + 256;
-    const size_t cb = static_cast<size_t>(fpk::attn_decode_counters(B, KVH)) * 4;
-    const size_t ob = (1 + static_cast<size_t>(B) * ((max_ctx + fpk::kDecodeChunk - 1) / fpk::kDecodeChunk)) * 4;
+    const size_t cb = static_cast<size_t>(fpk::attn_decode_counters(B, KVH, max_ctx)) * 4;
+    const size_t ob = (1 + static_cast<size_t>(B) * ((max_ctx + 127) / 128)) * 4;
     fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&work), wb + cb + ob, S(stream)), "alloc");
     int* counters = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(work) + wb);
-    int* items = counters + fpk::attn_decode_counters(B, KVH);
+    int* items = counters + fpk::attn_decode_counters(B, KVH, max_ctx);
     fpe::check(cudaMemsetAsync(counters, 0, cb, S(stream)), "memset");
     std::vector<int> hc(B), hi(ob / 4);
     {  // work-item table from the contexts (host; this entry is a test / tooling path)
@@ -464,7 +464,7 @@ int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t h
       fpe::check(cudaStreamSynchronize(S(stream)), "sync");
       for (int b = 0; b < B; ++b)
         if (hc[b] < 1 || hc[b] > max_ctx) throw std::invalid_argument("attn_decode: ctx out of [1, max_ctx]");
-      fpk::attn_decode_items(hc.data(), B, hi.data());
+      fpk::attn_decode_items(hc.data(), B, KVH, hd, H / KVH, hi.data());
       fpe::check(cudaMemcpyAsync(items, hi.data(), ob, cudaMemcpyHostToDevice, S(stream)), "items h2d");
     }
     fpk::attn_decode(static_cast<const bf16*>(q), B, H, KVH, hd, pv, layer, slot, ctx, items, max_ctx, work,
@@ -476,14 +476,15 @@ int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t h
 
 int64_t fp_k_attn_workspace_bytes(int32_t B, int32_t H, int32_t KVH, int32_t hd, int32_t max_ctx) {
   return static_cast<int64_t>(fpk::attn_decode_workspace(B, H, hd, max_ctx)) * 4 + 256 +
-         static_cast<int64_t>(fpk::attn_decode_counters(B, KVH)) * 4;
+         static_cast<int64_t>(fpk::attn_decode_counters(B, KVH, max_ctx)) * 4;
 }
 
-int fp_k_attn_items(const int32_t* ctx_host, int32_t B, int32_t max_ctx, int32_t* items_host) {
+int fp_k_attn_items(const int32_t* ctx_host, int32_t B, int32_t H, int32_t KVH, int32_t hd, int32_t max_ctx,
+                    int32_t* items_host) {
   return guarded([&] {
     for (int b = 0; b < B; ++b)
       if (ctx_host[b] < 1 || ctx_host[b] > max_ctx) throw std::invalid_argument("attn_items: ctx out of [1, max_ctx]");
-    fpk::attn_decode_items(ctx_host, B, items_host);
+    fpk::attn_decode_items(ctx_host, B, KVH, hd, H / KVH, items_host);
   });
 }
 

@@ -273,14 +273,15 @@ void Engine::alloc_ws() {
   dec_.q = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxao * 2));
   dec_.attn = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxao * 2));
   dec_.act = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxF * 2));
-  const int ns_cap = (cfg_.max_prompt + cfg_.max_new + fpk::kDecodeChunk - 1) / fpk::kDecodeChunk;
-  dec_.rows = static_cast<int*>(dalloc((static_cast<size_t>(7 + ns_cap) * B + 1) * 4));
+  const int items_cap = (cfg_.max_prompt + cfg_.max_new + 127) / 128;  // work items per row (attn_decode_items)
+  dec_.rows = static_cast<int*>(dalloc((static_cast<size_t>(7 + items_cap) * B + 1) * 4));
   dec_.vocab_part = dalloc(static_cast<size_t>(B) * vt * 24);
   dec_.tgt_z = static_cast<float*>(dalloc(B * 4));
   const Dims& a = cfg_.model[kActor];
   dec_.attn_work = static_cast<float*>(
       dalloc(fpk::attn_decode_workspace(B, a.H, a.hd, cfg_.max_prompt + cfg_.max_new) * sizeof(float)));
-  const size_t cnt = static_cast<size_t>(fpk::attn_decode_counters(B, a.KVH)) * sizeof(int);
+  const size_t cnt =
+      static_cast<size_t>(fpk::attn_decode_counters(B, a.KVH, cfg_.max_prompt + cfg_.max_new)) * sizeof(int);
   dec_.attn_cnt = static_cast<int*>(dalloc(cnt));
   FP_CUDA(cudaMemsetAsync(dec_.attn_cnt, 0, cnt, s_decode_));
 }
@@ -500,8 +501,8 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
   const int Bb = graph ? bucket_of(B) : B;
   if (Bb > dec_.cap) throw std::invalid_argument("engine: decode batch exceeds max_live");
   cudaStream_t st = s_decode_;
-  const int ns_cap = (cfg_.max_prompt + cfg_.max_new + fpk::kDecodeChunk - 1) / fpk::kDecodeChunk;
-  std::vector<int> h(static_cast<size_t>(7 + ns_cap) * Bb + 1);
+  const int items_cap = (cfg_.max_prompt + cfg_.max_new + 127) / 128;
+  std::vector<int> h(static_cast<size_t>(7 + items_cap) * Bb + 1);
   int max_ctx = 0;
   double ctx_sum = 0.0;
   for (int b = 0; b < Bb; ++b) {
@@ -517,7 +518,8 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
     max_ctx = std::max(max_ctx, r.pos + 1);
     if (!pad) ctx_sum += r.pos + 1;
   }
-  const int n_pairs = fpk::attn_decode_items(h.data() + 2 * Bb, Bb, h.data() + 7 * Bb);
+  const Dims& A = models_[kActor].dims;
+  const int n_pairs = fpk::attn_decode_items(h.data() + 2 * Bb, Bb, A.KVH, A.hd, A.H / A.KVH, h.data() + 7 * Bb);
   upload(dec_.rows, h.data(), (static_cast<size_t>(7) * Bb + 1 + n_pairs) * 4, st);
   if (!graph) {
     decode_kernels(Bb, max_ctx, mode, inv_temp, sample_seed, ctx_sum);

@@ -97,7 +97,19 @@ struct DecCfg {
 // the sample's context cx and number of non-empty splits nsb.
 struct DecItem {
   int j, b, kvh, split, t0, t1, cx, nsb;
+  int sub;  // 7: the whole split; c < 4: only sub-chunk c of it
 };
+// items[] entry -> (b, split, sub) and the token range of the item
+__device__ __forceinline__ void item_entry(int e, int cx, DecItem& it) {
+  it.b = e >> 11;
+  it.split = (e >> 3) & 255;
+  it.sub = e & 7;
+  it.cx = cx;
+  const int s0 = it.split * kDecodeChunk;
+  it.t0 = it.sub == 7 ? s0 : s0 + it.sub * 32 * kSubUnits;
+  it.t1 = min(cx, it.sub == 7 ? s0 + kDecodeChunk : it.t0 + 32 * kSubUnits);
+  it.nsb = (cx + kDecodeChunk - 1) / kDecodeChunk;
+}
 // Issue cursor: the item, its current / end 32-token unit, and (lane l) the
 // pool page id of the item's l-th 64-token page — fetched once per item, so
 // issuing a unit needs no dependent global load.
@@ -114,7 +126,8 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
     int bt_stride, int rows_per_page, int layer_rows, int layer, const int* __restrict__ slot,
     const int* __restrict__ ctx, const int* __restrict__ items, int B, int H, int KVH, int nsplit_max,
     float scale_log2,
-    float* __restrict__ part_o, float* __restrict__ part_ml, bf16* __restrict__ out, int* __restrict__ counters) {
+    float* __restrict__ part_o, float* __restrict__ part_ml, float* __restrict__ sub_o, float* __restrict__ sub_ml,
+    bf16* __restrict__ out, int* __restrict__ counters) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   using C = DecCfg<HD, DEEP>;
   static_assert(G <= 8, "GQA group must fit the first 8 MMA rows");
@@ -148,17 +161,12 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
     const int pr = j / KVH;
     it.kvh = j - pr * KVH;
     const int e = items[1 + pr];
-    it.b = e >> 8;
-    it.split = e & 255;
-    it.cx = ctx[it.b];
-    it.t0 = it.split * kDecodeChunk;
-    it.t1 = min(it.cx, it.t0 + kDecodeChunk);
-    it.nsb = (it.cx + kDecodeChunk - 1) / kDecodeChunk;
+    item_entry(e, ctx[e >> 11], it);
   };
   int wr = 0, rd = 0;
   auto begin_item = [&](Cursor& c) {  // all lanes: page ids, hand the item to the consumer
     if (lane == 0) {
-      ring[wr & 7][0] = make_int4(c.it.j, c.it.b, c.it.kvh, c.it.split);
+      ring[wr & 7][0] = make_int4(c.it.j, c.it.b, c.it.kvh, c.it.split | c.it.sub << 16);
       ring[wr & 7][1] = make_int4(c.it.t0, c.it.t1, c.it.cx, c.it.nsb);
     }
     ++wr;
@@ -223,7 +231,7 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
   auto pop = [&]() {
     const int4 x = ring[rd & 7][0], y = ring[rd & 7][1];
     ++rd;
-    cur = DecItem{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+    cur = DecItem{x.x, x.y, x.z, x.w & 0xffff, y.x, y.y, y.z, y.w, x.w >> 16};
   };
   pop();
   int cu = cur.t0 >> 5, cue = ((cur.t1 - 1) >> 5) + 1;
@@ -367,47 +375,96 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
       acc_has = false;
       const int nsb = cur.nsb, b = cur.b, kvh = cur.kvh, split = cur.split;
       const size_t row0 = static_cast<size_t>(b) * H + kvh * G;
-      if (nsb == 1) {
-        // single split: the combine is the identity (f = 1), normalise here
-        if (r0 < G) {
-          bf16* og = out + (row0 + r0) * HD + 2 * (lane & 3);
-#pragma unroll
-          for (int dn = 0; dn < HD / 8; ++dn)
-            *reinterpret_cast<__nv_bfloat162*>(og + dn * 8) =
-                __floats2bfloat162_rn(__fdiv_rn(acc_o[dn][0], acc_l), __fdiv_rn(acc_o[dn][1], acc_l));
-        }
-      } else {
-        if (r0 < G) {
-          const size_t pb = (row0 + r0) * nsplit_max + split;
-          float* po = part_o + pb * HD + 2 * (lane & 3);
-#pragma unroll
-          for (int dn = 0; dn < HD / 8; ++dn)
-            *reinterpret_cast<float2*>(po + dn * 8) = make_float2(acc_o[dn][0], acc_o[dn][1]);
-          if ((lane & 3) == 0) {
-            part_ml[pb * 2] = acc_m;
-            part_ml[pb * 2 + 1] = acc_l;
-          }
-        }
-        // the last split of (sample, kv head) to finish merges all of them:
-        // a release-ordered ticket (the warp's partial stores are ordered
-        // before it by __syncwarp) instead of a full __threadfence, whose L1
-        // invalidation would evict every warp's cached tables; the merge
-        // reads the partials through L2 (ld.global.cg).
+      // release-ordered ticket (the warp's stores before it are ordered by
+      // __syncwarp); returns whether this warp was the last of `n`. Cheaper
+      // than a full __threadfence, whose L1 invalidation would evict every
+      // warp's cached tables; merges read the partials through L2 (.cg).
+      auto ticket = [&](int* ctr, int n) {
         __syncwarp();
         int last = 0;
         if (lane == 0) {
           int old;
-          asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;"
-                       : "=r"(old)
-                       : "l"(counters + 2 + b * KVH + kvh)
-                       : "memory");
-          last = old == nsb - 1;
+          asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+          last = old == n - 1;
+          if (last) *ctr = 0;  // ready for the next launch
         }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {
-          if (lane == 0) counters[2 + b * KVH + kvh] = 0;  // ready for the next launch
-          for (int g = 0; g < G; ++g) combine_row(part_o, part_ml, (row0 + g) * nsplit_max, nsb, HD, lane, 32,
-                                                  out + (row0 + g) * HD);
+        return __shfl_sync(0xffffffffu, last, 0) != 0;
+      };
+      // after the split's partial is stored: the last split to finish merges all
+      auto merge_splits = [&]() {
+        if (ticket(counters + 2 + b * KVH + kvh, nsb))
+          for (int g = 0; g < G; ++g)
+            combine_row(part_o, part_ml, (row0 + g) * nsplit_max, nsb, HD, lane, 32, out + (row0 + g) * HD);
+      };
+      if (cur.sub == 7) {
+        if (nsb == 1) {
+          // single split: the combine is the identity (f = 1), normalise here
+          if (r0 < G) {
+            bf16* og = out + (row0 + r0) * HD + 2 * (lane & 3);
+#pragma unroll
+            for (int dn = 0; dn < HD / 8; ++dn)
+              *reinterpret_cast<__nv_bfloat162*>(og + dn * 8) =
+                  __floats2bfloat162_rn(__fdiv_rn(acc_o[dn][0], acc_l), __fdiv_rn(acc_o[dn][1], acc_l));
+          }
+        } else {
+          if (r0 < G) {
+            const size_t pb = (row0 + r0) * nsplit_max + split;
+            float* po = part_o + pb * HD + 2 * (lane & 3);
+#pragma unroll
+            for (int dn = 0; dn < HD / 8; ++dn)
+              *reinterpret_cast<float2*>(po + dn * 8) = make_float2(acc_o[dn][0], acc_o[dn][1]);
+            if ((lane & 3) == 0) {
+              part_ml[pb * 2] = acc_m;
+              part_ml[pb * 2 + 1] = acc_l;
+            }
+          }
+          merge_splits();
+        }
+      } else {
+        // one sub-chunk of a cut split: park its partial; the last sub-chunk
+        // to finish folds them in order (== the whole-split fold) and flushes
+        if (r0 < G) {
+          const size_t sb = ((row0 + r0) * nsplit_max + split) * kSubUnits + cur.sub;
+          float* so = sub_o + sb * HD + 2 * (lane & 3);
+#pragma unroll
+          for (int dn = 0; dn < HD / 8; ++dn)
+            *reinterpret_cast<float2*>(so + dn * 8) = make_float2(acc_o[dn][0], acc_o[dn][1]);
+          if ((lane & 3) == 0) {
+            sub_ml[sb * 2] = acc_m;
+            sub_ml[sb * 2 + 1] = acc_l;
+          }
+        }
+        const int slen = min(cur.cx, (split + 1) * kDecodeChunk) - split * kDecodeChunk;
+        const int nsub = (slen + 32 * kSubUnits - 1) / (32 * kSubUnits);
+        if (ticket(counters + 2 + B * KVH + (b * KVH + kvh) * nsplit_max + split, nsub)) {
+          for (int g = 0; g < G; ++g) {
+            const size_t sb0 = ((row0 + g) * nsplit_max + split) * kSubUnits;
+            float M = __ldcg(sub_ml + sb0 * 2), L = __ldcg(sub_ml + sb0 * 2 + 1);
+            float O[HD / 32];
+#pragma unroll
+            for (int i = 0; i < HD / 32; ++i) O[i] = __ldcg(sub_o + sb0 * HD + lane + 32 * i);
+            for (int c = 1; c < nsub; ++c) {
+              float fa, fb;
+              sub_fold(M, L, __ldcg(sub_ml + (sb0 + c) * 2), __ldcg(sub_ml + (sb0 + c) * 2 + 1), fa, fb);
+#pragma unroll
+              for (int i = 0; i < HD / 32; ++i)
+                O[i] = sub_fold_o(O[i], __ldcg(sub_o + (sb0 + c) * HD + lane + 32 * i), fa, fb);
+            }
+            if (nsb == 1) {
+#pragma unroll
+              for (int i = 0; i < HD / 32; ++i)
+                out[(row0 + g) * HD + lane + 32 * i] = __float2bfloat16_rn(__fdiv_rn(O[i], L));
+            } else {
+              const size_t pb = (row0 + g) * nsplit_max + split;
+#pragma unroll
+              for (int i = 0; i < HD / 32; ++i) part_o[pb * HD + lane + 32 * i] = O[i];
+              if (lane == 0) {
+                part_ml[pb * 2] = M;
+                part_ml[pb * 2 + 1] = L;
+              }
+            }
+          }
+          if (nsb > 1) merge_splits();
         }
       }
       pop();
@@ -433,16 +490,19 @@ void launch_cfg(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, co
     cudaFuncSetAttribute(attn_decode_mma_kernel<HD, G, DEEP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr = true;
   }
+  const size_t rows = static_cast<size_t>(B) * H * nsplit;
   float* part_o = work;
-  float* part_ml = work + static_cast<size_t>(B) * H * nsplit * HD;
+  float* part_ml = part_o + rows * HD;
+  float* sub_o = part_ml + rows * 2;
+  float* sub_ml = sub_o + rows * kSubUnits * HD;
   const int layer_rows = KVH * 2 * kPT;
   const int rows_per_page = static_cast<int>(pool.page_bytes / (static_cast<size_t>(HD) * 2));
   const float scale = kLog2e / sqrtf(static_cast<float>(HD));
-  const int max_items = nsplit * B * KVH;  // upper bound of the non-empty items
+  const int max_items = nsplit * kSubUnits * B * KVH;  // upper bound of the items (cut splits included)
   const int grid = std::max(1, std::min(148, (max_items + C::kWarps - 1) / C::kWarps));
   launch_pdl(attn_decode_mma_kernel<HD, G, DEEP>, dim3(grid), dim3(C::kWarps * 32), C::kSmem, st, map, q,
              pool.block_table, pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, items, B, H, KVH, nsplit,
-             scale, part_o, part_ml, out, counters);
+             scale, part_o, part_ml, sub_o, sub_ml, out, counters);
   count_launch();
 }
 
@@ -503,19 +563,15 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
   const int n_items = items[0] * KVH;
   const int n_teams = gridDim.x * C::kTeams;
 
-  auto decode = [&](int j, DecItem& it) {
+  auto decode = [&](int j, DecItem& it) {  // (the host never cuts splits for this kernel)
     it.j = j;
     it.b = it.kvh = it.split = it.t0 = it.t1 = it.cx = it.nsb = 0;
+    it.sub = 7;
     if (j >= n_items) return;
     const int pr = j / KVH;
     it.kvh = j - pr * KVH;
     const int e = items[1 + pr];
-    it.b = e >> 8;
-    it.split = e & 255;
-    it.cx = ctx[it.b];
-    it.t0 = it.split * kDecodeChunk;
-    it.t1 = min(it.cx, it.t0 + kDecodeChunk);
-    it.nsb = (it.cx + kDecodeChunk - 1) / kDecodeChunk;
+    item_entry(e, ctx[e >> 11], it);
   };
   auto put = [&](int idx, int j) {  // leader lane only
     DecItem it;
@@ -525,7 +581,7 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
   };
   auto get = [&](int idx) {
     const int4 x = ring[idx & 3][0], y = ring[idx & 3][1];
-    return DecItem{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+    return DecItem{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w, 7};
   };
   // this warp's units of an item: sub-chunk tw
   auto my_units = [&](const DecItem& it, int& ua, int& ub) {
@@ -773,34 +829,44 @@ void launch_team(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, c
   count_launch();
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 template <int HD, int G>
 void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
             const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out, int* counters,
             cudaStream_t st) {
-  static const int team_mode = [] {  // FUSEPLAN_ATTN_TEAM=0 selects the warp-per-item kernels (A/B runs)
-    const char* e = std::getenv("FUSEPLAN_ATTN_TEAM");
-    return e ? std::atoi(e) : 1;
-  }();
-  // the team kernel wins while the (sample, kv head) pairs cannot fill the
-  // warp-per-item grid (small batches); identical numerics either way
-  if (HD == 64 && G == 1 && team_mode && (team_mode == 2 || B * KVH * 4 <= 148 * DecCfg<HD, false>::kWarps)) {
-    launch_team(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);
-    return;
+  switch (attn_decode_variant(B, KVH, HD, G, nullptr)) {
+    case 2: launch_team(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st); break;
+    case 1:
+      launch_cfg<HD, G, true>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);
+      break;
+    default:
+      launch_cfg<HD, G, false>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);
   }
-  // DEEP when the (sample, kv head) pairs cannot fill the WIDE grid's warps
-  // four times over; FUSEPLAN_ATTN_DEEP=0/1 forces a shape (A/B runs)
-  static const int force = [] {
-    const char* e = std::getenv("FUSEPLAN_ATTN_DEEP");
-    return e ? std::atoi(e) : -1;
-  }();
-  const bool deep = force >= 0 ? force == 1 : B * KVH * 4 <= 148 * DecCfg<HD, false>::kWarps;
-  if (deep)
-    launch_cfg<HD, G, true>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);
-  else
-    launch_cfg<HD, G, false>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);
 }
 
 }  // namespace
+
+// The team kernel (hd 64, G 1) while the (sample, kv head) pairs cannot fill
+// the warp-per-item grid four times over, else deep below that for other
+// shapes, else wide; identical numerics. FUSEPLAN_ATTN_TEAM=0 / FUSEPLAN_ATTN_DEEP=0|1
+// force shapes for A/B runs.
+int attn_decode_variant(int B, int KVH, int hd, int G, int* warps) {
+  static const int team_mode = env_int("FUSEPLAN_ATTN_TEAM", 1);
+  static const int deep_mode = env_int("FUSEPLAN_ATTN_DEEP", -1);
+  const int wide_warps = hd == 64 ? DecCfg<64, false>::kWarps : DecCfg<128, false>::kWarps;
+  const bool small = B * KVH * 4 <= 148 * wide_warps;
+  int v = 0;
+  if (hd == 64 && G == 1 && team_mode && (team_mode == 2 || small)) v = 2;
+  else if (deep_mode >= 0 ? deep_mode == 1 : small) v = 1;
+  if (warps) *warps = v == 2 ? TeamCfg::kWarps : v == 1 ? (hd == 64 ? DecCfg<64, true>::kWarps
+                                                                     : DecCfg<128, true>::kWarps)
+                                                        : wide_warps;
+  return v;
+}
 
 bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer,
                      const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out,

@@ -141,20 +141,30 @@ CUtensorMap make_kv_map(const void* pool, long long rows, int hd);
 // Tokens per decode-attention split (position-determined).
 constexpr int kDecodeChunk = 512;
 // Tensor-core decode attention (attn_decode.cu); false if (hd, group) unsupported or no map.
-// Work items are (sample, non-empty split, kv head), handed out dynamically
-// through counters[0..1] in the order of `items` (attn_decode_items: the
-// (sample, split) pairs, longest first); the splits of a (sample, kv head)
-// merge inside the kernel (the last to finish merges; tickets counters[2 + b *
-// KVH + kvh]). counters: attn_decode_counters(B, KVH) ints, zero, left zero.
+// Work items are (sample, non-empty split, kv head) — or, for long splits when
+// a batch is large enough that the warp-per-item kernel runs, one 128-token
+// sub-chunk of a split (its partial is folded with the others by the last to
+// finish, in sub-chunk order: the same bits as one warp folding them) —
+// handed out dynamically through counters[0..1] in the order of `items`
+// (attn_decode_items, longest first). The splits of a (sample, kv head) merge
+// inside the kernel too (tickets). counters: attn_decode_counters ints, zero,
+// left zero.
 bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer,
                      const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out,
                      int* counters, cudaStream_t st);
-inline int attn_decode_counters(int B, int KVH) { return 2 + B * KVH; }
-// Host: the item table of attn_decode_mma from the contexts: items[0] = n,
-// items[1..n] = b << 8 | split over the non-empty splits, longest first (a
-// longest-processing-time order for the dynamic schedule); ties by (b, split).
-// Capacity: 1 + B * ceil(max_ctx / kDecodeChunk) ints.
-int attn_decode_items(const int* ctx, int B, int* items);
+inline int attn_decode_counters(int B, int KVH, int max_ctx) {
+  const int ns = (max_ctx + kDecodeChunk - 1) / kDecodeChunk;
+  return 2 + B * KVH + B * KVH * ns;  // work queue, split tickets, sub-chunk tickets
+}
+// Which kernel shape attn_decode_mma runs for a batch: 0 warp-per-item wide,
+// 1 warp-per-item deep, 2 team; `warps` = its warps per CTA.
+int attn_decode_variant(int B, int KVH, int hd, int G, int* warps);
+// Host: the item table from the contexts: items[0] = n, items[1..n] =
+// b << 11 | split << 3 | sub (sub 7: the whole split), longest first (an LPT
+// order for the dynamic schedule); ties by (b, split, sub). Splits longer than
+// the mean work per warp are cut into sub-chunks when the wide kernel runs.
+// Capacity: 1 + B * ceil(max_ctx / 128) ints.
+int attn_decode_items(const int* ctx, int B, int KVH, int hd, int G, int* items);
 void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, float rope_theta, bf16* q_out,
               bf16* k_out, bf16* v_out, const KvPoolView* pool, int layer, const int* slot, cudaStream_t st);
 
@@ -162,7 +172,7 @@ void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, fl
 // Decode: q [B, H, hd] (one token per row), paged K/V of `layer`; ctx[b]
 // tokens visible (including the one just appended). out [B, H, hd] bf16.
 // work: float scratch of attn_decode_workspace(B, H, hd, max_ctx) floats.
-size_t attn_decode_workspace(int B, int H, int hd, int max_ctx);
+size_t attn_decode_workspace(int B, int H, int hd, int max_ctx);  // split + sub-chunk partials
 // counters / items (see attn_decode_mma) enable the tensor-core kernel with
 // its fused split merge; nullptr runs the CUDA-core kernel + combine kernel.
 // probe_begin / probe_end (optional) bracket the main split kernel (not the combine).

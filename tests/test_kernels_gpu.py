@@ -169,7 +169,8 @@ def test_add_norm(lib):
 
 
 @pytest.mark.parametrize("hd,H,KVH", [(64, 12, 12), (128, 32, 8), (32, 8, 8), (128, 16, 16), (64, 32, 4)])
-@pytest.mark.parametrize("ctx_list", [[1, 63, 64, 65, 300], [1000, 7, 257], [2000, 513, 512, 511]])
+@pytest.mark.parametrize("ctx_list", [[1, 63, 64, 65, 300], [1000, 7, 257], [2000, 513, 512, 511],
+                                      list(range(7, 7 + 13 * 80, 13))])  # 80 rows: wide kernel, cut splits
 @pytest.mark.parametrize("tma", [True, False])
 def test_attn_decode(lib, hd, H, KVH, ctx_list, tma):
     L, layer, PT = 3, 1, 64

@@ -37,7 +37,7 @@ ws = torch.zeros(int(lib.fp_k_attn_workspace_bytes(B, H, KVH, hd, max_ctx)), dty
 ns = (max_ctx + 63) // 64  # >= splits at any chunk >= 64
 items_h = (C.c_int32 * (1 + B * ns))()
 ctx_h = (C.c_int32 * B)(*[int(c) for c in ctx])
-assert lib.fp_k_attn_items(ctx_h, B, max_ctx, items_h) == 0
+assert lib.fp_k_attn_items(ctx_h, B, H, KVH, hd, max_ctx, items_h) == 0
 items = torch.tensor(list(items_h), dtype=torch.int32, device="cuda")
 
 

@@ -55,8 +55,9 @@ def case(kind, M, N, K):
           f"epi {np.median(per[:, 5] - per[:, 4]):.2f} total {np.median(per[:, 5]):.2f}", flush=True)
 
 
-for kind, M, N, K in (("bf16", 16, 2304, 768), ("bf16", 350, 2304, 768), ("swiglu", 64, 6144, 768),
-                      ("swiglu", 350, 6144, 768), ("f32", 350, 768, 768), ("f32", 350, 768, 3072),
-                      ("vocab", 350, 50257, 768), ("vocab", 16, 50257, 768), ("bf16", 4096, 6144, 768),
-                      ("bf16", 16384, 2304, 768)):
+cases = (("bf16", 8, 2304, 768), ("bf16", 128, 2304, 768), ("swiglu", 8, 6144, 768), ("swiglu", 128, 6144, 768),
+         ("f32", 8, 768, 768), ("f32", 128, 768, 768), ("f32", 8, 768, 3072), ("f32", 128, 768, 3072),
+         ("vocab", 8, 50257, 768), ("vocab", 128, 50257, 768), ("vocab", 350, 50257, 768),
+         ("bf16", 4096, 6144, 768), ("bf16", 16384, 2304, 768))
+for kind, M, N, K in cases:
     case(kind, M, N, K)
