@@ -57,6 +57,7 @@ typedef struct fp_run_options {
   int32_t resident;        /* 1: prompts already resident (same as previous call), experience kept on device */
   int32_t probe_attention; /* 1: time each decode-attention launch (stats.attn_probe_*) */
   int32_t handoff_dp;      /* > 0: pack the experience into length-balanced DP mini-batches (fp_exec_handoff) */
+  int32_t claim_max_live;  /* > 0: a generating rank scores only while its decode batch <= this */
 } fp_run_options;
 
 typedef struct fp_comm {

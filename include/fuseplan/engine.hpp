@@ -52,6 +52,7 @@ struct EngineOptions {
   std::uint64_t sample_seed = 11;  // Philox streams of the sampler
   float kl_beta = 0.05f, gamma = 1.0f, lam = 0.95f;
   int claim_tokens = 8192;         // scoring batch granularity (tokens)
+  int claim_max_live = 0;          // > 0: a generating rank claims scoring work only while its decode batch <= this
   int run_ahead = 4;               // decode steps the host may enqueue ahead of the GPU
   bool resident = false;           // prompts already on the device (same ids as last call), experience left there
   bool probe_attention = false;    // time every decode-attention launch (bench roofline)

@@ -109,7 +109,8 @@ class RunOptions(C.Structure):
     _fields_ = [("token_mode", C.c_int32), ("schedule", C.c_int32), ("temperature", C.c_float),
                 ("token_seed", C.c_uint64), ("sample_seed", C.c_uint64), ("kl_beta", C.c_float),
                 ("gamma", C.c_float), ("lam", C.c_float), ("claim_tokens", C.c_int32), ("run_ahead", C.c_int32),
-                ("resident", C.c_int32), ("probe_attention", C.c_int32), ("handoff_dp", C.c_int32)]
+                ("resident", C.c_int32), ("probe_attention", C.c_int32), ("handoff_dp", C.c_int32),
+                ("claim_max_live", C.c_int32)]
 
 
 class Comm(C.Structure):

@@ -202,6 +202,7 @@ int fp_execute(fp_engine* e, const fp_gen_sample* batch, int32_t n, const fp_gen
     eo.resident = o->resident != 0;
     eo.probe_attention = o->probe_attention != 0;
     eo.handoff_dp = o->handoff_dp;
+    eo.claim_max_live = o->claim_max_live;
     fuseplan::CommSetup cs;
     if (comm) {
       cs.rank = comm->rank;

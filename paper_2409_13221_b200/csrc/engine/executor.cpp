@@ -412,6 +412,11 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
       // generating, the remainder goes in any size.
       const bool hungry = gen_done_me && inflight.empty();
       if (toks < opts.claim_tokens && !all_gen_done && !hungry && !(gen_done_me && G == 1)) return;
+      // while this rank's decode batch is large (bandwidth-bound steps) scoring
+      // waits; it overlaps the latency-bound tail instead
+      if (!gen_done_me && !all_gen_done && opts.claim_max_live > 0 &&
+          static_cast<int>(live.size()) > opts.claim_max_live)
+        return;
       if (!hdr->n_claimed.compare_exchange_strong(c, end)) continue;
       std::vector<fpe::Engine::InferItem> items;
       for (int i = c; i < end; ++i) {

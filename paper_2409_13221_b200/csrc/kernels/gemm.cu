@@ -96,15 +96,15 @@ CUtensorMap out_map_2d(const void* ptr, CUtensorMapDataType dt, int esize, int r
 
 unsigned long long* g_trace = nullptr;
 
-template <int BN, class Epi>
+template <int BN, class Epi, int ST = 0>
 void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int splits, const Epi& epi,
             cudaStream_t st, bool weight_is_a = true, bool cluster_split = false) {
-  using C = GemmCfg<BN, EpiStages<Epi>::value>;
+  using C = GemmCfg<BN, ST ? ST : EpiStages<Epi>::value>;
   if (K % kBK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
   if (a_rows <= 0 || b_rows <= 0) return;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr_set = true;
   }
   const CUtensorMap ma = make_map(A, a_rows, K, 128);
@@ -136,7 +136,7 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
   attr[1].val.clusterDim.z = g.cz;
   cfg.attrs = attr;
   cfg.numAttrs = g.cz > 1 ? 2 : 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi>, ma, mb, g, epi);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi, ST>, ma, mb, g, epi);
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm launch: ") + cudaGetErrorString(e));
   fpk::count_launch();
 }
@@ -202,6 +202,15 @@ void dispatch_bn_small(int M, int a_ctas, F&& f) {
   }
 }
 
+// Large GEMMs (several waves of CTAs) take the 2-stage / 2-CTAs-per-SM shape.
+bool many_waves(int M, int N, int BN) {
+  static const int on = [] {
+    const char* e = std::getenv("FUSEPLAN_GEMM_2CTA");
+    return e ? std::atoi(e) : 1;
+  }();
+  return on && static_cast<long long>((N + 127) / 128) * ((M + BN - 1) / BN) >= 2 * 148;
+}
+
 template <class Epi, class F>
 void dispatch_bn(int M, int a_ctas, F&& f) {
   switch (pick_bn(M, a_ctas)) {
@@ -245,7 +254,10 @@ void gemm_bf16(const bf16* W, int N, int K, const bf16* X, int M, bf16* out, int
   if ((ld_out * 2) % 16) throw std::invalid_argument("gemm_bf16: ld_out must be a multiple of 8");
   dispatch_bn<EpiStoreBF16>(M, (N + 127) / 128, [&]<int BN>() {
     EpiStoreBF16 e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, ld_out, 128, BN)};
-    launch<BN>(W, N, X, M, K, 1, e, st);
+    if (many_waves(M, N, BN))
+      launch<BN, EpiStoreBF16, 2>(W, N, X, M, K, 1, e, st);
+    else
+      launch<BN>(W, N, X, M, K, 1, e, st);
   });
 }
 
@@ -268,7 +280,10 @@ void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float*
   if (N % 4) throw std::invalid_argument("gemm_f32: N must be a multiple of 4");
   dispatch_bn<EpiStoreF32>(M, (N + 127) / 128, [&]<int BN>() {
     EpiStoreF32 e{out_map_2d(resid, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, N, N, 128, BN), 1};
-    launch<BN>(W, N, X, M, K, 1, e, st);
+    if (BN <= 128 && many_waves(M, N, BN))  // (the fp32 staging tile of BN 256 needs a deeper ring)
+      launch<BN, EpiStoreF32, 2>(W, N, X, M, K, 1, e, st);
+    else
+      launch<BN>(W, N, X, M, K, 1, e, st);
   });
 }
 
@@ -289,7 +304,10 @@ void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out,
   if (F % 64) throw std::invalid_argument("gemm_swiglu: F must be a multiple of 64");
   dispatch_bn<int>(M, (2 * F + 127) / 128, [&]<int BN>() {
     EpiSwiGLU<BN> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, BN)};
-    launch<BN>(Wgu, 2 * F, X, M, K, 1, e, st);
+    if (many_waves(M, 2 * F, BN))
+      launch<BN, EpiSwiGLU<BN>, 2>(Wgu, 2 * F, X, M, K, 1, e, st);
+    else
+      launch<BN>(Wgu, 2 * F, X, M, K, 1, e, st);
   });
 }
 

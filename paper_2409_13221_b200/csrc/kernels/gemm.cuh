@@ -108,11 +108,13 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const 
 //   __device__ void finish(State&, int a_row0, int b_row0, int split, int r, int half) const;
 //   static constexpr bool kTmaStore; __device__ void store(const uint8_t* smem,
 //     int a_row0, int b_row0, int split) const;   (one thread, after a barrier)
-template <int BN, class Epi>
+// ST > 0 overrides the ring depth (a 2-stage ring lets two CTAs share an SM:
+// one's epilogue overlaps the other's mainloop — the large-M GEMMs).
+template <int BN, class Epi, int ST = 0>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const GemmGeom g, const __grid_constant__ Epi epi) {
-  using C = GemmCfg<BN, EpiStages<Epi>::value>;
+  using C = GemmCfg<BN, ST ? ST : EpiStages<Epi>::value>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ __align__(8) uint64_t full_bar[C::kStages];
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int r = quarter * 32 + lane_id();
   constexpr int kPStride = (BN < 32 ? 32 : BN) + 4;  // padded fp32 row of the parked partial (32-column chunks)
   constexpr int kPOff = 64 * 1024;                // parked partial: after any epilogue staging
-  static_assert(BN > 64 || kPOff + 128 * kPStride * 4 <= C::kStages * C::kStageBytes, "partial does not fit");
+  constexpr bool kClusterOK = BN <= 64 && kPOff + 128 * kPStride * 4 <= C::kStages * C::kStageBytes;
   auto run_epi = [&](auto&& load) {
     typename Epi::State st{};
 #pragma unroll 1
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
     }
     if (g.cz > 1) {
-      if constexpr (BN <= 64) {
+      if constexpr (kClusterOK) {
         float* P = reinterpret_cast<float*>(smem + kPOff) + r * kPStride;
         for (int c0 = 32 * half; c0 < BN; c0 += 64) {
           float v[32];
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       if (tr && threadIdx.x == 64) tr[5] = gtime();
     }
   }
-  if constexpr (BN <= 64) {
+  if constexpr (kClusterOK) {
     if (g.cz > 1) {
       cluster_sync();
       if (warp >= 2 && cluster_ctarank() == 0) {

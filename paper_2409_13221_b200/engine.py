@@ -131,12 +131,12 @@ class Engine:
                 kl_beta: float = 0.05, gamma: float = 1.0, lam: float = 0.95, claim_tokens: int = 8192,
                 run_ahead: int = 4, rank: int = 0, world: int = 1, shm_name: str | None = None,
                 prompts: np.ndarray | None = None, resident: bool = False,
-                probe_attention: bool = False, handoff_dp: int = 0) -> ExecOutput:
+                probe_attention: bool = False, handoff_dp: int = 0, claim_max_live: int = 0) -> ExecOutput:
         keep: list = []
         n = len(batch)
         opts = _lib.RunOptions(TOKEN_MODES[token_mode], SCHEDULES[schedule], temperature, token_seed, sample_seed,
                                kl_beta, gamma, lam, claim_tokens, run_ahead, int(resident), int(probe_attention),
-                               handoff_dp)
+                               handoff_dp, claim_max_live)
         comm = _lib.Comm(rank, world, shm_name.encode() if shm_name else None)
         pp = None
         if prompts is not None:
