@@ -154,6 +154,8 @@ int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t h
  * capturable; tooling / roofline): items_dev from fp_k_attn_items (host ctx),
  * workspace of fp_k_attn_workspace_bytes, zero-filled before its first use
  * (the kernel leaves its counters zero). */
+/* Debug: per-warp (begin ns, end ns, units) of the next decode-attention launches (NULL disables). */
+void fp_k_attn_trace(void* buf);
 int64_t fp_k_attn_workspace_bytes(int32_t B, int32_t H, int32_t KVH, int32_t hd, int32_t max_ctx);
 int fp_k_attn_items(const int32_t* ctx_host, int32_t B, int32_t H, int32_t KVH, int32_t hd, int32_t max_ctx,
                     int32_t* items_host); /* items_host: 1 + B * ceil(max_ctx / 128) ints */

@@ -185,6 +185,7 @@ ENGINE_SYMBOLS = {
     "fp_k_add_norm": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, C.c_int32, C.c_int32, _vp]),
     "fp_k_attn_decode": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int32,
                                    C.c_int32, _vp, C.c_int32, _vp, _vp, C.c_int32, _vp, _vp]),
+    "fp_k_attn_trace": (None, [_vp]),
     "fp_k_attn_workspace_bytes": (C.c_int64, [C.c_int32] * 5),
     "fp_k_attn_items": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp]),
     "fp_k_attn_decode_ws": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int32,

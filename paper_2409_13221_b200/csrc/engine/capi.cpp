@@ -475,6 +475,8 @@ int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t h
   });
 }
 
+void fp_k_attn_trace(void* buf) { fpk::set_attn_trace(static_cast<unsigned long long*>(buf)); }
+
 int64_t fp_k_attn_workspace_bytes(int32_t B, int32_t H, int32_t KVH, int32_t hd, int32_t max_ctx) {
   return static_cast<int64_t>(fpk::attn_decode_workspace(B, H, hd, max_ctx)) * 4 + 256 +
          static_cast<int64_t>(fpk::attn_decode_counters(B, KVH, max_ctx)) * 4;

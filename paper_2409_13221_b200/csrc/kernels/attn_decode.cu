@@ -29,6 +29,12 @@ namespace fpk {
 namespace {
 
 constexpr int kPT = 64;
+__device__ unsigned long long* g_attn_trace = nullptr;  // debug tracing (set_attn_trace)
+__device__ __forceinline__ unsigned long long gtime_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 constexpr int kTileBytes = 32 * 128;  // one 32-row x 64-column bf16 box (a TMA box)
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -128,6 +134,7 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
     float scale_log2,
     float* __restrict__ part_o, float* __restrict__ part_ml, float* __restrict__ sub_o, float* __restrict__ sub_ml,
     bf16* __restrict__ out, int* __restrict__ counters) {
+  const unsigned long long t_entry = g_attn_trace ? gtime_ns() : 0ull;
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   using C = DecCfg<HD, DEEP>;
   static_assert(G <= 8, "GQA group must fit the first 8 MMA rows");
@@ -245,7 +252,9 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
   bool acc_has = false;
   bool fresh = true;
 
-  for (int c = 0; cur.j < n_items; ++c) {
+  const unsigned long long t_begin = g_attn_trace ? gtime_ns() : 0ull;
+  int c = 0;
+  for (; cur.j < n_items; ++c) {
     const int k = c % C::kStages;
     mbar_wait(&bar[k], (c / C::kStages) & 1);
     if (fresh) {  // new item: Q fragments from the stage's q slot, reset the running state
@@ -472,6 +481,13 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
       cue = ((cur.t1 - 1) >> 5) + 1;
       fresh = true;
     }
+  }
+  if (g_attn_trace && lane == 0) {  // debug: per-warp busy interval and units (tools/attn_roofline.py --trace)
+    unsigned long long* t = g_attn_trace + 4ull * (blockIdx.x * C::kWarps + warp);
+    t[0] = t_entry;
+    t[1] = t_begin;
+    t[2] = gtime_ns();
+    t[3] = c;
   }
   // the last warp out resets the work counter for the next launch
   if (lane == 0 && atomicAdd(&counters[1], 1) == static_cast<int>(gridDim.x) * C::kWarps - 1) {
@@ -849,6 +865,8 @@ void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const 
 }
 
 }  // namespace
+
+void set_attn_trace(unsigned long long* buf) { cudaMemcpyToSymbol(g_attn_trace, &buf, sizeof(buf)); }
 
 // The team kernel (hd 64, G 1) while the (sample, kv head) pairs cannot fill
 // the warp-per-item grid four times over, else deep below that for other

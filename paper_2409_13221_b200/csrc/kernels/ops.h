@@ -152,6 +152,9 @@ constexpr int kDecodeChunk = 512;
 bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer,
                      const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out,
                      int* counters, cudaStream_t st);
+// Debug: per-warp (entry ns, loop-begin ns, end ns, units) of subsequent
+// warp-per-item decode-attention launches into buf (4 x 148 x warps); nullptr disables.
+void set_attn_trace(unsigned long long* buf);
 inline int attn_decode_counters(int B, int KVH, int max_ctx) {
   const int ns = (max_ctx + kDecodeChunk - 1) / kDecodeChunk;
   return 2 + B * KVH + B * KVH * ns;  // work queue, split tickets, sub-chunk tickets

@@ -67,6 +67,23 @@ for _ in range(20):
     times.append(e0.elapsed_time(e1))
 times.sort()
 ms = times[len(times) // 2]
+if "--trace" in sys.argv:
+    import numpy as np
+    tr = torch.zeros(4 * 148 * 12, dtype=torch.int64, device="cuda")
+    lib.fp_k_attn_trace(p(tr))
+    flush.zero_()
+    run(s.cuda_stream)
+    torch.cuda.synchronize()
+    lib.fp_k_attn_trace(None)
+    t = tr.view(-1, 4).cpu().numpy()
+    t = t[t[:, 0] > 0]
+    t0 = t[:, 0].min()
+    pro = (t[:, 1] - t[:, 0]) / 1e3
+    end = (t[:, 2] - t0) / 1e3
+    print(f"trace: warps {len(t)}, entry spread {(t[:, 0].max() - t0) / 1e3:.2f} us, prologue med/max "
+          f"{np.median(pro):.2f}/{pro.max():.2f} us, end min/med/max {end.min():.1f}/{np.median(end):.1f}/"
+          f"{end.max():.1f} us (from first entry), units min/med/max {t[:, 3].min()}/{int(np.median(t[:, 3]))}/"
+          f"{t[:, 3].max()}")
 alg = float(ctx.sum()) * 2 * KVH * hd * 2 + B * H * hd * 2
 print(json.dumps({"kernel": "attn_decode_mma_kernel<64,1>", "B": B, "ctx_sum": int(ctx.sum()),
                   "algorithmic_bytes": alg, "median_ms": ms, "achieved_GBps": alg / (ms / 1e3) / 1e9,
