@@ -155,7 +155,7 @@ def run_reference(args, world, rank):
     ref_lib = ROOT / "oracle" / "_ref" / "libfuseplan_ref.so"
     if ref_lib.exists():
         rs = Sched(str(ref_lib))
-        cfg = gen_config(w, args.gpus)
+        cfg = gen_config(w, args.gpus, calibrated=True)
         t0 = time.perf_counter()
         rs.simulate_fused(batch, cfg, round(0.2 * len(batch)))
         sim = time.perf_counter() - t0
@@ -202,7 +202,7 @@ def main():
     w = workload_for(G)
     eng = Engine(w, device=local, max_samples=w.n_prompts, max_live=min(w.n_prompts, 2 * w.n_prompts // G))
     batch = batch_for(w, eng.sched)
-    cfg = gen_config(w, G)
+    cfg = gen_config(w, G, calibrated=True)  # decision-clock constants fitted to measured B200 steps
     r_t = round(args.r_ratio * len(batch)) if G > 1 else 0
     shm = None
     if dist:

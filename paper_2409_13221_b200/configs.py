@@ -103,16 +103,29 @@ def model_spec(name: str, d: Dims):
     return ModelSpec(name, d.num_layers, d.num_heads, d.hidden, d.ffn)
 
 
+def calibration(w: Workload) -> dict | None:
+    """CostModel constants fitted to measured B200 steps by tools/calibrate.py
+    (profiles/r01_calibration_<workload>.json), or None."""
+    import json
+    from pathlib import Path
+    p = Path(__file__).resolve().parent.parent / "profiles" / f"r01_calibration_{w.name}.json"
+    return json.loads(p.read_text()) if p.exists() else None
+
+
 def gen_config(w: Workload, instances: int, *, bs_max: int = 512, kv_capacity: float = 0.0,
                interconnect_bandwidth: float = 770e9, decode_step_base: float = 1e-3,
-               time_per_token_coeff: float = 1e-12):
+               time_per_token_coeff: float = 1e-12, calibrated: bool = False):
     """Decision-clock configuration (GenSimConfig) of a workload on `instances` B200s.
 
     instance_gpus = 1 (one engine per B200). The cost constants are the
-    calibration knobs of SURVEY §8f row 1; the defaults are B200-ish (decode
-    step ~1 ms on the plateau, NVLink peer bandwidth 770 GB/s measured).
+    calibration knobs of SURVEY §8f row 1; calibrated=True takes them from the
+    fit of measured B200 steps (tools/calibrate.py) when one exists.
     """
     from .sched import ClusterSpec, CostModel, GenSimConfig
+    cal = calibration(w) if calibrated else None
+    if cal:  # measured decode plateau / step base and forward cost (SURVEY §8f row 1)
+        bs_max, decode_step_base = int(cal["bs_max"]), float(cal["decode_step_base"])
+        time_per_token_coeff = float(cal["time_per_token_coeff"])
     return GenSimConfig(
         actor=model_spec("actor", w.actor), num_instances=instances, instance_gpus=1,
         tasks=[("ref", model_spec("ref", w.ref)), ("reward", model_spec("reward", w.reward)),

@@ -23,8 +23,8 @@ torch.cuda.set_device(local)
 w = scaled(WORKLOADS["gpt2s"], n_prompts=512 * world)
 eng = Engine(w, device=local, max_samples=w.n_prompts, max_live=min(w.n_prompts, 2 * w.n_prompts // world))
 batch = batch_for(w, eng.sched)
-cfg = gen_config(w, world)
-r_t = round(0.2 * len(batch))
+cfg = gen_config(w, world, calibrated=True)
+r_t = round((float(sys.argv[3]) if len(sys.argv) > 3 else 0.2) * len(batch))
 name = [f"/fp_prof_{uuid.uuid4().hex[:10]}" if rank == 0 else None]
 dist.broadcast_object_list(name, src=0)
 prompts = eng.synthetic_prompts(len(batch), 7)
