@@ -606,14 +606,11 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
     if (it.j >= n_items || ub < ua) ub = ua;
   };
 
-  pdl_wait();  // q, the new K/V and the counters come from earlier kernels
-  if (tw == 0 && lane == 0) {
-    const int first = static_cast<int>(blockIdx.x) * C::kTeams + team;  // static first item
-    put(0, first * 1);
-    put(1, n_teams + atomicAdd(&counters[0], 1));
-  }
+  // item 0 of each team is static (its index), so it is decoded before
+  // griddepcontrol.wait; item 1 comes from the counter after it
+  if (tw == 0 && lane == 0) put(0, static_cast<int>(blockIdx.x) * C::kTeams + team);
   team_bar(team);
-  int known = 1;  // highest item index whose info is in the ring
+  int known = 0;  // highest item index whose info is in the ring
 
   // issue cursor over (item index, unit) of this warp's sub-chunks
   int in_i = 0, in_u = 0, in_ue = 0, in_ua = 0, in_pg = 0;
@@ -636,26 +633,46 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
     }
   };
   int n_iss = 0, n_con = 0;
+  auto issue_unit = [&](bool with_q) {  // all lanes
+    const int k = n_iss % C::kStages;
+    const int pid = __shfl_sync(0xffffffffu, in_pg, (in_u >> 1) - (in_ua >> 1));
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      const int rk = pid * rows_per_page + layer * layer_rows + in_it.kvh * 2 * kPT + (in_u & 1) * 32;
+      uint8_t* dst = my_smem + k * C::kStageBytes;
+      const bool first = in_u == in_ua;
+      mbar_arrive_expect_tx(&bar[k], C::kKV + (first ? HD * 2 : 0));
+      tma_load_2d(dst, &kv_map, &bar[k], 0, rk);
+      tma_load_2d(dst + 32 * 128, &kv_map, &bar[k], 0, rk + kPT);
+      if (first && with_q)
+        bulk_load(dst + C::kKV, q + (static_cast<size_t>(in_it.b) * H + in_it.kvh) * HD, HD * 2, &bar[k]);
+    }
+    ++n_iss;
+    ++in_u;
+  };
   auto pump = [&]() {  // all lanes
     advance_item();
     while (in_ok && in_u < in_ue && n_iss - n_con < C::kStages) {
-      const int k = n_iss % C::kStages;
-      const int pid = __shfl_sync(0xffffffffu, in_pg, (in_u >> 1) - (in_ua >> 1));
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const int rk = pid * rows_per_page + layer * layer_rows + in_it.kvh * 2 * kPT + (in_u & 1) * 32;
-        uint8_t* dst = my_smem + k * C::kStageBytes;
-        const bool first = in_u == in_ua;
-        mbar_arrive_expect_tx(&bar[k], C::kKV + (first ? HD * 2 : 0));
-        tma_load_2d(dst, &kv_map, &bar[k], 0, rk);
-        tma_load_2d(dst + 32 * 128, &kv_map, &bar[k], 0, rk + kPT);
-        if (first) bulk_load(dst + C::kKV, q + (static_cast<size_t>(in_it.b) * H + in_it.kvh) * HD, HD * 2, &bar[k]);
-      }
-      ++n_iss;
-      ++in_u;
+      issue_unit(true);
       advance_item();
     }
   };
+  // before waiting on the previous kernel: the cached units of item 0 (only
+  // tokens written by earlier steps; the q row follows after the wait)
+  bool q_late = false;
+  if (in_ok && in_u < in_ue) {
+    const int u_new = (in_it.cx - 1) >> 5;
+    while (n_iss < C::kStages && in_u < in_ue && in_u < u_new) {
+      q_late |= in_u == in_ua;
+      issue_unit(false);
+    }
+  }
+  pdl_wait();  // q, the new K/V and the counters come from earlier kernels
+  if (q_late && lane == 0)  // stage 0 (the sub-chunk's first unit) already expects the q bytes
+    bulk_load(my_smem + C::kKV, q + (static_cast<size_t>(in_it.b) * H + in_it.kvh) * HD, HD * 2, &bar[0]);
+  if (tw == 0 && lane == 0) put(1, n_teams + atomicAdd(&counters[0], 1));
+  team_bar(team);
+  known = 1;
   pump();
 
   const int r0 = lane >> 2;
