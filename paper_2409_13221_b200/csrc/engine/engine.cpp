@@ -103,6 +103,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
   }
   for (int s = cfg_.max_live - 1; s >= 0; --s) free_slots_.push_back(s);
   if (const char* g = std::getenv("FUSEPLAN_DECODE_GRAPHS")) use_graphs_ = std::atoi(g) != 0;  // A/B switch
+  if (const char* g = std::getenv("FUSEPLAN_L2_PREFETCH")) l2_prefetch_ = std::atoi(g) != 0;
   pad_slot_ = cfg_.max_live;  // decode padding rows: block-table row of zeros -> scratch page 0
   slot_pages_.assign(cfg_.max_live + 1, {});
   bt_host_.assign(static_cast<size_t>(cfg_.max_live + 1) * max_pages_per_sample_, 0);
@@ -573,8 +574,15 @@ void Engine::decode_kernels(int B, int max_ctx, int mode, float inv_temp, uint64
   int nparts = 0;
   for (int l = 0; l < D.L; ++l) {
     const LayerW& L = w.layers[l];
+    const size_t wq = static_cast<size_t>(D.qkv_width()) * D.d * 2, wo = static_cast<size_t>(D.d) * D.H * D.hd * 2;
+    const size_t wgu = static_cast<size_t>(2) * D.F * D.d * 2, wdn = static_cast<size_t>(D.d) * D.F * 2;
+    fpk::L2Prefetch pf1, pf2;  // this layer's weights into L2 ahead of their GEMMs
+    if (l2_prefetch_) {
+      pf1.p[0] = L.wqkv, pf1.bytes[0] = wq, pf1.p[1] = L.wo, pf1.bytes[1] = wo;
+      pf2.p[0] = L.wgu, pf2.bytes[0] = wgu, pf2.p[1] = L.wd, pf2.bytes[1] = wdn;
+    }
     fpk::add_norm(dec_.x, nparts ? dec_.parts : nullptr, nparts, stride, L.ln1, dec_.h, B, D.d, nullptr, 0, nullptr,
-                  nullptr, st);
+                  nullptr, st, pf1);
     fpk::gemm_qkv_rope(L.wqkv, D.d, dec_.h, B, D.H, D.KVH, D.hd, pos, rope_cs_, pv, l, slot, dec_.q, st);
     if (probe_on_) {
       ProbeRec pr{probe_event(), probe_event(), 0.0};
@@ -587,7 +595,7 @@ void Engine::decode_kernels(int B, int max_ctx, int mode, float inv_temp, uint64
       fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, items, max_ctx, dec_.attn_work, dec_.attn, dec_.attn_cnt, st);
     }
     fpk::gemm_f32_splitk(L.wo, D.d, D.H * D.hd, dec_.attn, B, dec_.parts, so, st);
-    fpk::add_norm(dec_.x, dec_.parts, so, stride, L.ln2, dec_.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
+    fpk::add_norm(dec_.x, dec_.parts, so, stride, L.ln2, dec_.h, B, D.d, nullptr, 0, nullptr, nullptr, st, pf2);
     fpk::gemm_swiglu_decode(L.wgu, D.F, D.d, dec_.h, B, dec_.act, st);
     fpk::gemm_f32_splitk(L.wd, D.d, D.F, dec_.act, B, dec_.parts, sd, st);
     nparts = sd;

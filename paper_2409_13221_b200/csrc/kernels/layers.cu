@@ -104,8 +104,14 @@ template <int NS>  // number of split-K partials
 __global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__ parts, size_t split_stride,
                                 const float* __restrict__ gain, bf16* __restrict__ y, int d,
                                 const int* __restrict__ gather, int rows, const bf16* __restrict__ value_w,
-                                float* __restrict__ value) {
+                                float* __restrict__ value, L2Prefetch pf) {
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
+  if (threadIdx.x < 2 && pf.bytes[threadIdx.x]) {  // the next GEMMs' weights: block slices, 32 KB requests
+    const size_t n = pf.bytes[threadIdx.x], per = ((n + gridDim.x - 1) / gridDim.x + 15) & ~size_t(15);
+    const char* base = static_cast<const char*>(pf.p[threadIdx.x]);
+    for (size_t o = blockIdx.x * per; o < min(n, (blockIdx.x + 1) * per); o += 32768)
+      prefetch_l2(base + o, static_cast<uint32_t>(min(size_t(32768), min(n, (blockIdx.x + 1) * per) - o)));
+  }
   pdl_wait();     // PDL-launched: x and the partials come from the previous kernels
   __shared__ float red[32];
   const int i = blockIdx.x;
@@ -330,7 +336,7 @@ void assemble_batch(const AssembleArgs& a, int n, cudaStream_t st) {
 }
 
 void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, const float* gain, bf16* y, int M, int d,
-              const int* gather, int M_out, const bf16* value_w, float* value, cudaStream_t st) {
+              const int* gather, int M_out, const bf16* value_w, float* value, cudaStream_t st, const L2Prefetch& pf) {
   const int rows = gather ? M_out : M;
   if (rows <= 0) return;
   const int ns = parts ? nsplit : 0;
@@ -338,7 +344,7 @@ void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, con
   const dim3 grid(rows), block(((d / 4 + 31) / 32) * 32);
   const size_t sm = 0;
 #define FP_AN(N_) \
-  case N_: launch_pdl(add_norm_kernel<N_>, dim3(grid), dim3(block), sm, st, x, parts, split_stride, gain, y, d, gather, rows, value_w, value); break;
+  case N_: launch_pdl(add_norm_kernel<N_>, dim3(grid), dim3(block), sm, st, x, parts, split_stride, gain, y, d, gather, rows, value_w, value, pf); break;
   switch (ns) {
     FP_AN(0) FP_AN(1) FP_AN(2) FP_AN(3) FP_AN(4) FP_AN(5) FP_AN(6) FP_AN(7) FP_AN(8)
     default: throw std::invalid_argument("add_norm: at most 8 split-K partials");

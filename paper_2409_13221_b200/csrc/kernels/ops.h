@@ -75,8 +75,15 @@ void assemble_batch(const AssembleArgs& a, int n, cudaStream_t st);
 // For output row i (src = gather ? gather[i] : i): xs = x[src] + sum_s parts[s][src];
 // if !gather, x[src] = xs. y[i] = bf16(rmsnorm(xs) * g). If value_w != nullptr,
 // instead value[i] = dot(rmsnorm(xs) * g, value_w) and y is not written.
+// Weight ranges to pull into L2 while a small kernel runs (the next GEMMs'
+// weights: their first TMA loads then hit L2 instead of waiting on DRAM).
+struct L2Prefetch {
+  const void* p[2] = {nullptr, nullptr};
+  size_t bytes[2] = {0, 0};
+};
 void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, const float* gain, bf16* y, int M,
-              int d, const int* gather, int M_out, const bf16* value_w, float* value, cudaStream_t st);
+              int d, const int* gather, int M_out, const bf16* value_w, float* value, cudaStream_t st,
+              const L2Prefetch& pf = L2Prefetch{});
 
 // RoPE on q, k of a packed qkv [M, (H + 2 KVH) * hd] row block; q -> q_out
 // [M, H, hd]; k, v -> either contiguous k_out/v_out [M, KVH, hd] and/or the

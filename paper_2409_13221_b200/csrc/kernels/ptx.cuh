@@ -55,6 +55,11 @@ __device__ __forceinline__ float4 ld_dsmem_v4(uint32_t addr) {
   return v;
 }
 
+// Pull [p, p + bytes) into L2 (bytes a multiple of 16); no completion tracking.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
