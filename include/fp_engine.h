@@ -88,6 +88,18 @@ int fp_engine_kv_bytes_per_token(const fp_engine* e, int64_t* bytes);
 /* Synthetic prompt ids [n][max_prompt] for token_seed. */
 int fp_synthetic_prompts(const fp_engine* e, int32_t n, uint64_t token_seed, int32_t* out);
 
+/* Weight sync (reference: the per-iteration actor weight redistribution,
+ * workflow.cpp:94-102): every rank calls it with the same
+ * model slot, src rank and comm (a fresh shm name); rank r ends with src's
+ * weights, pulled over NVLink (scatter + all-gather). seconds: this rank's time. */
+int fp_engine_broadcast_model(fp_engine* e, int32_t model, int32_t src, const fp_comm* comm, double* seconds);
+/* Device pointer and size of a model's weight blob (engine layout), e.g. for a
+ * trainer writing updated weights in place before fp_engine_broadcast_model. */
+int fp_engine_model_ptr(const fp_engine* e, int32_t model, void** dev_ptr, int64_t* bytes);
+/* Tooling: regenerate a model's synthetic weights from `seed`; order-independent
+ * 64-bit checksum of its blob. */
+int fp_engine_reinit_model(fp_engine* e, int32_t model, uint64_t seed);
+int fp_engine_model_checksum(fp_engine* e, int32_t model, uint64_t* sum);
 /* Run the stage. prompts: [n][max_prompt] ids or NULL (synthetic). */
 int fp_execute(fp_engine* e, const fp_gen_sample* batch, int32_t n, const fp_gen_config* cfg, int32_t r_t,
                const fp_run_options* opts, const fp_comm* comm, const int32_t* prompts, fp_exec** out);

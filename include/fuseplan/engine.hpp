@@ -131,6 +131,15 @@ void destroy_engine(GpuEngine* e);
 /// Synthetic prompts (hash of token_seed) of shape [n][max_prompt].
 std::vector<int> synthetic_prompts(const GpuEngine* e, int n, std::uint64_t token_seed);
 
+// Weight sync across the ranks of one box: model slot
+// 0 actor, 1 ref, 2 critic, 3 reward; every rank calls it with the same src
+// and comm (a fresh shm name). Returns this rank's seconds.
+double broadcast_model(GpuEngine* e, int model, int src, const CommSetup& comm);
+// Test / tooling helpers: regenerate a model's synthetic weights with another
+// seed; an order-independent 64-bit checksum of its weight blob.
+void reinit_model(GpuEngine* e, int model, std::uint64_t seed);
+std::uint64_t model_checksum(GpuEngine* e, int model);
+
 ExecResult execute(GpuEngine* e, const std::vector<GenSample>& batch, const GenSimConfig& cfg, int r_t,
                    const EngineOptions& opts, const CommSetup& comm, const std::vector<int>* prompts = nullptr);
 

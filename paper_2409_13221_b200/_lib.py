@@ -158,6 +158,10 @@ ENGINE_SYMBOLS = {
     "fp_engine_create": (C.c_int, [P(EngineSetup), P(_vp)]),
     "fp_engine_destroy": (None, [_vp]),
     "fp_engine_model_size": (C.c_int, [_vp, C.c_int32, _i64p, _i64p]),
+    "fp_engine_broadcast_model": (C.c_int, [_vp, C.c_int32, C.c_int32, P(Comm), _f64p]),
+    "fp_engine_model_ptr": (C.c_int, [_vp, C.c_int32, P(C.c_void_p), _i64p]),
+    "fp_engine_reinit_model": (C.c_int, [_vp, C.c_int32, C.c_uint64]),
+    "fp_engine_model_checksum": (C.c_int, [_vp, C.c_int32, P(C.c_uint64)]),
     "fp_engine_kv_bytes_per_token": (C.c_int, [_vp, _i64p]),
     "fp_synthetic_prompts": (C.c_int, [_vp, C.c_int32, C.c_uint64, _i32p]),
     "fp_execute": (C.c_int, [_vp, P(GenSample), C.c_int32, P(GenConfig), C.c_int32, P(RunOptions), P(Comm), _i32p,

@@ -157,6 +157,46 @@ int fp_engine_model_size(const fp_engine* e, int32_t model, int64_t* bytes, int6
   });
 }
 
+int fp_engine_broadcast_model(fp_engine* e, int32_t model, int32_t src, const fp_comm* comm, double* seconds) {
+  return guarded([&] {
+    need(e, "engine");
+    need(comm, "comm");
+    fuseplan::CommSetup c;
+    c.rank = comm->rank;
+    c.world = comm->world;
+    c.shm_name = comm->shm_name ? comm->shm_name : "";
+    const double t = fuseplan::broadcast_model(e->g, model, src, c);
+    if (seconds) *seconds = t;
+  });
+}
+
+int fp_engine_model_ptr(const fp_engine* e, int32_t model, void** dev_ptr, int64_t* bytes) {
+  return guarded([&] {
+    need(e, "engine");
+    if (model < 0 || model > 3) throw std::invalid_argument("model index out of range");
+    const fpe::ModelW& w = fp_engine_internal(e->g).model(model);
+    if (dev_ptr) *dev_ptr = w.blob;
+    if (bytes) *bytes = static_cast<int64_t>(w.bytes);
+  });
+}
+
+int fp_engine_reinit_model(fp_engine* e, int32_t model, uint64_t seed) {
+  return guarded([&] {
+    need(e, "engine");
+    if (model < 0 || model > 3) throw std::invalid_argument("model index out of range");
+    fuseplan::reinit_model(e->g, model, seed);
+  });
+}
+
+int fp_engine_model_checksum(fp_engine* e, int32_t model, uint64_t* sum) {
+  return guarded([&] {
+    need(e, "engine");
+    need(sum, "sum");
+    if (model < 0 || model > 3) throw std::invalid_argument("model index out of range");
+    *sum = fuseplan::model_checksum(e->g, model);
+  });
+}
+
 int fp_engine_kv_bytes_per_token(const fp_engine* e, int64_t* bytes) {
   return guarded([&] {
     need(e, "engine");

@@ -174,14 +174,38 @@ void Engine::init_model(int m) {
   const size_t per_layer = al(qw * d * 2) + al(d * ao * 2) + al(2 * F * d * 2) + al(d * F * 2) + 2 * al(d * 4);
   bytes += D.L * per_layer + al(d * 4) + (w.lm_head ? al(V * d * 2) : al(d * 2));
   FP_CUDA(cudaMalloc(&w.blob, bytes));
+  FP_CUDA(cudaMemsetAsync(w.blob, 0, bytes, s_decode_));  // padding included: checksums see defined bytes
   w.bytes = bytes;
+  fill_model(m, cfg_.weight_seed);
+}
+
+void Engine::reinit_model(int m, uint64_t seed) {
+  fill_model(m, seed);
+  FP_CUDA(cudaStreamSynchronize(s_decode_));
+}
+
+uint64_t Engine::model_checksum(int m) {
+  unsigned long long* d = static_cast<unsigned long long*>(decode_scratch(sizeof(unsigned long long)));
+  FP_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s_decode_));
+  fpk::checksum64(models_[m].blob, models_[m].bytes, d, s_decode_);
+  unsigned long long h = 0;
+  FP_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s_decode_));
+  FP_CUDA(cudaStreamSynchronize(s_decode_));
+  return h;
+}
+
+void Engine::fill_model(int m, uint64_t wseed) {
+  ModelW& w = models_[m];
+  const Dims& D = cfg_.model[m];
+  const size_t d = D.d, F = D.F, V = D.V, qw = D.qkv_width(), ao = static_cast<size_t>(D.H) * D.hd;
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   uint8_t* p = static_cast<uint8_t*>(w.blob);
   auto take = [&](size_t b) {
     uint8_t* r = p;
     p += al(b);
     return r;
   };
-  const uint64_t seed = cfg_.weight_seed;
+  const uint64_t seed = wseed;
   cudaStream_t st = s_decode_;
   w.embed = reinterpret_cast<bf16*>(take(V * d * 2));
   fpk::init_bf16(w.embed, V * d, seed, fpk::weight_tag(m, 0, fpk::kTagEmbed), 1.0f, st);

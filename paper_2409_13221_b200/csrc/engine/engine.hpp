@@ -90,6 +90,8 @@ class Engine {
 
   const EngineConfig& config() const { return cfg_; }
   const ModelW& model(int m) const { return models_[m]; }
+  void reinit_model(int m, uint64_t seed);     // synthetic weights from another seed (same layout)
+  uint64_t model_checksum(int m);             // sum of the blob's 64-bit words (synchronises)
   cudaStream_t decode_stream() const { return s_decode_; }
   cudaStream_t infer_stream() const { return s_infer_; }
   cudaStream_t copy_stream() const { return s_copy_; }
@@ -248,6 +250,7 @@ class Engine {
   };
 
   void init_model(int m);
+  void fill_model(int m, uint64_t seed);
   void alloc_ws();
   void forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, int n_tiles, bool use_pool,
                       cudaStream_t st);

@@ -81,6 +81,7 @@ struct Header {
   int world, n, max_pages, pad_;
   cudaIpcMemHandle_t h_hist_tok[kMaxRanks], h_hist_logp[kMaxRanks], h_pool[kMaxRanks];
   cudaIpcMemHandle_t h_exp[kMaxRanks];  // experience arrays (hand-off)
+  cudaIpcMemHandle_t h_model[kMaxRanks];  // weight blobs (broadcast_model)
 };
 
 class Region {
@@ -209,6 +210,60 @@ GpuEngine* create_engine(const EngineSetup& s) {
 }
 
 void destroy_engine(GpuEngine* e) { delete e; }
+
+// Weight sync: after a training step updated a model on
+// rank `src`, every rank pulls it over NVLink. Scatter + all-gather of 1/G
+// slices through CUDA IPC peer pointers: src sends each byte once, every
+// rank receives (G-1)/G of the blob from G-1 peers in parallel, and the
+// copy kernels pull 1 MiB pieces with 16-byte vector loads.
+double broadcast_model(GpuEngine* ge, int model, int src, const CommSetup& comm) {
+  fpe::Engine& E = *ge->eng;
+  FP_CUDA(cudaSetDevice(E.config().device));
+  const int G = comm.world, me = comm.rank;
+  if (model < 0 || model > 3) throw std::invalid_argument("broadcast_model: model index out of range");
+  if (G < 1 || G > kMaxRanks || me < 0 || me >= G || src < 0 || src >= G)
+    throw std::invalid_argument("broadcast_model: bad rank/world/src");
+  if (G == 1) return 0.0;
+  Region region(comm, 1, 1, 1);
+  Header* hdr = region.hdr();
+  uint8_t* blob = static_cast<uint8_t*>(E.model(model).blob);
+  const size_t bytes = E.model(model).bytes;  // a multiple of 256
+  FP_CUDA(cudaIpcGetMemHandle(&hdr->h_model[me], blob));
+  region.barrier();
+  std::vector<const uint8_t*> base(G);
+  for (int r = 0; r < G; ++r) base[r] = r == me ? blob : static_cast<const uint8_t*>(E.open_ipc(hdr->h_model[r]));
+  const size_t per = ((bytes + G - 1) / G + 255) & ~size_t(255);
+  cudaStream_t st = E.decode_stream();
+  auto pull = [&](int from, int slice, std::vector<fpk::CopyChunk>& list) {
+    const size_t b0 = std::min(bytes, slice * per), b1 = std::min(bytes, (slice + 1) * per);
+    for (size_t o = b0; o < b1; o += (1u << 20))
+      list.push_back({base[from] + o, blob + o, std::min<size_t>(1u << 20, b1 - o)});
+  };
+  auto run = [&](const std::vector<fpk::CopyChunk>& list) {
+    if (!list.empty()) {
+      void* dl = E.decode_scratch(list.size() * sizeof(fpk::CopyChunk));
+      E.upload(dl, list.data(), list.size() * sizeof(fpk::CopyChunk), st);
+      fpk::copy_chunks(static_cast<const fpk::CopyChunk*>(dl), static_cast<int>(list.size()), st);
+    }
+    FP_CUDA(cudaStreamSynchronize(st));
+    region.barrier();
+  };
+  FP_CUDA(cudaStreamSynchronize(st));
+  region.barrier();
+  const auto t0 = Clock::now();
+  std::vector<fpk::CopyChunk> l1, l2;
+  if (me != src) pull(src, me, l1);  // scatter: my slice from src
+  run(l1);
+  if (me != src)  // all-gather: every other slice from the rank that holds it
+    for (int c = 0; c < G; ++c)
+      if (c != me) pull(c, c, l2);
+  run(l2);
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+void reinit_model(GpuEngine* ge, int model, std::uint64_t seed) { ge->eng->reinit_model(model, seed); }
+
+std::uint64_t model_checksum(GpuEngine* ge, int model) { return ge->eng->model_checksum(model); }
 
 std::vector<int> synthetic_prompts(const GpuEngine* e, int n, std::uint64_t token_seed) {
   const int P = e->setup.max_prompt, V = e->setup.actor.vocab;

@@ -381,4 +381,19 @@ void rope_table(float2* tab, int max_pos, int hd, float rope_theta, cudaStream_t
   fpk::count_launch();
 }
 
+__global__ void checksum64_kernel(const unsigned long long* __restrict__ w, size_t n, unsigned long long* out) {
+  unsigned long long acc = 0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    acc += w[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);  // integer sums: order-independent
+}
+
+void checksum64(const void* p, size_t bytes, unsigned long long* out, cudaStream_t st) {
+  checksum64_kernel<<<296, 256, 0, st>>>(static_cast<const unsigned long long*>(p), bytes / 8, out);
+  fpk::count_launch();
+}
+
 }  // namespace fpk

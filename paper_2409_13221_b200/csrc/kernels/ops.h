@@ -218,6 +218,8 @@ void copy_words(const CopyChunk* d_list, int n, cudaStream_t st);
 // cur_tok[slot[i]] = gen[i] > 0 ? hist[sid[i]][gen[i]-1] : prompts[sid[i]][P[i]-1]
 void cur_from_hist(const int* d_quad, int n, const int* hist_tok, int max_new, const int* prompts, int max_prompt,
                    int* cur_tok, cudaStream_t st);  // d_quad: [4][n] = slot, sid, gen, P
+// *out += sum of the 64-bit words of [p, p + bytes) (bytes % 8 == 0; *out zeroed by the caller)
+void checksum64(const void* p, size_t bytes, unsigned long long* out, cudaStream_t st);
 // dst[idx[i]] = val[i]
 void scatter_int(const int* idx, const int* val, int n, int* dst, cudaStream_t st);
 

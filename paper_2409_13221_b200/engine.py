@@ -120,6 +120,24 @@ class Engine:
         out.update({k: a[:T] for k, a in zip(names, arrays)})
         return out
 
+    MODELS = {"actor": 0, "ref": 1, "critic": 2, "reward": 3}
+
+    def broadcast_model(self, model: str, src: int, rank: int, world: int, shm_name: str | None) -> float:
+        """Weight sync over NVLink (fp_engine_broadcast_model): every rank calls it; returns seconds."""
+        comm = _lib.Comm(rank, world, shm_name.encode() if shm_name else None)
+        t = C.c_double()
+        check(self.lib, self.lib.fp_engine_broadcast_model(self.h, self.MODELS[model], src, C.byref(comm),
+                                                           C.byref(t)))
+        return t.value
+
+    def reinit_model(self, model: str, seed: int) -> None:
+        check(self.lib, self.lib.fp_engine_reinit_model(self.h, self.MODELS[model], seed))
+
+    def model_checksum(self, model: str) -> int:
+        v = C.c_uint64()
+        check(self.lib, self.lib.fp_engine_model_checksum(self.h, self.MODELS[model], C.byref(v)))
+        return v.value
+
     def synthetic_prompts(self, n: int, token_seed: int) -> np.ndarray:
         out = np.zeros((n, self.setup.max_prompt), dtype=np.int32)
         check(self.lib, self.lib.fp_synthetic_prompts(self.h, n, token_seed,

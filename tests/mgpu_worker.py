@@ -60,6 +60,16 @@ def main():
                        "n_migrated": len(fused.plan.migrated), "trigger": fused.plan.trigger_time}
         res["moves_match"] = sorted((s, t) for s, _, t in out.moves) == sorted(ref_moves)
     dist.barrier()
+    # weight sync: rank 0 gets new actor weights, every rank pulls them
+    c0 = eng.model_checksum("actor")
+    if rank == 0:
+        eng.reinit_model("actor", 4321)
+    dist.barrier()
+    t_bc = eng.broadcast_model("actor", 0, rank, world, name[0] + "_bc")
+    sums = [None] * world
+    dist.all_gather_object(sums, (c0, eng.model_checksum("actor"), t_bc))
+    res["bcast"] = {"same": len({s[1] for s in sums}) == 1, "changed": all(s[1] != s[0] for s in sums),
+                    "seconds": max(s[2] for s in sums)}
     if rank == 0:
         # single-GPU stage-barrier run of the same batch on this device
         eng1 = Engine(w, device=local, max_samples=w.n_prompts, max_live=w.n_prompts)

@@ -105,3 +105,16 @@ def test_handoff_packs_balanced_minibatches(toy, dp):
         assert np.array_equal(h[k], getattr(x, k)[idx]), k
     assert np.array_equal(h["score"], x.score[h["order"]])
     assert h["bytes"] == 4 * (8 * len(idx) + len(batch)) and h["peer_bytes"] == 0
+
+
+def test_model_reinit_and_checksum(toy):
+    """Weight-sync helpers: a reseeded model has a different blob, reseeding back restores it
+    bit for bit (the checksum is an order-independent sum of 64-bit words)."""
+    w, eng, batch, _ = toy
+    c0 = eng.model_checksum("actor")
+    assert c0 == eng.model_checksum("actor")
+    eng.reinit_model("actor", 4321)
+    assert eng.model_checksum("actor") != c0
+    eng.reinit_model("actor", 1234)  # the engine's default weight seed
+    assert eng.model_checksum("actor") == c0
+    assert eng.broadcast_model("actor", 0, 0, 1, None) == 0.0  # world 1: nothing to do

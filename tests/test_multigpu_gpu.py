@@ -41,6 +41,7 @@ def test_fused_migration_matches_single_gpu(tmp_path, world, mode, mech):
     assert res["plan"]["mechanism"] == ("kv_transfer" if mech == "kv" else "recompute_prefill")
     assert res["moves_match"], res
     assert res["handoff_ok"] and res["handoff_peer_bytes"] > 0, res
+    assert res["bcast"]["same"] and res["bcast"]["changed"], res["bcast"]
     if mech == "kv":
         # KV pages are moved verbatim: bit-identical to the single-GPU run
         assert res["identical"], res["diffs_vs_1gpu"]
