@@ -1,6 +1,8 @@
 // fuseplan-b200 — Engine: weights, paged KV pool, prefill / decode / scoring.
 #include "engine.hpp"
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cmath>
@@ -73,6 +75,12 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
   FP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   FP_CUDA(cudaStreamCreateWithPriority(&s_decode_, cudaStreamNonBlocking, prio_hi));
   FP_CUDA(cudaStreamCreateWithPriority(&s_infer_, cudaStreamNonBlocking, prio_lo));
+  FP_CUDA(cudaEventCreateWithFlags(&infer_switch_, cudaEventDisableTiming));
+  {
+    const char* e = std::getenv("FUSEPLAN_SCORE_SMS");
+    const int sms = e ? std::atoi(e) : 0;  // off by default: measured no net gain on gpt2s
+    if (sms > 0) create_green_scoring(sms);
+  }
   FP_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
   ring_ = new PinnedRing();
   const Dims& a = cfg_.model[kActor];
@@ -137,6 +145,54 @@ void* Engine::open_ipc(const cudaIpcMemHandle_t& h) {
   return p;
 }
 
+// Green context (driver API, resolved through the runtime so the library does
+// not link libcuda): an SM partition of `sms` SMs (multiple of 8) with its own
+// low-priority stream. Kernels are launched into it with the runtime API and
+// use the primary context's memory. Silently absent if unsupported.
+void Engine::create_green_scoring(int sms) {
+  using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+  using Split = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned);
+  using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
+  using Create = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
+  using MkStream = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
+  auto sym = [](const char* name) -> void* {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return p;
+  };
+  auto get_res = reinterpret_cast<GetRes>(sym("cuDeviceGetDevResource"));
+  auto split = reinterpret_cast<Split>(sym("cuDevSmResourceSplitByCount"));
+  auto gen = reinterpret_cast<GenDesc>(sym("cuDevResourceGenerateDesc"));
+  auto create = reinterpret_cast<Create>(sym("cuGreenCtxCreate"));
+  auto mk = reinterpret_cast<MkStream>(sym("cuGreenCtxStreamCreate"));
+  if (!get_res || !split || !gen || !create || !mk) return;
+  CUdevResource all{}, part{}, rest{};
+  unsigned n = 1;
+  if (get_res(static_cast<CUdevice>(cfg_.device), &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return;
+  if (sms >= static_cast<int>(all.sm.smCount)) return;
+  if (split(&part, &n, &all, &rest, 0, static_cast<unsigned>(sms)) != CUDA_SUCCESS || n != 1) return;
+  CUdevResourceDesc desc;
+  if (gen(&desc, &part, 1) != CUDA_SUCCESS) return;
+  CUgreenCtx g;
+  if (create(&g, desc, static_cast<CUdevice>(cfg_.device), CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return;
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  CUstream st;
+  if (mk(&st, g, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS) return;
+  green_ctx_ = g;
+  s_infer_green_ = reinterpret_cast<cudaStream_t>(st);
+  score_sms_ = static_cast<int>(part.sm.smCount);
+}
+
+void Engine::set_infer_confined(bool on) {
+  if (!s_infer_green_ || on == infer_confined_) return;
+  FP_CUDA(cudaEventRecord(infer_switch_, infer_stream()));
+  infer_confined_ = on;
+  FP_CUDA(cudaStreamWaitEvent(infer_stream(), infer_switch_, 0));
+}
+
 Engine::~Engine() {
   cudaSetDevice(cfg_.device);
   cudaDeviceSynchronize();
@@ -153,12 +209,21 @@ Engine::~Engine() {
   delete ring_;
   cudaStreamDestroy(s_decode_);
   cudaStreamDestroy(s_infer_);
+  if (s_infer_green_) cudaStreamDestroy(s_infer_green_);
+  if (green_ctx_) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuGreenCtxDestroy", &p, cudaEnableDefault, &q) == cudaSuccess && p)
+      reinterpret_cast<CUresult (*)(CUgreenCtx)>(p)(static_cast<CUgreenCtx>(green_ctx_));
+  }
+  if (infer_switch_) cudaEventDestroy(infer_switch_);
   cudaStreamDestroy(s_copy_);
 }
 
 void Engine::synchronize() {
   FP_CUDA(cudaStreamSynchronize(s_decode_));
   FP_CUDA(cudaStreamSynchronize(s_infer_));
+  if (s_infer_green_) FP_CUDA(cudaStreamSynchronize(s_infer_green_));
   FP_CUDA(cudaStreamSynchronize(s_copy_));
 }
 
@@ -635,7 +700,7 @@ void Engine::decode_kernels(int B, int max_ctx, int mode, float inv_temp, uint64
 // ---------------------------------------------------------------------------
 
 void Engine::infer(const std::vector<InferItem>& items, float beta, float gamma, float lam) {
-  cudaStream_t st = s_infer_;
+  cudaStream_t st = infer_stream();
   PackedWs& ws = inf_;
   std::vector<int> sid, P, R, cu, roff, tiles;
   std::vector<int64_t> off_out;

@@ -93,7 +93,13 @@ class Engine {
   void reinit_model(int m, uint64_t seed);     // synthetic weights from another seed (same layout)
   uint64_t model_checksum(int m);             // sum of the blob's 64-bit words (synchronises)
   cudaStream_t decode_stream() const { return s_decode_; }
-  cudaStream_t infer_stream() const { return s_infer_; }
+  // The scoring stream in use: while generation runs, scoring may be confined
+  // to a green-context SM partition (FUSEPLAN_SCORE_SMS, default off) so that
+  // decode kernels never queue behind scoring CTAs on the other SMs; after
+  // generation it gets the whole GPU. Switching orders the two streams.
+  cudaStream_t infer_stream() const { return infer_confined_ && s_infer_green_ ? s_infer_green_ : s_infer_; }
+  void set_infer_confined(bool on);
+  int score_sms() const { return score_sms_; }
   cudaStream_t copy_stream() const { return s_copy_; }
 
   // ---- batch data (global sample ids) -------------------------------------------
@@ -258,6 +264,12 @@ class Engine {
   EngineConfig cfg_;
   ModelW models_[4];
   cudaStream_t s_decode_ = nullptr, s_infer_ = nullptr, s_copy_ = nullptr;
+  cudaStream_t s_infer_green_ = nullptr;  // scoring stream of a green context (SM partition), or null
+  void* green_ctx_ = nullptr;
+  int score_sms_ = 0;
+  bool infer_confined_ = false;
+  cudaEvent_t infer_switch_ = nullptr;
+  void create_green_scoring(int sms);
   // pool
   uint8_t* pool_ = nullptr;
   size_t page_bytes_ = 0, layer_bytes_ = 0;

@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -346,6 +347,7 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
   const long long launches0 = fpk::launch_count();
   if (!(opts.resident && E.prompts_tag() == ptag)) E.load_prompts(prompts.data(), n, ptag);
   if (opts.probe_attention) E.set_attn_probe(true);
+  E.set_infer_confined(false);
   cudaStream_t sd = E.decode_stream(), si = E.infer_stream();
   FP_CUDA(cudaStreamSynchronize(sd));
   region.barrier();
@@ -484,6 +486,15 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
         res.stats.infer_tokens += batch[sid].prompt_len + batch[sid].target_output_len;
       }
       res.stats.infer_samples += end - c;
+      // while this rank still generates a large batch, scoring stays in its SM
+      // partition; in the latency-bound tail (few rows) it may use every SM
+      static const int confine_min_live = [] {
+        const char* e = std::getenv("FUSEPLAN_CONFINE_MIN_LIVE");
+        return e ? std::atoi(e) : 0;
+      }();
+      E.set_infer_confined(!gen_done_me && opts.schedule == Schedule::kFused &&
+                           static_cast<int>(live.size()) >= confine_min_live);
+      si = E.infer_stream();
       // local finishes may still be in flight on the decode stream
       if (!step_end.empty()) FP_CUDA(cudaStreamWaitEvent(si, step_end.back(), 0));
       Batch bt;
