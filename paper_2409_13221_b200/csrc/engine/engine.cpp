@@ -4,6 +4,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -587,7 +588,14 @@ int Engine::bucket_of(int B) {
 void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed) {
   const int B = static_cast<int>(rows.size());
   if (B == 0) return;
-  const bool graph = use_graphs_ && !probe_on_;
+  // FUSEPLAN_TRACE_STEP=k: the engine's k-th decode step runs eagerly with
+  // globaltimer stamps in every GEMM / attention launch (tools/step_trace.py)
+  static const int trace_step = [] {
+    const char* e = std::getenv("FUSEPLAN_TRACE_STEP");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool tracing = ++decode_calls_ == trace_step;
+  const bool graph = use_graphs_ && !probe_on_ && !tracing;
   const int Bb = graph ? bucket_of(B) : B;
   if (Bb > dec_.cap) throw std::invalid_argument("engine: decode batch exceeds max_live");
   cudaStream_t st = s_decode_;
@@ -612,7 +620,38 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
   const int n_pairs = fpk::attn_decode_items(h.data() + 2 * Bb, Bb, A.KVH, A.hd, A.H / A.KVH, h.data() + 7 * Bb);
   upload(dec_.rows, h.data(), (static_cast<size_t>(7) * Bb + 1 + n_pairs) * 4, st);
   if (!graph) {
+    unsigned long long* arena = nullptr;
+    const size_t words = size_t(1) << 22;
+    if (tracing) {
+      FP_CUDA(cudaMalloc(&arena, words * 8));
+      FP_CUDA(cudaMemsetAsync(arena, 0, words * 8, st));
+      FP_CUDA(cudaStreamSynchronize(st));
+      fpk::trace_arm(arena, words);
+    }
     decode_kernels(Bb, max_ctx, mode, inv_temp, sample_seed, ctx_sum);
+    if (tracing) {
+      FP_CUDA(cudaStreamSynchronize(st));
+      const std::vector<fpk::TraceRec> recs = fpk::trace_disarm();
+      size_t used = 0;
+      for (const auto& r : recs) used = std::max(used, r.off + static_cast<size_t>(r.units) * (r.kind == 0 ? 8 : 4));
+      std::vector<unsigned long long> h(used);
+      FP_CUDA(cudaMemcpy(h.data(), arena, used * 8, cudaMemcpyDeviceToHost));
+      cudaFree(arena);
+      const char* path = std::getenv("FUSEPLAN_TRACE_OUT");
+      FILE* f = std::fopen(path ? path : "fp_step_trace.json", "w");
+      if (f) {
+        std::fprintf(f, "{\"B\": %d, \"max_ctx\": %d, \"ctx_sum\": %.0f, \"launches\": [", B, max_ctx, ctx_sum);
+        for (size_t i = 0; i < recs.size(); ++i) {
+          const int wpu = recs[i].kind == 0 ? 8 : 4;
+          std::fprintf(f, "%s{\"kind\": %d, \"units\": %d, \"data\": [", i ? ", " : "", recs[i].kind, recs[i].units);
+          for (int u = 0; u < recs[i].units * wpu; ++u)
+            std::fprintf(f, "%s%llu", u ? "," : "", h[recs[i].off + u]);
+          std::fprintf(f, "]}");
+        }
+        std::fprintf(f, "]}\n");
+        std::fclose(f);
+      }
+    }
     return;
   }
   const int ctx_cap = cfg_.max_prompt + cfg_.max_new;

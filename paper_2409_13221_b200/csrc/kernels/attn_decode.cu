@@ -29,7 +29,7 @@ namespace fpk {
 namespace {
 
 constexpr int kPT = 64;
-__device__ unsigned long long* g_attn_trace = nullptr;  // debug tracing (set_attn_trace)
+unsigned long long* g_attn_trace_host = nullptr;  // debug tracing (set_attn_trace)
 __device__ __forceinline__ unsigned long long gtime_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -133,8 +133,8 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
     const int* __restrict__ ctx, const int* __restrict__ items, int B, int H, int KVH, int nsplit_max,
     float scale_log2,
     float* __restrict__ part_o, float* __restrict__ part_ml, float* __restrict__ sub_o, float* __restrict__ sub_ml,
-    bf16* __restrict__ out, int* __restrict__ counters) {
-  const unsigned long long t_entry = g_attn_trace ? gtime_ns() : 0ull;
+    bf16* __restrict__ out, int* __restrict__ counters, unsigned long long* __restrict__ trace) {
+  const unsigned long long t_entry = trace ? gtime_ns() : 0ull;
   pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
   using C = DecCfg<HD, DEEP>;
   static_assert(G <= 8, "GQA group must fit the first 8 MMA rows");
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
   bool acc_has = false;
   bool fresh = true;
 
-  const unsigned long long t_begin = g_attn_trace ? gtime_ns() : 0ull;
+  const unsigned long long t_begin = trace ? gtime_ns() : 0ull;
   int c = 0;
   for (; cur.j < n_items; ++c) {
     const int k = c % C::kStages;
@@ -482,8 +482,8 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
       fresh = true;
     }
   }
-  if (g_attn_trace && lane == 0) {  // debug: per-warp busy interval and units (tools/attn_roofline.py --trace)
-    unsigned long long* t = g_attn_trace + 4ull * (blockIdx.x * C::kWarps + warp);
+  if (trace && lane == 0) {  // debug: per-warp busy interval and units (tools/attn_roofline.py --trace)
+    unsigned long long* t = trace + 4ull * (blockIdx.x * C::kWarps + warp);
     t[0] = t_entry;
     t[1] = t_begin;
     t[2] = gtime_ns();
@@ -518,7 +518,8 @@ void launch_cfg(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, co
   const int grid = std::max(1, std::min(148, (max_items + C::kWarps - 1) / C::kWarps));
   launch_pdl(attn_decode_mma_kernel<HD, G, DEEP>, dim3(grid), dim3(C::kWarps * 32), C::kSmem, st, map, q,
              pool.block_table, pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, items, B, H, KVH, nsplit,
-             scale, part_o, part_ml, sub_o, sub_ml, out, counters);
+             scale, part_o, part_ml, sub_o, sub_ml, out, counters,
+             g_attn_trace_host ? g_attn_trace_host : trace_slot(1, grid * C::kWarps, 4));
   count_launch();
 }
 
@@ -554,9 +555,11 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
     const __grid_constant__ CUtensorMap kv_map, const bf16* __restrict__ q, const int* __restrict__ block_table,
     int bt_stride, int rows_per_page, int layer_rows, int layer, const int* __restrict__ slot,
     const int* __restrict__ ctx, const int* __restrict__ items, int H, int KVH, int nsplit_max, float scale_log2,
-    float* __restrict__ part_o, float* __restrict__ part_ml, bf16* __restrict__ out, int* __restrict__ counters) {
+    float* __restrict__ part_o, float* __restrict__ part_ml, bf16* __restrict__ out, int* __restrict__ counters,
+    unsigned long long* __restrict__ trace) {
   constexpr int HD = 64;
   using C = TeamCfg;
+  const unsigned long long t_entry = trace ? gtime_ns() : 0ull;
   pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -833,6 +836,11 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
       }
     }
   }
+  if (trace && tw == 0 && lane == 0) {  // per CTA: entry, -, last team's end
+    unsigned long long* t = trace + 4ull * blockIdx.x;
+    if (team == 0) t[0] = t[1] = t_entry;
+    atomicMax(t + 2, gtime_ns());
+  }
   // the last team out resets the work counter for the next launch
   if (tw == 0 && lane == 0 && atomicAdd(&counters[1], 1) == n_teams - 1) {
     counters[0] = 0;
@@ -858,7 +866,7 @@ void launch_team(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, c
   const int grid = std::max(1, std::min(148, (max_items + C::kTeams - 1) / C::kTeams));
   launch_pdl(attn_decode_team_kernel, dim3(grid), dim3(C::kWarps * 32), C::kSmem, st, map, q, pool.block_table,
              pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, items, H, KVH, nsplit, scale, part_o,
-             part_ml, out, counters);
+             part_ml, out, counters, trace_slot(2, grid, 4));
   count_launch();
 }
 
@@ -883,7 +891,7 @@ void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const 
 
 }  // namespace
 
-void set_attn_trace(unsigned long long* buf) { cudaMemcpyToSymbol(g_attn_trace, &buf, sizeof(buf)); }
+void set_attn_trace(unsigned long long* buf) { g_attn_trace_host = buf; }
 
 // The team kernel (hd 64, G 1) while the (sample, kv head) pairs cannot fill
 // the warp-per-item grid four times over, else deep below that for other

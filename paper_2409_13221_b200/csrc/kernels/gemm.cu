@@ -117,6 +117,11 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
   g.kb_per_split = (g.k_blocks + splits - 1) / splits;
   g.weight_is_a = weight_is_a ? 1 : 0;
   g.trace = g_trace;
+  if (!g.trace) {
+    const long long ctas = static_cast<long long>((a_rows + 127) / 128) * ((b_rows + BN - 1) / BN) *
+                           ((g.k_blocks + g.kb_per_split - 1) / g.kb_per_split);
+    g.trace = trace_slot(0, static_cast<int>(ctas), 8);
+  }
   const int z = (g.k_blocks + g.kb_per_split - 1) / g.kb_per_split;
   if (cluster_split && (BN > 64 || z > 8)) throw std::invalid_argument("gemm: cluster split needs BN <= 64, z <= 8");
   g.cz = cluster_split ? z : 1;
@@ -202,6 +207,22 @@ void dispatch_bn_small(int M, int a_ctas, F&& f) {
   }
 }
 
+// Decode GEMMs in a lean ring (<= ~110 KB of shared memory) so that the CTAs
+// of the next GEMM in the step fit on an SM beside the current one's: with
+// PDL they become resident early and stream their weights while the previous
+// kernels run; for M <= FUSEPLAN_DECODE_LEAN (default 128, 0 disables).
+template <int BN>
+struct Lean {
+  static constexpr int v = BN <= 16 ? 6 : BN <= 32 ? 5 : BN <= 64 ? 4 : BN <= 128 ? 3 : 2;
+};
+bool lean(int M) {  // (large batches keep the deep ring: their mainloops are bandwidth-hungry)
+  static const int max_m = [] {
+    const char* e = std::getenv("FUSEPLAN_DECODE_LEAN");
+    return e ? std::atoi(e) : 128;
+  }();
+  return M <= max_m;
+}
+
 // Large GEMMs (several waves of CTAs) take the 2-stage / 2-CTAs-per-SM shape.
 bool many_waves(int M, int N, int BN) {
   static const int on = [] {
@@ -239,6 +260,34 @@ CUtensorMap make_kv_map(const void* pool, long long rows, int hd) {
 
 void set_gemm_trace(unsigned long long* buf) { g_trace = buf; }
 
+namespace {
+unsigned long long* g_arena = nullptr;
+size_t g_arena_words = 0, g_arena_used = 0;
+std::vector<TraceRec> g_recs;
+}  // namespace
+
+void trace_arm(unsigned long long* arena, size_t words) {
+  g_arena = arena;
+  g_arena_words = words;
+  g_arena_used = 0;
+  g_recs.clear();
+}
+
+unsigned long long* trace_slot(int kind, int units, int words_per_unit) {
+  if (!g_arena) return nullptr;
+  const size_t w = static_cast<size_t>(units) * words_per_unit;
+  if (g_arena_used + w > g_arena_words) return nullptr;
+  g_recs.push_back({kind, units, g_arena_used});
+  unsigned long long* p = g_arena + g_arena_used;
+  g_arena_used += w;
+  return p;
+}
+
+std::vector<TraceRec> trace_disarm() {
+  g_arena = nullptr;
+  return std::move(g_recs);
+}
+
 int gemm_splits(int N, int K) {
   const int kb = K / kBK;
   const int tiles = (N + 127) / 128;
@@ -272,7 +321,10 @@ void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* o
     const uint64_t str[2] = {static_cast<uint64_t>(N) * 4, static_cast<uint64_t>(M) * N * 4};
     const uint32_t box[3] = {128u, static_cast<uint32_t>(BN), 1u};
     EpiStoreF32 e{encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE), 0};
-    launch<BN>(W, N, X, M, K, splits, e, st);
+    if (BN <= 128 && lean(M))  // (the fp32 staging tile of BN 256 needs the deep ring)
+      launch<BN, EpiStoreF32, Lean<BN>::v>(W, N, X, M, K, splits, e, st);
+    else
+      launch<BN>(W, N, X, M, K, splits, e, st);
   });
 }
 
@@ -292,7 +344,10 @@ void gemm_swiglu_decode(const bf16* Wgu, int F, int K, const bf16* X, int M, bf1
   const int z = cluster_splits(2 * F, K);
   auto go = [&]<int BN>() {
     EpiSwiGLU<BN> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, BN)};
-    launch<BN>(Wgu, 2 * F, X, M, K, z, e, st, true, z > 1);
+    if (z == 1 && lean(M))
+      launch<BN, EpiSwiGLU<BN>, Lean<BN>::v>(Wgu, 2 * F, X, M, K, z, e, st);
+    else
+      launch<BN>(Wgu, 2 * F, X, M, K, z, e, st, true, z > 1);
   };
   if (z > 1)
     dispatch_bn_small(M, (2 * F + 127) / 128 * z, go);
@@ -320,7 +375,10 @@ void gemm_qkv_rope(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH
   auto go = [&]<int BN>() {
     EpiRopeKV<BN> e{q_out, pool, slot, pos, cs, layer, H, KVH, hd, M};
     e.pool.kv_map = nullptr;  // host pointer: not dereferenced on the device
-    launch<BN>(Wqkv, N, X, M, K, z, e, st, true, z > 1);
+    if (z == 1 && lean(M))
+      launch<BN, EpiRopeKV<BN>, Lean<BN>::v>(Wqkv, N, X, M, K, z, e, st);
+    else
+      launch<BN>(Wqkv, N, X, M, K, z, e, st, true, z > 1);
   };
   if (z > 1)
     dispatch_bn_small(M, (N + 127) / 128 * z, go);

@@ -8,6 +8,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <vector>
+
 namespace fpk {
 
 using bf16 = __nv_bfloat16;
@@ -162,6 +164,19 @@ bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolV
 // Debug: per-warp (entry ns, loop-begin ns, end ns, units) of subsequent
 // warp-per-item decode-attention launches into buf (4 x 148 x warps); nullptr disables.
 void set_attn_trace(unsigned long long* buf);
+// Step timeline tracing (tools/step_trace.py): while armed, every GEMM and
+// decode-attention launch gets its own slice of the arena for globaltimer
+// stamps (GEMM: 8 words per CTA; attention: 4 words per warp or per team
+// CTA) and a host record. Eager launches only (the engine disables the step
+// graph for the traced step).
+struct TraceRec {
+  int kind;    // 0 GEMM, 1 warp-per-item attention, 2 team attention
+  int units;   // CTAs (GEMM, team) or warps (attention)
+  size_t off;  // word offset in the arena
+};
+void trace_arm(unsigned long long* arena, size_t words);
+unsigned long long* trace_slot(int kind, int units, int words_per_unit);  // nullptr when not armed
+std::vector<TraceRec> trace_disarm();
 inline int attn_decode_counters(int B, int KVH, int max_ctx) {
   const int ns = (max_ctx + kDecodeChunk - 1) / kDecodeChunk;
   return 2 + B * KVH + B * KVH * ns;  // work queue, split tickets, sub-chunk tickets

@@ -1,0 +1,62 @@
+"""In-step timeline of one decode step (globaltimer stamps from every GEMM CTA and
+decode-attention warp / team CTA; the other kernels show up as gaps).
+
+    python tools/step_trace.py run STEP [out.json]    # gpt2s bench batch, stage barrier, traces decode step STEP
+    python tools/step_trace.py show out.json
+"""
+import json
+import os
+import subprocess
+import sys
+
+KIND = {0: "gemm", 1: "attn", 2: "attn-team"}
+
+
+def run(step, out):
+    env = dict(os.environ, FUSEPLAN_TRACE_STEP=str(step), FUSEPLAN_TRACE_OUT=out)
+    code = ("import sys; sys.path.insert(0, '.');"
+            "from paper_2409_13221_b200.configs import WORKLOADS, batch_for, gen_config;"
+            "from paper_2409_13221_b200.engine import Engine;"
+            "w = WORKLOADS['gpt2s']; e = Engine(w); b = batch_for(w, e.sched);"
+            "e.execute(b, gen_config(w, 1), 0, token_mode='sample', schedule='stage_barrier', resident=True)")
+    subprocess.run([sys.executable, "-c", code], env=env, check=True)
+    show(out)
+
+
+def show(path):
+    d = json.load(open(path))
+    rows = []
+    for i, L in enumerate(d["launches"]):
+        x = L["data"]
+        if L["kind"] == 0:  # 8 words per CTA: entry, setup, first_full, last_full, acc, epi_done
+            cta = [x[k:k + 8] for k in range(0, len(x), 8)]
+            cta = [c for c in cta if c[0] > 0]
+            beg, end = min(c[0] for c in cta), max(max(c[5], c[4], c[0]) for c in cta)
+            first = sorted(c[2] - c[0] for c in cta if c[2])
+            extra = f"ctas {len(cta):4d}, first-data median {first[len(first) // 2] / 1e3:5.2f} us" if first else ""
+        else:  # 4 words per warp / CTA: entry, loop-begin, end, units
+            w = [x[k:k + 4] for k in range(0, len(x), 4)]
+            w = [v for v in w if v[0] > 0]
+            beg, end = min(v[0] for v in w), max(v[2] for v in w)
+            extra = f"units {len(w):5d} (warps/CTAs)"
+        rows.append((beg, end, KIND[L["kind"]], extra))
+    t0 = rows[0][0]
+    print(f"decode step: B={d['B']} max_ctx={d['max_ctx']} ctx_sum={d['ctx_sum']:.0f}")
+    prev = None
+    busy = {}
+    for beg, end, kind, extra in rows:
+        gap = (beg - prev) / 1e3 if prev is not None else 0.0
+        print(f"  {kind:9s} start {(beg - t0) / 1e3:8.2f} us  dur {(end - beg) / 1e3:7.2f} us  gap-before "
+              f"{gap:6.2f} us  {extra}")
+        busy[kind] = busy.get(kind, 0.0) + (end - beg) / 1e3
+        prev = end
+    total = (rows[-1][1] - t0) / 1e3
+    print(f"  span {total:.1f} us; busy " + ", ".join(f"{k} {v:.1f} us" for k, v in busy.items()) +
+          f"; gaps (other kernels + launch) {total - sum(busy.values()):.1f} us")
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "run":
+        run(int(sys.argv[2]), sys.argv[3] if len(sys.argv) > 3 else "gpurun_out/step_trace.json")
+    else:
+        show(sys.argv[2])
