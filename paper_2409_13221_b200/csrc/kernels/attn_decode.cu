@@ -534,31 +534,36 @@ void launch_cfg(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, co
 // 4 units per item instead of 16, so long items no longer serialise on one
 // warp and the dynamic queue balances at a 4x finer grain. The sub-chunk fold
 // is part of the numerics for every batch size (batch-independent results).
+template <int T>  // warps per team (4: one sub-chunk each; 2: two contiguous sub-chunks each)
 struct TeamCfg {
-  static constexpr int kTeamWarps = 4;
-  static constexpr int kTeams = 3;
+  static constexpr int kTeamWarps = T;
+  static constexpr int kTeams = 12 / T;
   static constexpr int kWarps = kTeams * kTeamWarps;
   static constexpr int kStages = 2;
   static constexpr int kSubUnits = fpk::kSubUnits;                      // units per sub-chunk
   static constexpr int kSubs = kDecodeChunk / (32 * kSubUnits);         // sub-chunks per item
   static constexpr int kKV = 2 * 32 * 128;                              // K + V of one unit (hd 64)
-  static constexpr int kStageBytes = kKV + 1024;                        // + q slot
-  static constexpr int kSmem = kWarps * kStages * kStageBytes + 1024;
+  static constexpr int kStageBytes = kKV;                               // (q slots live after the stages)
+  static constexpr int kQOff = kWarps * kStages * kStageBytes;         // q slot (warp, stage): 128 B each
+  static constexpr int kSmem = kQOff + kWarps * kStages * 128 + 1024;
 };
-static_assert(TeamCfg::kSubs == TeamCfg::kTeamWarps, "one sub-chunk per team warp");
+static_assert(TeamCfg<4>::kSubs % 4 == 0, "sub-chunks split evenly over team warps");
 
+template <int T>
 __device__ __forceinline__ void team_bar(int team) {
-  asm volatile("bar.sync %0, 128;" ::"r"(1 + team) : "memory");
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(32 * T) : "memory");
 }
 
-__global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kernel(
+template <int T>
+__global__ void __launch_bounds__(TeamCfg<T>::kWarps * 32, 1) attn_decode_team_kernel(
     const __grid_constant__ CUtensorMap kv_map, const bf16* __restrict__ q, const int* __restrict__ block_table,
     int bt_stride, int rows_per_page, int layer_rows, int layer, const int* __restrict__ slot,
     const int* __restrict__ ctx, const int* __restrict__ items, int H, int KVH, int nsplit_max, float scale_log2,
     float* __restrict__ part_o, float* __restrict__ part_ml, bf16* __restrict__ out, int* __restrict__ counters,
     unsigned long long* __restrict__ trace) {
   constexpr int HD = 64;
-  using C = TeamCfg;
+  using C = TeamCfg<T>;
+  constexpr int kSubsPerWarp = C::kSubs / T;
   const unsigned long long t_entry = trace ? gtime_ns() : 0ull;
   pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
@@ -572,6 +577,7 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
   const int team = warp / C::kTeamWarps, tw = warp % C::kTeamWarps;
   uint64_t* bar = full_bar[warp];
   uint8_t* my_smem = smem + warp * C::kStages * C::kStageBytes;
+  auto qslot = [&](int stage) { return smem + C::kQOff + (warp * C::kStages + stage) * 128; };
   int4(*ring)[2] = ring_s[team];
   if (lane == 0) {
     if (warp == 0) tma_prefetch_desc(&kv_map);
@@ -602,17 +608,17 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
     const int4 x = ring[idx & 3][0], y = ring[idx & 3][1];
     return DecItem{x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w, 7};
   };
-  // this warp's units of an item: sub-chunk tw
+  // this warp's units of an item: its contiguous sub-chunks
   auto my_units = [&](const DecItem& it, int& ua, int& ub) {
-    ua = (it.t0 >> 5) + tw * C::kSubUnits;
-    ub = min(((it.t1 - 1) >> 5) + 1, ua + C::kSubUnits);
+    ua = (it.t0 >> 5) + tw * kSubsPerWarp * C::kSubUnits;
+    ub = min(((it.t1 - 1) >> 5) + 1, ua + kSubsPerWarp * C::kSubUnits);
     if (it.j >= n_items || ub < ua) ub = ua;
   };
 
   // item 0 of each team is static (its index), so it is decoded before
   // griddepcontrol.wait; item 1 comes from the counter after it
   if (tw == 0 && lane == 0) put(0, static_cast<int>(blockIdx.x) * C::kTeams + team);
-  team_bar(team);
+  team_bar<T>(team);
   int known = 0;  // highest item index whose info is in the ring
 
   // issue cursor over (item index, unit) of this warp's sub-chunks
@@ -623,7 +629,7 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
     my_units(in_it, in_ua, in_ue);
     in_u = in_ua;
     const int p0 = in_ua >> 1;
-    in_pg = (in_ue > in_ua && lane < 2) ? block_table[slot[in_it.b] * bt_stride + p0 + lane] : 0;
+    in_pg = (in_ue > in_ua && lane < 2 * kSubsPerWarp) ? block_table[slot[in_it.b] * bt_stride + p0 + lane] : 0;
   };
   if (in_ok) load_item();
   auto advance_item = [&]() {  // move past empty / finished items while their infos are known
@@ -648,7 +654,7 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
       tma_load_2d(dst, &kv_map, &bar[k], 0, rk);
       tma_load_2d(dst + 32 * 128, &kv_map, &bar[k], 0, rk + kPT);
       if (first && with_q)
-        bulk_load(dst + C::kKV, q + (static_cast<size_t>(in_it.b) * H + in_it.kvh) * HD, HD * 2, &bar[k]);
+        bulk_load(qslot(k), q + (static_cast<size_t>(in_it.b) * H + in_it.kvh) * HD, HD * 2, &bar[k]);
     }
     ++n_iss;
     ++in_u;
@@ -672,9 +678,9 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
   }
   pdl_wait();  // q, the new K/V and the counters come from earlier kernels
   if (q_late && lane == 0)  // stage 0 (the sub-chunk's first unit) already expects the q bytes
-    bulk_load(my_smem + C::kKV, q + (static_cast<size_t>(in_it.b) * H + in_it.kvh) * HD, HD * 2, &bar[0]);
+    bulk_load(qslot(0), q + (static_cast<size_t>(in_it.b) * H + in_it.kvh) * HD, HD * 2, &bar[0]);
   if (tw == 0 && lane == 0) put(1, n_teams + atomicAdd(&counters[0], 1));
-  team_bar(team);
+  team_bar<T>(team);
   known = 1;
   pump();
 
@@ -695,7 +701,7 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
       const int k = n_con % C::kStages;
       mbar_wait(&bar[k], (n_con / C::kStages) & 1);
       if (u == ua) {
-        const bf16* qs = reinterpret_cast<const bf16*>(my_smem + k * C::kStageBytes + C::kKV);
+        const bf16* qs = reinterpret_cast<const bf16*>(qslot(k));
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const int col = kk * 16 + 2 * (lane & 3);
@@ -777,22 +783,30 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
       __syncwarp();
       ++n_con;
       pump();
-    }
-    // park this warp's sub-partial (row 0 lives in lanes 0..3)
-    const int sl = i & 1;
-    if (lane < 4) {
+      // end of a sub-chunk: park its partial (row 0 lives in lanes 0..3), restart the softmax
+      const int rel = u + 1 - (it.t0 >> 5);
+      if (rel % C::kSubUnits == 0 || u + 1 == ub) {
+        const int sx = (rel - 1) / C::kSubUnits;
+        if (lane < 4) {
 #pragma unroll
-      for (int dn = 0; dn < HD / 8; ++dn) {
-        sub_o[team][sl][tw][dn * 8 + 2 * lane] = o[dn][0];
-        sub_o[team][sl][tw][dn * 8 + 2 * lane + 1] = o[dn][1];
-      }
-      if (lane == 0) {
-        sub_ml[team][sl][tw][0] = m_run;
-        sub_ml[team][sl][tw][1] = l_run;
+          for (int dn = 0; dn < HD / 8; ++dn) {
+            sub_o[team][i & 1][sx][dn * 8 + 2 * lane] = o[dn][0];
+            sub_o[team][i & 1][sx][dn * 8 + 2 * lane + 1] = o[dn][1];
+          }
+          if (lane == 0) {
+            sub_ml[team][i & 1][sx][0] = m_run;
+            sub_ml[team][i & 1][sx][1] = l_run;
+          }
+        }
+        m_run = -INFINITY;
+        l_run = 0.f;
+#pragma unroll
+        for (int d = 0; d < HD / 8; ++d) o[d][0] = o[d][1] = o[d][2] = o[d][3] = 0.f;
       }
     }
+    const int sl = i & 1;
     if (tw == 0 && lane == 0) put(i + 2, n_teams + atomicAdd(&counters[0], 1));
-    team_bar(team);
+    team_bar<T>(team);
     known = i + 2;
     pump();
     if (tw != 0) continue;
@@ -848,13 +862,14 @@ __global__ void __launch_bounds__(TeamCfg::kWarps * 32, 1) attn_decode_team_kern
   }
 }
 
+template <int T>
 void launch_team(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
                  const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out, int* counters,
                  cudaStream_t st) {
-  using C = TeamCfg;
+  using C = TeamCfg<T>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(attn_decode_team_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(attn_decode_team_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr = true;
   }
   float* part_o = work;
@@ -864,7 +879,7 @@ void launch_team(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, c
   const float scale = kLog2e / sqrtf(64.f);
   const int max_items = nsplit * B * KVH;
   const int grid = std::max(1, std::min(148, (max_items + C::kTeams - 1) / C::kTeams));
-  launch_pdl(attn_decode_team_kernel, dim3(grid), dim3(C::kWarps * 32), C::kSmem, st, map, q, pool.block_table,
+  launch_pdl(attn_decode_team_kernel<T>, dim3(grid), dim3(C::kWarps * 32), C::kSmem, st, map, q, pool.block_table,
              pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, items, H, KVH, nsplit, scale, part_o,
              part_ml, out, counters, trace_slot(2, grid, 4));
   count_launch();
@@ -880,7 +895,8 @@ void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const 
             const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out, int* counters,
             cudaStream_t st) {
   switch (attn_decode_variant(B, KVH, HD, G, nullptr)) {
-    case 2: launch_team(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st); break;
+    case 2: launch_team<4>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st); break;
+    case 3: launch_team<2>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st); break;
     case 1:
       launch_cfg<HD, G, true>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);
       break;
@@ -902,12 +918,14 @@ int attn_decode_variant(int B, int KVH, int hd, int G, int* warps) {
   static const int deep_mode = env_int("FUSEPLAN_ATTN_DEEP", -1);
   const int wide_warps = hd == 64 ? DecCfg<64, false>::kWarps : DecCfg<128, false>::kWarps;
   const bool small = B * KVH * 4 <= 148 * wide_warps;
+  static const int team2_max_b = env_int("FUSEPLAN_ATTN_TEAM2_MAX_B", 0);
   int v = 0;
-  if (hd == 64 && G == 1 && team_mode && (team_mode == 2 || small)) v = 2;
+  if (hd == 64 && G == 1 && team_mode == 3) v = 3;
+  else if (hd == 64 && G == 1 && team_mode && (team_mode == 2 || small)) v = 2;
+  else if (hd == 64 && G == 1 && team_mode && B <= team2_max_b) v = 3;
   else if (deep_mode >= 0 ? deep_mode == 1 : small) v = 1;
-  if (warps) *warps = v == 2 ? TeamCfg::kWarps : v == 1 ? (hd == 64 ? DecCfg<64, true>::kWarps
-                                                                     : DecCfg<128, true>::kWarps)
-                                                        : wide_warps;
+  if (warps) *warps = v >= 2 ? 12 : v == 1 ? (hd == 64 ? DecCfg<64, true>::kWarps : DecCfg<128, true>::kWarps)
+                                            : wide_warps;
   return v;
 }
 
