@@ -118,3 +118,51 @@ def test_model_reinit_and_checksum(toy):
     eng.reinit_model("actor", 1234)  # the engine's default weight seed
     assert eng.model_checksum("actor") == c0
     assert eng.broadcast_model("actor", 0, 0, 1, None) == 0.0  # world 1: nothing to do
+
+
+@pytest.fixture(scope="module")
+def small64():
+    """hd 64 model (the tcgen05 QKV+RoPE+KV-append epilogue and the tensor-core decode
+    attention variants run end to end; the toy config's hd 32 takes the CUDA-core path)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from model_oracle import Oracle
+    from paper_2409_13221_b200.configs import Dims, Workload, batch_for
+    from paper_2409_13221_b200.engine import Engine
+    d = Dims(2, 256, 4, 4, 64, 512, 2048)
+    w = Workload("small64", d, d, d, d, 160, 24, 600, zipf_s=0.5)
+    eng = Engine(w, device=0)
+    batch = batch_for(w, eng.sched)
+    yield w, eng, batch, Oracle(w)
+    eng.close()
+
+
+def test_hd64_forced_experience_matches_oracle(small64):
+    from paper_2409_13221_b200.configs import gen_config
+    from model_oracle import forced_response
+    w, eng, batch, orc = small64
+    out = eng.execute(batch, gen_config(w, 1), 0, token_mode="forced", schedule="fused", claim_tokens=4096)
+    prompts = eng.synthetic_prompts(w.n_prompts, 7)
+    # the longest samples cross the 512-token split (multi-split merge) and batch sizes span
+    # the team (small) and wide (large) attention kernels as samples retire
+    longest = sorted(range(len(batch)), key=lambda i: -batch[i].target_output_len)[:3]
+    for i in sorted(set(longest + list(range(0, len(batch), 23)))):
+        s = batch[i]
+        got = out.experience.sample(i)
+        want_tokens = forced_response(i, s.target_output_len, w.max_new, w.actor.vocab, 7)
+        assert np.array_equal(got["tokens"], want_tokens)
+        ref = orc.experience(prompts[i, :s.prompt_len], want_tokens, 0.05, 1.0, 0.95)
+        for k, (mx, mean) in _cmp(got, ref).items():
+            scale = max(1.0, float(np.max(np.abs(ref[k]))))
+            assert mx <= TOL_MAX * scale and mean <= TOL_MEAN * scale, (i, k, mx, mean)
+
+
+def test_hd64_schedules_identical(small64):
+    """Serial vs fused on the hd-64 model: bit-identical experience (batch-independent kernels)."""
+    from paper_2409_13221_b200.configs import gen_config
+    w, eng, batch, _ = small64
+    a = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="fused", claim_tokens=4096)
+    b = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="stage_barrier")
+    for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret", "score"):
+        assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
