@@ -43,6 +43,11 @@ struct GemmCfg {
 };
 
 template <class E, class = void>
+struct EpiHasPrologue : std::false_type {};
+template <class E>
+struct EpiHasPrologue<E, std::void_t<decltype(&E::prologue)>> : std::true_type {};
+
+template <class E, class = void>
 struct EpiStages {
   static constexpr int value = 0;
 };
@@ -210,8 +215,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int kPStride = (BN < 32 ? 32 : BN) + 4;  // padded fp32 row of the parked partial (32-column chunks)
   constexpr int kPOff = 64 * 1024;                // parked partial: after any epilogue staging
   constexpr bool kClusterOK = BN <= 64 && kPOff + 128 * kPStride * 4 <= C::kStages * C::kStageBytes;
+  typename Epi::State st{};
   auto run_epi = [&](auto&& load) {
-    typename Epi::State st{};
 #pragma unroll 1
     for (int pass = 0; pass < Epi::kPasses; ++pass) {  // two-pass epilogues re-read TMEM (cheap)
       if (pass) epi.next_pass(st, a_row0, b_row0, r, half);
@@ -242,6 +247,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   };
   if (warp >= 2) {
     pdl_wait();
+    // epilogue inputs that do not depend on the accumulator (e.g. positions,
+    // pages, rope tables) are fetched while the mainloop runs
+    if constexpr (EpiHasPrologue<Epi>::value) epi.prologue(st, a_row0, b_row0);
     if (nkb > 0) {
       mbar_wait(&acc_bar, 0);
       if (tr && threadIdx.x == 64) tr[4] = gtime();
@@ -399,7 +407,18 @@ struct EpiRopeKV {
   template <class S> __device__ void next_pass(S&, int, int, int, int) const {}
   struct State {
     uint8_t* smem;
+    int pj, pagej;  // lane j: position and pool page of this warp's j-th column (prologue)
   };
+  __device__ void prologue(State& st, int, int b0) const {
+    const int ew = (threadIdx.x >> 5) - 2, lane = threadIdx.x & 31;
+    const int nb = min(BN, M - b0);
+    const int bl = ew + 8 * lane;
+    st.pj = st.pagej = 0;
+    if (bl < nb) {
+      st.pj = pos[b0 + bl];
+      st.pagej = pool.block_table[slot[b0 + bl] * pool.bt_stride + st.pj / pool.page_tokens];
+    }
+  }
   __device__ void operator()(State& st, uint8_t* smem, int, int, int, int r, int, int c0,
                              const float (&v)[32]) const {
     st.smem = smem;
@@ -415,45 +434,57 @@ struct EpiRopeKV {
     const int hh = hd >> 1;
     const int nb = min(BN, M - b0);
     __nv_bfloat16* pool_base = reinterpret_cast<__nv_bfloat16*>(pool.base);
-    // lane j fetches position and page of the warp's j-th column once
-    int pj = 0, pagej = 0;
-    {
-      const int bl = ew + 8 * lane;
-      if (bl < nb) {
-        pj = pos[b0 + bl];
-        pagej = pool.block_table[slot[b0 + bl] * pool.bt_stride + pj / pool.page_tokens];
-      }
-    }
+    const int pj = st.pj, pagej = st.pagej;
     const int ncol = (nb - ew + 7) >> 3;  // columns of this warp
-    for (int k = 0; k < ncol; ++k) {
-      const int bl = ew + 8 * k;
-      const int b = b0 + bl;
-      const int p = __shfl_sync(0xffffffffu, pj, k);
-      const int page = __shfl_sync(0xffffffffu, pagej, k);
+    // per pair slot k2 (lane, lane + 32) the head / feature are column-independent
+    int fl2[2], i2[2], head2[2];
 #pragma unroll
-      for (int k2 = 0; k2 < 2; ++k2) {  // 64 pairs per column: lane, lane + 32
-        const int pr = lane + 32 * k2;
-        const int i = pr % hh;
-        const int fl = (pr / hh) * hd + i;  // tile-local feature of the pair's low element
-        const int head = (a0 + fl) / hd;    // [0, H) q, [H, H + KVH) k, then v
-        __nv_bfloat16 o1 = tile[bl * 128 + fl], o2 = tile[bl * 128 + fl + hh];
-        if (head < H + KVH) {
-          const float2 c = cs[p * hh + i];
-          float r1, r2;
-          rope_pair(__bfloat162float(o1), __bfloat162float(o2), c.x, c.y, r1, r2);
-          o1 = f2bf(r1);
-          o2 = f2bf(r2);
+    for (int k2 = 0; k2 < 2; ++k2) {
+      const int pr = lane + 32 * k2;
+      i2[k2] = pr % hh;
+      fl2[k2] = (pr / hh) * hd + i2[k2];  // tile-local feature of the pair's low element
+      head2[k2] = (a0 + fl2[k2]) / hd;    // [0, H) q, [H, H + KVH) k, then v
+    }
+    // four columns at a time: their (cos, sin) loads are issued together
+    for (int k0 = 0; k0 < ncol; k0 += 4) {
+      float2 c[4][2];
+      int pk[4], pgk[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int k = min(k0 + kk, ncol - 1);
+        pk[kk] = __shfl_sync(0xffffffffu, pj, k);
+        pgk[kk] = __shfl_sync(0xffffffffu, pagej, k);
+#pragma unroll
+        for (int k2 = 0; k2 < 2; ++k2)
+          c[kk][k2] = head2[k2] < H + KVH ? __ldg(cs + pk[kk] * hh + i2[k2]) : make_float2(1.f, 0.f);
+      }
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (k0 + kk >= ncol) break;
+        const int bl = ew + 8 * (k0 + kk);
+        const int b = b0 + bl;
+        const int p = pk[kk];
+#pragma unroll
+        for (int k2 = 0; k2 < 2; ++k2) {  // 64 pairs per column: lane, lane + 32
+          const int i = i2[k2], fl = fl2[k2], head = head2[k2];
+          __nv_bfloat16 o1 = tile[bl * 128 + fl], o2 = tile[bl * 128 + fl + hh];
+          if (head < H + KVH) {
+            float r1, r2;
+            rope_pair(__bfloat162float(o1), __bfloat162float(o2), c[kk][k2].x, c[kk][k2].y, r1, r2);
+            o1 = f2bf(r1);
+            o2 = f2bf(r2);
+          }
+          __nv_bfloat16* dst;
+          if (head < H) {
+            dst = q_out + (static_cast<size_t>(b) * H + head) * hd;
+          } else {
+            const bool is_v = head >= H + KVH;
+            const int kh = head - H - (is_v ? KVH : 0);
+            dst = pool_base + kv_elem_offset(pool, pgk[kk], layer, kh, hd, p % pool.page_tokens, is_v);
+          }
+          dst[i] = o1;
+          dst[i + hh] = o2;
         }
-        __nv_bfloat16* dst;
-        if (head < H) {
-          dst = q_out + (static_cast<size_t>(b) * H + head) * hd;
-        } else {
-          const bool is_v = head >= H + KVH;
-          const int kh = head - H - (is_v ? KVH : 0);
-          dst = pool_base + kv_elem_offset(pool, page, layer, kh, hd, p % pool.page_tokens, is_v);
-        }
-        dst[i] = o1;
-        dst[i + hh] = o2;
       }
     }
   }

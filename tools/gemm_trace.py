@@ -31,6 +31,16 @@ def case(kind, M, N, K):
         s = lib.fp_k_gemm_splits(N, K)
         out = torch.empty(s, M, N, device="cuda")
         f = lambda: lib.fp_k_gemm_f32(p(W), N, K, p(X), M, p(out), s, None)  # noqa: E731
+    elif kind == "qkvrope":  # decode QKV + RoPE + KV append (gpt2s heads)
+        H, KVH, hd, L, PT = 12, 12, 64, 12, 64
+        pos = torch.randint(0, 1000, (M,), device="cuda", dtype=torch.int32)
+        maxp = 18
+        pool = torch.zeros(M * maxp + 1, L, KVH, 2, PT, hd, device="cuda", dtype=torch.bfloat16)
+        bt = (torch.arange(M * maxp, device="cuda", dtype=torch.int32) + 1).view(M, maxp)
+        slot = torch.arange(M, device="cuda", dtype=torch.int32)
+        q = torch.empty(M, H, hd, device="cuda", dtype=torch.bfloat16)
+        f = lambda: lib.fp_k_qkv_rope(p(W), K, p(X), M, H, KVH, hd, p(pos), 1152, 10000.0, p(pool), L, 3, p(bt), maxp,  # noqa
+                                      p(slot), p(q), None)
     else:  # vocab sampling head: A = X rows, B = W (vocab)
         sid = torch.arange(M, device="cuda", dtype=torch.int32)
         stp = torch.zeros(M, device="cuda", dtype=torch.int32)
@@ -55,7 +65,9 @@ def case(kind, M, N, K):
           f"epi {np.median(per[:, 5] - per[:, 4]):.2f} total {np.median(per[:, 5]):.2f}", flush=True)
 
 
-cases = (("bf16", 8, 2304, 768), ("bf16", 128, 2304, 768), ("swiglu", 8, 6144, 768), ("swiglu", 128, 6144, 768),
+cases = (("qkvrope", 50, 2304, 768), ("qkvrope", 284, 2304, 768), ("bf16", 284, 2304, 768),
+         ("swiglu", 284, 6144, 768), ("f32", 284, 768, 768), ("f32", 284, 768, 3072),
+         ("bf16", 8, 2304, 768), ("bf16", 128, 2304, 768), ("swiglu", 8, 6144, 768), ("swiglu", 128, 6144, 768),
          ("f32", 8, 768, 768), ("f32", 128, 768, 768), ("f32", 8, 768, 3072), ("f32", 128, 768, 3072),
          ("vocab", 8, 50257, 768), ("vocab", 128, 50257, 768), ("vocab", 350, 50257, 768),
          ("bf16", 4096, 6144, 768), ("bf16", 16384, 2304, 768))

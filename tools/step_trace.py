@@ -43,16 +43,18 @@ def show(path):
     t0 = rows[0][0]
     print(f"decode step: B={d['B']} max_ctx={d['max_ctx']} ctx_sum={d['ctx_sum']:.0f}")
     prev = None
-    busy = {}
+    eff = {}
     for beg, end, kind, extra in rows:
-        gap = (beg - prev) / 1e3 if prev is not None else 0.0
-        print(f"  {kind:9s} start {(beg - t0) / 1e3:8.2f} us  dur {(end - beg) / 1e3:7.2f} us  gap-before "
-              f"{gap:6.2f} us  {extra}")
-        busy[kind] = busy.get(kind, 0.0) + (end - beg) / 1e3
+        # launches overlap under PDL (CTAs start early and wait): the effective
+        # time of a launch is from the previous traced launch's end to its own end
+        e = (end - max(beg, prev if prev is not None else beg)) / 1e3
+        print(f"  {kind:9s} start {(beg - t0) / 1e3:8.2f} us  end {(end - t0) / 1e3:8.2f} us  "
+              f"effective {e:6.2f} us  {extra}")
+        eff[kind] = eff.get(kind, 0.0) + e
         prev = end
     total = (rows[-1][1] - t0) / 1e3
-    print(f"  span {total:.1f} us; busy " + ", ".join(f"{k} {v:.1f} us" for k, v in busy.items()) +
-          f"; gaps (other kernels + launch) {total - sum(busy.values()):.1f} us")
+    print(f"  span {total:.1f} us; effective " + ", ".join(f"{k} {v:.1f} us" for k, v in eff.items()) +
+          " (gemm includes the untraced add_norm / embed / finalize kernels between launches)")
 
 
 if __name__ == "__main__":
