@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <numeric>
 
 #include "philox.cuh"
@@ -77,6 +78,9 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
   FP_CUDA(cudaStreamCreateWithPriority(&s_decode_, cudaStreamNonBlocking, prio_hi));
   FP_CUDA(cudaStreamCreateWithPriority(&s_infer_, cudaStreamNonBlocking, prio_lo));
   FP_CUDA(cudaEventCreateWithFlags(&infer_switch_, cudaEventDisableTiming));
+  FP_CUDA(cudaStreamCreateWithPriority(&s_decode2_, cudaStreamNonBlocking, prio_hi));
+  FP_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+  FP_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
   {
     const char* e = std::getenv("FUSEPLAN_SCORE_SMS");
     const int sms = e ? std::atoi(e) : 0;  // off by default: measured no net gain on gpt2s
@@ -218,6 +222,9 @@ Engine::~Engine() {
       reinterpret_cast<CUresult (*)(CUgreenCtx)>(p)(static_cast<CUgreenCtx>(green_ctx_));
   }
   if (infer_switch_) cudaEventDestroy(infer_switch_);
+  cudaEventDestroy(ev_fork_);
+  cudaEventDestroy(ev_join_);
+  cudaStreamDestroy(s_decode2_);
   cudaStreamDestroy(s_copy_);
 }
 
@@ -355,26 +362,30 @@ void Engine::alloc_ws() {
   packed(pre_, prefill_cap, false);
   packed(inf_, infer_cap, true);
 
-  const int B = bucket_of(cfg_.max_live);
-  dec_.cap = B;
-  dec_.x = static_cast<float*>(dalloc(static_cast<size_t>(B) * maxd * 4));
-  dec_.parts = static_cast<float*>(dalloc(static_cast<size_t>(16) * B * maxd * 4));
-  dec_.h = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxd * 2));
-  dec_.qkv = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxq * 2));
-  dec_.q = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxao * 2));
-  dec_.attn = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxao * 2));
-  dec_.act = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxF * 2));
-  const int items_cap = (cfg_.max_prompt + cfg_.max_new + 127) / 128;  // work items per row (attn_decode_items)
-  dec_.rows = static_cast<int*>(dalloc((static_cast<size_t>(7 + items_cap) * B + 1) * 4));
-  dec_.vocab_part = dalloc(static_cast<size_t>(B) * vt * 24);
-  dec_.tgt_z = static_cast<float*>(dalloc(B * 4));
-  const Dims& a = cfg_.model[kActor];
-  dec_.attn_work = static_cast<float*>(
-      dalloc(fpk::attn_decode_workspace(B, a.H, a.hd, cfg_.max_prompt + cfg_.max_new) * sizeof(float)));
-  const size_t cnt =
-      static_cast<size_t>(fpk::attn_decode_counters(B, a.KVH, cfg_.max_prompt + cfg_.max_new)) * sizeof(int);
-  dec_.attn_cnt = static_cast<int*>(dalloc(cnt));
-  FP_CUDA(cudaMemsetAsync(dec_.attn_cnt, 0, cnt, s_decode_));
+  const int Bcap = bucket_of(cfg_.max_live);
+  auto decode_ws = [&](DecodeWs& dw, int B) {
+    dw.cap = B;
+    dw.x = static_cast<float*>(dalloc(static_cast<size_t>(B) * maxd * 4));
+    dw.parts = static_cast<float*>(dalloc(static_cast<size_t>(16) * B * maxd * 4));
+    dw.h = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxd * 2));
+    dw.qkv = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxq * 2));
+    dw.q = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxao * 2));
+    dw.attn = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxao * 2));
+    dw.act = static_cast<bf16*>(dalloc(static_cast<size_t>(B) * maxF * 2));
+    const int items_cap = (cfg_.max_prompt + cfg_.max_new + 127) / 128;  // work items per row (attn_decode_items)
+    dw.rows = static_cast<int*>(dalloc((static_cast<size_t>(7 + items_cap) * B + 1) * 4));
+    dw.vocab_part = dalloc(static_cast<size_t>(B) * vt * 24);
+    dw.tgt_z = static_cast<float*>(dalloc(B * 4));
+    const Dims& a = cfg_.model[kActor];
+    dw.attn_work = static_cast<float*>(
+        dalloc(fpk::attn_decode_workspace(B, a.H, a.hd, cfg_.max_prompt + cfg_.max_new) * sizeof(float)));
+    const size_t cnt =
+        static_cast<size_t>(fpk::attn_decode_counters(B, a.KVH, cfg_.max_prompt + cfg_.max_new)) * sizeof(int);
+    dw.attn_cnt = static_cast<int*>(dalloc(cnt));
+    FP_CUDA(cudaMemsetAsync(dw.attn_cnt, 0, cnt, s_decode_));
+  };
+  decode_ws(dec_, Bcap);
+  decode_ws(dec2_, bucket_of((cfg_.max_live + 1) / 2));  // second half of a split step
 }
 
 // ---------------------------------------------------------------------------
@@ -585,24 +596,15 @@ int Engine::bucket_of(int B) {
 // step — ~10 kernels per layer with PDL edges — replays as one CUDA graph per
 // (bucket, mode, temperature, seed): host launch cost and inter-kernel gaps
 // vanish. The probe mode (per-launch CUDA events) runs the step eagerly.
-void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed) {
-  const int B = static_cast<int>(rows.size());
-  if (B == 0) return;
-  // FUSEPLAN_TRACE_STEP=k: the engine's k-th decode step runs eagerly with
-  // globaltimer stamps in every GEMM / attention launch (tools/step_trace.py)
-  static const int trace_step = [] {
-    const char* e = std::getenv("FUSEPLAN_TRACE_STEP");
-    return e ? std::atoi(e) : -1;
-  }();
-  const bool tracing = ++decode_calls_ == trace_step;
-  const bool graph = use_graphs_ && !probe_on_ && !tracing;
-  const int Bb = graph ? bucket_of(B) : B;
-  if (Bb > dec_.cap) throw std::invalid_argument("engine: decode batch exceeds max_live");
-  cudaStream_t st = s_decode_;
+// Host row table of one decode group, padded to Bb rows (padding rows decode a
+// dummy token into the scratch slot / page / history row): [7][Bb] columns +
+// the attention work-item table. Returns the ints to upload.
+size_t Engine::build_rows(const DecodeRow* rows, int B, int Bb, std::vector<int>& h, int& max_ctx,
+                          double& ctx_sum) {
   const int items_cap = (cfg_.max_prompt + cfg_.max_new + 127) / 128;
-  std::vector<int> h(static_cast<size_t>(7 + items_cap) * Bb + 1);
-  int max_ctx = 0;
-  double ctx_sum = 0.0;
+  h.assign(static_cast<size_t>(7 + items_cap) * Bb + 1, 0);
+  max_ctx = 0;
+  ctx_sum = 0.0;
   for (int b = 0; b < Bb; ++b) {
     const bool pad = b >= B;
     const DecodeRow r = pad ? DecodeRow{cfg_.max_samples, pad_slot_, 0, 0, 0} : rows[b];
@@ -618,7 +620,73 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
   }
   const Dims& A = models_[kActor].dims;
   const int n_pairs = fpk::attn_decode_items(h.data() + 2 * Bb, Bb, A.KVH, A.hd, A.H / A.KVH, h.data() + 7 * Bb);
-  upload(dec_.rows, h.data(), (static_cast<size_t>(7) * Bb + 1 + n_pairs) * 4, st);
+  return static_cast<size_t>(7) * Bb + 1 + n_pairs;
+}
+
+// One decode step. Rows are padded to a batch-size bucket so that the whole
+// step — ~7 kernels per layer with PDL edges — replays as one CUDA graph per
+// (bucket, mode, temperature, seed): host launch cost and inter-kernel gaps
+// vanish. Large batches are cut into two halves that run as two dependent-
+// kernel chains on two streams in the same graph (the rows are independent and
+// every kernel is batch-independent, so the bits do not change): one half's
+// latency-bound GEMM chain overlaps the other half's bandwidth-bound attention,
+// which is capped to part of the SMs. The probe mode (per-launch CUDA events)
+// and the traced step run eagerly.
+void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed) {
+  const int B = static_cast<int>(rows.size());
+  if (B == 0) return;
+  // FUSEPLAN_TRACE_STEP=k: the engine's k-th decode step runs eagerly with
+  // globaltimer stamps in every GEMM / attention launch (tools/step_trace.py)
+  static const int trace_step = [] {
+    const char* e = std::getenv("FUSEPLAN_TRACE_STEP");
+    return e ? std::atoi(e) : -1;
+  }();
+  static const int split_min = [] {  // FUSEPLAN_DECODE_SPLIT: batch size from which the step runs as two halves
+    const char* e = std::getenv("FUSEPLAN_DECODE_SPLIT");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const int split_ctas = [] {  // FUSEPLAN_SPLIT_ATTN_CTAS: attention CTAs per half
+    const char* e = std::getenv("FUSEPLAN_SPLIT_ATTN_CTAS");
+    return e ? std::atoi(e) : 74;
+  }();
+  const bool tracing = ++decode_calls_ == trace_step;
+  const bool graph = use_graphs_ && !probe_on_ && !tracing;
+  cudaStream_t st = s_decode_;
+  const int ctx_cap = cfg_.max_prompt + cfg_.max_new;
+  if (graph && split_min > 0 && B >= split_min) {
+    // balanced halves: rows in decreasing context length, dealt alternately
+    std::vector<int> order(B);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return rows[x].pos > rows[y].pos; });
+    std::vector<DecodeRow> g[2];
+    for (int k = 0; k < B; ++k) g[k & 1].push_back(rows[order[k]]);
+    const int Bb0 = bucket_of(static_cast<int>(g[0].size())), Bb1 = bucket_of(static_cast<int>(g[1].size()));
+    if (Bb0 > dec_.cap || Bb1 > dec2_.cap) throw std::invalid_argument("engine: decode batch exceeds max_live");
+    std::vector<int> h;
+    int mc;
+    double cs;
+    size_t n = build_rows(g[0].data(), static_cast<int>(g[0].size()), Bb0, h, mc, cs);
+    upload(dec_.rows, h.data(), n * 4, st);
+    n = build_rows(g[1].data(), static_cast<int>(g[1].size()), Bb1, h, mc, cs);
+    upload(dec2_.rows, h.data(), n * 4, st);
+    auto both = [&]() {
+      FP_CUDA(cudaEventRecord(ev_fork_, st));
+      FP_CUDA(cudaStreamWaitEvent(s_decode2_, ev_fork_, 0));
+      decode_kernels(dec_, st, Bb0, ctx_cap, mode, inv_temp, sample_seed, 0.0, split_ctas);
+      decode_kernels(dec2_, s_decode2_, Bb1, ctx_cap, mode, inv_temp, sample_seed, 0.0, split_ctas);
+      FP_CUDA(cudaEventRecord(ev_join_, s_decode2_));
+      FP_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
+    };
+    run_graph(GraphKey{Bb0, Bb1, mode, inv_temp, sample_seed}, both);
+    return;
+  }
+  const int Bb = graph ? bucket_of(B) : B;
+  if (Bb > dec_.cap) throw std::invalid_argument("engine: decode batch exceeds max_live");
+  std::vector<int> h;
+  int max_ctx;
+  double ctx_sum;
+  const size_t n = build_rows(rows.data(), B, Bb, h, max_ctx, ctx_sum);
+  upload(dec_.rows, h.data(), n * 4, st);
   if (!graph) {
     unsigned long long* arena = nullptr;
     const size_t words = size_t(1) << 22;
@@ -628,14 +696,14 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
       FP_CUDA(cudaStreamSynchronize(st));
       fpk::trace_arm(arena, words);
     }
-    decode_kernels(Bb, max_ctx, mode, inv_temp, sample_seed, ctx_sum);
+    decode_kernels(dec_, st, Bb, max_ctx, mode, inv_temp, sample_seed, ctx_sum, 148);
     if (tracing) {
       FP_CUDA(cudaStreamSynchronize(st));
       const std::vector<fpk::TraceRec> recs = fpk::trace_disarm();
       size_t used = 0;
       for (const auto& r : recs) used = std::max(used, r.off + static_cast<size_t>(r.units) * (r.kind == 0 ? 8 : 4));
-      std::vector<unsigned long long> h(used);
-      FP_CUDA(cudaMemcpy(h.data(), arena, used * 8, cudaMemcpyDeviceToHost));
+      std::vector<unsigned long long> th(used);
+      FP_CUDA(cudaMemcpy(th.data(), arena, used * 8, cudaMemcpyDeviceToHost));
       cudaFree(arena);
       const char* path = std::getenv("FUSEPLAN_TRACE_OUT");
       FILE* f = std::fopen(path ? path : "fp_step_trace.json", "w");
@@ -645,7 +713,7 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
           const int wpu = recs[i].kind == 0 ? 8 : 4;
           std::fprintf(f, "%s{\"kind\": %d, \"units\": %d, \"data\": [", i ? ", " : "", recs[i].kind, recs[i].units);
           for (int u = 0; u < recs[i].units * wpu; ++u)
-            std::fprintf(f, "%s%llu", u ? "," : "", h[recs[i].off + u]);
+            std::fprintf(f, "%s%llu", u ? "," : "", th[recs[i].off + u]);
           std::fprintf(f, "]}");
         }
         std::fprintf(f, "]}\n");
@@ -654,21 +722,25 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
     }
     return;
   }
-  const int ctx_cap = cfg_.max_prompt + cfg_.max_new;
-  const GraphKey key{Bb, mode, inv_temp, sample_seed};
+  run_graph(GraphKey{Bb, 0, mode, inv_temp, sample_seed},
+            [&]() { decode_kernels(dec_, st, Bb, ctx_cap, mode, inv_temp, sample_seed, 0.0, 148); });
+}
+
+// Replay the step graph of `key`; the first sight of a key runs eagerly (sets
+// kernel attributes, fills the tensor-map cache), the second captures.
+void Engine::run_graph(const GraphKey& key, const std::function<void()>& body) {
+  cudaStream_t st = s_decode_;
   auto it = graphs_.find(key);
   if (it == graphs_.end()) {
-    // first sight of this key: run eagerly (sets kernel attributes, builds the
-    // tensor-map cache), capture from the second occurrence on
     if (!graph_seen_.count(key)) {
       graph_seen_.insert(key);
-      decode_kernels(Bb, ctx_cap, mode, inv_temp, sample_seed, 0.0);
+      body();
       return;
     }
     cudaGraph_t g = nullptr;
     const long long n0 = fpk::launch_count();
     FP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    decode_kernels(Bb, ctx_cap, mode, inv_temp, sample_seed, 0.0);
+    body();
     FP_CUDA(cudaStreamEndCapture(st, &g));
     const long long nk = fpk::launch_count() - n0;
     fpk::count_launches(-nk);  // captured, not launched: counted at each replay
@@ -681,24 +753,24 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
   fpk::count_launches(it->second.kernels);
 }
 
-void Engine::decode_kernels(int B, int max_ctx, int mode, float inv_temp, uint64_t sample_seed, double ctx_sum) {
-  cudaStream_t st = s_decode_;
+void Engine::decode_kernels(DecodeWs& dw, cudaStream_t st, int B, int max_ctx, int mode, float inv_temp,
+                            uint64_t sample_seed, double ctx_sum, int attn_ctas) {
   const ModelW& w = models_[kActor];
   const Dims& D = w.dims;
-  const int* slot = dec_.rows;
-  const int* pos = dec_.rows + B;
-  const int* ctx = dec_.rows + 2 * B;
-  const int* dst = dec_.rows + 3 * B;
-  const int* target = dec_.rows + 4 * B;
-  const int* sid = dec_.rows + 5 * B;
-  const int* step = dec_.rows + 6 * B;
-  const int* items = dec_.rows + 7 * B;
+  const int* slot = dw.rows;
+  const int* pos = dw.rows + B;
+  const int* ctx = dw.rows + 2 * B;
+  const int* dst = dw.rows + 3 * B;
+  const int* target = dw.rows + 4 * B;
+  const int* sid = dw.rows + 5 * B;
+  const int* step = dw.rows + 6 * B;
+  const int* items = dw.rows + 7 * B;
   const fpk::KvPoolView pv = pool_view();
   const size_t stride = static_cast<size_t>(B) * D.d;
   const int so = fpk::gemm_splits(D.d, D.H * D.hd);
   const int sd = fpk::gemm_splits(D.d, D.F);
 
-  fpk::embed(d_cur_tok_, slot, B, w.embed, D.d, dec_.x, st);
+  fpk::embed(d_cur_tok_, slot, B, w.embed, D.d, dw.x, st);
   int nparts = 0;
   for (int l = 0; l < D.L; ++l) {
     const LayerW& L = w.layers[l];
@@ -709,29 +781,30 @@ void Engine::decode_kernels(int B, int max_ctx, int mode, float inv_temp, uint64
       pf1.p[0] = L.wqkv, pf1.bytes[0] = wq, pf1.p[1] = L.wo, pf1.bytes[1] = wo;
       pf2.p[0] = L.wgu, pf2.bytes[0] = wgu, pf2.p[1] = L.wd, pf2.bytes[1] = wdn;
     }
-    fpk::add_norm(dec_.x, nparts ? dec_.parts : nullptr, nparts, stride, L.ln1, dec_.h, B, D.d, nullptr, 0, nullptr,
+    fpk::add_norm(dw.x, nparts ? dw.parts : nullptr, nparts, stride, L.ln1, dw.h, B, D.d, nullptr, 0, nullptr,
                   nullptr, st, pf1);
-    fpk::gemm_qkv_rope(L.wqkv, D.d, dec_.h, B, D.H, D.KVH, D.hd, pos, rope_cs_, pv, l, slot, dec_.q, st);
+    fpk::gemm_qkv_rope(L.wqkv, D.d, dw.h, B, D.H, D.KVH, D.hd, pos, rope_cs_, pv, l, slot, dw.q, st);
     if (probe_on_) {
       ProbeRec pr{probe_event(), probe_event(), 0.0};
       const double kv_tok = 2.0 * D.KVH * D.hd * 2.0;  // K + V of one layer, bf16
       pr.bytes = ctx_sum * kv_tok + static_cast<double>(B) * D.H * D.hd * 2.0;
-      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, items, max_ctx, dec_.attn_work, dec_.attn, dec_.attn_cnt, st, pr.a,
+      fpk::attn_decode(dw.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, items, max_ctx, dw.attn_work, dw.attn, dw.attn_cnt, st, pr.a,
                        pr.b);
       probes_.push_back(pr);
     } else {
-      fpk::attn_decode(dec_.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, items, max_ctx, dec_.attn_work, dec_.attn, dec_.attn_cnt, st);
+      fpk::attn_decode(dw.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, items, max_ctx, dw.attn_work, dw.attn, dw.attn_cnt, st,
+                       nullptr, nullptr, attn_ctas);
     }
-    fpk::gemm_f32_splitk(L.wo, D.d, D.H * D.hd, dec_.attn, B, dec_.parts, so, st);
-    fpk::add_norm(dec_.x, dec_.parts, so, stride, L.ln2, dec_.h, B, D.d, nullptr, 0, nullptr, nullptr, st, pf2);
-    fpk::gemm_swiglu_decode(L.wgu, D.F, D.d, dec_.h, B, dec_.act, st);
-    fpk::gemm_f32_splitk(L.wd, D.d, D.F, dec_.act, B, dec_.parts, sd, st);
+    fpk::gemm_f32_splitk(L.wo, D.d, D.H * D.hd, dw.attn, B, dw.parts, so, st);
+    fpk::add_norm(dw.x, dw.parts, so, stride, L.ln2, dw.h, B, D.d, nullptr, 0, nullptr, nullptr, st, pf2);
+    fpk::gemm_swiglu_decode(L.wgu, D.F, D.d, dw.h, B, dw.act, st);
+    fpk::gemm_f32_splitk(L.wd, D.d, D.F, dw.act, B, dw.parts, sd, st);
     nparts = sd;
   }
-  fpk::add_norm(dec_.x, dec_.parts, nparts, stride, w.lnf, dec_.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
-  fpk::gemm_vocab(dec_.h, B, D.d, w.head, D.V, mode, inv_temp, target, sid, step, sample_seed, dec_.vocab_part,
-                  dec_.tgt_z, st);
-  fpk::vocab_finalize(dec_.vocab_part, dec_.tgt_z, B, D.V, mode, target, sid, step, sample_seed, nullptr, nullptr, dst,
+  fpk::add_norm(dw.x, dw.parts, nparts, stride, w.lnf, dw.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
+  fpk::gemm_vocab(dw.h, B, D.d, w.head, D.V, mode, inv_temp, target, sid, step, sample_seed, dw.vocab_part,
+                  dw.tgt_z, st);
+  fpk::vocab_finalize(dw.vocab_part, dw.tgt_z, B, D.V, mode, target, sid, step, sample_seed, nullptr, nullptr, dst,
                       d_hist_tok_, d_hist_logp_, slot, d_cur_tok_, st);
   FP_CUDA(cudaGetLastError());
 }

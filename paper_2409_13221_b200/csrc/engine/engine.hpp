@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <set>
 #include <stdexcept>
@@ -203,11 +204,12 @@ class Engine {
   bool l2_prefetch_ = false;  // decode: pull each layer's weights into L2 ahead of its GEMMs (measured slower: off)
   int pad_slot_ = 0;
   struct GraphKey {
-    int B, mode;
+    int B, B1, mode;  // B1: second half of a split step (0: unsplit)
     float inv_temp;
     uint64_t seed;
     bool operator<(const GraphKey& o) const {
       if (B != o.B) return B < o.B;
+      if (B1 != o.B1) return B1 < o.B1;
       if (mode != o.mode) return mode < o.mode;
       if (inv_temp != o.inv_temp) return inv_temp < o.inv_temp;
       return seed < o.seed;
@@ -219,7 +221,13 @@ class Engine {
   };
   std::map<GraphKey, StepGraph> graphs_;
   std::set<GraphKey> graph_seen_;
-  void decode_kernels(int B, int max_ctx, int mode, float inv_temp, uint64_t sample_seed, double ctx_sum);
+  struct DecodeWs;
+  void decode_kernels(DecodeWs& dw, cudaStream_t st, int B, int max_ctx, int mode, float inv_temp,
+                      uint64_t sample_seed, double ctx_sum, int attn_ctas);
+  size_t build_rows(const DecodeRow* rows, int B, int Bb, std::vector<int>& h, int& max_ctx, double& ctx_sum);
+  void run_graph(const GraphKey& key, const std::function<void()>& body);
+  cudaStream_t s_decode2_ = nullptr;
+  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   uint64_t prompts_tag_ = 0;
   CUtensorMap kv_map_{};
   bool has_kv_map_ = false;
@@ -292,7 +300,7 @@ class Engine {
   size_t handoff_bytes_ = 0;
   Experience hand_;
   std::vector<int64_t> resp_off_;
-  DecodeWs dec_;
+  DecodeWs dec_, dec2_;
   PinnedRing* ring_ = nullptr;
   void* scratch_ = nullptr;
   size_t scratch_bytes_ = 0;

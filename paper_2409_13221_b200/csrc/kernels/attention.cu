@@ -487,7 +487,7 @@ void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView&
                  const int* ctx, const int* items, int max_ctx, float* work, bf16* out, int* counters,
                  cudaStream_t st,
                  cudaEvent_t probe_begin,
-                 cudaEvent_t probe_end) {
+                 cudaEvent_t probe_end, int max_ctas) {
   if (B <= 0) return;
   if (probe_begin) cudaEventRecord(probe_begin, st);
   if (pool.page_tokens != kPT) throw std::invalid_argument("attn_decode: page_tokens must be 64");
@@ -495,7 +495,7 @@ void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView&
   const int G = H / KVH;
 #define FP_DEC(HD_, G_) \
   if (hd == HD_ && G == G_) { launch_decode<HD_, G_>(q, B, H, KVH, pool, layer, slot, ctx, ns, work, st); } else
-  if (attn_decode_mma(q, B, H, KVH, hd, pool, layer, slot, ctx, items, ns, work, out, counters, st)) {
+  if (attn_decode_mma(q, B, H, KVH, hd, pool, layer, slot, ctx, items, ns, work, out, counters, st, max_ctas)) {
     if (probe_end) cudaEventRecord(probe_end, st);
     return;  // splits merged in-kernel
   } else FP_DEC(32, 1) FP_DEC(64, 1) FP_DEC(128, 1) FP_DEC(64, 4) FP_DEC(128, 4) FP_DEC(128, 8) FP_DEC(64, 8) {

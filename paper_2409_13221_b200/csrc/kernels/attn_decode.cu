@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(DecCfg<HD, DEEP>::kWarps * 32, 1) attn_decode_
 template <int HD, int G, bool DEEP>
 void launch_cfg(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
             const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out, int* counters,
-            cudaStream_t st) {
+            cudaStream_t st, int max_ctas) {
   using C = DecCfg<HD, DEEP>;
   static bool attr = false;
   if (!attr) {
@@ -515,7 +515,7 @@ void launch_cfg(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, co
   const int rows_per_page = static_cast<int>(pool.page_bytes / (static_cast<size_t>(HD) * 2));
   const float scale = kLog2e / sqrtf(static_cast<float>(HD));
   const int max_items = nsplit * kSubUnits * B * KVH;  // upper bound of the items (cut splits included)
-  const int grid = std::max(1, std::min(148, (max_items + C::kWarps - 1) / C::kWarps));
+  const int grid = std::max(1, std::min(max_ctas, (max_items + C::kWarps - 1) / C::kWarps));
   launch_pdl(attn_decode_mma_kernel<HD, G, DEEP>, dim3(grid), dim3(C::kWarps * 32), C::kSmem, st, map, q,
              pool.block_table, pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, items, B, H, KVH, nsplit,
              scale, part_o, part_ml, sub_o, sub_ml, out, counters,
@@ -865,7 +865,7 @@ __global__ void __launch_bounds__(TeamCfg<T>::kWarps * 32, 1) attn_decode_team_k
 template <int T>
 void launch_team(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
                  const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out, int* counters,
-                 cudaStream_t st) {
+                 cudaStream_t st, int max_ctas) {
   using C = TeamCfg<T>;
   static bool attr = false;
   if (!attr) {
@@ -878,7 +878,7 @@ void launch_team(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, c
   const int rows_per_page = static_cast<int>(pool.page_bytes / (static_cast<size_t>(64) * 2));
   const float scale = kLog2e / sqrtf(64.f);
   const int max_items = nsplit * B * KVH;
-  const int grid = std::max(1, std::min(148, (max_items + C::kTeams - 1) / C::kTeams));
+  const int grid = std::max(1, std::min(max_ctas, (max_items + C::kTeams - 1) / C::kTeams));
   launch_pdl(attn_decode_team_kernel<T>, dim3(grid), dim3(C::kWarps * 32), C::kSmem, st, map, q, pool.block_table,
              pool.bt_stride, rows_per_page, layer_rows, layer, slot, ctx, items, H, KVH, nsplit, scale, part_o,
              part_ml, out, counters, trace_slot(2, grid, 4));
@@ -893,15 +893,17 @@ int env_int(const char* name, int dflt) {
 template <int HD, int G>
 void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
             const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out, int* counters,
-            cudaStream_t st) {
+            cudaStream_t st, int max_ctas) {
   switch (attn_decode_variant(B, KVH, HD, G, nullptr)) {
-    case 2: launch_team<4>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st); break;
-    case 3: launch_team<2>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st); break;
+    case 2: launch_team<4>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st, max_ctas); break;
+    case 3: launch_team<2>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st, max_ctas); break;
     case 1:
-      launch_cfg<HD, G, true>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);
+      launch_cfg<HD, G, true>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st,
+                              max_ctas);
       break;
     default:
-      launch_cfg<HD, G, false>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);
+      launch_cfg<HD, G, false>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st,
+                               max_ctas);
   }
 }
 
@@ -931,12 +933,12 @@ int attn_decode_variant(int B, int KVH, int hd, int G, int* warps) {
 
 bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer,
                      const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out,
-                     int* counters, cudaStream_t st) {
+                     int* counters, cudaStream_t st, int max_ctas) {
   if (!pool.kv_map || !counters || !items) return false;
   const int G = H / KVH;
 #define FP_MMA(HD_, G_)                                                                            \
   if (hd == HD_ && G == G_) {                                                                      \
-    launch<HD_, G_>(*pool.kv_map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st);      \
+    launch<HD_, G_>(*pool.kv_map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st, max_ctas);      \
     return true;                                                                                   \
   }
   FP_MMA(64, 1) FP_MMA(128, 1) FP_MMA(64, 4) FP_MMA(128, 4) FP_MMA(128, 8) FP_MMA(64, 8)

@@ -160,7 +160,7 @@ constexpr int kDecodeChunk = 512;
 // left zero.
 bool attn_decode_mma(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer,
                      const int* slot, const int* ctx, const int* items, int nsplit, float* work, bf16* out,
-                     int* counters, cudaStream_t st);
+                     int* counters, cudaStream_t st, int max_ctas = 148);
 // Debug: per-warp (entry ns, loop-begin ns, end ns, units) of subsequent
 // warp-per-item decode-attention launches into buf (4 x 148 x warps); nullptr disables.
 void set_attn_trace(unsigned long long* buf);
@@ -204,7 +204,7 @@ size_t attn_decode_workspace(int B, int H, int hd, int max_ctx);  // split + sub
 void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView& pool, int layer, const int* slot,
                  const int* ctx, const int* items, int max_ctx, float* work, bf16* out, int* counters,
                  cudaStream_t st,
-                 cudaEvent_t probe_begin = nullptr, cudaEvent_t probe_end = nullptr);
+                 cudaEvent_t probe_begin = nullptr, cudaEvent_t probe_end = nullptr, int max_ctas = 148);
 // Varlen causal attention over packed q [M, H, hd], k/v [M, KVH, hd];
 // sequences [cu[i], cu[i+1]). tiles: host-built table of (seq, q_tile) pairs
 // (attn_varlen_tiles). out [M, H, hd].
