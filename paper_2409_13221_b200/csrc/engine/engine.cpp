@@ -117,6 +117,7 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
   for (int s = cfg_.max_live - 1; s >= 0; --s) free_slots_.push_back(s);
   if (const char* g = std::getenv("FUSEPLAN_DECODE_GRAPHS")) use_graphs_ = std::atoi(g) != 0;  // A/B switch
   if (const char* g = std::getenv("FUSEPLAN_L2_PREFETCH")) l2_prefetch_ = std::atoi(g) != 0;
+  if (const char* g = std::getenv("FUSEPLAN_FUSE_ROPE")) fuse_rope_ = std::atoi(g) != 0;
   pad_slot_ = cfg_.max_live;  // decode padding rows: block-table row of zeros -> scratch page 0
   slot_pages_.assign(cfg_.max_live + 1, {});
   bt_host_.assign(static_cast<size_t>(cfg_.max_live + 1) * max_pages_per_sample_, 0);
@@ -517,9 +518,14 @@ void Engine::forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, int
   for (int l = 0; l < D.L; ++l) {
     const LayerW& L = w.layers[l];
     fpk::add_norm(ws.x, nullptr, 0, 0, L.ln1, ws.h, M, D.d, nullptr, 0, nullptr, nullptr, st);
-    fpk::gemm_bf16(L.wqkv, D.qkv_width(), D.d, ws.h, M, ws.qkv, D.qkv_width(), st);
-    fpk::rope_qkv(ws.qkv, M, D.H, D.KVH, D.hd, ws.pos, cfg_.rope_theta, ws.q, ws.k, ws.v, use_pool ? &pv : nullptr,
-                  l, ws.slot, st);
+    if (fuse_rope_ && D.hd == models_[kActor].dims.hd) {  // the cos/sin table is the actor's head_dim
+      fpk::gemm_qkv_rope_packed(L.wqkv, D.d, ws.h, M, D.H, D.KVH, D.hd, ws.pos, rope_cs_, use_pool ? &pv : nullptr, l,
+                                ws.slot, ws.q, ws.k, ws.v, st);
+    } else {
+      fpk::gemm_bf16(L.wqkv, D.qkv_width(), D.d, ws.h, M, ws.qkv, D.qkv_width(), st);
+      fpk::rope_qkv(ws.qkv, M, D.H, D.KVH, D.hd, ws.pos, cfg_.rope_theta, ws.q, ws.k, ws.v, use_pool ? &pv : nullptr,
+                    l, ws.slot, st);
+    }
     if (use_pool && l == D.L - 1) break;  // prefill only needs the last layer's K/V
     fpk::attn_varlen(ws.q, ws.k, ws.v, D.H, D.KVH, D.hd, ws.cu, ws.tiles, n_tiles, ws.attn, st);
     fpk::gemm_f32_residual(L.wo, D.d, D.H * D.hd, ws.attn, M, ws.x, st);

@@ -200,6 +200,7 @@ class Engine {
   };
   bool probe_on_ = false;
   bool use_graphs_ = true;
+  bool fuse_rope_ = true;  // prefill / scoring: RoPE + K/V writes in the QKV GEMM epilogue
   int decode_calls_ = 0;
   bool l2_prefetch_ = false;  // decode: pull each layer's weights into L2 ahead of its GEMMs (measured slower: off)
   int pad_slot_ = 0;

@@ -386,6 +386,24 @@ void gemm_qkv_rope(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH
     dispatch_bn<int>(M, (N + 127) / 128, go);
 }
 
+void gemm_qkv_rope_packed(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH, int hd, const int* pos,
+                          const float2* cs, const KvPoolView* pool, int layer, const int* slot, bf16* q_out,
+                          bf16* k_out, bf16* v_out, cudaStream_t st) {
+  if (128 % hd != 0) throw std::invalid_argument("gemm_qkv_rope: head_dim must divide 128");
+  const int N = (H + 2 * KVH) * hd;
+  dispatch_bn<int>(M, (N + 127) / 128, [&]<int BN>() {
+    EpiRopeKV<BN> e{q_out, pool ? *pool : KvPoolView{}, slot, pos, cs, layer, H, KVH, hd, M};
+    e.pool.kv_map = nullptr;
+    e.k_out = k_out;
+    e.v_out = v_out;
+    e.use_pool = pool != nullptr;
+    if (many_waves(M, N, BN))
+      launch<BN, EpiRopeKV<BN>, 2>(Wqkv, N, X, M, K, 1, e, st);
+    else
+      launch<BN>(Wqkv, N, X, M, K, 1, e, st);
+  });
+}
+
 constexpr int kVocabBN = 256;
 
 int vocab_tiles(int V) { return 2 * ((V + kVocabBN - 1) / kVocabBN); }  // partials per row: 2 column halves per tile

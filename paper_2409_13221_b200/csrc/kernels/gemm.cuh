@@ -402,6 +402,9 @@ struct EpiRopeKV {
   const int* pos;
   const float2* cs;
   int layer, H, KVH, hd, M;
+  __nv_bfloat16* k_out = nullptr;  // optional packed K / V [M, KVH, hd] (prefill / scoring attention)
+  __nv_bfloat16* v_out = nullptr;
+  int use_pool = 1;                // write the new K / V into the paged pool
   static constexpr bool kTmaStore = false;
   static constexpr int kPasses = 1;
   template <class S> __device__ void next_pass(S&, int, int, int, int) const {}
@@ -416,7 +419,7 @@ struct EpiRopeKV {
     st.pj = st.pagej = 0;
     if (bl < nb) {
       st.pj = pos[b0 + bl];
-      st.pagej = pool.block_table[slot[b0 + bl] * pool.bt_stride + st.pj / pool.page_tokens];
+      if (use_pool) st.pagej = pool.block_table[slot[b0 + bl] * pool.bt_stride + st.pj / pool.page_tokens];
     }
   }
   __device__ void operator()(State& st, uint8_t* smem, int, int, int, int r, int, int c0,
@@ -474,16 +477,25 @@ struct EpiRopeKV {
             o1 = f2bf(r1);
             o2 = f2bf(r2);
           }
-          __nv_bfloat16* dst;
           if (head < H) {
-            dst = q_out + (static_cast<size_t>(b) * H + head) * hd;
+            __nv_bfloat16* dst = q_out + (static_cast<size_t>(b) * H + head) * hd;
+            dst[i] = o1;
+            dst[i + hh] = o2;
           } else {
             const bool is_v = head >= H + KVH;
             const int kh = head - H - (is_v ? KVH : 0);
-            dst = pool_base + kv_elem_offset(pool, pgk[kk], layer, kh, hd, p % pool.page_tokens, is_v);
+            if (use_pool) {
+              __nv_bfloat16* dst = pool_base + kv_elem_offset(pool, pgk[kk], layer, kh, hd, p % pool.page_tokens, is_v);
+              dst[i] = o1;
+              dst[i + hh] = o2;
+            }
+            __nv_bfloat16* packed = is_v ? v_out : k_out;
+            if (packed) {
+              __nv_bfloat16* dst = packed + (static_cast<size_t>(b) * KVH + kh) * hd;
+              dst[i] = o1;
+              dst[i + hh] = o2;
+            }
           }
-          dst[i] = o1;
-          dst[i + hh] = o2;
         }
       }
     }

@@ -144,6 +144,12 @@ void rope_table(float2* tab, int max_pos, int hd, float rope_theta, cudaStream_t
 void gemm_qkv_rope(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH, int hd, const int* pos,
                    const float2* cs, const KvPoolView& pool, int layer, const int* slot, bf16* q_out,
                    cudaStream_t st);
+// The same for packed rows (prefill / scoring): q_out [M, H, hd]; K / V into
+// k_out / v_out [M, KVH, hd] (optional) and, with a pool, at (slot[m], pos[m]).
+// Bit-identical to gemm_bf16 + rope_qkv (same tiles, roundings and table).
+void gemm_qkv_rope_packed(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH, int hd, const int* pos,
+                          const float2* cs, const KvPoolView* pool, int layer, const int* slot, bf16* q_out,
+                          bf16* k_out, bf16* v_out, cudaStream_t st);
 // 2-D TMA map over the pool viewed as [rows, hd] bf16 rows (one row = one
 // token's K or V of one (page, layer, kv head)); box {64, 32}, 128 B swizzle.
 CUtensorMap make_kv_map(const void* pool, long long rows, int hd);

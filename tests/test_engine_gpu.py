@@ -166,3 +166,24 @@ def test_hd64_schedules_identical(small64):
     b = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="stage_barrier")
     for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret", "score"):
         assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
+
+
+def test_fused_rope_prefill_scoring_bit_identical(small64):
+    """Prefill / scoring with RoPE + K/V writes in the QKV GEMM epilogue give the same
+    bits as the separate GEMM + rope kernels (same tiles, roundings and cos/sin)."""
+    import os
+    from paper_2409_13221_b200.configs import gen_config
+    from paper_2409_13221_b200.engine import Engine
+    w, eng, batch, _ = small64
+    a = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="fused", claim_tokens=4096)
+    os.environ["FUSEPLAN_FUSE_ROPE"] = "0"
+    try:
+        eng2 = Engine(w, device=0)
+    finally:
+        del os.environ["FUSEPLAN_FUSE_ROPE"]
+    try:
+        b = eng2.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="fused", claim_tokens=4096)
+    finally:
+        eng2.close()
+    for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret", "score"):
+        assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
