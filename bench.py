@@ -292,6 +292,15 @@ def main():
         eng.close()
         return
     hbm, tflops, src = peaks()
+    w_bytes = eng.model_size(0)[0]
+    kvb = eng.kv_bytes_per_token()
+    dec_s = sum(o.stats["decode_gpu_seconds"] for o in outs_v)
+    dec_b = sum(o.stats["decode_steps"] * w_bytes + o.stats["decode_ctx_tokens"] * kvb for o in outs_v)
+    decode_roofline = {"bound": "hbm", "bytes_per_step": dec_b / len(outs_v), "seconds_per_step": dec_s / len(outs_v),
+                       "achieved": dec_b / dec_s / 1e9 if dec_s else None, "peak": hbm, "unit": "GB/s",
+                       "frac": dec_b / dec_s / 1e9 / hbm if dec_s else None,
+                       "note": "decode_steps x actor weight bytes + sum over rows and steps of ctx x K/V bytes per "
+                               "token, / sum of decode-step GPU time (rank 0)"}
     achieved = (probe_bytes / (probe_ms / 1000.0)) / 1e9 if probe_ms > 0 else None
     # traffic: DRAM bytes per launch from the committed ncu --set full capture
     # of this kernel (profiles/attn_decode_traffic.json), as its DRAM /
@@ -319,6 +328,9 @@ def main():
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": src, "launches": probe_n,
                      "bytes_per_launch": probe_bytes / max(probe_n, 1),
                      "share_of_step": (probe_ms / ms_p) if ms_p else None},
+        # the whole decode step against HBM — weights once per step
+        # plus K/V of every visible token, over the decode GPU time of the value steps
+        "decode_roofline": decode_roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "stage_barrier": {"value": sb, "unit": UNIT, "speedup_fused": (value / sb) if sb else None},
