@@ -116,7 +116,7 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const 
 // ST > 0 overrides the ring depth (a 2-stage ring lets two CTAs share an SM:
 // one's epilogue overlaps the other's mainloop — the large-M GEMMs).
 template <int BN, class Epi, int ST = 0>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kGemmThreads, ST == 2 ? 2 : 1)  // the 2-stage shape must fit twice per SM
     tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                    const GemmGeom g, const __grid_constant__ Epi epi) {
   using C = GemmCfg<BN, ST ? ST : EpiStages<Epi>::value>;
@@ -448,12 +448,13 @@ struct EpiRopeKV {
       fl2[k2] = (pr / hh) * hd + i2[k2];  // tile-local feature of the pair's low element
       head2[k2] = (a0 + fl2[k2]) / hd;    // [0, H) q, [H, H + KVH) k, then v
     }
-    // four columns at a time: their (cos, sin) loads are issued together
-    for (int k0 = 0; k0 < ncol; k0 += 4) {
-      float2 c[4][2];
-      int pk[4], pgk[4];
+    // eight columns at a time: their (cos, sin) loads are issued together
+    constexpr int kG = 4;  // (8 would cost registers: the 2-CTA shape needs <= 102 per thread)
+    for (int k0 = 0; k0 < ncol; k0 += kG) {
+      float2 c[kG][2];
+      int pk[kG], pgk[kG];
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+      for (int kk = 0; kk < kG; ++kk) {
         const int k = min(k0 + kk, ncol - 1);
         pk[kk] = __shfl_sync(0xffffffffu, pj, k);
         pgk[kk] = __shfl_sync(0xffffffffu, pagej, k);
@@ -462,7 +463,7 @@ struct EpiRopeKV {
           c[kk][k2] = head2[k2] < H + KVH ? __ldg(cs + pk[kk] * hh + i2[k2]) : make_float2(1.f, 0.f);
       }
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
+      for (int kk = 0; kk < kG; ++kk) {
         if (k0 + kk >= ncol) break;
         const int bl = ew + 8 * (k0 + kk);
         const int b = b0 + bl;
