@@ -179,7 +179,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--r-ratio", type=float, default=0.2)
+    ap.add_argument("--r-ratio", default="0.2",
+                    help="migration threshold R_t / n, or 'auto': the best ratio of sweep_threshold under the "
+                         "calibrated CostModel (the paper's workflow, SURVEY §8f row 1)")
     ap.add_argument("--token-mode", default="sample", choices=["forced", "greedy", "sample"])
     ap.add_argument("--claim-tokens", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -203,7 +205,12 @@ def main():
     eng = Engine(w, device=local, max_samples=w.n_prompts, max_live=min(w.n_prompts, 2 * w.n_prompts // G))
     batch = batch_for(w, eng.sched)
     cfg = gen_config(w, G, calibrated=True)  # decision-clock constants fitted to measured B200 steps
-    r_t = round(args.r_ratio * len(batch)) if G > 1 else 0
+    if args.r_ratio == "auto" and G > 1:
+        sw = eng.sched.sweep_threshold(batch, cfg)
+        ratio = sw.curve[sw.best_index][0]
+    else:
+        ratio = float(args.r_ratio) if args.r_ratio != "auto" else 0.2
+    r_t = round(ratio * len(batch)) if G > 1 else 0
     shm = None
     if dist:
         obj = [f"/fp_bench_{uuid.uuid4().hex[:12]}" if rank == 0 else None]
@@ -319,7 +326,7 @@ def main():
                 f"{args.token_mode} tokens",
         "config": {"workload": "GPT-2-small-shape actor/ref/critic/reward (L12 d768 H12 ffn3072 V50257), "
                                f"{w.n_prompts // G} prompts x {w.prompt_len} tokens per GPU, <= {w.max_new} new",
-                   "prompts": n_total, "schedule": "fused", "r_t": r_t, "token_mode": args.token_mode,
+                   "prompts": n_total, "schedule": "fused", "r_t": r_t, "r_ratio": ratio if G > 1 else 0.0, "token_mode": args.token_mode,
                    "claim_tokens": args.claim_tokens,
                    "l2": "inputs larger than L2 (KV pool and weights >> 126 MB)",
                    "parallelism": f"dp{G} (one engine per B200)"},
