@@ -677,6 +677,8 @@ __global__ void __launch_bounds__(TeamCfg<T>::kWarps * 32, 1) attn_decode_team_k
     }
   }
   pdl_wait();  // q, the new K/V and the counters come from earlier kernels
+  const unsigned long long t_wait = trace ? gtime_ns() : 0ull;
+  unsigned long long t_first = 0ull;
   if (q_late && lane == 0)  // stage 0 (the sub-chunk's first unit) already expects the q bytes
     bulk_load(qslot(0), q + (static_cast<size_t>(in_it.b) * H + in_it.kvh) * HD, HD * 2, &bar[0]);
   if (tw == 0 && lane == 0) put(1, n_teams + atomicAdd(&counters[0], 1));
@@ -807,6 +809,7 @@ __global__ void __launch_bounds__(TeamCfg<T>::kWarps * 32, 1) attn_decode_team_k
     const int sl = i & 1;
     if (tw == 0 && lane == 0) put(i + 2, n_teams + atomicAdd(&counters[0], 1));
     team_bar<T>(team);
+    if (i == 0 && trace) t_first = gtime_ns();
     known = i + 2;
     pump();
     if (tw != 0) continue;
@@ -850,9 +853,9 @@ __global__ void __launch_bounds__(TeamCfg<T>::kWarps * 32, 1) attn_decode_team_k
       }
     }
   }
-  if (trace && tw == 0 && lane == 0) {  // per CTA: entry, -, last team's end
+  if (trace && tw == 0 && lane == 0) {  // per CTA: entry, team 0's wait return, last team's end, team 0's first item
     unsigned long long* t = trace + 4ull * blockIdx.x;
-    if (team == 0) t[0] = t[1] = t_entry;
+    if (team == 0) t[0] = t_entry, t[1] = t_wait, t[3] = t_first;
     atomicMax(t + 2, gtime_ns());
   }
   // the last team out resets the work counter for the next launch

@@ -9,6 +9,10 @@ import os
 import subprocess
 import sys
 
+import numpy as np
+
+DETAIL = '--detail' in sys.argv
+
 KIND = {0: "gemm", 1: "attn", 2: "attn-team"}
 
 
@@ -39,6 +43,10 @@ def show(path):
             w = [v for v in w if v[0] > 0]
             beg, end = min(v[0] for v in w), max(v[2] for v in w)
             extra = f"units {len(w):5d} (warps/CTAs)"
+        if L["kind"] == 2 and DETAIL:  # team CTAs: entry, wait return, end, first item done
+            for nm, col in (("entry", 0), ("wait", 1), ("first", 3), ("end", 2)):
+                v = np.array([c[col] for c in w if c[col] > 0], dtype=np.float64)
+                extra += f"\n      {nm:5s} " + " ".join(f"{(q - beg) / 1e3:6.2f}" for q in np.percentile(v, [0, 10, 50, 90, 100]))
         rows.append((beg, end, KIND[L["kind"]], extra))
     t0 = rows[0][0]
     print(f"decode step: B={d['B']} max_ctx={d['max_ctx']} ctx_sum={d['ctx_sum']:.0f}")
