@@ -27,7 +27,8 @@ CXX = os.environ.get("CXX", "g++")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 INC = [f"-I{REPO / 'include'}", f"-I{CSRC / 'kernels'}", f"-I{CSRC / 'engine'}", "-I/usr/local/cuda/include"]
 CXXFLAGS = ["-std=c++20", "-O2", "-fPIC", "-Wall", "-Wno-unused-function", "-DFUSEPLAN_B200_EXTENSIONS"]
-NVFLAGS = ["-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", *ARCH]
+NVFLAGS = ["-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr", *ARCH,
+           *os.environ.get("FUSEPLAN_NVCC_EXTRA", "").split()]  # e.g. -DFP_GEMM_EXP (experiment builds)
 
 
 def _sources():

@@ -215,6 +215,22 @@ template <int BN>
 struct Lean {
   static constexpr int v = BN <= 16 ? 6 : BN <= 32 ? 5 : BN <= 64 ? 4 : BN <= 128 ? 3 : 2;
 };
+// A ring holding a decode CTA's whole K range (K = 768: 12 stages at BN 16):
+// every weight tile is in flight before griddepcontrol.wait, so the mainloop
+// after it only waits for the activation tiles.
+template <int BN>
+struct Full {
+  static constexpr int kStage = kTileA + BN * kBK * 2;
+  static constexpr int kFit = (216 * 1024) / kStage;
+  static constexpr int v = kFit > 12 ? 12 : kFit;
+};
+bool full_ring(long long ctas) {  // FUSEPLAN_DECODE_FULL: grids of at most this many CTAs take the Full ring
+  static const int max_ctas = [] {
+    const char* e = std::getenv("FUSEPLAN_DECODE_FULL");
+    return e ? std::atoi(e) : 0;
+  }();
+  return ctas <= max_ctas;
+}
 bool lean(int M) {  // (large batches keep the deep ring: their mainloops are bandwidth-hungry)
   static const int max_m = [] {
     const char* e = std::getenv("FUSEPLAN_DECODE_LEAN");
@@ -321,7 +337,9 @@ void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* o
     const uint64_t str[2] = {static_cast<uint64_t>(N) * 4, static_cast<uint64_t>(M) * N * 4};
     const uint32_t box[3] = {128u, static_cast<uint32_t>(BN), 1u};
     EpiStoreF32 e{encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE), 0};
-    if (BN <= 128 && lean(M))  // (the fp32 staging tile of BN 256 needs the deep ring)
+    if (BN <= 128 && lean(M) && full_ring(static_cast<long long>((N + 127) / 128) * z * ((M + BN - 1) / BN)))
+      launch<BN, EpiStoreF32, Full<BN>::v>(W, N, X, M, K, splits, e, st);
+    else if (BN <= 128 && lean(M))  // (the fp32 staging tile of BN 256 needs the deep ring)
       launch<BN, EpiStoreF32, Lean<BN>::v>(W, N, X, M, K, splits, e, st);
     else
       launch<BN>(W, N, X, M, K, splits, e, st);
@@ -344,7 +362,9 @@ void gemm_swiglu_decode(const bf16* Wgu, int F, int K, const bf16* X, int M, bf1
   const int z = cluster_splits(2 * F, K);
   auto go = [&]<int BN>() {
     EpiSwiGLU<BN> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, BN)};
-    if (z == 1 && lean(M))
+    if (z == 1 && lean(M) && full_ring(static_cast<long long>((2 * F + 127) / 128) * ((M + BN - 1) / BN)))
+      launch<BN, EpiSwiGLU<BN>, Full<BN>::v>(Wgu, 2 * F, X, M, K, z, e, st);
+    else if (z == 1 && lean(M))
       launch<BN, EpiSwiGLU<BN>, Lean<BN>::v>(Wgu, 2 * F, X, M, K, z, e, st);
     else
       launch<BN>(Wgu, 2 * F, X, M, K, z, e, st, true, z > 1);
@@ -375,7 +395,9 @@ void gemm_qkv_rope(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH
   auto go = [&]<int BN>() {
     EpiRopeKV<BN> e{q_out, pool, slot, pos, cs, layer, H, KVH, hd, M};
     e.pool.kv_map = nullptr;  // host pointer: not dereferenced on the device
-    if (z == 1 && lean(M))
+    if (z == 1 && lean(M) && full_ring(static_cast<long long>((N + 127) / 128) * ((M + BN - 1) / BN)))
+      launch<BN, EpiRopeKV<BN>, Full<BN>::v>(Wqkv, N, X, M, K, z, e, st);
+    else if (z == 1 && lean(M))
       launch<BN, EpiRopeKV<BN>, Lean<BN>::v>(Wqkv, N, X, M, K, z, e, st);
     else
       launch<BN>(Wqkv, N, X, M, K, z, e, st, true, z > 1);

@@ -183,25 +183,27 @@ __global__ void __launch_bounds__(kGemmThreads, ST == 2 ? 2 : 1)  // the 2-stage
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_bf16(128, BN);
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % C::kStages;
-      const uint32_t ph = (i / C::kStages) & 1;
-      mbar_wait(&full_bar[s], ph);
-      if (tr && lane_id() == 0 && (i == 0 || i == nkb - 1)) tr[i == 0 ? 2 : 3] = gtime();
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sa = smem_u32(smem + s * C::kStageBytes);
-        const uint32_t sb = sa + kTileA;
+    // One thread issues: stage descriptors are the stage-0 ones plus the
+    // stage offset (>> 4, the descriptor's address unit), so a stage costs a
+    // wait, four MMAs and a commit — the issue loop, not the tensor core,
+    // paces small-N decode GEMMs.
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN);
+      const uint64_t da = sdesc_k128(smem_u32(smem)), db = sdesc_k128(smem_u32(smem) + kTileA);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % C::kStages;
+        mbar_wait(&full_bar[s], (i / C::kStages) & 1);
+        if (tr && (i == 0 || i == nkb - 1)) tr[i == 0 ? 2 : 3] = gtime();
+        tc_fence_after();
+        const uint64_t off = static_cast<uint64_t>((s * C::kStageBytes) >> 4);
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          tc_mma_bf16(tmem, sdesc_k128(sa + k * 32), sdesc_k128(sb + k * 32), idesc, (i > 0 || k > 0) ? 1u : 0u);
-        }
+        for (int k = 0; k < kBK / 16; ++k)
+          tc_mma_bf16(tmem, da + off + 2 * k, db + off + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
         tc_commit(&empty_bar[s]);
-        if (i == nkb - 1) tc_commit(&acc_bar);
       }
-      __syncwarp();
+      if (nkb > 0) tc_commit(&acc_bar);
     }
+    __syncwarp();
   }
   // Epilogue warps 2..9 -> TMEM lane quarters (warp % 4), two halves. Without
   // a cluster split, each reads its accumulator chunks from TMEM. With one
