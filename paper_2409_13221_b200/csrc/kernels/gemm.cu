@@ -104,7 +104,8 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
   if (a_rows <= 0 || b_rows <= 0) return;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         C::kSmem + EpiSmemExtra<Epi>::value);
     attr_set = true;
   }
   const CUtensorMap ma = make_map(A, a_rows, K, 128);
@@ -130,7 +131,7 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((a_rows + 127) / 128, (b_rows + BN - 1) / BN, z);
   cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.dynamicSmemBytes = C::kSmem + EpiSmemExtra<Epi>::value;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -221,7 +222,7 @@ struct Lean {
 template <int BN>
 struct Full {
   static constexpr int kStage = kTileA + BN * kBK * 2;
-  static constexpr int kFit = (216 * 1024) / kStage;
+  static constexpr int kFit = (216 * 1024 - BN * 64 * 8) / kStage;  // (room for EpiRopeKV's cos/sin cache)
   static constexpr int v = kFit > 12 ? 12 : kFit;
 };
 bool full_ring(long long ctas) {  // FUSEPLAN_DECODE_FULL: grids of at most this many CTAs take the Full ring

@@ -47,6 +47,17 @@ struct EpiHasPrologue : std::false_type {};
 template <class E>
 struct EpiHasPrologue<E, std::void_t<decltype(&E::prologue)>> : std::true_type {};
 
+// Dynamic shared memory an epilogue needs beyond the ring (Epi::kSmemExtra),
+// at offset kStages * kStageBytes; its prologue may fill it during the mainloop.
+template <class E, class = void>
+struct EpiSmemExtra {
+  static constexpr int value = 0;
+};
+template <class E>
+struct EpiSmemExtra<E, std::void_t<decltype(E::kSmemExtra)>> {
+  static constexpr int value = E::kSmemExtra;
+};
+
 template <class E, class = void>
 struct EpiStages {
   static constexpr int value = 0;
@@ -251,7 +262,7 @@ __global__ void __launch_bounds__(kGemmThreads, ST == 2 ? 2 : 1)  // the 2-stage
     pdl_wait();
     // epilogue inputs that do not depend on the accumulator (e.g. positions,
     // pages, rope tables) are fetched while the mainloop runs
-    if constexpr (EpiHasPrologue<Epi>::value) epi.prologue(st, a_row0, b_row0);
+    if constexpr (EpiHasPrologue<Epi>::value) epi.prologue(st, a_row0, b_row0, smem + C::kStages * C::kStageBytes);
     if (nkb > 0) {
       mbar_wait(&acc_bar, 0);
       if (tr && threadIdx.x == 64) tr[4] = gtime();
@@ -410,11 +421,17 @@ struct EpiRopeKV {
   static constexpr bool kTmaStore = false;
   static constexpr int kPasses = 1;
   template <class S> __device__ void next_pass(S&, int, int, int, int) const {}
+  // BN <= 64 (decode): the (cos, sin) of every column's position are fetched
+  // into shared memory by the prologue, under the mainloop, instead of by
+  // dependent loads after it — [column][pair index], hd / 2 <= 64 pairs.
+  static constexpr bool kCache = BN <= 64;
+  static constexpr int kSmemExtra = kCache ? BN * 64 * 8 : 0;
   struct State {
     uint8_t* smem;
     int pj, pagej;  // lane j: position and pool page of this warp's j-th column (prologue)
+    const float2* cs_s;
   };
-  __device__ void prologue(State& st, int, int b0) const {
+  __device__ void prologue(State& st, int, int b0, uint8_t* extra) const {
     const int ew = (threadIdx.x >> 5) - 2, lane = threadIdx.x & 31;
     const int nb = min(BN, M - b0);
     const int bl = ew + 8 * lane;
@@ -422,6 +439,26 @@ struct EpiRopeKV {
     if (bl < nb) {
       st.pj = pos[b0 + bl];
       if (use_pool) st.pagej = pool.block_table[slot[b0 + bl] * pool.bt_stride + st.pj / pool.page_tokens];
+    }
+    if constexpr (kCache) {
+      float2* cache = reinterpret_cast<float2*>(extra);
+      st.cs_s = cache;
+      const int hh = hd >> 1;
+      const int ncol = (nb - ew + 7) >> 3;
+      float2 c[BN / 8][2];
+#pragma unroll
+      for (int k = 0; k < BN / 8; ++k) {  // all loads in flight together
+        const int p = __shfl_sync(0xffffffffu, st.pj, k);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2)
+          if (k < ncol && lane + 32 * h2 < hh) c[k][h2] = __ldg(cs + p * hh + lane + 32 * h2);
+      }
+#pragma unroll
+      for (int k = 0; k < BN / 8; ++k)
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2)
+          if (k < ncol && lane + 32 * h2 < hh) cache[(ew + 8 * k) * 64 + lane + 32 * h2] = c[k][h2];
+      __syncwarp();  // each warp reads back only its own columns
     }
   }
   __device__ void operator()(State& st, uint8_t* smem, int, int, int, int r, int, int c0,
@@ -433,73 +470,82 @@ struct EpiRopeKV {
   }
   __device__ void finish(State& st, int a0, int b0, int, int, int) const {
     epi_bar_sync();
-    const __nv_bfloat16* tile = reinterpret_cast<const __nv_bfloat16*>(st.smem);
-    const int ew = (threadIdx.x >> 5) - 2;  // epilogue warp 0..7: columns ew, ew + 8, ...
+    const uint32_t tile_s = smem_u32(st.smem);  // staged tile [column][128] bf16 (shared-space accesses below)
+    const int ew = (threadIdx.x >> 5) - 2;      // epilogue warp 0..7: columns ew, ew + 8, ...
     const int lane = threadIdx.x & 31;
     const int hh = hd >> 1;
     const int nb = min(BN, M - b0);
-    __nv_bfloat16* pool_base = reinterpret_cast<__nv_bfloat16*>(pool.base);
     const int pj = st.pj, pagej = st.pagej;
     const int ncol = (nb - ew + 7) >> 3;  // columns of this warp
-    // per pair slot k2 (lane, lane + 32) the head / feature are column-independent
-    int fl2[2], i2[2], head2[2];
+    // (1) rotate the q / k pairs of this warp's columns in place; per pair
+    // slot k2 (lane, lane + 32) the feature is column-independent
+    int fl2[2], i2[2], rot2[2];
 #pragma unroll
     for (int k2 = 0; k2 < 2; ++k2) {
       const int pr = lane + 32 * k2;
       i2[k2] = pr % hh;
       fl2[k2] = (pr / hh) * hd + i2[k2];  // tile-local feature of the pair's low element
-      head2[k2] = (a0 + fl2[k2]) / hd;    // [0, H) q, [H, H + KVH) k, then v
+      rot2[k2] = (a0 + fl2[k2]) / hd < H + KVH;
     }
-    // eight columns at a time: their (cos, sin) loads are issued together
-    constexpr int kG = 4;  // (8 would cost registers: the 2-CTA shape needs <= 102 per thread)
+    constexpr int kG = 4;  // columns whose (cos, sin) and tile values are loaded together
     for (int k0 = 0; k0 < ncol; k0 += kG) {
       float2 c[kG][2];
-      int pk[kG], pgk[kG];
+      __nv_bfloat16 t1[kG][2], t2[kG][2];
 #pragma unroll
       for (int kk = 0; kk < kG; ++kk) {
         const int k = min(k0 + kk, ncol - 1);
-        pk[kk] = __shfl_sync(0xffffffffu, pj, k);
-        pgk[kk] = __shfl_sync(0xffffffffu, pagej, k);
+        const int p = __shfl_sync(0xffffffffu, pj, k);
 #pragma unroll
-        for (int k2 = 0; k2 < 2; ++k2)
-          c[kk][k2] = head2[k2] < H + KVH ? __ldg(cs + pk[kk] * hh + i2[k2]) : make_float2(1.f, 0.f);
+        for (int k2 = 0; k2 < 2; ++k2) {
+          if constexpr (kCache)
+            c[kk][k2] = lds_f2(smem_u32(st.cs_s) + ((ew + 8 * k) * 64 + i2[k2]) * 8);
+          else
+            c[kk][k2] = rot2[k2] ? __ldg(cs + p * hh + i2[k2]) : make_float2(1.f, 0.f);
+          const uint32_t ta = tile_s + ((ew + 8 * k) * 128 + fl2[k2]) * 2;
+          t1[kk][k2] = lds_bf16(ta);
+          t2[kk][k2] = lds_bf16(ta + hh * 2);
+        }
       }
 #pragma unroll
       for (int kk = 0; kk < kG; ++kk) {
         if (k0 + kk >= ncol) break;
         const int bl = ew + 8 * (k0 + kk);
-        const int b = b0 + bl;
-        const int p = pk[kk];
 #pragma unroll
-        for (int k2 = 0; k2 < 2; ++k2) {  // 64 pairs per column: lane, lane + 32
-          const int i = i2[k2], fl = fl2[k2], head = head2[k2];
-          __nv_bfloat16 o1 = tile[bl * 128 + fl], o2 = tile[bl * 128 + fl + hh];
-          if (head < H + KVH) {
-            float r1, r2;
-            rope_pair(__bfloat162float(o1), __bfloat162float(o2), c[kk][k2].x, c[kk][k2].y, r1, r2);
-            o1 = f2bf(r1);
-            o2 = f2bf(r2);
-          }
-          if (head < H) {
-            __nv_bfloat16* dst = q_out + (static_cast<size_t>(b) * H + head) * hd;
-            dst[i] = o1;
-            dst[i + hh] = o2;
-          } else {
-            const bool is_v = head >= H + KVH;
-            const int kh = head - H - (is_v ? KVH : 0);
-            if (use_pool) {
-              __nv_bfloat16* dst = pool_base + kv_elem_offset(pool, pgk[kk], layer, kh, hd, p % pool.page_tokens, is_v);
-              dst[i] = o1;
-              dst[i + hh] = o2;
-            }
-            __nv_bfloat16* packed = is_v ? v_out : k_out;
-            if (packed) {
-              __nv_bfloat16* dst = packed + (static_cast<size_t>(b) * KVH + kh) * hd;
-              dst[i] = o1;
-              dst[i + hh] = o2;
-            }
-          }
+        for (int k2 = 0; k2 < 2; ++k2) {
+          if (!rot2[k2]) continue;  // v: stored as computed
+          float r1, r2;
+          rope_pair(__bfloat162float(t1[kk][k2]), __bfloat162float(t2[kk][k2]), c[kk][k2].x, c[kk][k2].y, r1, r2);
+          const uint32_t ta = tile_s + (bl * 128 + fl2[k2]) * 2;
+          sts_bf16(ta, f2bf(r1));
+          sts_bf16(ta + hh * 2, f2bf(r2));
         }
+      }
+    }
+    __syncwarp();
+    // (2) 16-byte copies out: per column 16 chunks of 8 features, each inside
+    // one head — q rows are contiguous in q_out, k / v rows go to the token's
+    // pool page slot (and / or the packed buffers)
+    __nv_bfloat16* pool_base = reinterpret_cast<__nv_bfloat16*>(pool.base);
+    const size_t page_elems = pool.page_bytes / 2, layer_off = static_cast<size_t>(layer) * pool.layer_bytes / 2;
+    for (int it = 0; it * 2 < ncol; ++it) {
+      const int k = it * 2 + (lane >> 4);
+      const int kc = min(k, ncol - 1);
+      const int p = __shfl_sync(0xffffffffu, pj, kc), pg = __shfl_sync(0xffffffffu, pagej, kc);
+      if (k >= ncol) continue;
+      const int bl = ew + 8 * k, b = b0 + bl;
+      const int f = (lane & 15) * 8, feat = a0 + f, head = feat / hd, e = feat - head * hd;
+      const uint4 v = lds_v4(tile_s + (bl * 128 + f) * 2);
+      if (head < H) {
+        *reinterpret_cast<uint4*>(q_out + static_cast<size_t>(b) * H * hd + feat) = v;
+      } else {
+        const bool is_v = head >= H + KVH;
+        const int kh = head - H - (is_v ? KVH : 0);
+        if (use_pool)
+          *reinterpret_cast<uint4*>(pool_base + static_cast<size_t>(pg) * page_elems + layer_off +
+                                    (kh * 2 + (is_v ? 1 : 0)) * pool.page_tokens * hd +
+                                    (p % pool.page_tokens) * hd + e) = v;
+        __nv_bfloat16* packed = is_v ? v_out : k_out;
+        if (packed) *reinterpret_cast<uint4*>(packed + (static_cast<size_t>(b) * KVH + kh) * hd + e) = v;
       }
     }
   }
