@@ -387,12 +387,14 @@ struct EpiSwiGLU {
     const int t = r;
     const int f = t & 63, j0 = (t >> 6) * 16;
     if (c0 < BN) {
+      float gte[16], up[16];  // all loads first: the tile stores could alias them as far as the compiler knows
 #pragma unroll
-      for (int j = j0; j < j0 + 16; ++j) {
-        const float gte = xch[j * 128 + f];
-        const float up = xch[j * 128 + 64 + f];
-        tile[(c0 + j) * 64 + f] = f2bf(__fdividef(gte, 1.0f + __expf(-gte)) * up);
+      for (int j = 0; j < 16; ++j) {
+        gte[j] = xch[(j0 + j) * 128 + f];
+        up[j] = xch[(j0 + j) * 128 + 64 + f];
       }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) tile[(c0 + j0 + j) * 64 + f] = f2bf(__fdividef(gte[j], 1.0f + __expf(-gte[j])) * up[j]);
     }
     half_bar_sync(half);
   }
