@@ -331,8 +331,9 @@ struct EpiStoreBF16 {
   struct State {};
   __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int, int c0, const float (&v)[32]) const {
     __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);
+    const uint32_t t = smem_u32(tile) + (c0 * 128 + r) * 2;  // c0 < BN + 32: inside the staging area
 #pragma unroll
-    for (int j = 0; j < 32; ++j) tile[(c0 + j) * 128 + r] = f2bf(v[j]);  // c0 < BN + 32: inside the staging area
+    for (int j = 0; j < 32; ++j) sts_bf16(t + j * 256, f2bf(v[j]));
   }
   __device__ void finish(State&, int, int, int, int, int) const {}
   __device__ void store(const uint8_t* smem, int a0, int b0, int) const { tma_store_2d(&map, smem, a0, b0); }
@@ -351,8 +352,9 @@ struct EpiStoreF32 {
   struct State {};
   __device__ void operator()(State&, uint8_t* smem, int, int, int, int r, int, int c0, const float (&v)[32]) const {
     float* tile = reinterpret_cast<float*>(smem);
+    const uint32_t t = smem_u32(tile) + (c0 * 128 + r) * 4;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) tile[(c0 + j) * 128 + r] = v[j];
+    for (int j = 0; j < 32; ++j) sts_f32(t + j * 512, v[j]);
   }
   __device__ void finish(State&, int, int, int, int, int) const {}
   __device__ void store(const uint8_t* smem, int a0, int b0, int split) const {
@@ -381,8 +383,9 @@ struct EpiSwiGLU {
                              const float (&v)[32]) const {
     __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);                       // [BN][64]
     float* xch = reinterpret_cast<float*>(smem + kTileBytes) + half * 32 * 128;          // [32][128]
+    const uint32_t xa = smem_u32(xch) + r * 4;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) xch[j * 128 + r] = v[j];
+    for (int j = 0; j < 32; ++j) sts_f32(xa + j * 512, v[j]);
     half_bar_sync(half);
     const int t = r;
     const int f = t & 63, j0 = (t >> 6) * 16;
@@ -467,8 +470,9 @@ struct EpiRopeKV {
                              const float (&v)[32]) const {
     st.smem = smem;
     __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(smem);
+    const uint32_t t = smem_u32(tile) + (c0 * 128 + r) * 2;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) tile[(c0 + j) * 128 + r] = f2bf(v[j]);
+    for (int j = 0; j < 32; ++j) sts_bf16(t + j * 256, f2bf(v[j]));
   }
   __device__ void finish(State& st, int a0, int b0, int, int, int) const {
     epi_bar_sync();
