@@ -390,14 +390,15 @@ struct EpiSwiGLU {
     const int t = r;
     const int f = t & 63, j0 = (t >> 6) * 16;
     if (c0 < BN) {
-      float gte[16], up[16];  // all loads first: the tile stores could alias them as far as the compiler knows
+      float gte[16], up[16];  // all loads first, then the tile stores
+      const uint32_t xr = smem_u32(xch) + (j0 * 128 + f) * 4, tr = smem_u32(tile) + ((c0 + j0) * 64 + f) * 2;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        gte[j] = xch[(j0 + j) * 128 + f];
-        up[j] = xch[(j0 + j) * 128 + 64 + f];
+        gte[j] = lds_f32(xr + j * 512);
+        up[j] = lds_f32(xr + j * 512 + 256);
       }
 #pragma unroll
-      for (int j = 0; j < 16; ++j) tile[(c0 + j0 + j) * 64 + f] = f2bf(__fdividef(gte[j], 1.0f + __expf(-gte[j])) * up[j]);
+      for (int j = 0; j < 16; ++j) sts_bf16(tr + j * 128, f2bf(__fdividef(gte[j], 1.0f + __expf(-gte[j])) * up[j]));
     }
     half_bar_sync(half);
   }
