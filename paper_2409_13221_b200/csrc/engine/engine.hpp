@@ -202,6 +202,7 @@ class Engine {
   bool use_graphs_ = true;
   bool fuse_rope_ = true;  // prefill / scoring: RoPE + K/V writes in the QKV GEMM epilogue
   int decode_calls_ = 0;
+  bool fuse_norm_ = false;    // decode: add_norm fused into the split-K O / down GEMMs (FUSEPLAN_FUSE_NORM; measured slower)
   bool l2_prefetch_ = false;  // decode: pull each layer's weights into L2 ahead of its GEMMs (measured slower: off)
   int pad_slot_ = 0;
   struct GraphKey {
@@ -259,6 +260,7 @@ class Engine {
     int cap = 0;
     float *x = nullptr, *parts = nullptr, *attn_work = nullptr;
     int* attn_cnt = nullptr;  // split-merge tickets of the decode attention (B x KVH, kept zero)
+    int* norm_cnt = nullptr;  // grid counters of the split-K GEMMs' fused norm (2, kept zero)
     bf16 *h = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
     int* rows = nullptr;  // 7 x cap: slot, pos, ctx, dst, target, sid, step
     void* vocab_part = nullptr;

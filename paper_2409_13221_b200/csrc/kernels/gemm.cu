@@ -347,6 +347,54 @@ void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* o
   });
 }
 
+// CTAs of tc_gemm_kernel<BN, Epi, ST> the device holds at once (1 per SM for
+// the default rings, 2 for the lean / 2-stage ones).
+template <int BN, class Epi, int ST>
+int resident_limit() {
+  static int lim = -1;
+  if (lim < 0) {
+    using C = GemmCfg<BN, ST ? ST : EpiStages<Epi>::value>;
+    const int smem = C::kSmem + EpiSmemExtra<Epi>::value;
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_gemm_kernel<BN, Epi, ST>, kGemmThreads, smem);
+    lim = per * sms;
+  }
+  return lim;
+}
+
+bool gemm_f32_splitk_norm(const bf16* W, int N, int K, const bf16* X, int M, float* out, int splits,
+                          const NormFuse& nf, cudaStream_t st) {
+  if (N % 4 || N > 1024 || !nf.x || !nf.gain || !nf.y || !nf.counters) return false;
+  const int kb = K / kBK;
+  splits = std::max(1, std::min(splits, kb));
+  const int per = (kb + splits - 1) / splits;
+  const int z = (kb + per - 1) / per;
+  if (z > 8) return false;
+  bool done = false;
+  dispatch_bn<EpiStoreF32>(M, (N + 127) / 128 * z, [&]<int BN>() {
+    const uint64_t dims[3] = {static_cast<uint64_t>(N), static_cast<uint64_t>(M), static_cast<uint64_t>(z)};
+    const uint64_t str[2] = {static_cast<uint64_t>(N) * 4, static_cast<uint64_t>(M) * N * 4};
+    const uint32_t box[3] = {128u, static_cast<uint32_t>(BN), 1u};
+    EpiStoreF32 e{encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE), 0};
+    e.nf = nf;
+    e.parts = out;
+    e.M = M, e.d = N, e.ns = z;
+    e.total = (N + 127) / 128 * z * ((M + BN - 1) / BN);
+    if (BN <= 128 && lean(M)) {
+      if (e.total > resident_limit<BN, EpiStoreF32, Lean<BN>::v>()) return;
+      launch<BN, EpiStoreF32, Lean<BN>::v>(W, N, X, M, K, splits, e, st);
+    } else {
+      if (e.total > resident_limit<BN, EpiStoreF32, 0>()) return;
+      launch<BN>(W, N, X, M, K, splits, e, st);
+    }
+    done = true;
+  });
+  return done;
+}
+
 void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float* resid, cudaStream_t st) {
   if (N % 4) throw std::invalid_argument("gemm_f32: N must be a multiple of 4");
   dispatch_bn<EpiStoreF32>(M, (N + 127) / 128, [&]<int BN>() {

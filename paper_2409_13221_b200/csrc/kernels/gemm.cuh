@@ -18,6 +18,7 @@
 
 #include <type_traits>
 
+#include "norm.cuh"
 #include "ops.h"
 #include "ptx.cuh"
 
@@ -57,6 +58,11 @@ template <class E>
 struct EpiSmemExtra<E, std::void_t<decltype(E::kSmemExtra)>> {
   static constexpr int value = E::kSmemExtra;
 };
+
+template <class E, class = void>
+struct EpiHasPost : std::false_type {};
+template <class E>
+struct EpiHasPost<E, std::void_t<decltype(&E::post)>> : std::true_type {};
 
 template <class E, class = void>
 struct EpiStages {
@@ -281,6 +287,7 @@ __global__ void __launch_bounds__(kGemmThreads, ST == 2 ? 2 : 1)  // the 2-stage
     } else {
       run_epi(tmem_load);
       if (tr && threadIdx.x == 64) tr[5] = gtime();
+      if constexpr (EpiHasPost<Epi>::value) epi.post();
     }
   }
   if constexpr (kClusterOK) {
@@ -346,6 +353,63 @@ struct EpiStoreBF16 {
 struct EpiStoreF32 {
   CUtensorMap map;
   int accumulate;
+  // fused add_norm over the partials (x == nullptr: off); M, d = rows, N
+  NormFuse nf{};
+  const float* parts = nullptr;
+  int M = 0, d = 0, ns = 0, total = 0;
+  // After this CTA's partial is in global memory (thread 64 waited for its
+  // bulk store): arrive on counters[0], wait for every CTA of the grid (all
+  // are resident — the host checks), then normalise rows cta, cta + total, ...
+  // with the first 32 * ceil(d / 128) epilogue threads, as add_norm_kernel.
+  __device__ void post() const {
+    if (!nf.x) return;
+    const int t = static_cast<int>(threadIdx.x) - 64;
+    if (t == 0) {
+      asm volatile("fence.proxy.async;" ::: "memory");
+      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(nf.counters) : "memory");
+      int seen = 0;
+      do {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(nf.counters) : "memory");
+      } while (seen < total);
+    }
+    epi_bar_sync();
+    __shared__ float red[8];
+    const int d4 = d >> 2, nthr = ((d4 + 31) / 32) * 32;
+    const int cta = static_cast<int>(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
+    if (t < nthr) {
+      const int w = t >> 5, l = t & 31, j = t;
+      const bool on = j < d4;
+      const size_t ps4 = static_cast<size_t>(M) * d / 4;
+      for (int row = cta; row < M; row += total) {
+        float4* xr = reinterpret_cast<float4*>(nf.x + static_cast<size_t>(row) * d);
+        const float4* pr = reinterpret_cast<const float4*>(parts + static_cast<size_t>(row) * d);
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (on) {
+          v = xr[j];
+          float4 p[8];
+#pragma unroll
+          for (int s = 0; s < 8; ++s)
+            if (s < ns) p[s] = __ldcg(pr + s * ps4 + j);  // written by other CTAs of this grid: L2
+#pragma unroll
+          for (int s = 0; s < 8; ++s)
+            if (s < ns) v.x += p[s].x, v.y += p[s].y, v.z += p[s].z, v.w += p[s].w;
+          xr[j] = v;
+        }
+        const float ss = group_sum(sumsq4(v), red, w, l, nthr >> 5,
+                                   [&] { asm volatile("bar.sync 3, %0;" ::"r"(nthr) : "memory"); });
+        const float inv = rsqrtf(ss / d + kNormEps);
+        float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (on) {
+          g = reinterpret_cast<const float4*>(nf.gain)[j];
+          reinterpret_cast<uint2*>(nf.y + static_cast<size_t>(row) * d)[j] = norm_scale4(v, inv, g);
+        }
+      }
+    }
+    if (t == 0 && atomicAdd(nf.counters + 1, 1) == total - 1) {  // last out: reset for the next launch
+      atomicExch(nf.counters, 0);
+      atomicExch(nf.counters + 1, 0);
+    }
+  }
   static constexpr bool kTmaStore = true;
   static constexpr int kPasses = 1;
   template <class S> __device__ void next_pass(S&, int, int, int, int) const {}

@@ -10,6 +10,7 @@
 #include "ops.h"
 #include "philox.cuh"
 #include "ptx.cuh"
+#include "norm.cuh"
 
 namespace fpk {
 
@@ -85,15 +86,7 @@ __global__ void embed_kernel(const int* __restrict__ tok, const int* __restrict_
 }
 
 __device__ float block_sum(float v, float* red) {
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) red[w] = v;
-  __syncthreads();
-  const int nw = blockDim.x >> 5;
-  float t = (l < nw) ? red[l] : 0.f;
-  t = warp_sum(t);
-  __syncthreads();
-  return t;
+  return group_sum(v, red, threadIdx.x >> 5, threadIdx.x & 31, blockDim.x >> 5, [] { __syncthreads(); });
 }
 
 // One block per output row, one float4 of the row per thread (blockDim =
@@ -132,9 +125,9 @@ __global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__
     for (int s = 0; s < NS; ++s) v.x += p[s].x, v.y += p[s].y, v.z += p[s].z, v.w += p[s].w;
     if (!gather && NS > 0) xr[j] = v;
   }
-  float ss = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  float ss = sumsq4(v);
   ss = block_sum(ss, red);
-  const float inv = rsqrtf(ss / d + kEps);
+  const float inv = rsqrtf(ss / d + kNormEps);
   float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
   if (on) g = reinterpret_cast<const float4*>(gain)[j];
   if (value_w) {
@@ -151,7 +144,7 @@ __global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__
   }
   if (on) {
     uint2* yr = reinterpret_cast<uint2*>(y + static_cast<size_t>(i) * d);
-    yr[j] = make_uint2(pack_bf16x2(v.x * inv * g.x, v.y * inv * g.y), pack_bf16x2(v.z * inv * g.z, v.w * inv * g.w));
+    yr[j] = norm_scale4(v, inv, g);
   }
 }
 
