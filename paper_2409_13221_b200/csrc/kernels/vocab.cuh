@@ -111,10 +111,13 @@ struct EpiVocab {
     const float c2 = inv_temp * kLog2E;
     if (st.pass == 1) {  // sampling walk: first column whose running mass reaches thr
       if (st.acc >= st.thr) return;
+      float e[32];  // the chunk's masses first (independent MUFU work), then the serial walk over them
+#pragma unroll
+      for (int j = 0; j < 32; ++j) e[j] = exp2f(v[j] * c2 - st.m);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         if (j < nvalid && st.acc < st.thr) {
-          st.acc += exp2f(v[j] * c2 - st.m);
+          st.acc += e[j];
           st.idx = base + j;
           st.zsel = v[j] * inv_temp;
         }

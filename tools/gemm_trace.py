@@ -3,6 +3,7 @@
     python tools/gemm_trace.py            # decode-shaped cases of every epilogue
 """
 import ctypes as C
+import os
 import sys
 
 import numpy as np
@@ -46,7 +47,10 @@ def case(kind, M, N, K):
         stp = torch.zeros(M, device="cuda", dtype=torch.int32)
         tok = torch.empty(M, device="cuda", dtype=torch.int32)
         lp = torch.empty(M, device="cuda")
-        f = lambda: lib.fp_k_vocab(p(X), M, K, p(W), N, 2, 1.0, None, p(sid), p(stp), 7, p(tok), p(lp), None)  # noqa
+        mode = int(os.environ.get("FP_VOCAB_MODE", "2"))  # 0 forced, 1 greedy, 2 sample
+        tgt = torch.zeros(M, device="cuda", dtype=torch.int32)
+        f = lambda: lib.fp_k_vocab(p(X), M, K, p(W), N, mode, 1.0, p(tgt) if mode == 0 else None, p(sid), p(stp), 7,  # noqa
+                                   p(tok), p(lp), None)
     for _ in range(3):
         flush.zero_()
         tr.zero_()
@@ -71,5 +75,7 @@ cases = (("qkvrope", 50, 2304, 768), ("qkvrope", 284, 2304, 768), ("bf16", 284, 
          ("f32", 8, 768, 768), ("f32", 128, 768, 768), ("f32", 8, 768, 3072), ("f32", 128, 768, 3072),
          ("vocab", 8, 50257, 768), ("vocab", 128, 50257, 768), ("vocab", 350, 50257, 768),
          ("bf16", 4096, 6144, 768), ("bf16", 16384, 2304, 768))
+only = os.environ.get("FP_TRACE_ONLY")  # e.g. "vocab": run just those cases
 for kind, M, N, K in cases:
-    case(kind, M, N, K)
+    if not only or kind == only:
+        case(kind, M, N, K)
