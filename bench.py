@@ -12,6 +12,8 @@ per-token KL / reward / GAE / returns — through the C ABI (fp_execute).
 N = 1: BASELINE.json configs[1] (GPT-2-small shape, 512 prompts x 128 tokens,
 <= 1024 new). N > 1: weak scaling, 512 prompts per GPU, fused schedule with
 the one-shot long-tail migration at r_t = 20% of the batch.
+--workload 1.3b: configs[2] shapes (all four models 1.3B), 256 prompts per GPU
+(2048 at 8 GPUs), same schedule.
 
 `value`  — samples/s with prompts resident and the experience left in HBM;
 `e2e`    — the same through host buffers (prompt upload and experience
@@ -104,10 +106,22 @@ def dist_setup():
     return world, rank, local, pg
 
 
-def workload_for(n_gpus):
+# prompts per GPU (weak scaling). gpt2s: configs[1] (512 prompts on one B200).
+# 1.3b: configs[2] (2048 prompts at 8 GPUs = 256 per GPU; all four models 1.3B).
+PER_GPU = {"gpt2s": 512, "1.3b": 256}
+DESC = {"gpt2s": "GPT-2-small-shape", "1.3b": "1.3B-shape (Llama-style)"}
+
+
+def workload_for(n_gpus, name="gpt2s"):
     from paper_2409_13221_b200.configs import WORKLOADS, scaled
-    w = WORKLOADS["gpt2s"]
-    return scaled(w, n_prompts=w.n_prompts * n_gpus)
+    w = WORKLOADS[name]
+    return scaled(w, n_prompts=PER_GPU[name] * n_gpus)
+
+
+def workload_desc(w, G):
+    a = w.actor
+    return (f"{DESC[w.name]} actor/ref/critic/reward (L{a.num_layers} d{a.hidden} H{a.num_heads} ffn{a.ffn} "
+            f"V{a.vocab}), {w.n_prompts // G} prompts x {w.prompt_len} tokens per GPU, <= {w.max_new} new")
 
 
 def cpu_oracle_rate(w, batch, n_samples: int, time_budget: float = 30.0):
@@ -139,7 +153,7 @@ def run_reference(args, world, rank):
         return
     from paper_2409_13221_b200.configs import batch_for, gen_config
     from paper_2409_13221_b200.sched import Sched
-    w = workload_for(args.gpus)
+    w = workload_for(args.gpus, args.workload)
     sched = Sched()
     batch = batch_for(w, sched)
     cores = os.cpu_count() or 1
@@ -186,6 +200,8 @@ def main():
     ap.add_argument("--claim-tokens", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-barrier-arm", action="store_true")
+    ap.add_argument("--workload", default="gpt2s", choices=sorted(PER_GPU),
+                    help="gpt2s = BASELINE configs[1] (the default bench line); 1.3b = configs[2] shapes")
     ap.add_argument("--quick", action="store_true", help="value pass only (for profiling)")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup()
@@ -201,7 +217,7 @@ def main():
     from paper_2409_13221_b200.engine import Engine
 
     G = world
-    w = workload_for(G)
+    w = workload_for(G, args.workload)
     eng = Engine(w, device=local, max_samples=w.n_prompts, max_live=min(w.n_prompts, 2 * w.n_prompts // G))
     batch = batch_for(w, eng.sched)
     cfg = gen_config(w, G, calibrated=True)  # decision-clock constants fitted to measured B200 steps
@@ -279,13 +295,14 @@ def main():
     probe_n = sum(o.stats["attn_probe_launches"] for o in outs_p)
 
     e2e = sb = None
+    outs_s = None
     h2d = len(batch) * w.prompt_len * 4 + len(batch) * 4 * 6
     d2h = int(st["total_resp"]) * 4 * 8 + len(batch) * 4
     if not args.quick:
         ms_e, outs_e = timed("fused", False, args.steps)
         e2e = n_total * args.steps / (ms_e / 1000.0)
         if not args.no_barrier_arm:
-            ms_s, _ = timed("stage_barrier", True, args.steps)
+            ms_s, outs_s = timed("stage_barrier", True, args.steps)
             sb = n_total * args.steps / (ms_s / 1000.0)
 
     cpu = None
@@ -308,6 +325,27 @@ def main():
                        "frac": dec_b / dec_s / 1e9 / hbm if dec_s else None,
                        "note": "decode_steps x actor weight bytes + sum over rows and steps of ctx x K/V bytes per "
                                "token, / sum of decode-step GPU time (rank 0)"}
+    # scoring (Ref/Critic/Reward forward over prompt + response) against the
+    # bf16 tensor peak: algorithmic flops = 2 x dense weights per token (ref
+    # adds the vocab head for its log-probs) + causal attention 2 T^2 H hd L,
+    # over the scoring stream's busy GPU time (stage-barrier arm when run, so
+    # decode does not share the SMs)
+    def fwd_flops(d, T, vocab_head):
+        dense = d.param_count(lm_head=False) - d.vocab * d.hidden
+        return 2 * T * (dense + (d.hidden * d.vocab if vocab_head else d.hidden)) + \
+            2 * T * T * d.num_heads * d.head_dim * d.num_layers
+    src_outs, src_name = (outs_s, "stage_barrier") if outs_s else (outs_v, "fused (overlaps decode)")
+    inf_flops = sum(fwd_flops(w.ref, s.prompt_len + s.target_output_len, True) +
+                    fwd_flops(w.critic, s.prompt_len + s.target_output_len, False) +
+                    fwd_flops(w.reward, s.prompt_len + s.target_output_len, False) for s in batch if s.id % G == 0)
+    inf_s = statistics.mean(o.stats["infer_busy_seconds"] for o in src_outs)
+    inf_tf = inf_flops / inf_s / 1e12 if inf_s else None
+    inference_roofline = {"bound": "tensor", "achieved": inf_tf, "peak": tflops, "unit": "TFLOP/s",
+                          "frac": inf_tf / tflops if inf_tf else None, "flops_per_step": inf_flops,
+                          "seconds_per_step": inf_s, "arm": src_name,
+                          "note": "ref/critic/reward forward over rank 0's samples (prompt + target response): "
+                                  "2 x dense weights per token (+ vocab head for ref) + causal attention "
+                                  "2 T^2 H hd L; / the scoring stream's busy GPU time"}
     achieved = (probe_bytes / (probe_ms / 1000.0)) / 1e9 if probe_ms > 0 else None
     # traffic: DRAM bytes per launch from the committed ncu --set full capture
     # of this kernel (profiles/attn_decode_traffic.json), as its DRAM /
@@ -322,10 +360,10 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_v / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic: hash-seeded random-init weights and prompts, Zipf(s=1.0) output lengths on [16, 1024], "
+        "data": "synthetic: hash-seeded random-init weights and prompts, "
+                f"Zipf(s={w.zipf_s}) output lengths on [{w.zipf_lo}, {w.max_new}], "
                 f"{args.token_mode} tokens",
-        "config": {"workload": "GPT-2-small-shape actor/ref/critic/reward (L12 d768 H12 ffn3072 V50257), "
-                               f"{w.n_prompts // G} prompts x {w.prompt_len} tokens per GPU, <= {w.max_new} new",
+        "config": {"workload": workload_desc(w, G),
                    "prompts": n_total, "schedule": "fused", "r_t": r_t, "r_ratio": ratio if G > 1 else 0.0, "token_mode": args.token_mode,
                    "claim_tokens": args.claim_tokens,
                    "l2": "inputs larger than L2 (KV pool and weights >> 126 MB)",
@@ -338,6 +376,7 @@ def main():
         # the whole decode step against HBM — weights once per step
         # plus K/V of every visible token, over the decode GPU time of the value steps
         "decode_roofline": decode_roofline,
+        "inference_roofline": inference_roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "stage_barrier": {"value": sb, "unit": UNIT, "speedup_fused": (value / sb) if sb else None},
