@@ -23,8 +23,11 @@ from pathlib import Path
 import numpy as np
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
-from paper_2409_13221_b200.configs import WORKLOADS, batch_for, gen_config  # noqa: E402
+from paper_2409_13221_b200.configs import WORKLOADS, batch_for, gen_config, scaled  # noqa: E402
 from paper_2409_13221_b200.engine import Engine  # noqa: E402
+
+
+PER_GPU = {"1.3b": 256}  # bench.py --workload 1.3b: 256 prompts per GPU
 
 
 def per_layer_params(d):  # core.cpp:56-60 (the reference's count; SwiGLU's third matrix is in the coefficient)
@@ -50,6 +53,8 @@ def main():
     wname = sys.argv[1] if len(sys.argv) > 1 else "gpt2s"
     out_path = Path(sys.argv[2]) if len(sys.argv) > 2 else None
     w = WORKLOADS[wname]
+    if wname in PER_GPU:  # the bench's per-GPU batch (the full 1.3b batch needs a KV pool beyond one GPU)
+        w = scaled(w, n_prompts=PER_GPU[wname])
     eng = Engine(w)
     batch = batch_for(w, eng.sched)
     cfg0 = gen_config(w, 1)

@@ -1,4 +1,8 @@
-"""Microbenchmark of the tcgen05 GEMM launchers (CUDA events, warm, L2 flushed between reps)."""
+"""Microbenchmark of the tcgen05 GEMM launchers (CUDA events, warm, L2 flushed between reps).
+
+    python tools/gemm_bench.py                 # the decode / prefill shape table
+    python tools/gemm_bench.py KIND M N K      # one shape (for an ncu capture)
+"""
 import ctypes as C
 import sys
 
@@ -46,6 +50,9 @@ def run(kind, M, N, K):
           flush=True)
 
 
+if len(sys.argv) == 5:
+    run(sys.argv[1], *map(int, sys.argv[2:]))
+    sys.exit(0)
 for kind, N, K in (("bf16", 2304, 768), ("swiglu", 6144, 768), ("f32", 768, 3072), ("f32", 768, 768),
                    ("bf16", 6144, 768), ("bf16", 12288, 4096)):
     for M in (16, 64, 128, 256, 512):
