@@ -112,10 +112,11 @@ PER_GPU = {"gpt2s": 512, "1.3b": 256}
 DESC = {"gpt2s": "GPT-2-small-shape", "1.3b": "1.3B-shape (Llama-style)"}
 
 
-def workload_for(n_gpus, name="gpt2s"):
+def workload_for(n_gpus, name="gpt2s", zipf_s=None):
     from paper_2409_13221_b200.configs import WORKLOADS, scaled
     w = WORKLOADS[name]
-    return scaled(w, n_prompts=PER_GPU[name] * n_gpus)
+    w = scaled(w, n_prompts=PER_GPU[name] * n_gpus)
+    return w if zipf_s is None else scaled(w, zipf_s=zipf_s)
 
 
 def workload_desc(w, G):
@@ -153,7 +154,7 @@ def run_reference(args, world, rank):
         return
     from paper_2409_13221_b200.configs import batch_for, gen_config
     from paper_2409_13221_b200.sched import Sched
-    w = workload_for(args.gpus, args.workload)
+    w = workload_for(args.gpus, args.workload, args.zipf_s)
     sched = Sched()
     batch = batch_for(w, sched)
     cores = os.cpu_count() or 1
@@ -202,6 +203,9 @@ def main():
     ap.add_argument("--no-barrier-arm", action="store_true")
     ap.add_argument("--workload", default="gpt2s", choices=sorted(PER_GPU),
                     help="gpt2s = BASELINE configs[1] (the default bench line); 1.3b = configs[2] shapes")
+    ap.add_argument("--zipf-s", type=float, default=None,
+                    help="output-length skew (configs[4] sweep): 0 = uniform on [16, max_new]; default = the "
+                         "workload's (1.0)")
     ap.add_argument("--quick", action="store_true", help="value pass only (for profiling)")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup()
@@ -217,7 +221,7 @@ def main():
     from paper_2409_13221_b200.engine import Engine
 
     G = world
-    w = workload_for(G, args.workload)
+    w = workload_for(G, args.workload, args.zipf_s)
     eng = Engine(w, device=local, max_samples=w.n_prompts, max_live=min(w.n_prompts, 2 * w.n_prompts // G))
     batch = batch_for(w, eng.sched)
     cfg = gen_config(w, G, calibrated=True)  # decision-clock constants fitted to measured B200 steps
@@ -364,7 +368,7 @@ def main():
                 f"Zipf(s={w.zipf_s}) output lengths on [{w.zipf_lo}, {w.max_new}], "
                 f"{args.token_mode} tokens",
         "config": {"workload": workload_desc(w, G),
-                   "prompts": n_total, "schedule": "fused", "r_t": r_t, "r_ratio": ratio if G > 1 else 0.0, "token_mode": args.token_mode,
+                   "prompts": n_total, "zipf_s": w.zipf_s, "schedule": "fused", "r_t": r_t, "r_ratio": ratio if G > 1 else 0.0, "token_mode": args.token_mode,
                    "claim_tokens": args.claim_tokens,
                    "l2": "inputs larger than L2 (KV pool and weights >> 126 MB)",
                    "parallelism": f"dp{G} (one engine per B200)"},
