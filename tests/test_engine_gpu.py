@@ -209,3 +209,49 @@ def test_fused_norm_decode_bit_identical(small64):
         eng2.close()
     for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret", "score"):
         assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
+
+
+@pytest.fixture(scope="module")
+def gqa128():
+    """hd 128 with GQA (4 query heads per KV head): the head shape of configs[2] (1.3B,
+    hd 128) and configs[3] (Llama-3-8B, GQA 32/8, hd 128) on a 2-layer model the oracle
+    finishes in seconds."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from model_oracle import Oracle
+    from paper_2409_13221_b200.configs import Dims, Workload, batch_for
+    from paper_2409_13221_b200.engine import Engine
+    d = Dims(2, 512, 4, 1, 128, 1024, 4096)
+    w = Workload("gqa128", d, d, d, d, 96, 40, 640, zipf_s=0.5)
+    eng = Engine(w, device=0)
+    batch = batch_for(w, eng.sched)
+    yield w, eng, batch, Oracle(w)
+    eng.close()
+
+
+def test_hd128_gqa_forced_experience_matches_oracle(gqa128):
+    from paper_2409_13221_b200.configs import gen_config
+    from model_oracle import forced_response
+    w, eng, batch, orc = gqa128
+    out = eng.execute(batch, gen_config(w, 1), 0, token_mode="forced", schedule="fused", claim_tokens=4096)
+    prompts = eng.synthetic_prompts(w.n_prompts, 7)
+    longest = sorted(range(len(batch)), key=lambda i: -batch[i].target_output_len)[:2]
+    for i in sorted(set(longest + list(range(0, len(batch), 19)))):
+        s = batch[i]
+        got = out.experience.sample(i)
+        want_tokens = forced_response(i, s.target_output_len, w.max_new, w.actor.vocab, 7)
+        assert np.array_equal(got["tokens"], want_tokens)
+        ref = orc.experience(prompts[i, :s.prompt_len], want_tokens, 0.05, 1.0, 0.95)
+        for k, (mx, mean) in _cmp(got, ref).items():
+            scale = max(1.0, float(np.max(np.abs(ref[k]))))
+            assert mx <= TOL_MAX * scale and mean <= TOL_MEAN * scale, (i, k, mx, mean)
+
+
+def test_hd128_gqa_schedules_identical(gqa128):
+    from paper_2409_13221_b200.configs import gen_config
+    w, eng, batch, _ = gqa128
+    a = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="fused", claim_tokens=4096)
+    b = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="stage_barrier")
+    for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret", "score"):
+        assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
