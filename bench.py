@@ -108,8 +108,10 @@ def dist_setup():
 
 # prompts per GPU (weak scaling). gpt2s: configs[1] (512 prompts on one B200).
 # 1.3b: configs[2] (2048 prompts at 8 GPUs = 256 per GPU; all four models 1.3B).
-PER_GPU = {"gpt2s": 512, "1.3b": 256}
-DESC = {"gpt2s": "GPT-2-small-shape", "1.3b": "1.3B-shape (Llama-style)"}
+# 8b: configs[3] shapes (Llama-3-8B GQA 32/8 actor + 8B ref/critic/reward) at a
+# REDUCED batch, 64 prompts per GPU: the config's 4096 prompts need 8 GPUs.
+PER_GPU = {"gpt2s": 512, "1.3b": 256, "8b": 64}
+DESC = {"gpt2s": "GPT-2-small-shape", "1.3b": "1.3B-shape (Llama-style)", "8b": "Llama-3-8B-shape (GQA 32/8)"}
 
 
 def workload_for(n_gpus, name="gpt2s", zipf_s=None):
@@ -202,7 +204,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-barrier-arm", action="store_true")
     ap.add_argument("--workload", default="gpt2s", choices=sorted(PER_GPU),
-                    help="gpt2s = BASELINE configs[1] (the default bench line); 1.3b = configs[2] shapes")
+                    help="gpt2s = BASELINE configs[1] (the default bench line); 1.3b = configs[2] shapes; "
+                         "8b = configs[3] shapes at a reduced batch (64 prompts per GPU)")
     ap.add_argument("--zipf-s", type=float, default=None,
                     help="output-length skew (configs[4] sweep): 0 = uniform on [16, max_new]; default = the "
                          "workload's (1.0)")
