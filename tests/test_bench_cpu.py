@@ -30,3 +30,13 @@ def test_13b_workload_is_configs2_at_8_gpus():
     for d in (w.actor, w.ref, w.critic, w.reward):
         assert (d.num_layers, d.hidden, d.num_heads, d.ffn, d.vocab) == (24, 2048, 16, 5632, 32000)
     assert "L24 d2048" in b.workload_desc(w, 8)
+
+
+def test_8b_workload_shapes():
+    b = _bench()
+    w = b.workload_for(4, "8b")
+    assert w.n_prompts == 256 and w.max_new == 4096
+    a = w.actor
+    assert (a.num_layers, a.hidden, a.num_heads, a.num_kv_heads, a.head_dim, a.ffn, a.vocab) == \
+        (32, 4096, 32, 8, 128, 14336, 128256)
+    assert b.workload_for(2, "gpt2s", 0.0).zipf_s == 0.0
