@@ -27,7 +27,7 @@ from paper_2409_13221_b200.configs import WORKLOADS, batch_for, gen_config, scal
 from paper_2409_13221_b200.engine import Engine  # noqa: E402
 
 
-PER_GPU = {"1.3b": 256}  # bench.py --workload 1.3b: 256 prompts per GPU
+PER_GPU = {"1.3b": 256, "8b": 64}  # bench.py --workload: prompts per GPU
 
 
 def per_layer_params(d):  # core.cpp:56-60 (the reference's count; SwiGLU's third matrix is in the coefficient)
