@@ -58,6 +58,17 @@ typedef struct fp_run_options {
   int32_t probe_attention; /* 1: time each decode-attention launch (stats.attn_probe_*) */
   int32_t handoff_dp;      /* > 0: pack the experience into length-balanced DP mini-batches (fp_exec_handoff) */
   int32_t claim_max_live;  /* > 0: a generating rank scores only while its decode batch <= this */
+  /* Free-run (north_star "retires each sample as it emits EOS"): eos_id >= 0
+   * retires a sample at its first emitted eos_id (kept as the last response
+   * token) or at max_new; greedy / sample modes; the fused trigger is then
+   * online. eos_lag: steps between a decode step and the host reading its ids. */
+  int32_t eos_id, eos_lag;
+  /* 1: online fused trigger on world > 1 (fewer than r_t unfinished samples
+   * batch-wide; plan_migration on the ranks' live state). 0: decision clock. */
+  int32_t online_trigger;
+  /* Filtered sampling (FP_TOKENS_SAMPLE): top_k in [0, 1024] (0 off), top_p in (0, 1] (1 off). */
+  int32_t top_k;
+  float top_p;
 } fp_run_options;
 
 typedef struct fp_comm {
@@ -74,6 +85,8 @@ typedef struct fp_exec_stats {
   double attn_probe_ms, attn_probe_bytes;
   int64_t attn_probe_launches;
   double ipc_seconds;
+  int64_t eos_retired, overrun_rows; /* free-run: EOS retirements; row-steps decoded past an unseen EOS */
+  int32_t online;                    /* 1: the trigger was taken online */
 } fp_exec_stats;
 
 typedef struct fp_engine fp_engine;
@@ -96,6 +109,23 @@ int fp_engine_broadcast_model(fp_engine* e, int32_t model, int32_t src, const fp
 /* Device pointer and size of a model's weight blob (engine layout), e.g. for a
  * trainer writing updated weights in place before fp_engine_broadcast_model. */
 int fp_engine_model_ptr(const fp_engine* e, int32_t model, void** dev_ptr, int64_t* bytes);
+/* Weight loading (the models InferenceTask / GenSimConfig::actor name,
+ * genfuse.hpp:45-57): copy one standard row-major host tensor into the
+ * engine's layout (repacked on the way: the gate / up rows are interleaved in
+ * 64-row groups for the SwiGLU epilogue). model: 0 actor, 1 ref, 2 critic,
+ * 3 reward; layer: 0 for the per-model tensors. Shapes (d hidden, F ffn,
+ * V vocab, H/KVH heads, hd head_dim), dtype bf16 unless noted:
+ *   FP_W_EMBED [V][d]; FP_W_QKV [(H + 2 KVH) hd][d] (q heads, then k, then v);
+ *   FP_W_O [d][H hd]; FP_W_GATE, FP_W_UP [F][d]; FP_W_DOWN [d][F];
+ *   FP_W_ATTN_NORM, FP_W_MLP_NORM, FP_W_FINAL_NORM [d] fp32 gains;
+ *   FP_W_HEAD [V][d] (actor / ref); FP_W_VALUE_HEAD [d] (critic / reward).
+ * n_elems must equal the tensor's size. Synchronous. */
+enum {
+  FP_W_EMBED = 0, FP_W_QKV = 1, FP_W_O = 2, FP_W_GATE = 3, FP_W_UP = 4, FP_W_DOWN = 5, FP_W_ATTN_NORM = 6,
+  FP_W_MLP_NORM = 7, FP_W_FINAL_NORM = 8, FP_W_HEAD = 9, FP_W_VALUE_HEAD = 10
+};
+int fp_engine_load_weights(fp_engine* e, int32_t model, int32_t tensor, int32_t layer, const void* host,
+                           int64_t n_elems);
 /* Tooling: regenerate a model's synthetic weights from `seed`; order-independent
  * 64-bit checksum of its blob. */
 int fp_engine_reinit_model(fp_engine* e, int32_t model, uint64_t seed);
@@ -114,6 +144,14 @@ int fp_exec_finish(const fp_exec* x, double* finish_seconds, int32_t* finish_ins
 int fp_exec_decision(const fp_exec* x, fp_result** out);
 /* Trigger / plan actually executed (fused, world > 1); moves in application order. */
 int fp_exec_moves(const fp_exec* x, int32_t* n_moves, int32_t* sample, int32_t* from, int32_t* to);
+/* Samples this rank received at the migration, (sample, source rank) in
+ * application order — what the executor actually pulled (in flight: KV
+ * pages or recompute; queued: re-queued). */
+int fp_exec_received(const fp_exec* x, int32_t* n, int32_t* sample, int32_t* from);
+/* Trigger state the executed plan was taken on (GenState, genfuse.hpp:67-79):
+ * time, and per unfinished sample id / instance / kv_bytes / generated /
+ * prompt_len / admitted (fp_remaining of fp_sched.h); NULL to query the count. */
+int fp_exec_trigger_state(const fp_exec* x, double* time, int32_t* n, fp_remaining* samples);
 /* Experience hand-off (handoff_dp > 0; balance_minibatch, workflow.hpp:63-66):
  * order[n], group_off[dp+1], packed_off[n+1] (response-token offsets in
  * order); this rank's groups [*group_begin, *group_end) and device pointers
@@ -142,6 +180,9 @@ int fp_k_gemm_splits(int32_t N, int32_t K);
 /* Debug: record 8 globaltimer stamps per CTA of subsequent GEMMs into buf (device, NULL disables). */
 int fp_k_gemm_trace(void* buf);
 int fp_k_gemm_swiglu(const void* Wgu, int32_t F, int32_t K, const void* X, int32_t M, void* out, void* stream);
+/* The decode-step SwiGLU GEMM (lean rings, cluster split-K over K for small M). */
+int fp_k_gemm_swiglu_decode(const void* Wgu, int32_t F, int32_t K, const void* X, int32_t M, void* out,
+                            void* stream);
 /* Decode QKV projection with RoPE and the KV append fused (one kernel):
  * q_out [M, H, hd] = rope(bf16(X Wqkv^T))[q heads]; K, V of row m -> pool
  * (layout of fp_k_attn_decode) at token (slot[m], pos[m]) of `layer`.
@@ -154,6 +195,12 @@ int fp_k_qkv_rope(const void* Wqkv, int32_t K, const void* X, int32_t M, int32_t
 int fp_k_vocab(const void* X, int32_t M, int32_t K, const void* W, int32_t V, int32_t mode, float inv_temp,
                const int32_t* target, const int32_t* sample_id, const int32_t* step, uint64_t seed, int32_t* token,
                float* logp, void* stream);
+/* Filtered sampling (top-k / top-p) through the engine's kernels:
+ * gemm_vocab_logits -> topk_sample -> vocab_finalize. z_out (optional, [M][V]
+ * fp32) receives the temperature-scaled logits the filter saw. */
+int fp_k_vocab_filtered(const void* X, int32_t M, int32_t K, const void* W, int32_t V, float inv_temp, int32_t top_k,
+                        float top_p, const int32_t* sample_id, const int32_t* step, uint64_t seed, int32_t* token,
+                        float* logp, float* z_out, void* stream);
 int fp_k_add_norm(float* x, const float* parts, int32_t nsplit, const float* gain, void* y, int32_t M, int32_t d,
                   void* stream);
 /* Paged decode attention. pool: [num_pages][L][KVH][2][64][hd] bf16; block_table [slots][bt_stride].

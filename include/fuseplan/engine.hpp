@@ -61,6 +61,29 @@ struct EngineOptions {
   // packs groups [r dp / world, (r + 1) dp / world) contiguously on its GPU,
   // pulling samples scored on other GPUs over NVLink. dp % world == 0.
   int handoff_dp = 0;
+  // Free-run generation (north_star: "retires each sample as it emits EOS"):
+  // eos_id >= 0 retires a sample at the first emitted eos_id (kept as its last
+  // response token) or at max_new; target_output_len is then unused, KV
+  // reservations use prompt + max_new, and the trigger is online. Greedy or
+  // sample token modes only. The host learns the emitted ids eos_lag steps
+  // late (a retired row decodes at most eos_lag extra, discarded, steps).
+  int eos_id = -1;
+  int eos_lag = 1;
+  // Trigger of the fused schedule on G > 1 instances. false: the decision
+  // clock's (bit-exact with simulate_fused; teacher-forced lengths); true:
+  // online — the first rank that sees fewer than r_t unfinished samples in the
+  // whole batch raises the trigger, every rank pauses at its next step
+  // boundary, publishes its live state, and all ranks plan with the
+  // reference's plan_migration on that state (genfuse.cpp:416-467) and place
+  // the migrants with apply_migration's rules (genfuse.cpp:136-208).
+  bool online_trigger = false;
+  // Sampling filters (token_mode kSample): top_k > 0 keeps the logits >= the
+  // k-th largest (k <= 1024); top_p < 1 keeps the shortest prefix of those
+  // (sorted by probability; the top 1024 when top_k == 0) whose mass reaches
+  // top_p of theirs. 0 / 1: off. The reported log-prob is the token's under
+  // the full temperature softmax.
+  int top_k = 0;
+  float top_p = 1.0f;
 };
 
 /// Multi-process coordination (G > 1): every rank passes the same shm name.
@@ -91,6 +114,8 @@ struct ExecStats {
   std::int64_t gpu_launches = 0;    // kernels this rank launched
   double attn_probe_ms = 0.0, attn_probe_bytes = 0.0;  // probe_attention totals
   std::int64_t attn_probe_launches = 0;
+  std::int64_t eos_retired = 0;     // free-run: samples retired on an emitted EOS (this rank)
+  std::int64_t overrun_rows = 0;    // free-run: row-steps decoded after an EOS the host had not seen yet
 };
 
 // Experience hand-off (EngineOptions::handoff_dp > 0).
@@ -112,8 +137,12 @@ struct Handoff {
 };
 
 struct ExecResult {
-  GenStageResult decision;          // decision-clock result of the same schedule
-  TriggerSnapshot trigger;          // plan taken (fused, G > 1)
+  GenStageResult decision;          // decision-clock result of the same schedule (planned lengths)
+  TriggerSnapshot trigger;          // plan executed (fused, G > 1): decision clock's, or the online one
+  bool online = false;              // the trigger was taken online (EngineOptions::online_trigger / eos_id)
+  // In-flight and queued samples this rank received at the migration:
+  // (sample, source rank), in application order.
+  std::vector<int> received_sample, received_from;
   std::vector<double> finish_wall;  // per sample: GPU-clock finish time (seconds), on its final instance
   std::vector<int> finish_instance;
   ExperienceBatch experience;       // complete on rank 0 (gathered), local part elsewhere
@@ -138,6 +167,8 @@ double broadcast_model(GpuEngine* e, int model, int src, const CommSetup& comm);
 // Test / tooling helpers: regenerate a model's synthetic weights with another
 // seed; an order-independent 64-bit checksum of its weight blob.
 void reinit_model(GpuEngine* e, int model, std::uint64_t seed);
+// Copy one row-major host tensor into the engine's layout (fp_engine.h FP_W_*).
+void load_weights(GpuEngine* e, int model, int tensor, int layer, const void* host, std::int64_t n_elems);
 std::uint64_t model_checksum(GpuEngine* e, int model);
 
 ExecResult execute(GpuEngine* e, const std::vector<GenSample>& batch, const GenSimConfig& cfg, int r_t,

@@ -10,8 +10,9 @@ B200 engine computes for the experience-collection path:
     (actor / reference) or a d -> 1 value head (critic / reward);
   * actor log-probs of the response tokens (teacher-forced: the full causal
     forward equals incremental decode), greedy incremental decode with a KV
-    cache (for the token agreement rate), Gumbel-max sampling with the same
-    Philox4x32-10 streams as the GPU sampler;
+    cache (for the token agreement rate), exact two-level inverse-CDF sampling
+    (half-tile by mass, then inside it) replayed in the kernel's fp32 summation
+    order with the same Philox4x32-10 streams as the GPU sampler;
   * reference log-probs, critic values at positions P-1 .. P+R-2, reward score
     at position P+R-1;
   * post-processing: KL, reward shaping, GAE (the recursion of
@@ -60,14 +61,63 @@ def to_bf16(x: np.ndarray) -> np.ndarray:
     return b.astype(np.uint32).view(np.float32)
 
 
-def uniform_weight(seed, tag, n, scale) -> np.ndarray:
+_CLIB = None
+
+
+def _clib():
+    """oracle/_ref/liboracle_c.so (oracle/weights_oracle.c): the same values, threaded."""
+    global _CLIB
+    if _CLIB is None:
+        import ctypes
+        import os
+        from pathlib import Path
+        p = Path(__file__).resolve().parent / "_ref" / "liboracle_c.so"
+        _CLIB = False
+        if p.exists() and not os.environ.get("FP_ORACLE_NUMPY_WEIGHTS"):
+            lib = ctypes.CDLL(str(p))
+            if hasattr(lib, "oracle_uniform_weight"):
+                f = ctypes.POINTER(ctypes.c_float)
+                lib.oracle_uniform_weight.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_float,
+                                                      f, ctypes.c_int]
+                lib.oracle_gain.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, f, ctypes.c_int]
+                _CLIB = lib
+    return _CLIB or None
+
+
+def _threads() -> int:
+    import os
+    return max(1, min(32, len(os.sched_getaffinity(0))))
+
+
+def uniform_weight_np(seed, tag, n, scale) -> np.ndarray:
     t = unit24(hash3(seed, tag, np.arange(n, dtype=np.uint64))) * np.float32(2.0) - np.float32(1.0)
     return to_bf16(t * np.float32(scale))
 
 
-def gain(seed, tag, n) -> np.ndarray:
+def gain_np(seed, tag, n) -> np.ndarray:
     t = unit24(hash3(seed, tag, np.arange(n, dtype=np.uint64))) * np.float32(2.0) - np.float32(1.0)
     return np.float32(1.0) + np.float32(0.1) * t
+
+
+def uniform_weight(seed, tag, n, scale) -> np.ndarray:
+    lib = _clib()
+    if lib is None:
+        return uniform_weight_np(seed, tag, n, scale)
+    import ctypes
+    out = np.empty(n, dtype=np.float32)
+    lib.oracle_uniform_weight(seed, tag, n, float(np.float32(scale)), out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                              _threads())
+    return out
+
+
+def gain(seed, tag, n) -> np.ndarray:
+    lib = _clib()
+    if lib is None:
+        return gain_np(seed, tag, n)
+    import ctypes
+    out = np.empty(n, dtype=np.float32)
+    lib.oracle_gain(seed, tag, n, out.ctypes.data_as(ctypes.POINTER(ctypes.c_float)), _threads())
+    return out
 
 
 def fsqrt(x) -> np.float32:
@@ -172,7 +222,7 @@ def log_softmax(z):
 
 
 # ---------------------------------------------------------------------------
-# Philox4x32-10 + Gumbel (the GPU sampler's streams)
+# Philox4x32-10 + two-level inverse-CDF sampling (the GPU sampler's streams)
 
 def philox4x32_10(ctr: np.ndarray, k0: int, k1: int) -> np.ndarray:
     """ctr uint32 [..., 4] -> uint32 [..., 4]."""
@@ -281,6 +331,55 @@ def sample_token(logits: np.ndarray, inv_temp: float, seed: int, sid: int, step:
         if acc >= thr:
             break
     return tok
+
+
+def _order_key(z: np.ndarray) -> np.ndarray:
+    b = np.ascontiguousarray(z, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    neg = (b & np.uint64(0x80000000)) != 0
+    return np.where(neg, (~b) & np.uint64(0xFFFFFFFF), b | np.uint64(0x80000000))
+
+
+def filtered_sample(z: np.ndarray, top_k: int, top_p: float, seed: int, sid: int, step: int, k_max: int = 1024):
+    """Top-k / top-p sampling of csrc/kernels/sampling.cu on one row of z = logit / T
+    (fp32), in the kernel's order: candidates = every z >= the k-th largest
+    (ties kept), sorted by (z desc, id asc); masses 2^((z - z_0) log2 e) summed
+    in 32 lane-contiguous chunks; nucleus = the shortest prefix reaching
+    top_p of the candidates' mass; inverse-CDF draw at u * mass(nucleus),
+    u = Philox(seed; 0xFFFFFFFE, step, sid, 0xF00D). Returns (token, kept ids)."""
+    z = np.asarray(z, dtype=np.float32)
+    V = len(z)
+    k = min(V, min(top_k, k_max) if top_k > 0 else k_max)
+    key = _order_key(z)
+    kth = np.sort(key)[::-1][k - 1]
+    ids = np.flatnonzero(key >= kth)
+    ids = ids[np.lexsort((ids, -key[ids].astype(np.int64)))]  # key desc, id asc
+    n = len(ids)
+    e = np.exp2((z[ids] - z[ids[0]]).astype(np.float32) * np.float32(1.4426950408889634)).astype(np.float32)
+    chunk = (n + 31) // 32
+    csum = np.zeros(n, dtype=np.float32)
+    lane_sum = []
+    for l in range(32):
+        c0, c1 = min(n, l * chunk), min(n, l * chunk + chunk)
+        run = np.float32(0)
+        for i in range(c0, c1):
+            run = np.float32(run + e[i])
+            csum[i] = run
+        lane_sum.append(run)
+    base = np.float32(0)
+    for l in range(32):
+        c0, c1 = min(n, l * chunk), min(n, l * chunk + chunk)
+        for i in range(c0, c1):
+            csum[i] = np.float32(csum[i] + base)
+        base = np.float32(base + lane_sum[l])
+    cut = n - 1
+    if top_p < 1.0:
+        need = np.float32(np.float32(top_p) * csum[n - 1])
+        hit = np.flatnonzero(csum >= need)
+        cut = min(int(hit[0]) if len(hit) else n, n - 1)
+    thr = np.float32(_unit(_philox1(seed, 0xFFFFFFFE, step, sid)) * csum[cut])
+    hit = np.flatnonzero(csum[:cut + 1] >= thr)
+    sel = min(int(hit[0]) if len(hit) else cut + 1, cut)
+    return int(ids[sel]), set(int(i) for i in ids[:cut + 1])
 
 
 # ---------------------------------------------------------------------------

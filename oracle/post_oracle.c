@@ -1,7 +1,7 @@
 /* ORACLE — test infrastructure only; never linked into the product path.
  *
  * CPU restatement (C, fp64) of the per-token experience post-processing that
- * the GPU kernel csrc/kernels/postprocess.cu performs in fp32:
+ * the GPU kernel csrc/kernels/post.cu performs in fp32:
  *
  *   kl_t      = logp_actor_t - logp_ref_t                      (builder-stated;
  *   reward_t  = -beta * kl_t + [t == R-1] * score               PPO/KL math is a

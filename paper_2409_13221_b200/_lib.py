@@ -110,7 +110,8 @@ class RunOptions(C.Structure):
                 ("token_seed", C.c_uint64), ("sample_seed", C.c_uint64), ("kl_beta", C.c_float),
                 ("gamma", C.c_float), ("lam", C.c_float), ("claim_tokens", C.c_int32), ("run_ahead", C.c_int32),
                 ("resident", C.c_int32), ("probe_attention", C.c_int32), ("handoff_dp", C.c_int32),
-                ("claim_max_live", C.c_int32)]
+                ("claim_max_live", C.c_int32), ("eos_id", C.c_int32), ("eos_lag", C.c_int32),
+                ("online_trigger", C.c_int32), ("top_k", C.c_int32), ("top_p", C.c_float)]
 
 
 class Comm(C.Structure):
@@ -124,7 +125,8 @@ class ExecStats(C.Structure):
                 ("decode_ctx_tokens", C.c_int64), ("prefill_tokens", C.c_int64), ("infer_tokens", C.c_int64),
                 ("infer_samples", C.c_int64), ("migrated_in", C.c_int64), ("migrated_bytes", C.c_int64),
                 ("total_resp", C.c_int64), ("gpu_launches", C.c_int64), ("attn_probe_ms", C.c_double),
-                ("attn_probe_bytes", C.c_double), ("attn_probe_launches", C.c_int64), ("ipc_seconds", C.c_double)]
+                ("attn_probe_bytes", C.c_double), ("attn_probe_launches", C.c_int64), ("ipc_seconds", C.c_double),
+                ("eos_retired", C.c_int64), ("overrun_rows", C.c_int64), ("online", C.c_int32)]
 
 
 P = C.POINTER
@@ -161,6 +163,7 @@ ENGINE_SYMBOLS = {
     "fp_engine_broadcast_model": (C.c_int, [_vp, C.c_int32, C.c_int32, P(Comm), _f64p]),
     "fp_engine_model_ptr": (C.c_int, [_vp, C.c_int32, P(C.c_void_p), _i64p]),
     "fp_engine_reinit_model": (C.c_int, [_vp, C.c_int32, C.c_uint64]),
+    "fp_engine_load_weights": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int64]),
     "fp_engine_model_checksum": (C.c_int, [_vp, C.c_int32, P(C.c_uint64)]),
     "fp_engine_kv_bytes_per_token": (C.c_int, [_vp, _i64p]),
     "fp_synthetic_prompts": (C.c_int, [_vp, C.c_int32, C.c_uint64, _i32p]),
@@ -171,6 +174,8 @@ ENGINE_SYMBOLS = {
     "fp_exec_finish": (C.c_int, [_vp, _f64p, _i32p]),
     "fp_exec_decision": (C.c_int, [_vp, P(_vp)]),
     "fp_exec_moves": (C.c_int, [_vp, _i32p, _i32p, _i32p, _i32p]),
+    "fp_exec_received": (C.c_int, [_vp, _i32p, _i32p, _i32p]),
+    "fp_exec_trigger_state": (C.c_int, [_vp, _f64p, _i32p, P(Remaining)]),
     "fp_exec_handoff": (C.c_int, [_vp, _i32p, _i32p, _i32p, _i32p, _i32p, _i64p, P(C.c_void_p), _f64p, _i64p,
                                   _i64p]),
     "fp_exec_handoff_download": (C.c_int, [_vp, P(C.c_void_p)]),
@@ -182,10 +187,13 @@ ENGINE_SYMBOLS = {
     "fp_k_gemm_splits": (C.c_int, [C.c_int32, C.c_int32]),
     "fp_k_gemm_trace": (C.c_int, [_vp]),
     "fp_k_gemm_swiglu": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, _vp]),
+    "fp_k_gemm_swiglu_decode": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, _vp]),
     "fp_k_qkv_rope": (C.c_int, [_vp, C.c_int32, _vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int32,
                                 C.c_float, _vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, _vp, _vp]),
     "fp_k_vocab": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int32, C.c_float, _vp, _vp, _vp,
                              C.c_uint64, _vp, _vp, _vp]),
+    "fp_k_vocab_filtered": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_float, C.c_int32, C.c_float,
+                                      _vp, _vp, C.c_uint64, _vp, _vp, _vp, _vp]),
     "fp_k_add_norm": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, C.c_int32, C.c_int32, _vp]),
     "fp_k_attn_decode": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int32,
                                    C.c_int32, _vp, C.c_int32, _vp, _vp, C.c_int32, _vp, _vp]),

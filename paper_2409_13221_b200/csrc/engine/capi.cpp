@@ -180,6 +180,14 @@ int fp_engine_model_ptr(const fp_engine* e, int32_t model, void** dev_ptr, int64
   });
 }
 
+int fp_engine_load_weights(fp_engine* e, int32_t model, int32_t tensor, int32_t layer, const void* host,
+                           int64_t n_elems) {
+  return guarded([&] {
+    need(e, "engine");
+    fuseplan::load_weights(e->g, model, tensor, layer, host, n_elems);
+  });
+}
+
 int fp_engine_reinit_model(fp_engine* e, int32_t model, uint64_t seed) {
   return guarded([&] {
     need(e, "engine");
@@ -243,6 +251,11 @@ int fp_execute(fp_engine* e, const fp_gen_sample* batch, int32_t n, const fp_gen
     eo.probe_attention = o->probe_attention != 0;
     eo.handoff_dp = o->handoff_dp;
     eo.claim_max_live = o->claim_max_live;
+    eo.eos_id = o->eos_id;
+    eo.eos_lag = o->eos_lag;
+    eo.online_trigger = o->online_trigger != 0;
+    eo.top_k = o->top_k;
+    eo.top_p = o->top_p;
     fuseplan::CommSetup cs;
     if (comm) {
       cs.rank = comm->rank;
@@ -288,6 +301,9 @@ int fp_exec_stats_get(const fp_exec* x, fp_exec_stats* s) {
     s->attn_probe_bytes = t.attn_probe_bytes;
     s->attn_probe_launches = t.attn_probe_launches;
     s->ipc_seconds = t.ipc_seconds;
+    s->eos_retired = t.eos_retired;
+    s->overrun_rows = t.overrun_rows;
+    s->online = x->r.online ? 1 : 0;
   });
 }
 
@@ -339,6 +355,32 @@ int fp_exec_moves(const fp_exec* x, int32_t* n_moves, int32_t* sample, int32_t* 
       if (from) from[i] = t.move_from[i];
       if (to) to[i] = t.move_to[i];
     }
+  });
+}
+
+int fp_exec_received(const fp_exec* x, int32_t* n, int32_t* sample, int32_t* from) {
+  return guarded([&] {
+    need(x, "exec");
+    const auto& r = x->r;
+    if (n) *n = static_cast<int32_t>(r.received_sample.size());
+    for (size_t i = 0; i < r.received_sample.size(); ++i) {
+      if (sample) sample[i] = r.received_sample[i];
+      if (from) from[i] = r.received_from[i];
+    }
+  });
+}
+
+int fp_exec_trigger_state(const fp_exec* x, double* time, int32_t* n, fp_remaining* samples) {
+  return guarded([&] {
+    need(x, "exec");
+    const fuseplan::GenState& st = x->r.trigger.state;
+    if (time) *time = st.time;
+    if (n) *n = static_cast<int32_t>(st.samples.size());
+    if (samples)
+      for (size_t i = 0; i < st.samples.size(); ++i) {
+        const auto& r = st.samples[i];
+        samples[i] = fp_remaining{r.id, r.instance, r.kv_bytes, r.generated, r.prompt_len, r.admitted ? 1 : 0};
+      }
   });
 }
 
@@ -432,6 +474,15 @@ int fp_k_gemm_swiglu(const void* Wgu, int32_t F, int32_t K, const void* X, int32
   });
 }
 
+int fp_k_gemm_swiglu_decode(const void* Wgu, int32_t F, int32_t K, const void* X, int32_t M, void* out,
+                            void* stream) {
+  return guarded([&] {
+    fpk::gemm_swiglu_decode(static_cast<const bf16*>(Wgu), F, K, static_cast<const bf16*>(X), M,
+                            static_cast<bf16*>(out), S(stream));
+    after_launch();
+  });
+}
+
 int fp_k_qkv_rope(const void* Wqkv, int32_t K, const void* X, int32_t M, int32_t H, int32_t KVH, int32_t hd,
                   const int32_t* pos, int32_t max_pos, float rope_theta, void* pool, int32_t num_layers,
                   int32_t layer, const int32_t* block_table, int32_t bt_stride, const int32_t* slot, void* q_out,
@@ -466,6 +517,32 @@ int fp_k_vocab(const void* X, int32_t M, int32_t K, const void* W, int32_t V, in
     after_launch();
     fpe::check(cudaFreeAsync(part, S(stream)), "free");
     fpe::check(cudaFreeAsync(tz, S(stream)), "free");
+  });
+}
+
+int fp_k_vocab_filtered(const void* X, int32_t M, int32_t K, const void* W, int32_t V, float inv_temp, int32_t top_k,
+                        float top_p, const int32_t* sample_id, const int32_t* step, uint64_t seed, int32_t* token,
+                        float* logp, float* z_out, void* stream) {
+  return guarded([&] {
+    void* part = nullptr;
+    float *tz = nullptr, *z = z_out;
+    int* pick = nullptr;
+    const int ldv = z_out ? V : (V + 3) & ~3;
+    if (z_out && V % 4) throw std::invalid_argument("fp_k_vocab_filtered: z_out needs V % 4 == 0");
+    fpe::check(cudaMallocAsync(&part, static_cast<size_t>(M) * fpk::vocab_tiles(V) * 24 + 256, S(stream)), "alloc");
+    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&tz), static_cast<size_t>(M) * 4 + 256, S(stream)), "alloc");
+    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&pick), static_cast<size_t>(M) * 4 + 256, S(stream)), "alloc");
+    if (!z) fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&z), static_cast<size_t>(M) * ldv * 4 + 256, S(stream)), "alloc");
+    fpk::gemm_vocab_logits(static_cast<const bf16*>(X), M, K, static_cast<const bf16*>(W), V, inv_temp, part, z, ldv,
+                           S(stream));
+    fpk::topk_sample(z, ldv, M, V, top_k, top_p, sample_id, step, seed, pick, tz, S(stream));
+    fpk::vocab_finalize(part, tz, M, V, 0, pick, sample_id, step, seed, token, logp, nullptr, nullptr, nullptr, nullptr,
+                        nullptr, S(stream));
+    after_launch();
+    fpe::check(cudaFreeAsync(part, S(stream)), "free");
+    fpe::check(cudaFreeAsync(tz, S(stream)), "free");
+    fpe::check(cudaFreeAsync(pick, S(stream)), "free");
+    if (!z_out) fpe::check(cudaFreeAsync(z, S(stream)), "free");
   });
 }
 

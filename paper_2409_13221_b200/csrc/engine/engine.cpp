@@ -259,6 +259,50 @@ void Engine::reinit_model(int m, uint64_t seed) {
   FP_CUDA(cudaStreamSynchronize(s_decode_));
 }
 
+void Engine::load_tensor(int m, int tensor, int layer, const void* host, int64_t n_elems) {
+  if (m < 0 || m > 3) throw std::invalid_argument("load_weights: model index out of range");
+  ModelW& w = models_[m];
+  const Dims& D = w.dims;
+  const bool per_layer = tensor >= 1 && tensor <= 7;
+  if (per_layer && (layer < 0 || layer >= D.L)) throw std::invalid_argument("load_weights: layer out of range");
+  if (!per_layer && layer != 0) throw std::invalid_argument("load_weights: per-model tensors take layer 0");
+  if (!host) throw std::invalid_argument("load_weights: null host tensor");
+  const size_t d = D.d, F = D.F, V = D.V, qw = D.qkv_width(), ao = static_cast<size_t>(D.H) * D.hd;
+  void* dst = nullptr;
+  size_t elems = 0, esize = 2;
+  switch (tensor) {
+    case 0: dst = w.embed, elems = V * d; break;
+    case 1: dst = w.layers[layer].wqkv, elems = qw * d; break;
+    case 2: dst = w.layers[layer].wo, elems = d * ao; break;
+    case 3:
+    case 4: dst = w.layers[layer].wgu, elems = F * d; break;
+    case 5: dst = w.layers[layer].wd, elems = d * F; break;
+    case 6: dst = w.layers[layer].ln1, elems = d, esize = 4; break;
+    case 7: dst = w.layers[layer].ln2, elems = d, esize = 4; break;
+    case 8: dst = w.lnf, elems = d, esize = 4; break;
+    case 9:
+      if (!w.lm_head) throw std::invalid_argument("load_weights: critic / reward models have a value head, not an LM head");
+      dst = w.head, elems = V * d;
+      break;
+    case 10:
+      if (w.lm_head) throw std::invalid_argument("load_weights: actor / reference models have an LM head, not a value head");
+      dst = w.vhead, elems = d;
+      break;
+    default: throw std::invalid_argument("load_weights: unknown tensor kind");
+  }
+  if (n_elems < 0 || static_cast<size_t>(n_elems) != elems)
+    throw std::invalid_argument("load_weights: element count does not match the tensor's shape");
+  FP_CUDA(cudaStreamSynchronize(s_decode_));
+  if (tensor == 3 || tensor == 4) {
+    // [F][d] gate (or up) rows -> rows (f / 64) * 128 + (up ? 64 : 0) + f % 64 of W_gu
+    const size_t group = 64 * d * 2;
+    uint8_t* base = static_cast<uint8_t*>(dst) + (tensor == 4 ? group : 0);
+    FP_CUDA(cudaMemcpy2D(base, 2 * group, host, group, group, F / 64, cudaMemcpyHostToDevice));
+  } else {
+    FP_CUDA(cudaMemcpy(dst, host, elems * esize, cudaMemcpyHostToDevice));
+  }
+}
+
 uint64_t Engine::model_checksum(int m) {
   unsigned long long* d = static_cast<unsigned long long*>(decode_scratch(sizeof(unsigned long long)));
   FP_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s_decode_));
@@ -641,7 +685,10 @@ size_t Engine::build_rows(const DecodeRow* rows, int B, int Bb, std::vector<int>
 // latency-bound GEMM chain overlaps the other half's bandwidth-bound attention,
 // which is capped to part of the SMs. The probe mode (per-launch CUDA events)
 // and the traced step run eagerly.
-void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed) {
+void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed, int top_k,
+                    float top_p) {
+  if (mode != 2 || top_p >= 1.f) top_p = 1.f;
+  if (mode != 2) top_k = 0;
   const int B = static_cast<int>(rows.size());
   if (B == 0) return;
   // FUSEPLAN_TRACE_STEP=k: the engine's k-th decode step runs eagerly with
@@ -681,12 +728,12 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
     auto both = [&]() {
       FP_CUDA(cudaEventRecord(ev_fork_, st));
       FP_CUDA(cudaStreamWaitEvent(s_decode2_, ev_fork_, 0));
-      decode_kernels(dec_, st, Bb0, ctx_cap, mode, inv_temp, sample_seed, 0.0, split_ctas);
-      decode_kernels(dec2_, s_decode2_, Bb1, ctx_cap, mode, inv_temp, sample_seed, 0.0, split_ctas);
+      decode_kernels(dec_, st, Bb0, ctx_cap, mode, inv_temp, sample_seed, 0.0, split_ctas, top_k, top_p);
+      decode_kernels(dec2_, s_decode2_, Bb1, ctx_cap, mode, inv_temp, sample_seed, 0.0, split_ctas, top_k, top_p);
       FP_CUDA(cudaEventRecord(ev_join_, s_decode2_));
       FP_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
     };
-    run_graph(GraphKey{Bb0, Bb1, mode, inv_temp, sample_seed}, both);
+    run_graph(GraphKey{Bb0, Bb1, mode, inv_temp, sample_seed, top_k, top_p}, both);
     return;
   }
   const int Bb = graph ? bucket_of(B) : B;
@@ -705,7 +752,7 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
       FP_CUDA(cudaStreamSynchronize(st));
       fpk::trace_arm(arena, words);
     }
-    decode_kernels(dec_, st, Bb, max_ctx, mode, inv_temp, sample_seed, ctx_sum, 148);
+    decode_kernels(dec_, st, Bb, max_ctx, mode, inv_temp, sample_seed, ctx_sum, 148, top_k, top_p);
     if (tracing) {
       FP_CUDA(cudaStreamSynchronize(st));
       const std::vector<fpk::TraceRec> recs = fpk::trace_disarm();
@@ -731,8 +778,8 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
     }
     return;
   }
-  run_graph(GraphKey{Bb, 0, mode, inv_temp, sample_seed},
-            [&]() { decode_kernels(dec_, st, Bb, ctx_cap, mode, inv_temp, sample_seed, 0.0, 148); });
+  run_graph(GraphKey{Bb, 0, mode, inv_temp, sample_seed, top_k, top_p},
+            [&]() { decode_kernels(dec_, st, Bb, ctx_cap, mode, inv_temp, sample_seed, 0.0, 148, top_k, top_p); });
 }
 
 // Replay the step graph of `key`; the first sight of a key runs eagerly (sets
@@ -763,7 +810,7 @@ void Engine::run_graph(const GraphKey& key, const std::function<void()>& body) {
 }
 
 void Engine::decode_kernels(DecodeWs& dw, cudaStream_t st, int B, int max_ctx, int mode, float inv_temp,
-                            uint64_t sample_seed, double ctx_sum, int attn_ctas) {
+                            uint64_t sample_seed, double ctx_sum, int attn_ctas, int top_k, float top_p) {
   const ModelW& w = models_[kActor];
   const Dims& D = w.dims;
   const int* slot = dw.rows;
@@ -823,10 +870,21 @@ void Engine::decode_kernels(DecodeWs& dw, cudaStream_t st, int B, int max_ctx, i
     nparts = sd;
   }
   if (!h_ready) fpk::add_norm(dw.x, dw.parts, nparts, stride, w.lnf, dw.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
-  fpk::gemm_vocab(dw.h, B, D.d, w.head, D.V, mode, inv_temp, target, sid, step, sample_seed, dw.vocab_part,
-                  dw.tgt_z, st);
-  fpk::vocab_finalize(dw.vocab_part, dw.tgt_z, B, D.V, mode, target, sid, step, sample_seed, nullptr, nullptr, dst,
-                      d_hist_tok_, d_hist_logp_, slot, d_cur_tok_, st);
+  if (top_k > 0 || top_p < 1.f) {  // filtered sampling: z materialised, radix-select filter, then forced finalize
+    if (!dw.logits) {  // first use runs eagerly (run_graph), never inside a capture
+      dw.logits = static_cast<float*>(dalloc(static_cast<size_t>(dw.cap) * logits_ld() * sizeof(float)));
+      dw.pick = static_cast<int*>(dalloc(static_cast<size_t>(dw.cap) * sizeof(int)));
+    }
+    fpk::gemm_vocab_logits(dw.h, B, D.d, w.head, D.V, inv_temp, dw.vocab_part, dw.logits, logits_ld(), st);
+    fpk::topk_sample(dw.logits, logits_ld(), B, D.V, top_k, top_p, sid, step, sample_seed, dw.pick, dw.tgt_z, st);
+    fpk::vocab_finalize(dw.vocab_part, dw.tgt_z, B, D.V, 0, dw.pick, sid, step, sample_seed, nullptr, nullptr, dst,
+                        d_hist_tok_, d_hist_logp_, slot, d_cur_tok_, st);
+  } else {
+    fpk::gemm_vocab(dw.h, B, D.d, w.head, D.V, mode, inv_temp, target, sid, step, sample_seed, dw.vocab_part,
+                    dw.tgt_z, st);
+    fpk::vocab_finalize(dw.vocab_part, dw.tgt_z, B, D.V, mode, target, sid, step, sample_seed, nullptr, nullptr, dst,
+                        d_hist_tok_, d_hist_logp_, slot, d_cur_tok_, st);
+  }
   FP_CUDA(cudaGetLastError());
 }
 

@@ -92,6 +92,9 @@ class Engine {
   const EngineConfig& config() const { return cfg_; }
   const ModelW& model(int m) const { return models_[m]; }
   void reinit_model(int m, uint64_t seed);     // synthetic weights from another seed (same layout)
+  // Copy one row-major host tensor (fp_engine.h FP_W_*) into the model's blob,
+  // repacking the gate / up rows into the 64-row interleave. Synchronous.
+  void load_tensor(int m, int tensor, int layer, const void* host, int64_t n_elems);
   uint64_t model_checksum(int m);             // sum of the blob's 64-bit words (synchronises)
   cudaStream_t decode_stream() const { return s_decode_; }
   // The scoring stream in use: while generation runs, scoring may be confined
@@ -136,7 +139,9 @@ class Engine {
   };
   // One decode step for `rows`: writes hist[sid][step] (token, logp) and the
   // next input token. mode 0 forced (target), 1 greedy, 2 sample.
-  void decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed);
+  // top_k / top_p (mode 2): filtered sampling (EngineOptions::top_k / top_p).
+  void decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed, int top_k = 0,
+              float top_p = 1.f);
   void set_use_graphs(bool on) { use_graphs_ = on; }
   static int bucket_of(int B);
 
@@ -209,11 +214,15 @@ class Engine {
     int B, B1, mode;  // B1: second half of a split step (0: unsplit)
     float inv_temp;
     uint64_t seed;
+    int top_k;
+    float top_p;
     bool operator<(const GraphKey& o) const {
       if (B != o.B) return B < o.B;
       if (B1 != o.B1) return B1 < o.B1;
       if (mode != o.mode) return mode < o.mode;
       if (inv_temp != o.inv_temp) return inv_temp < o.inv_temp;
+      if (top_k != o.top_k) return top_k < o.top_k;
+      if (top_p != o.top_p) return top_p < o.top_p;
       return seed < o.seed;
     }
   };
@@ -225,7 +234,7 @@ class Engine {
   std::set<GraphKey> graph_seen_;
   struct DecodeWs;
   void decode_kernels(DecodeWs& dw, cudaStream_t st, int B, int max_ctx, int mode, float inv_temp,
-                      uint64_t sample_seed, double ctx_sum, int attn_ctas);
+                      uint64_t sample_seed, double ctx_sum, int attn_ctas, int top_k, float top_p);
   size_t build_rows(const DecodeRow* rows, int B, int Bb, std::vector<int>& h, int& max_ctx, double& ctx_sum);
   void run_graph(const GraphKey& key, const std::function<void()>& body);
   cudaStream_t s_decode2_ = nullptr;
@@ -265,7 +274,10 @@ class Engine {
     int* rows = nullptr;  // 7 x cap: slot, pos, ctx, dst, target, sid, step
     void* vocab_part = nullptr;
     float* tgt_z = nullptr;
+    float* logits = nullptr;  // filtered sampling: [cap][ldv] z (allocated on first use)
+    int* pick = nullptr;      // filtered sampling: chosen token per row
   };
+  int logits_ld() const { return (cfg_.model[kActor].V + 3) & ~3; }
 
   void init_model(int m);
   void fill_model(int m, uint64_t seed);

@@ -498,6 +498,22 @@ void gemm_vocab(const bf16* X, int M, int K, const bf16* Whead, int V, int mode,
   else go(EpiVocab<kSample>{});
 }
 
+void gemm_vocab_logits(const bf16* X, int M, int K, const bf16* Whead, int V, float inv_temp, void* part,
+                       float* logits, int ldv, cudaStream_t st) {
+  if (ldv < V || ldv % 4) throw std::invalid_argument("gemm_vocab_logits: ldv must be >= V and a multiple of 4");
+  EpiVocab<kLogits> e{};
+  e.part = static_cast<VocabPartial*>(part);
+  e.tgt_z = nullptr;
+  e.info = VocabRowInfo{nullptr, nullptr, nullptr};
+  e.inv_temp = inv_temp;
+  e.vocab = V;
+  e.rows = M;
+  e.n_tiles = vocab_tiles(V);
+  e.logits = logits;
+  e.ldv = ldv;
+  launch<kVocabBN>(X, M, Whead, V, K, 1, e, st, /*weight_is_a=*/false);
+}
+
 // One warp per row: merge the row's partials in partial order. The sampling
 // walk over partials is sequential in lane 0 so that its float order is
 // fixed (the CPU oracle replays it).

@@ -52,6 +52,9 @@ int gemm_splits(int N, int K);
 void set_gemm_trace(unsigned long long* buf);
 
 struct VocabOut;  // fwd
+// Largest top_k of the filtered sampler (topk_sample); top_p alone filters
+// within the top kTopKMax logits.
+constexpr int kTopKMax = 1024;
 // Vocab head: rows X [M, K] against W_head [V, K]; writes per-(row, tile)
 // partials into `part` (M x vocab_tiles(V) VocabPartial = 24 B each, two
 // 128-column halves per 256-wide vocab tile) and, in
@@ -60,6 +63,20 @@ int vocab_tiles(int V);
 void gemm_vocab(const bf16* X, int M, int K, const bf16* Whead, int V, int mode, float inv_temp,
                 const int* target, const int* sample_id, const int* step, uint64_t seed, void* part, float* tgt_z,
                 cudaStream_t st);
+// Filtered sampling, step 1: the same head GEMM keeping the log-softmax
+// partials and writing z = logit * inv_temp to logits [M][ldv] (fp32).
+void gemm_vocab_logits(const bf16* X, int M, int K, const bf16* Whead, int V, float inv_temp, void* part,
+                       float* logits, int ldv, cudaStream_t st);
+// Step 2 (sampling.cu), one CTA per row: the k-th largest z by an exact
+// radix select (k = top_k, or kTopKMax when top_k == 0; ties at the boundary
+// kept), the candidates sorted by (z desc, id asc), the nucleus = the
+// shortest sorted prefix whose softmax mass reaches top_p of the candidates'
+// mass, and an inverse-CDF draw in that order with
+// u = Philox(seed, sample_id, step, counter kFilterDraw). pick[row] = token,
+// pick_z[row] = its z (step 3 is vocab_finalize in forced mode on pick:
+// log-prob under the full temperature softmax, scatter, next input).
+void topk_sample(const float* logits, int ldv, int M, int V, int top_k, float top_p, const int* sample_id,
+                 const int* step, uint64_t seed, int* pick, float* pick_z, cudaStream_t st);
 // Merge partials: token[row] (forced -> target), logp[row]; optional scatter
 // into per-sample buffers: out_tok[dst[row]] / out_logp[dst[row]] when dst != nullptr.
 // cur_tok[cur_idx[row]] = token (next decode input) when cur_tok != nullptr.

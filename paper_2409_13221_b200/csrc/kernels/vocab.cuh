@@ -28,6 +28,10 @@
 namespace fpk {
 
 enum TokenMode : int { kForced = 0, kGreedy = 1, kSample = 2 };
+// Filtered sampling (top-k / top-p): the epilogue keeps the log-softmax
+// statistics and writes z = logit / T to a [rows, ldv] fp32 buffer, which
+// topk_sample() filters and samples from.
+constexpr int kLogits = 3;
 constexpr float kLog2E = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr uint32_t kRowDraw = 0xFFFFFFFFu;  // Philox counter word of the tile choice
@@ -59,6 +63,8 @@ struct EpiVocab {
   int rows;
   int n_tiles;
   uint32_t seed_lo, seed_hi;
+  float* logits;  // kLogits: [rows][ldv]
+  int ldv;
 
   static constexpr bool kTmaStore = false;
   static constexpr int kPasses = MODE == kSample ? 2 : 1;
@@ -135,7 +141,19 @@ struct EpiVocab {
       if (j < nvalid) acc += exp2f(v[j] * c2 - nm);
     st.m = nm;
     st.s = acc;
-    if constexpr (MODE == kForced) {
+    if constexpr (MODE == kLogits) {
+      float* dst = logits + static_cast<size_t>(row) * ldv + base;
+      if (nvalid == 32) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(dst + j) =
+              make_float4(v[j] * inv_temp, v[j + 1] * inv_temp, v[j + 2] * inv_temp, v[j + 3] * inv_temp);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nvalid) dst[j] = v[j] * inv_temp;
+      }
+    } else if constexpr (MODE == kForced) {
       const int t = info.target[row];
       if (t >= base && t < base + nvalid) {
 #pragma unroll

@@ -56,6 +56,9 @@ class ExecOutput:
     step_rows: np.ndarray = None  # per decode step of this rank: batch rows
     step_ms: np.ndarray = None    # per decode step: GPU ms
     handoff: dict = None          # handoff_dp > 0: order, group_off, packed_off, this rank's packed arrays
+    received: list = None         # (sample, source rank) this rank pulled in at the migration
+    trigger_state: tuple = None   # (time, [Remaining...]) the executed plan was taken on
+    online: bool = False          # the trigger was taken online
 
 
 class Engine:
@@ -121,6 +124,31 @@ class Engine:
         return out
 
     MODELS = {"actor": 0, "ref": 1, "critic": 2, "reward": 3}
+    TENSORS = {"embed": 0, "wqkv": 1, "wo": 2, "wg": 3, "wu": 4, "wd": 5, "ln1": 6, "ln2": 7, "lnf": 8, "head": 9,
+               "vhead": 10}
+
+    def load_weights(self, model: str, tensors: dict) -> None:
+        """fp_engine_load_weights for every tensor of `tensors` (model_oracle.make_weights layout:
+        embed, layers[l][wqkv|wo|wg|wu|wd|ln1|ln2], lnf, head | vhead). Matrices are converted to
+        bf16 (round to nearest even), norm gains stay fp32."""
+        m = self.MODELS[model]
+
+        def put(name, layer, a):
+            a = np.ascontiguousarray(a, dtype=np.float32)
+            if name in ("ln1", "ln2", "lnf"):
+                buf = a
+            else:  # fp32 -> bf16 bits, round to nearest even
+                b = a.view(np.uint32).astype(np.uint64)
+                buf = ((b + 0x7FFF + ((b >> 16) & 1)) >> 16).astype(np.uint16)
+            check(self.lib, self.lib.fp_engine_load_weights(self.h, m, self.TENSORS[name], layer,
+                                                            buf.ctypes.data_as(C.c_void_p), buf.size))
+
+        for name in ("embed", "lnf", "head", "vhead"):
+            if name in tensors:
+                put(name, 0, tensors[name])
+        for l, lw in enumerate(tensors.get("layers", [])):
+            for name, a in lw.items():
+                put(name, l, a)
 
     def broadcast_model(self, model: str, src: int, rank: int, world: int, shm_name: str | None) -> float:
         """Weight sync over NVLink (fp_engine_broadcast_model): every rank calls it; returns seconds."""
@@ -149,12 +177,13 @@ class Engine:
                 kl_beta: float = 0.05, gamma: float = 1.0, lam: float = 0.95, claim_tokens: int = 8192,
                 run_ahead: int = 4, rank: int = 0, world: int = 1, shm_name: str | None = None,
                 prompts: np.ndarray | None = None, resident: bool = False,
-                probe_attention: bool = False, handoff_dp: int = 0, claim_max_live: int = 0) -> ExecOutput:
+                probe_attention: bool = False, handoff_dp: int = 0, claim_max_live: int = 0, eos_id: int = -1,
+                eos_lag: int = 1, online_trigger: bool = False, top_k: int = 0, top_p: float = 1.0) -> ExecOutput:
         keep: list = []
         n = len(batch)
         opts = _lib.RunOptions(TOKEN_MODES[token_mode], SCHEDULES[schedule], temperature, token_seed, sample_seed,
                                kl_beta, gamma, lam, claim_tokens, run_ahead, int(resident), int(probe_attention),
-                               handoff_dp, claim_max_live)
+                               handoff_dp, claim_max_live, eos_id, eos_lag, int(online_trigger), top_k, top_p)
         comm = _lib.Comm(rank, world, shm_name.encode() if shm_name else None)
         pp = None
         if prompts is not None:
@@ -202,6 +231,17 @@ class Engine:
             check(self.lib, self.lib.fp_exec_steps(x, C.byref(ns), srows.ctypes.data_as(C.POINTER(C.c_int32)),
                                                    sms.ctypes.data_as(C.POINTER(C.c_float))))
             handoff = self._handoff(x, n) if handoff_dp > 0 else None
-            return ExecOutput(stats, exp, fin, inst, decision, moves, srows[:ns.value], sms[:ns.value], handoff)
+            nr = C.c_int32()
+            check(self.lib, self.lib.fp_exec_received(x, C.byref(nr), None, None))
+            rs, rf = ((C.c_int32 * max(nr.value, 1))() for _ in range(2))
+            check(self.lib, self.lib.fp_exec_received(x, C.byref(nr), rs, rf))
+            tt, nt = C.c_double(), C.c_int32()
+            check(self.lib, self.lib.fp_exec_trigger_state(x, C.byref(tt), C.byref(nt), None))
+            tst = (_lib.Remaining * max(nt.value, 1))()
+            check(self.lib, self.lib.fp_exec_trigger_state(x, C.byref(tt), C.byref(nt), tst))
+            state = (tt.value, [(r.id, r.instance, r.kv_bytes, r.generated, r.prompt_len, bool(r.admitted))
+                                for r in tst[:nt.value]])
+            return ExecOutput(stats, exp, fin, inst, decision, moves, srows[:ns.value], sms[:ns.value], handoff,
+                              list(zip(rs[:nr.value], rf[:nr.value])), state, bool(st.online))
         finally:
             self.lib.fp_exec_free(x)

@@ -255,3 +255,112 @@ def test_hd128_gqa_schedules_identical(gqa128):
     b = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="stage_barrier")
     for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret", "score"):
         assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
+
+
+def test_kv_capped_admission_waves_match_decision_clock(toy):
+    """KV-gated admission (genfuse.cpp:226-236) on one GPU: with a KV capacity of a few
+    samples, admission comes in waves; the executed per-instance finish sequence (which
+    samples retire together, in which order) equals the decision clock's timeline."""
+    from paper_2409_13221_b200.configs import gen_config
+    w, eng, batch, _ = toy
+    kv_max = max(b.kv_bytes for b in batch)
+    total = sum(b.kv_bytes for b in batch)
+    cfg = gen_config(w, 1, kv_capacity=5.5 * kv_max)
+    assert cfg.cluster.kv_capacity_per_instance < total
+    out = eng.execute(batch, cfg, 0, token_mode="forced", schedule="stage_barrier")
+    dec = out.decision
+
+    def groups(times):
+        by = {}
+        for i, t in enumerate(times):
+            by.setdefault(t, []).append(i)
+        return [sorted(by[t]) for t in sorted(by)]
+
+    assert groups(list(dec.finish_time)) == groups(list(out.finish_seconds))
+    admits = [e[3] for e in dec.events if e[2] == "admit"]
+    assert admits == list(range(len(batch)))  # FIFO on one instance
+    # more than one wave: the step count exceeds the longest sample
+    assert out.stats["decode_steps"] > max(b.target_output_len for b in batch)
+    assert out.stats["prefill_tokens"] == sum(b.prompt_len - 1 for b in batch)
+
+
+def _eos_of(eng, w, batch):
+    from paper_2409_13221_b200.configs import gen_config
+    probe = eng.execute(batch[:12], gen_config(w, 1), 0, token_mode="greedy", schedule="stage_barrier")
+    vals, cnt = np.unique(probe.experience.tokens, return_counts=True)
+    return int(vals[np.argmax(cnt)])
+
+
+def test_free_run_eos_retirement(toy):
+    """Free-run greedy decode retiring at an emitted EOS (north_star): each response ends
+    at its first EOS or at max_new; the host's readback lag changes nothing; the scored
+    experience matches the oracle's teacher-forced pass over the GPU's tokens."""
+    from paper_2409_13221_b200.configs import gen_config
+    w, eng, batch, orc = toy
+    eos = _eos_of(eng, w, batch)
+    a = eng.execute(batch, gen_config(w, 1), 0, token_mode="greedy", schedule="fused", eos_id=eos, eos_lag=0,
+                    claim_tokens=512)
+    b = eng.execute(batch, gen_config(w, 1), 0, token_mode="greedy", schedule="stage_barrier", eos_id=eos,
+                    eos_lag=3)
+    for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret", "score"):
+        assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
+    assert np.array_equal(a.experience.resp_off, b.experience.resp_off)
+    assert a.stats["overrun_rows"] == 0 and b.stats["eos_retired"] == a.stats["eos_retired"] > 0
+    lens = np.diff(a.experience.resp_off)
+    assert lens.min() < lens.max()
+    prompts = eng.synthetic_prompts(w.n_prompts, 7)
+    for i in range(len(batch)):
+        tk = a.experience.sample(i)["tokens"]
+        first = np.flatnonzero(tk == eos)
+        assert (len(first) == 0 and len(tk) == w.max_new) or first[0] == len(tk) - 1, i
+    for i in range(0, len(batch), 5):
+        got = a.experience.sample(i)
+        ref = orc.experience(prompts[i, :batch[i].prompt_len], got["tokens"], 0.05, 1.0, 0.95)
+        for k, (mx, mean) in _cmp(got, ref).items():
+            scale = max(1.0, float(np.max(np.abs(ref[k]))))
+            assert mx <= TOL_MAX * scale and mean <= TOL_MEAN * scale, (i, k, mx, mean)
+
+
+@pytest.mark.parametrize("top_k,top_p", [(40, 1.0), (0, 0.9), (16, 0.8)])
+def test_filtered_sampling_in_engine(toy, top_k, top_p):
+    """top-k / top-p decode steps: schedule-independent bits, log-probs under the full
+    temperature softmax (the oracle's teacher-forced log-probs of the sampled tokens)."""
+    from paper_2409_13221_b200.configs import gen_config
+    w, eng, batch, orc = toy
+    kw = dict(token_mode="sample", temperature=0.9, top_k=top_k, top_p=top_p)
+    a = eng.execute(batch, gen_config(w, 1), 0, schedule="fused", claim_tokens=512, **kw)
+    b = eng.execute(batch, gen_config(w, 1), 0, schedule="stage_barrier", **kw)
+    for k in ("tokens", "logp_actor", "adv", "score"):
+        assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
+    unf = eng.execute(batch, gen_config(w, 1), 0, schedule="stage_barrier", token_mode="sample", temperature=0.9)
+    assert not np.array_equal(unf.experience.tokens, a.experience.tokens)  # the filter changes the draws
+    prompts = eng.synthetic_prompts(w.n_prompts, 7)
+    for i in range(0, len(batch), 7):
+        got = a.experience.sample(i)
+        ref = orc.score_sample(prompts[i, :batch[i].prompt_len], got["tokens"], temperature=0.9)
+        d = np.abs(got["logp_actor"] - ref["logp_actor"])
+        assert d.max() <= TOL_MAX and d.mean() <= TOL_MEAN, (i, d.max(), d.mean())
+
+
+def test_load_weights_bit_identical_to_seeded(toy):
+    """fp_engine_load_weights: the oracle's tensors (same bits as the hash-seeded
+    engine weights), loaded row-major into an engine seeded differently, give an
+    experience batch bit-identical to the seeded engine's."""
+    from model_oracle import make_weights
+    from paper_2409_13221_b200.configs import gen_config
+    from paper_2409_13221_b200.engine import Engine
+    w, eng, batch, orc = toy
+    e2 = Engine(w, device=0, weight_seed=999)
+    try:
+        assert e2.model_checksum("actor") != eng.model_checksum("actor")
+        for name, m in (("actor", 0), ("ref", 1), ("critic", 2), ("reward", 3)):
+            e2.load_weights(name, orc.models[m])
+            assert e2.model_checksum(name) == eng.model_checksum(name), name
+        a = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="stage_barrier")
+        b = e2.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="stage_barrier")
+        for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret", "score"):
+            assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
+        with pytest.raises(Exception):
+            e2.load_weights("critic", {"head": orc.models[0]["head"]})  # critic has a value head
+    finally:
+        e2.close()

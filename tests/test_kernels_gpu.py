@@ -326,3 +326,202 @@ def test_attn_decode_batch_independent(lib, hd, H, KVH):
         torch.cuda.synchronize()
         outs.append(out)
     assert torch.equal(outs[0], outs[1][:Bs])
+
+
+# ---------------------------------------------------------------------------
+# The shapes the bench runs: configs[2] (1.3B: d 2048, hd 128 MHA, F 5632,
+# V 32000) and configs[3] (Llama-3-8B: d 4096, GQA 32/8 hd 128, F 14336,
+# V 128256), at decode (M 1 / 64), mid (300) and full-batch (512) row counts.
+# Tolerances as above: fp32 outputs 1e-3, bf16 outputs 2e-2 of the output scale.
+
+BENCH_M = [1, 64, 300, 512]
+
+
+@pytest.mark.parametrize("M", BENCH_M)
+@pytest.mark.parametrize("N,K", [(6144, 2048), (6144, 4096)])  # QKV of 1.3B / 8B
+def test_gemm_bf16_bench_shapes(lib, M, N, K):
+    W = rand_bf16(N, K, scale=K ** -0.5, seed=21)
+    X = rand_bf16(M, K, seed=22)
+    out = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    ok(lib, lib.fp_k_gemm_bf16(ptr(W), N, K, ptr(X), M, ptr(out), N, stream()))
+    ref = X.float() @ W.float().T
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("M", BENCH_M)
+@pytest.mark.parametrize("N,K", [(2048, 2048), (2048, 5632), (4096, 4096), (4096, 14336)])  # O / down projections
+def test_gemm_f32_splitk_bench_shapes(lib, M, N, K):
+    W = rand_bf16(N, K, scale=K ** -0.5, seed=23)
+    X = rand_bf16(M, K, seed=24)
+    s = lib.fp_k_gemm_splits(N, K)
+    out = torch.zeros((s, M, N), device="cuda", dtype=torch.float32)
+    ok(lib, lib.fp_k_gemm_f32(ptr(W), N, K, ptr(X), M, ptr(out), s, stream()))
+    ref = X.float() @ W.float().T
+    torch.cuda.synchronize()
+    err = (out.sum(0) - ref).abs().max().item()
+    assert err <= 1e-3 * max(1.0, ref.abs().max().item()), err
+
+
+def _swiglu_case(F, K, M, seed):
+    G = rand_bf16(F, K, scale=K ** -0.5, seed=seed)
+    U = rand_bf16(F, K, scale=K ** -0.5, seed=seed + 1)
+    Wgu = torch.stack([G.view(F // 64, 64, K), U.view(F // 64, 64, K)], 1).reshape(2 * F, K).contiguous()
+    X = rand_bf16(M, K, seed=seed + 2)
+    ref = torch.nn.functional.silu(X.float() @ G.float().T) * (X.float() @ U.float().T)
+    return Wgu, X, ref
+
+
+@pytest.mark.parametrize("decode", [False, True])
+@pytest.mark.parametrize("M", BENCH_M)
+@pytest.mark.parametrize("F,K", [(5632, 2048), (14336, 4096)])
+def test_gemm_swiglu_bench_shapes(lib, M, F, K, decode):
+    Wgu, X, ref = _swiglu_case(F, K, M, 25)
+    out = torch.zeros((M, F), device="cuda", dtype=torch.bfloat16)
+    fn = lib.fp_k_gemm_swiglu_decode if decode else lib.fp_k_gemm_swiglu
+    ok(lib, fn(ptr(Wgu), F, K, ptr(X), M, ptr(out), stream()))
+    torch.cuda.synchronize()
+    err = (out.float() - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
+@pytest.mark.parametrize("M", [1, 64, 300])
+@pytest.mark.parametrize("V,K", [(32000, 2048), (128256, 4096)])
+def test_vocab_bench_shapes(lib, M, V, K):
+    X = rand_bf16(M, K, seed=26)
+    W = rand_bf16(V, K, scale=3 * K ** -0.5, seed=27)
+    logits = X.float() @ W.float().T
+    lsm = torch.log_softmax(logits, -1)
+    tgt = torch.randint(0, V, (M,), device="cuda", dtype=torch.int32)
+    tok = torch.zeros(M, device="cuda", dtype=torch.int32)
+    lp = torch.zeros(M, device="cuda", dtype=torch.float32)
+    ok(lib, lib.fp_k_vocab(ptr(X), M, K, ptr(W), V, 0, 1.0, ptr(tgt), None, None, 0, ptr(tok), ptr(lp), stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(tok, tgt)
+    assert (lp - lsm.gather(1, tgt.long()[:, None])[:, 0]).abs().max().item() < 2e-3
+    ok(lib, lib.fp_k_vocab(ptr(X), M, K, ptr(W), V, 1, 1.0, None, None, None, 0, ptr(tok), ptr(lp), stream()))
+    torch.cuda.synchronize()
+    top2 = logits.topk(2, -1).values
+    clear = (top2[:, 0] - top2[:, 1]) > 1e-3
+    assert torch.equal(tok.long()[clear], logits.argmax(-1)[clear])
+
+
+@pytest.mark.parametrize("M", [1, 64, 300])
+@pytest.mark.parametrize("H,KVH,K", [(16, 16, 2048), (32, 8, 4096)])
+def test_qkv_rope_bench_shapes(lib, H, KVH, K, M):
+    hd, L, layer, PT, max_pos, theta = 128, 2, 1, 64, 4352, 10000.0
+    N = (H + 2 * KVH) * hd
+    W = rand_bf16(N, K, scale=K ** -0.5, seed=28)
+    X = rand_bf16(M, K, seed=29)
+    g = torch.Generator(device="cuda").manual_seed(30)
+    pos = torch.randint(0, max_pos, (M,), device="cuda", generator=g, dtype=torch.int32)
+    maxp = (max_pos + PT - 1) // PT
+    npages = M * maxp + 1
+    pool = torch.zeros(npages, L, KVH, 2, PT, hd, device="cuda", dtype=torch.bfloat16)
+    bt = (torch.randperm(npages - 1, device="cuda", generator=g)[: M * maxp] + 1).to(torch.int32).view(M, maxp)
+    slot = torch.randperm(M, device="cuda", generator=g).to(torch.int32)
+    q = torch.zeros(M, H, hd, device="cuda", dtype=torch.bfloat16)
+    ok(lib, lib.fp_k_qkv_rope(ptr(W), K, ptr(X), M, H, KVH, hd, ptr(pos), max_pos, theta, ptr(pool), L, layer,
+                              ptr(bt.contiguous()), maxp, ptr(slot), ptr(q), stream()))
+    torch.cuda.synchronize()
+    qkv = (X.float() @ W.float().T).to(torch.bfloat16).float().view(M, H + 2 * KVH, hd)
+    half = hd // 2
+    inv = torch.exp2(-(2.0 * torch.arange(half, device="cuda") / hd) * np.log2(theta))
+    ang = pos.float()[:, None] * inv[None]
+    c, s = ang.cos()[:, None], ang.sin()[:, None]
+    x1, x2 = qkv[..., :half], qkv[..., half:]
+    rot = torch.cat([x1 * c - x2 * s, x2 * c + x1 * s], -1)
+    tol = 2e-2 * qkv.abs().max().item()
+    assert (q.float() - rot[:, :H]).abs().max().item() < tol
+    for m in range(0, M, max(1, M // 16)):
+        p = int(pos[m])
+        page = int(bt[int(slot[m]), p // PT])
+        assert (pool[page, layer, :, 0, p % PT].float() - rot[m, H:H + KVH]).abs().max().item() < tol, m
+        assert (pool[page, layer, :, 1, p % PT].float() - qkv[m, H + KVH:]).abs().max().item() < tol, m
+
+
+@pytest.mark.parametrize("hd,H,KVH", [(128, 32, 8), (128, 16, 16)])
+@pytest.mark.parametrize("ctx_list", [[4352, 4096, 1, 2047, 513], [4352] * 3 + list(range(100, 4300, 61))])
+def test_attn_decode_long_context(lib, hd, H, KVH, ctx_list):
+    """Decode attention at the 8B config's contexts (prompt 256 + up to 4096 new)."""
+    L, layer, PT = 2, 1, 64
+    B = len(ctx_list)
+    maxp = (max(ctx_list) + PT - 1) // PT
+    npages = B * maxp + 1
+    g = torch.Generator(device="cuda").manual_seed(31)
+    pool = (torch.randn(npages, L, KVH, 2, PT, hd, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    bt = (torch.randperm(npages - 1, device="cuda", generator=g)[: B * maxp] + 1).to(torch.int32).view(B, maxp)
+    slot = torch.arange(B, device="cuda", dtype=torch.int32)
+    ctx = torch.tensor(ctx_list, device="cuda", dtype=torch.int32)
+    q = torch.randn(B, H, hd, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.zeros(B, H, hd, device="cuda", dtype=torch.bfloat16)
+    ok(lib, lib.fp_k_attn_decode(ptr(q), B, H, KVH, hd, ptr(pool), npages, L, layer, ptr(bt.contiguous()), maxp,
+                                 ptr(slot), ptr(ctx), max(ctx_list), ptr(out), stream()))
+    torch.cuda.synchronize()
+    grp = H // KVH
+    for b in range(0, B, max(1, B // 12)):
+        pages = bt[b].long()
+        kv = pool[pages, layer].float()
+        k = kv[:, :, 0].permute(1, 0, 2, 3).reshape(KVH, -1, hd)[:, : ctx_list[b]].repeat_interleave(grp, 0)
+        v = kv[:, :, 1].permute(1, 0, 2, 3).reshape(KVH, -1, hd)[:, : ctx_list[b]].repeat_interleave(grp, 0)
+        s = torch.einsum("hd,hsd->hs", q[b].float(), k) / hd ** 0.5
+        ref = torch.einsum("hs,hsd->hd", s.softmax(-1), v)
+        assert (out[b].float() - ref).abs().max().item() < 2e-2, b
+
+
+# ---------------------------------------------------------------------------
+# Filtered sampling (top-k / top-p): the kernel's own z rows are replayed by
+# the oracle (model_oracle.filtered_sample), so only exp2 rounding may differ.
+
+@pytest.mark.parametrize("top_k,top_p", [(1, 1.0), (20, 1.0), (50, 0.9), (0, 0.8), (1024, 0.95)])
+@pytest.mark.parametrize("V", [3000, 32000])
+def test_vocab_filtered_matches_oracle(lib, V, top_k, top_p):
+    from model_oracle import filtered_sample
+    M, K = 24, 256
+    X = rand_bf16(M, K, seed=40)
+    W = rand_bf16(V, K, scale=4 * K ** -0.5, seed=41)
+    sid = torch.arange(M, device="cuda", dtype=torch.int32) * 5 + 1
+    stp = torch.arange(M, device="cuda", dtype=torch.int32) + 3
+    tok = torch.zeros(M, device="cuda", dtype=torch.int32)
+    lp = torch.zeros(M, device="cuda", dtype=torch.float32)
+    z = torch.zeros(M, V, device="cuda", dtype=torch.float32)
+    seed, inv_t = 0xABCDEF12345, 1.0 / 0.8
+    ok(lib, lib.fp_k_vocab_filtered(ptr(X), M, K, ptr(W), V, inv_t, top_k, top_p, ptr(sid), ptr(stp), seed, ptr(tok),
+                                    ptr(lp), ptr(z), stream()))
+    torch.cuda.synchronize()
+    zr = (X.float() @ W.float().T) * inv_t
+    assert (z - zr).abs().max().item() < 1e-3 * max(1.0, zr.abs().max().item())
+    lsm = torch.log_softmax(z, -1)
+    zn = z.cpu().numpy()
+    agree = 0
+    for i in range(M):
+        want, keep = filtered_sample(zn[i], top_k, top_p, seed, int(sid[i]), int(stp[i]))
+        t = int(tok[i])
+        assert t in keep  # never outside the filtered set
+        agree += int(t == want)
+        assert abs(float(lp[i]) - float(lsm[i, t])) < 2e-3  # log-prob under the full softmax
+    assert agree >= M - 1, agree
+    if top_k == 1:
+        assert torch.equal(tok.long(), z.argmax(-1))
+
+
+def test_vocab_filtered_distribution(lib):
+    """top-k = 5 over many Philox streams: frequencies follow the renormalised top-5 softmax."""
+    M, V, K = 4096, 300, 64
+    X = rand_bf16(1, K, seed=42).repeat(M, 1).contiguous()
+    W = rand_bf16(V, K, scale=6 * K ** -0.5, seed=43)
+    sid = torch.arange(M, device="cuda", dtype=torch.int32)
+    stp = torch.zeros(M, device="cuda", dtype=torch.int32)
+    tok = torch.zeros(M, device="cuda", dtype=torch.int32)
+    lp = torch.zeros(M, device="cuda", dtype=torch.float32)
+    ok(lib, lib.fp_k_vocab_filtered(ptr(X), M, K, ptr(W), V, 1.0, 5, 1.0, ptr(sid), ptr(stp), 7, ptr(tok), ptr(lp),
+                                    None, stream()))
+    torch.cuda.synchronize()
+    z = X[0].float() @ W.float().T
+    top = z.topk(5)
+    p = torch.softmax(top.values, -1)
+    freq = torch.bincount(tok.long(), minlength=V).float() / M
+    assert freq.sum().item() == pytest.approx(1.0)
+    assert (freq[top.indices].sum() - 1.0).abs().item() < 1e-6  # all mass inside the top 5
+    assert (freq[top.indices] - p).abs().max().item() < 0.03

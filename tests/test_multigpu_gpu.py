@@ -1,9 +1,10 @@
-"""Multi-GPU fused schedule on real B200s (needs >= 2 GPUs; skipped otherwise).
+"""Multi-rank executor on B200s (tests/mgpu_worker.py under torchrun, world 2).
 
-torchrun launches tests/mgpu_worker.py on 2 ranks: the long-tail migration
-(KV pages pulled over NVLink through CUDA IPC) must execute exactly the
-decision clock's moves, and the gathered experience must be bit-identical to
-a single-GPU stage-barrier run of the same batch.
+Two placements: one GPU per rank (needs 2 GPUs), and both ranks on cuda:0
+(FP_MGPU_SAME_DEVICE=1) so that the multi-rank path — long-tail migration
+through CUDA IPC, the cross-rank scoring queue, the hand-off and the weight
+broadcast — is exercised on a 1-GPU box too. See mgpu_worker.py for what each
+scenario checks.
 """
 import json
 import os
@@ -25,24 +26,41 @@ def _gpus():
         return 0
 
 
-@pytest.mark.parametrize("world", [2])
-@pytest.mark.parametrize("mode,mech", [("forced", "kv"), ("greedy", "kv"), ("forced", "recompute")])
-def test_fused_migration_matches_single_gpu(tmp_path, world, mode, mech):
-    if _gpus() < world:
+def _run(tmp_path, scenario, placement, world=2):
+    if placement == "own_device" and _gpus() < world:
         pytest.skip(f"needs {world} GPUs")
+    if placement == "same_device" and _gpus() < 1:
+        pytest.skip("needs a GPU")
     out = tmp_path / "res.json"
+    env = dict(os.environ)
+    if placement == "same_device":
+        env["FP_MGPU_SAME_DEVICE"] = "1"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29500 + os.getpid() % 1000),
-           str(ROOT / "tests" / "mgpu_worker.py"), str(out), mode, mech]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + (os.getpid() * 7 + hash(scenario)) % 1000),
+           str(ROOT / "tests" / "mgpu_worker.py"), str(out), scenario]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(out.read_text())
-    assert not res["plan"]["no_op"]
-    assert res["plan"]["mechanism"] == ("kv_transfer" if mech == "kv" else "recompute_prefill")
-    assert res["moves_match"], res
+    print(json.dumps({k: v for k, v in res.items() if k not in ("stats", "received", "moves")}))
+    return res
+
+
+def _common(res):
     assert res["handoff_ok"] and res["handoff_peer_bytes"] > 0, res
     assert res["bcast"]["same"] and res["bcast"]["changed"], res["bcast"]
-    if mech == "kv":
+    assert res["moves_equal_received"], (res["moves"], res["received"])
+
+
+@pytest.mark.parametrize("placement", ["same_device", "own_device"])
+@pytest.mark.parametrize("scenario", ["clock-forced-kv", "clock-greedy-kv", "clock-forced-recompute"])
+def test_clock_trigger_migration(tmp_path, placement, scenario):
+    res = _run(tmp_path, scenario, placement)
+    assert not res["plan"]["no_op"]
+    assert res["plan"]["mechanism"] == ("recompute_prefill" if "recompute" in scenario else "kv_transfer")
+    _common(res)
+    assert res["received"], "nothing migrated"
+    assert res["received_match_clock"], res["received"]
+    if "recompute" not in scenario:
         # KV pages are moved verbatim: bit-identical to the single-GPU run
         assert res["identical"], res["diffs_vs_1gpu"]
     else:
@@ -51,3 +69,27 @@ def test_fused_migration_matches_single_gpu(tmp_path, world, mode, mech):
         # within the engine tolerance
         assert res["diffs_vs_1gpu"]["tokens"] == 0
         assert max(res["max_abs"].values()) <= 0.15, res["max_abs"]
+
+
+@pytest.mark.parametrize("placement", ["same_device", "own_device"])
+def test_online_trigger_forced(tmp_path, placement):
+    res = _run(tmp_path, "online-forced", placement)
+    assert res["online"]
+    assert res["n_unfinished_at_trigger"] < res["r_t"]
+    assert res["moves_within_plan"], res
+    _common(res)
+    assert res["identical"], res["diffs_vs_1gpu"]
+
+
+@pytest.mark.parametrize("placement", ["same_device", "own_device"])
+def test_online_trigger_free_run_eos(tmp_path, placement):
+    res = _run(tmp_path, "online-eos", placement)
+    assert res["online"]
+    assert res["eos_semantics_ok"]
+    assert sum(s["eos_retired"] for s in res["stats"]) > 0, res["lengths"]
+    assert res["lengths"]["min"] < res["lengths"]["max"]
+    assert res["n_unfinished_at_trigger"] < res["r_t"]
+    assert res["moves_within_plan"], res
+    _common(res)
+    # lengths and every experience array equal a 1-GPU free-run (eos_lag 0 there, 2 here)
+    assert res["identical"], res["diffs_vs_1gpu"]

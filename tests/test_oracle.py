@@ -88,3 +88,17 @@ def test_forced_responses_deterministic():
     a = forced_response(3, 50, 512, 2048, 7)
     assert np.array_equal(a, forced_response(3, 50, 512, 2048, 7))
     assert a.min() >= 0 and a.max() < 2048
+
+
+def test_c_weight_generator_matches_numpy_restatement():
+    """oracle/weights_oracle.c (threaded, used for the bench-size oracle models)
+    gives the numpy restatement's bits."""
+    import model_oracle as mo
+    if mo._clib() is None:
+        pytest.skip("oracle C library not built (make -C oracle liboracle)")
+    for n, scale, tag in [(1, 0.5, 3), (4099, mo.fsqrt(np.float32(3.0) / np.float32(768)), mo.weight_tag(2, 7, 4)),
+                          (65536, mo.fsqrt(np.float32(3.0) / np.float32(14336)), mo.weight_tag(0, 31, 5))]:
+        a, b = mo.uniform_weight(1234, tag, n, scale), mo.uniform_weight_np(1234, tag, n, scale)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+        a, b = mo.gain(99, tag, n), mo.gain_np(99, tag, n)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
