@@ -127,11 +127,17 @@ def workload_desc(w, G):
             f"V{a.vocab}), {w.n_prompts // G} prompts x {w.prompt_len} tokens per GPU, <= {w.max_new} new")
 
 
+_ORACLES = {}
+
+
 def cpu_oracle_rate(w, batch, n_samples: int, time_budget: float = 30.0):
-    """Samples/s of the numpy CPU oracle on the first samples of the batch (all host threads)."""
+    """Samples/s of the numpy CPU oracle on the first samples of the batch (all host threads).
+    The oracle's weights are built once, outside the timed region."""
     sys.path.insert(0, str(ROOT / "oracle"))
     from model_oracle import Oracle, forced_response, synthetic_prompts
-    orc = Oracle(w)
+    if w.name not in _ORACLES:
+        _ORACLES[w.name] = Oracle(w)
+    orc = _ORACLES[w.name]
     prompts = synthetic_prompts(len(batch), w.prompt_len, w.actor.vocab, 7)
     t0 = time.perf_counter()
     done = 0
@@ -147,47 +153,76 @@ def cpu_oracle_rate(w, batch, n_samples: int, time_budget: float = 30.0):
     return done / dt, done, tokens, dt
 
 
+def python_batch(w):
+    """The batch the GPU arm runs, built without the product library: the
+    reference's make_batch (genfuse.cpp:403-414) from oracle/_ref when it was
+    built here, else the same arithmetic in Python (kv_bytes_per_token =
+    4 L hidden, core.cpp:90-93)."""
+    from paper_2409_13221_b200.configs import zipf_lengths
+    lens = zipf_lengths(w.n_prompts, w.max_new, w.zipf_s, w.zipf_lo, w.length_seed)
+    ref_lib = ROOT / "oracle" / "_ref" / "libfuseplan_ref.so"
+    if ref_lib.exists():
+        from paper_2409_13221_b200.configs import batch_for
+        from paper_2409_13221_b200.sched import Sched
+        return batch_for(w, Sched(str(ref_lib)), lengths=lens), "reference make_batch (oracle/_ref)"
+    from paper_2409_13221_b200.sched import GenSample
+    kv = 4.0 * w.actor.num_layers * w.actor.hidden
+    return [GenSample(i, w.prompt_len, L, 0, (w.prompt_len + L) * kv) for i, L in enumerate(lens)], "python"
+
+
 def run_reference(args, world, rank):
     """--impl reference: the reference's CPU path. The reference library only
     simulates this stage (cost formulas, no model math), so the
     CPU implementation of the path that produces experience is the oracle
-    port; the simulator's own runtime is reported beside it."""
+    port (numpy fp32, all host threads through BLAS); the simulator's own
+    runtime is reported beside it. Nothing here loads the product library."""
     if rank != 0:
         return
-    from paper_2409_13221_b200.configs import batch_for, gen_config
-    from paper_2409_13221_b200.sched import Sched
     w = workload_for(args.gpus, args.workload, args.zipf_s)
-    sched = Sched()
-    batch = batch_for(w, sched)
+    batch, batch_src = python_batch(w)
     cores = os.cpu_count() or 1
-    rates = []
+    n_sub = {"gpt2s": 2, "1.3b": 1, "8b": 1}.get(w.name, 2)
+    rates, walls = [], []
     info = None
     for step in range(args.warmup + args.steps):
-        r, done, toks, dt = cpu_oracle_rate(w, batch, n_samples=2, time_budget=20.0)
+        t0 = time.perf_counter()
+        r, done, toks, dt = cpu_oracle_rate(w, batch, n_samples=n_sub, time_budget=15.0)
         if step >= args.warmup:
             rates.append(r)
+            walls.append(time.perf_counter() - t0)
             info = (done, toks, dt)
     value = statistics.median(rates)
     sim = None
     ref_lib = ROOT / "oracle" / "_ref" / "libfuseplan_ref.so"
     if ref_lib.exists():
+        from paper_2409_13221_b200.configs import gen_config
+        from paper_2409_13221_b200.sched import Sched
         rs = Sched(str(ref_lib))
         cfg = gen_config(w, args.gpus, calibrated=True)
         t0 = time.perf_counter()
         rs.simulate_fused(batch, cfg, round(0.2 * len(batch)))
         sim = time.perf_counter() - t0
     sample = (f"{info[0]} of {len(batch)} prompts ({info[1]} tokens) teacher-forced through actor/ref/critic/reward "
-              f"+ KL/GAE post-processing, numpy fp32, {info[2]:.1f}s per step")
+              f"+ KL/GAE post-processing, numpy fp32; step = that subset")
+    cfg_line = config_dict(w, args.gpus, args)
+    cfg_line["cpu_subset"] = f"{info[0]} of {len(batch)} prompts per step (batch built by {batch_src})"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * len(batch) / value,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * statistics.median(walls),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "config": {"workload": w.name, "prompts": len(batch), "prompt_len": w.prompt_len,
-                                            "max_new": w.max_new},
+            "data": "synthetic", "config": cfg_line,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "reference_simulator_seconds": sim,
-            "note": "reference path is a discrete-event simulator without model math; CPU arm = oracle port"}
+            "note": "reference path is a discrete-event simulator without model math; CPU arm = oracle port; "
+                    "ms_per_step = measured wall time of the subset"}
     print(json.dumps(line), flush=True)
+
+
+def config_dict(w, G, args, r_t=None, ratio=None):
+    return {"workload": workload_desc(w, G), "prompts": w.n_prompts, "zipf_s": w.zipf_s, "schedule": "fused",
+            "r_t": r_t, "r_ratio": ratio, "token_mode": args.token_mode, "claim_tokens": args.claim_tokens,
+            "l2": "inputs larger than L2 (KV pool and weights >> 126 MB)",
+            "parallelism": f"dp{G} (one engine per B200)"}
 
 
 def main():
@@ -319,40 +354,56 @@ def main():
                "sample": f"{done} of {len(batch)} prompts ({toks} tokens) through the numpy oracle "
                          f"(teacher-forced actor/ref/critic/reward + post-processing), {dt:.1f}s"}
 
+    # per-rank decode / scoring totals of the value steps, summed over ranks
+    # (every rank decodes its own shard; any rank may score any sample)
+    mine = {"dec_s": sum(o.stats["decode_gpu_seconds"] for o in outs_v),
+            "steps": sum(o.stats["decode_steps"] for o in outs_v),
+            "rows": sum(o.stats["decode_rows"] for o in outs_v),
+            "ctx": sum(o.stats["decode_ctx_tokens"] for o in outs_v),
+            "inf_s": sum(o.stats["infer_busy_seconds"] for o in (outs_s or outs_v)),
+            "inf_steps": len(outs_s or outs_v)}
+    ranks = [mine]
+    if dist:
+        ranks = [None] * G
+        dist.all_gather_object(ranks, mine)
     if rank != 0:
         eng.close()
         return
     hbm, tflops, src = peaks()
-    w_bytes = eng.model_size(0)[0]
+    a = w.actor
+    embed_bytes = a.vocab * a.hidden * 2
+    w_step = eng.model_size(0)[0] - embed_bytes  # weights streamed once per step; the embedding is gathered
     kvb = eng.kv_bytes_per_token()
-    dec_s = sum(o.stats["decode_gpu_seconds"] for o in outs_v)
-    dec_b = sum(o.stats["decode_steps"] * w_bytes + o.stats["decode_ctx_tokens"] * kvb for o in outs_v)
+    dec_s = sum(r["dec_s"] for r in ranks)
+    dec_b = sum(r["steps"] * w_step + r["rows"] * (a.hidden * 2 + kvb) + r["ctx"] * kvb for r in ranks)
     decode_roofline = {"bound": "hbm", "bytes_per_step": dec_b / len(outs_v), "seconds_per_step": dec_s / len(outs_v),
                        "achieved": dec_b / dec_s / 1e9 if dec_s else None, "peak": hbm, "unit": "GB/s",
-                       "frac": dec_b / dec_s / 1e9 / hbm if dec_s else None,
-                       "note": "decode_steps x actor weight bytes + sum over rows and steps of ctx x K/V bytes per "
-                               "token, / sum of decode-step GPU time (rank 0)"}
+                       "frac": dec_b / dec_s / 1e9 / hbm if dec_s else None, "ranks": len(ranks),
+                       "note": "all ranks: decode steps x actor weight bytes without the embedding table + per row "
+                               "its gathered embedding row and K/V append + sum over rows of ctx x K/V bytes per "
+                               "token, / the ranks' summed decode-step GPU time"}
     # scoring (Ref/Critic/Reward forward over prompt + response) against the
     # bf16 tensor peak: algorithmic flops = 2 x dense weights per token (ref
     # adds the vocab head for its log-probs) + causal attention 2 T^2 H hd L,
-    # over the scoring stream's busy GPU time (stage-barrier arm when run, so
-    # decode does not share the SMs)
+    # over the scoring streams' busy GPU time summed over ranks (stage-barrier
+    # arm when run, so decode does not share the SMs); each sample is scored
+    # exactly once, on whichever rank claimed it
     def fwd_flops(d, T, vocab_head):
         dense = d.param_count(lm_head=False) - d.vocab * d.hidden
         return 2 * T * (dense + (d.hidden * d.vocab if vocab_head else d.hidden)) + \
             2 * T * T * d.num_heads * d.head_dim * d.num_layers
-    src_outs, src_name = (outs_s, "stage_barrier") if outs_s else (outs_v, "fused (overlaps decode)")
+    src_name = "stage_barrier" if outs_s else "fused (overlaps decode)"
     inf_flops = sum(fwd_flops(w.ref, s.prompt_len + s.target_output_len, True) +
                     fwd_flops(w.critic, s.prompt_len + s.target_output_len, False) +
-                    fwd_flops(w.reward, s.prompt_len + s.target_output_len, False) for s in batch if s.id % G == 0)
-    inf_s = statistics.mean(o.stats["infer_busy_seconds"] for o in src_outs)
+                    fwd_flops(w.reward, s.prompt_len + s.target_output_len, False) for s in batch)
+    inf_s = sum(r["inf_s"] for r in ranks) / ranks[0]["inf_steps"]
     inf_tf = inf_flops / inf_s / 1e12 if inf_s else None
     inference_roofline = {"bound": "tensor", "achieved": inf_tf, "peak": tflops, "unit": "TFLOP/s",
                           "frac": inf_tf / tflops if inf_tf else None, "flops_per_step": inf_flops,
-                          "seconds_per_step": inf_s, "arm": src_name,
-                          "note": "ref/critic/reward forward over rank 0's samples (prompt + target response): "
+                          "seconds_per_step": inf_s, "arm": src_name, "ranks": len(ranks),
+                          "note": "ref/critic/reward forward over every sample (prompt + target response): "
                                   "2 x dense weights per token (+ vocab head for ref) + causal attention "
-                                  "2 T^2 H hd L; / the scoring stream's busy GPU time"}
+                                  "2 T^2 H hd L; / the scoring streams' busy GPU time summed over ranks"}
     achieved = (probe_bytes / (probe_ms / 1000.0)) / 1e9 if probe_ms > 0 else None
     # traffic: DRAM bytes per launch from the committed ncu --set full capture
     # of this kernel (profiles/attn_decode_traffic.json), as its DRAM /
@@ -370,11 +421,7 @@ def main():
         "data": "synthetic: hash-seeded random-init weights and prompts, "
                 f"Zipf(s={w.zipf_s}) output lengths on [{w.zipf_lo}, {w.max_new}], "
                 f"{args.token_mode} tokens",
-        "config": {"workload": workload_desc(w, G),
-                   "prompts": n_total, "zipf_s": w.zipf_s, "schedule": "fused", "r_t": r_t, "r_ratio": ratio if G > 1 else 0.0, "token_mode": args.token_mode,
-                   "claim_tokens": args.claim_tokens,
-                   "l2": "inputs larger than L2 (KV pool and weights >> 126 MB)",
-                   "parallelism": f"dp{G} (one engine per B200)"},
+        "config": config_dict(w, G, args, r_t, ratio if G > 1 else 0.0),
         "roofline": {"kernel": "attn_decode (paged KV flash-decoding)", "bound": "hbm", "achieved": achieved,
                      "peak": hbm, "unit": "GB/s", "frac": (achieved / hbm) if achieved else None,
                      "traffic": traffic, "traffic_source": traffic_src, "peak_source": src, "launches": probe_n,

@@ -9,7 +9,7 @@
 Teacher-forced responses, bf16 engine vs the fp32 numpy oracle on the same
 weight bits. The measured max / mean |delta| per quantity is written to
 $FP_PARITY_LOG (JSON lines) when set. Gates: per-token log-probs and values
-mean |delta| <= 1e-2, max <= 0.15; GAE / returns relative to
+mean |delta| <= 1e-2, max <= 0.08; GAE / returns relative to
 max(1, max|A|); token ids exact.
 """
 import json
@@ -20,7 +20,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-MEAN_TOL, MAX_TOL = 1e-2, 0.15
+MEAN_TOL, MAX_TOL = 1e-2, 0.08  # measured (profiles/r02_parity_deltas.jsonl): mean <= 0.0094, max <= 0.030
 
 
 def _case(name, dims, n, prompt_len, max_new):
