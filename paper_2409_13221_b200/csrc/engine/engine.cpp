@@ -116,8 +116,12 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
   }
   for (int s = cfg_.max_live - 1; s >= 0; --s) free_slots_.push_back(s);
   if (const char* g = std::getenv("FUSEPLAN_DECODE_GRAPHS")) use_graphs_ = std::atoi(g) != 0;  // A/B switch
-  if (const char* g = std::getenv("FUSEPLAN_L2_PREFETCH")) l2_prefetch_ = std::atoi(g) != 0;
-  if (const char* g = std::getenv("FUSEPLAN_FUSE_NORM")) fuse_norm_ = std::atoi(g) != 0;
+  if (const char* g = std::getenv("FUSEPLAN_DECODE_CHAIN")) chain_ = std::atoi(g) != 0;  // A/B (tested)
+  {
+    int sms = 148;
+    FP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg_.device));
+    chain_ctas_ = sms;
+  }
   if (const char* g = std::getenv("FUSEPLAN_FUSE_ROPE")) fuse_rope_ = std::atoi(g) != 0;
   pad_slot_ = cfg_.max_live;  // decode padding rows: block-table row of zeros -> scratch page 0
   slot_pages_.assign(cfg_.max_live + 1, {});
@@ -429,8 +433,9 @@ void Engine::alloc_ws() {
         static_cast<size_t>(fpk::attn_decode_counters(B, a.KVH, cfg_.max_prompt + cfg_.max_new)) * sizeof(int);
     dw.attn_cnt = static_cast<int*>(dalloc(cnt));
     FP_CUDA(cudaMemsetAsync(dw.attn_cnt, 0, cnt, s_decode_));
-    dw.norm_cnt = static_cast<int*>(dalloc(2 * sizeof(int)));
-    FP_CUDA(cudaMemsetAsync(dw.norm_cnt, 0, 2 * sizeof(int), s_decode_));
+    const size_t ccnt = static_cast<size_t>(cfg_.model[kActor].L) * 8 * sizeof(int);
+    dw.chain_cnt = static_cast<int*>(dalloc(ccnt));
+    FP_CUDA(cudaMemsetAsync(dw.chain_cnt, 0, ccnt, s_decode_));
   };
   decode_ws(dec_, Bcap);
   decode_ws(dec2_, bucket_of((cfg_.max_live + 1) / 2));  // second half of a split step
@@ -827,25 +832,12 @@ void Engine::decode_kernels(DecodeWs& dw, cudaStream_t st, int B, int max_ctx, i
   const int sd = fpk::gemm_splits(D.d, D.F);
 
   fpk::embed(d_cur_tok_, slot, B, w.embed, D.d, dw.x, st);
-  int nparts = 0;
-  // the split-K O / down GEMMs normalise for the next GEMM themselves when
-  // their whole grid fits on the device at once (gemm_f32_splitk_norm checks)
-  const bool fuse_norm = fuse_norm_;
-  bool h_ready = false;  // dw.h already holds the next GEMM's input
+  fpk::add_norm(dw.x, nullptr, 0, stride, w.layers[0].ln1, dw.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
+  fpk::gemm_qkv_rope(w.layers[0].wqkv, D.d, dw.h, B, D.H, D.KVH, D.hd, pos, rope_cs_, pv, 0, slot, dw.q, st);
   for (int l = 0; l < D.L; ++l) {
     const LayerW& L = w.layers[l];
-    const size_t wq = static_cast<size_t>(D.qkv_width()) * D.d * 2, wo = static_cast<size_t>(D.d) * D.H * D.hd * 2;
-    const size_t wgu = static_cast<size_t>(2) * D.F * D.d * 2, wdn = static_cast<size_t>(D.d) * D.F * 2;
-    fpk::L2Prefetch pf1, pf2;  // this layer's weights into L2 ahead of their GEMMs
-    if (l2_prefetch_) {
-      pf1.p[0] = L.wqkv, pf1.bytes[0] = wq, pf1.p[1] = L.wo, pf1.bytes[1] = wo;
-      pf2.p[0] = L.wgu, pf2.bytes[0] = wgu, pf2.p[1] = L.wd, pf2.bytes[1] = wdn;
-    }
-    if (!h_ready)
-      fpk::add_norm(dw.x, nparts ? dw.parts : nullptr, nparts, stride, L.ln1, dw.h, B, D.d, nullptr, 0, nullptr,
-                    nullptr, st, pf1);
-    h_ready = false;
-    fpk::gemm_qkv_rope(L.wqkv, D.d, dw.h, B, D.H, D.KVH, D.hd, pos, rope_cs_, pv, l, slot, dw.q, st);
+    const bool last = l + 1 == D.L;
+    const float* next_gain = last ? w.lnf : w.layers[l + 1].ln1;
     if (probe_on_) {
       ProbeRec pr{probe_event(), probe_event(), 0.0};
       const double kv_tok = 2.0 * D.KVH * D.hd * 2.0;  // K + V of one layer, bf16
@@ -857,19 +849,28 @@ void Engine::decode_kernels(DecodeWs& dw, cudaStream_t st, int B, int max_ctx, i
       fpk::attn_decode(dw.q, B, D.H, D.KVH, D.hd, pv, l, slot, ctx, items, max_ctx, dw.attn_work, dw.attn, dw.attn_cnt, st,
                        nullptr, nullptr, attn_ctas);
     }
-    if (!(fuse_norm && fpk::gemm_f32_splitk_norm(L.wo, D.d, D.H * D.hd, dw.attn, B, dw.parts, so,
-                                                 fpk::NormFuse{dw.x, L.ln2, dw.h, dw.norm_cnt}, st))) {
-      fpk::gemm_f32_splitk(L.wo, D.d, D.H * D.hd, dw.attn, B, dw.parts, so, st);
-      fpk::add_norm(dw.x, dw.parts, so, stride, L.ln2, dw.h, B, D.d, nullptr, 0, nullptr, nullptr, st, pf2);
+    // O -> norm -> gate/up -> down -> norm -> next QKV: one persistent launch
+    // (decode_chain), or the six kernels it replaces (bit-identical)
+    if (chain_) {
+      fpk::DecodeChain c{};
+      c.wo = L.wo, c.wgu = L.wgu, c.wd = L.wd, c.wqkv = last ? nullptr : w.layers[l + 1].wqkv;
+      c.attn = dw.attn, c.h = dw.h, c.act = dw.act, c.parts = dw.parts, c.x = dw.x;
+      c.gain_mlp = L.ln2, c.gain_next = next_gain;
+      c.q_out = dw.q, c.pool = pv, c.slot = slot, c.pos = pos, c.cs = rope_cs_, c.layer = l;
+      c.H = D.H, c.KVH = D.KVH, c.hd = D.hd, c.d = D.d, c.F = D.F, c.ao = D.H * D.hd, c.B = B;
+      c.counters = dw.chain_cnt + 8 * l;
+      c.ctas = chain_ctas_;
+      if (fpk::decode_chain(c, st)) continue;
     }
+    fpk::gemm_f32_splitk(L.wo, D.d, D.H * D.hd, dw.attn, B, dw.parts, so, st);
+    fpk::add_norm(dw.x, dw.parts, so, stride, L.ln2, dw.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
     fpk::gemm_swiglu_decode(L.wgu, D.F, D.d, dw.h, B, dw.act, st);
-    const float* next_gain = l + 1 < D.L ? w.layers[l + 1].ln1 : w.lnf;
-    h_ready = fuse_norm && fpk::gemm_f32_splitk_norm(L.wd, D.d, D.F, dw.act, B, dw.parts, sd,
-                                                     fpk::NormFuse{dw.x, next_gain, dw.h, dw.norm_cnt}, st);
-    if (!h_ready) fpk::gemm_f32_splitk(L.wd, D.d, D.F, dw.act, B, dw.parts, sd, st);
-    nparts = sd;
+    fpk::gemm_f32_splitk(L.wd, D.d, D.F, dw.act, B, dw.parts, sd, st);
+    fpk::add_norm(dw.x, dw.parts, sd, stride, next_gain, dw.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
+    if (!last)
+      fpk::gemm_qkv_rope(w.layers[l + 1].wqkv, D.d, dw.h, B, D.H, D.KVH, D.hd, pos, rope_cs_, pv, l + 1, slot, dw.q,
+                         st);
   }
-  if (!h_ready) fpk::add_norm(dw.x, dw.parts, nparts, stride, w.lnf, dw.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
   if (top_k > 0 || top_p < 1.f) {  // filtered sampling: z materialised, radix-select filter, then forced finalize
     if (!dw.logits) {  // first use runs eagerly (run_graph), never inside a capture
       dw.logits = static_cast<float*>(dalloc(static_cast<size_t>(dw.cap) * logits_ld() * sizeof(float)));

@@ -207,8 +207,8 @@ class Engine {
   bool use_graphs_ = true;
   bool fuse_rope_ = true;  // prefill / scoring: RoPE + K/V writes in the QKV GEMM epilogue
   int decode_calls_ = 0;
-  bool fuse_norm_ = false;    // decode: add_norm fused into the split-K O / down GEMMs (FUSEPLAN_FUSE_NORM; measured slower)
-  bool l2_prefetch_ = false;  // decode: pull each layer's weights into L2 ahead of its GEMMs (measured slower: off)
+  bool chain_ = true;     // decode: the GEMM chain of a layer as one persistent kernel (fpk::decode_chain)
+  int chain_ctas_ = 148;  // its grid: one CTA per SM
   int pad_slot_ = 0;
   struct GraphKey {
     int B, B1, mode;  // B1: second half of a split step (0: unsplit)
@@ -269,7 +269,7 @@ class Engine {
     int cap = 0;
     float *x = nullptr, *parts = nullptr, *attn_work = nullptr;
     int* attn_cnt = nullptr;  // split-merge tickets of the decode attention (B x KVH, kept zero)
-    int* norm_cnt = nullptr;  // grid counters of the split-K GEMMs' fused norm (2, kept zero)
+    int* chain_cnt = nullptr;  // grid-barrier counters of decode_chain, 8 per layer (kept zero)
     bf16 *h = nullptr, *qkv = nullptr, *q = nullptr, *attn = nullptr, *act = nullptr;
     int* rows = nullptr;  // 7 x cap: slot, pos, ctx, dst, target, sid, step
     void* vocab_part = nullptr;

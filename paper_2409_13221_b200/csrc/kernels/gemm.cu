@@ -277,6 +277,13 @@ CUtensorMap make_kv_map(const void* pool, long long rows, int hd) {
 
 void set_gemm_trace(unsigned long long* buf) { g_trace = buf; }
 
+// Map / tile-width helpers of the persistent decode chain (chain.cu).
+CUtensorMap chain_operand_map(const void* ptr, int rows, int k, int box_rows) { return make_map(ptr, rows, k, box_rows); }
+CUtensorMap chain_out_map_bf16(const void* ptr, int rows, int cols, int ld, int box_cols, int box_rows) {
+  return out_map_2d(ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, cols, ld, box_cols, box_rows);
+}
+int chain_pick_bn(int M, int a_tiles) { return pick_bn(M, a_tiles); }
+
 namespace {
 unsigned long long* g_arena = nullptr;
 size_t g_arena_words = 0, g_arena_used = 0;

@@ -181,6 +181,31 @@ void gemm_qkv_rope(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH
 void gemm_qkv_rope_packed(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH, int hd, const int* pos,
                           const float2* cs, const KvPoolView* pool, int layer, const int* slot, bf16* q_out,
                           bf16* k_out, bf16* v_out, cudaStream_t st);
+// The decode layer's GEMM chain in one persistent launch (chain.cu): O-proj
+// split-K -> residual + RMSNorm (gain_mlp) -> gate/up SwiGLU -> down split-K ->
+// residual + RMSNorm (gain_next) -> [next layer's QKV + RoPE + KV append when
+// wqkv != nullptr]; grid-wide barriers between the phases. Bit-identical to
+// gemm_f32_splitk / add_norm / gemm_swiglu_decode / gemm_qkv_rope.
+// counters: 8 ints, zero, left zero. false: shape unsupported (nothing launched).
+struct DecodeChain {
+  const bf16 *wo, *wgu, *wd, *wqkv;  // layer l's O / gate-up / down; layer l+1's QKV (nullptr: last layer)
+  const bf16* attn;                   // [B][ao] attention output of layer l
+  bf16* h;                            // [B][d] norm output (GEMM input)
+  bf16* act;                          // [B][F]
+  float* parts;                       // [8][B][d] split-K partials
+  float* x;                           // [B][d] residual stream
+  const float *gain_mlp, *gain_next;  // ln2 of layer l; ln1 of layer l+1 or the final norm
+  bf16* q_out;                        // [B][H][hd] (layer l+1)
+  KvPoolView pool;
+  const int *slot, *pos;
+  const float2* cs;
+  int layer;                          // l (the QKV phase writes layer l + 1's K / V)
+  int H, KVH, hd, d, F, ao, B;
+  int* counters;
+  int ctas;                           // persistent grid size (<= SMs)
+};
+bool decode_chain(const DecodeChain& c, cudaStream_t st);
+
 // 2-D TMA map over the pool viewed as [rows, hd] bf16 rows (one row = one
 // token's K or V of one (page, layer, kv head)); box {64, 32}, 128 B swizzle.
 CUtensorMap make_kv_map(const void* pool, long long rows, int hd);

@@ -189,24 +189,27 @@ def test_fused_rope_prefill_scoring_bit_identical(small64):
         assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
 
 
-def test_fused_norm_decode_bit_identical(small64):
-    """The split-K O / down GEMMs with the following add_norm fused
-    (FUSEPLAN_FUSE_NORM=1: grid-wide partials counter, then norm.cuh rows)
-    give the same experience bits as the separate add_norm kernels."""
+@pytest.mark.parametrize("fixture", ["small64", "gqa128"])
+def test_decode_chain_bit_identical(request, fixture):
+    """The persistent decode-chain kernel (O -> norm -> gate/up -> down -> norm ->
+    next QKV in one launch, the default) gives the same experience bits as the six
+    separate kernels it replaces (FUSEPLAN_DECODE_CHAIN=0), on hd 64 MHA and hd 128
+    GQA, across batch sizes 1..160 as samples retire."""
     import os
     from paper_2409_13221_b200.configs import gen_config
     from paper_2409_13221_b200.engine import Engine
-    w, eng, batch, _ = small64
+    w, eng, batch, _ = request.getfixturevalue(fixture)
     a = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="fused", claim_tokens=4096)
-    os.environ["FUSEPLAN_FUSE_NORM"] = "1"
+    os.environ["FUSEPLAN_DECODE_CHAIN"] = "0"
     try:
         eng2 = Engine(w, device=0)
     finally:
-        del os.environ["FUSEPLAN_FUSE_NORM"]
+        del os.environ["FUSEPLAN_DECODE_CHAIN"]
     try:
         b = eng2.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="fused", claim_tokens=4096)
     finally:
         eng2.close()
+    assert a.stats["gpu_launches"] < b.stats["gpu_launches"]
     for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret", "score"):
         assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
 
