@@ -195,6 +195,18 @@ int fp_k_qkv_rope(const void* Wqkv, int32_t K, const void* X, int32_t M, int32_t
 int fp_k_vocab(const void* X, int32_t M, int32_t K, const void* W, int32_t V, int32_t mode, float inv_temp,
                const int32_t* target, const int32_t* sample_id, const int32_t* step, uint64_t seed, int32_t* token,
                float* logp, void* stream);
+/* The decode layer's GEMM chain in one persistent kernel (chain.cu): from the
+ * attention output attn [M][H hd] of layer `layer`: x += O-proj (split-K
+ * partials summed in order), h = rmsnorm(x) gain_mlp, act = SwiGLU(h Wgu),
+ * x += down(act), h = rmsnorm(x) gain_next, and — when Wqkv != NULL — the next
+ * layer's QKV with RoPE: q_out [M][H][hd], K / V appended to the pool at
+ * (slot, pos) of layer + 1 (pool layout of fp_k_attn_decode). parts: 8 x M x d
+ * fp32 scratch (holds the down partials on return); act [M][F]. */
+int fp_k_decode_chain(const void* Wo, const void* Wgu, const void* Wd, const void* Wqkv, const void* attn, void* h,
+                      void* act, float* parts, float* x, const float* gain_mlp, const float* gain_next, void* q_out,
+                      void* pool, int32_t num_layers, int32_t layer, const int32_t* block_table, int32_t bt_stride,
+                      const int32_t* slot, const int32_t* pos, int32_t max_pos, float rope_theta, int32_t M,
+                      int32_t d, int32_t H, int32_t KVH, int32_t hd, int32_t F, void* stream);
 /* Filtered sampling (top-k / top-p) through the engine's kernels:
  * gemm_vocab_logits -> topk_sample -> vocab_finalize. z_out (optional, [M][V]
  * fp32) receives the temperature-scaled logits the filter saw. */

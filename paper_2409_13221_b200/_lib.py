@@ -192,6 +192,8 @@ ENGINE_SYMBOLS = {
                                 C.c_float, _vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, _vp, _vp]),
     "fp_k_vocab": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int32, C.c_float, _vp, _vp, _vp,
                              C.c_uint64, _vp, _vp, _vp]),
+    "fp_k_decode_chain": (C.c_int, [_vp] * 11 + [_vp, _vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, _vp, C.c_int32,
+                                   C.c_float] + [C.c_int32] * 6 + [_vp]),
     "fp_k_vocab_filtered": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_float, C.c_int32, C.c_float,
                                       _vp, _vp, C.c_uint64, _vp, _vp, _vp, _vp]),
     "fp_k_add_norm": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, C.c_int32, C.c_int32, _vp]),

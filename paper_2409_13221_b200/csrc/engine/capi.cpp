@@ -520,6 +520,41 @@ int fp_k_vocab(const void* X, int32_t M, int32_t K, const void* W, int32_t V, in
   });
 }
 
+int fp_k_decode_chain(const void* Wo, const void* Wgu, const void* Wd, const void* Wqkv, const void* attn, void* h,
+                      void* act, float* parts, float* x, const float* gain_mlp, const float* gain_next, void* q_out,
+                      void* pool, int32_t num_layers, int32_t layer, const int32_t* block_table, int32_t bt_stride,
+                      const int32_t* slot, const int32_t* pos, int32_t max_pos, float rope_theta, int32_t M,
+                      int32_t d, int32_t H, int32_t KVH, int32_t hd, int32_t F, void* stream) {
+  return guarded([&] {
+    const size_t layer_bytes = static_cast<size_t>(KVH) * 2 * 64 * hd * 2;
+    float2* cs = nullptr;
+    const size_t cb = static_cast<size_t>(max_pos) * (hd / 2) * sizeof(float2);
+    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&cs), cb, S(stream)), "alloc");
+    fpk::rope_table(cs, max_pos, hd, rope_theta, S(stream));
+    int* cnt = nullptr;
+    fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&cnt), 64, S(stream)), "alloc");
+    fpe::check(cudaMemsetAsync(cnt, 0, 64, S(stream)), "memset");
+    fpk::DecodeChain c{};
+    c.wo = static_cast<const bf16*>(Wo), c.wgu = static_cast<const bf16*>(Wgu), c.wd = static_cast<const bf16*>(Wd);
+    c.wqkv = static_cast<const bf16*>(Wqkv);
+    c.attn = static_cast<const bf16*>(attn), c.h = static_cast<bf16*>(h), c.act = static_cast<bf16*>(act);
+    c.parts = parts, c.x = x, c.gain_mlp = gain_mlp, c.gain_next = gain_next;
+    c.q_out = static_cast<bf16*>(q_out);
+    c.pool = fpk::KvPoolView{static_cast<uint8_t*>(pool), layer_bytes * num_layers, layer_bytes, 64, block_table, bt_stride};
+    c.slot = slot, c.pos = pos, c.cs = cs, c.layer = layer;
+    c.H = H, c.KVH = KVH, c.hd = hd, c.d = d, c.F = F, c.ao = H * hd, c.B = M;
+    c.counters = cnt;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    c.ctas = sms;
+    if (!fpk::decode_chain(c, S(stream))) throw std::invalid_argument("fp_k_decode_chain: unsupported shape");
+    after_launch();
+    fpe::check(cudaFreeAsync(cs, S(stream)), "free");
+    fpe::check(cudaFreeAsync(cnt, S(stream)), "free");
+  });
+}
+
 int fp_k_vocab_filtered(const void* X, int32_t M, int32_t K, const void* W, int32_t V, float inv_temp, int32_t top_k,
                         float top_p, const int32_t* sample_id, const int32_t* step, uint64_t seed, int32_t* token,
                         float* logp, float* z_out, void* stream) {

@@ -77,15 +77,6 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
   FP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   FP_CUDA(cudaStreamCreateWithPriority(&s_decode_, cudaStreamNonBlocking, prio_hi));
   FP_CUDA(cudaStreamCreateWithPriority(&s_infer_, cudaStreamNonBlocking, prio_lo));
-  FP_CUDA(cudaEventCreateWithFlags(&infer_switch_, cudaEventDisableTiming));
-  FP_CUDA(cudaStreamCreateWithPriority(&s_decode2_, cudaStreamNonBlocking, prio_hi));
-  FP_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
-  FP_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
-  {
-    const char* e = std::getenv("FUSEPLAN_SCORE_SMS");
-    const int sms = e ? std::atoi(e) : 0;  // off by default: measured no net gain on gpt2s
-    if (sms > 0) create_green_scoring(sms);
-  }
   FP_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
   ring_ = new PinnedRing();
   const Dims& a = cfg_.model[kActor];
@@ -116,7 +107,9 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
   }
   for (int s = cfg_.max_live - 1; s >= 0; --s) free_slots_.push_back(s);
   if (const char* g = std::getenv("FUSEPLAN_DECODE_GRAPHS")) use_graphs_ = std::atoi(g) != 0;  // A/B switch
-  if (const char* g = std::getenv("FUSEPLAN_DECODE_CHAIN")) chain_ = std::atoi(g) != 0;  // A/B (tested)
+  // decode_chain for decode batches of at most chain_max_b_ rows (FUSEPLAN_DECODE_CHAIN: that bound;
+  // 0 = never) — bit-identical to the separate kernels, so the choice never changes a result
+  if (const char* g = std::getenv("FUSEPLAN_DECODE_CHAIN")) chain_max_b_ = std::atoi(g);
   {
     int sms = 148;
     FP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg_.device));
@@ -156,54 +149,6 @@ void* Engine::open_ipc(const cudaIpcMemHandle_t& h) {
   return p;
 }
 
-// Green context (driver API, resolved through the runtime so the library does
-// not link libcuda): an SM partition of `sms` SMs (multiple of 8) with its own
-// low-priority stream. Kernels are launched into it with the runtime API and
-// use the primary context's memory. Silently absent if unsupported.
-void Engine::create_green_scoring(int sms) {
-  using GetRes = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
-  using Split = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned);
-  using GenDesc = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
-  using Create = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
-  using MkStream = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
-  auto sym = [](const char* name) -> void* {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
-      return nullptr;
-    return p;
-  };
-  auto get_res = reinterpret_cast<GetRes>(sym("cuDeviceGetDevResource"));
-  auto split = reinterpret_cast<Split>(sym("cuDevSmResourceSplitByCount"));
-  auto gen = reinterpret_cast<GenDesc>(sym("cuDevResourceGenerateDesc"));
-  auto create = reinterpret_cast<Create>(sym("cuGreenCtxCreate"));
-  auto mk = reinterpret_cast<MkStream>(sym("cuGreenCtxStreamCreate"));
-  if (!get_res || !split || !gen || !create || !mk) return;
-  CUdevResource all{}, part{}, rest{};
-  unsigned n = 1;
-  if (get_res(static_cast<CUdevice>(cfg_.device), &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return;
-  if (sms >= static_cast<int>(all.sm.smCount)) return;
-  if (split(&part, &n, &all, &rest, 0, static_cast<unsigned>(sms)) != CUDA_SUCCESS || n != 1) return;
-  CUdevResourceDesc desc;
-  if (gen(&desc, &part, 1) != CUDA_SUCCESS) return;
-  CUgreenCtx g;
-  if (create(&g, desc, static_cast<CUdevice>(cfg_.device), CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return;
-  int lo = 0, hi = 0;
-  cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  CUstream st;
-  if (mk(&st, g, CU_STREAM_NON_BLOCKING, lo) != CUDA_SUCCESS) return;
-  green_ctx_ = g;
-  s_infer_green_ = reinterpret_cast<cudaStream_t>(st);
-  score_sms_ = static_cast<int>(part.sm.smCount);
-}
-
-void Engine::set_infer_confined(bool on) {
-  if (!s_infer_green_ || on == infer_confined_) return;
-  FP_CUDA(cudaEventRecord(infer_switch_, infer_stream()));
-  infer_confined_ = on;
-  FP_CUDA(cudaStreamWaitEvent(infer_stream(), infer_switch_, 0));
-}
-
 Engine::~Engine() {
   cudaSetDevice(cfg_.device);
   cudaDeviceSynchronize();
@@ -220,24 +165,12 @@ Engine::~Engine() {
   delete ring_;
   cudaStreamDestroy(s_decode_);
   cudaStreamDestroy(s_infer_);
-  if (s_infer_green_) cudaStreamDestroy(s_infer_green_);
-  if (green_ctx_) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuGreenCtxDestroy", &p, cudaEnableDefault, &q) == cudaSuccess && p)
-      reinterpret_cast<CUresult (*)(CUgreenCtx)>(p)(static_cast<CUgreenCtx>(green_ctx_));
-  }
-  if (infer_switch_) cudaEventDestroy(infer_switch_);
-  cudaEventDestroy(ev_fork_);
-  cudaEventDestroy(ev_join_);
-  cudaStreamDestroy(s_decode2_);
   cudaStreamDestroy(s_copy_);
 }
 
 void Engine::synchronize() {
   FP_CUDA(cudaStreamSynchronize(s_decode_));
   FP_CUDA(cudaStreamSynchronize(s_infer_));
-  if (s_infer_green_) FP_CUDA(cudaStreamSynchronize(s_infer_green_));
   FP_CUDA(cudaStreamSynchronize(s_copy_));
 }
 
@@ -438,7 +371,6 @@ void Engine::alloc_ws() {
     FP_CUDA(cudaMemsetAsync(dw.chain_cnt, 0, ccnt, s_decode_));
   };
   decode_ws(dec_, Bcap);
-  decode_ws(dec2_, bucket_of((cfg_.max_live + 1) / 2));  // second half of a split step
 }
 
 // ---------------------------------------------------------------------------
@@ -702,45 +634,10 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
     const char* e = std::getenv("FUSEPLAN_TRACE_STEP");
     return e ? std::atoi(e) : -1;
   }();
-  static const int split_min = [] {  // FUSEPLAN_DECODE_SPLIT: batch size from which the step runs as two halves
-    const char* e = std::getenv("FUSEPLAN_DECODE_SPLIT");
-    return e ? std::atoi(e) : 0;
-  }();
-  static const int split_ctas = [] {  // FUSEPLAN_SPLIT_ATTN_CTAS: attention CTAs per half
-    const char* e = std::getenv("FUSEPLAN_SPLIT_ATTN_CTAS");
-    return e ? std::atoi(e) : 74;
-  }();
   const bool tracing = ++decode_calls_ == trace_step;
   const bool graph = use_graphs_ && !probe_on_ && !tracing;
   cudaStream_t st = s_decode_;
   const int ctx_cap = cfg_.max_prompt + cfg_.max_new;
-  if (graph && split_min > 0 && B >= split_min) {
-    // balanced halves: rows in decreasing context length, dealt alternately
-    std::vector<int> order(B);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return rows[x].pos > rows[y].pos; });
-    std::vector<DecodeRow> g[2];
-    for (int k = 0; k < B; ++k) g[k & 1].push_back(rows[order[k]]);
-    const int Bb0 = bucket_of(static_cast<int>(g[0].size())), Bb1 = bucket_of(static_cast<int>(g[1].size()));
-    if (Bb0 > dec_.cap || Bb1 > dec2_.cap) throw std::invalid_argument("engine: decode batch exceeds max_live");
-    std::vector<int> h;
-    int mc;
-    double cs;
-    size_t n = build_rows(g[0].data(), static_cast<int>(g[0].size()), Bb0, h, mc, cs);
-    upload(dec_.rows, h.data(), n * 4, st);
-    n = build_rows(g[1].data(), static_cast<int>(g[1].size()), Bb1, h, mc, cs);
-    upload(dec2_.rows, h.data(), n * 4, st);
-    auto both = [&]() {
-      FP_CUDA(cudaEventRecord(ev_fork_, st));
-      FP_CUDA(cudaStreamWaitEvent(s_decode2_, ev_fork_, 0));
-      decode_kernels(dec_, st, Bb0, ctx_cap, mode, inv_temp, sample_seed, 0.0, split_ctas, top_k, top_p);
-      decode_kernels(dec2_, s_decode2_, Bb1, ctx_cap, mode, inv_temp, sample_seed, 0.0, split_ctas, top_k, top_p);
-      FP_CUDA(cudaEventRecord(ev_join_, s_decode2_));
-      FP_CUDA(cudaStreamWaitEvent(st, ev_join_, 0));
-    };
-    run_graph(GraphKey{Bb0, Bb1, mode, inv_temp, sample_seed, top_k, top_p}, both);
-    return;
-  }
   const int Bb = graph ? bucket_of(B) : B;
   if (Bb > dec_.cap) throw std::invalid_argument("engine: decode batch exceeds max_live");
   std::vector<int> h;
@@ -762,7 +659,8 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
       FP_CUDA(cudaStreamSynchronize(st));
       const std::vector<fpk::TraceRec> recs = fpk::trace_disarm();
       size_t used = 0;
-      for (const auto& r : recs) used = std::max(used, r.off + static_cast<size_t>(r.units) * (r.kind == 0 ? 8 : 4));
+      auto wpu_of = [](int kind) { return kind == 0 ? 8 : kind == 3 ? 16 : 4; };  // stamps per unit
+      for (const auto& r : recs) used = std::max(used, r.off + static_cast<size_t>(r.units) * wpu_of(r.kind));
       std::vector<unsigned long long> th(used);
       FP_CUDA(cudaMemcpy(th.data(), arena, used * 8, cudaMemcpyDeviceToHost));
       cudaFree(arena);
@@ -771,7 +669,7 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
       if (f) {
         std::fprintf(f, "{\"B\": %d, \"max_ctx\": %d, \"ctx_sum\": %.0f, \"launches\": [", B, max_ctx, ctx_sum);
         for (size_t i = 0; i < recs.size(); ++i) {
-          const int wpu = recs[i].kind == 0 ? 8 : 4;
+          const int wpu = wpu_of(recs[i].kind);
           std::fprintf(f, "%s{\"kind\": %d, \"units\": %d, \"data\": [", i ? ", " : "", recs[i].kind, recs[i].units);
           for (int u = 0; u < recs[i].units * wpu; ++u)
             std::fprintf(f, "%s%llu", u ? "," : "", th[recs[i].off + u]);
@@ -783,7 +681,7 @@ void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp
     }
     return;
   }
-  run_graph(GraphKey{Bb, 0, mode, inv_temp, sample_seed, top_k, top_p},
+  run_graph(GraphKey{Bb, mode, inv_temp, sample_seed, top_k, top_p},
             [&]() { decode_kernels(dec_, st, Bb, ctx_cap, mode, inv_temp, sample_seed, 0.0, 148, top_k, top_p); });
 }
 
@@ -851,7 +749,7 @@ void Engine::decode_kernels(DecodeWs& dw, cudaStream_t st, int B, int max_ctx, i
     }
     // O -> norm -> gate/up -> down -> norm -> next QKV: one persistent launch
     // (decode_chain), or the six kernels it replaces (bit-identical)
-    if (chain_) {
+    if (chain_ && B <= chain_max_b_) {
       fpk::DecodeChain c{};
       c.wo = L.wo, c.wgu = L.wgu, c.wd = L.wd, c.wqkv = last ? nullptr : w.layers[l + 1].wqkv;
       c.attn = dw.attn, c.h = dw.h, c.act = dw.act, c.parts = dw.parts, c.x = dw.x;

@@ -97,13 +97,8 @@ class Engine {
   void load_tensor(int m, int tensor, int layer, const void* host, int64_t n_elems);
   uint64_t model_checksum(int m);             // sum of the blob's 64-bit words (synchronises)
   cudaStream_t decode_stream() const { return s_decode_; }
-  // The scoring stream in use: while generation runs, scoring may be confined
-  // to a green-context SM partition (FUSEPLAN_SCORE_SMS, default off) so that
-  // decode kernels never queue behind scoring CTAs on the other SMs; after
-  // generation it gets the whole GPU. Switching orders the two streams.
-  cudaStream_t infer_stream() const { return infer_confined_ && s_infer_green_ ? s_infer_green_ : s_infer_; }
-  void set_infer_confined(bool on);
-  int score_sms() const { return score_sms_; }
+  // The scoring stream: low priority, so scoring CTAs fill the SMs decode leaves idle.
+  cudaStream_t infer_stream() const { return s_infer_; }
   cudaStream_t copy_stream() const { return s_copy_; }
 
   // ---- batch data (global sample ids) -------------------------------------------
@@ -208,17 +203,17 @@ class Engine {
   bool fuse_rope_ = true;  // prefill / scoring: RoPE + K/V writes in the QKV GEMM epilogue
   int decode_calls_ = 0;
   bool chain_ = true;     // decode: the GEMM chain of a layer as one persistent kernel (fpk::decode_chain)
+  int chain_max_b_ = 0;   // ... for decode batches up to this many rows (off: measured no faster)
   int chain_ctas_ = 148;  // its grid: one CTA per SM
   int pad_slot_ = 0;
   struct GraphKey {
-    int B, B1, mode;  // B1: second half of a split step (0: unsplit)
+    int B, mode;
     float inv_temp;
     uint64_t seed;
     int top_k;
     float top_p;
     bool operator<(const GraphKey& o) const {
       if (B != o.B) return B < o.B;
-      if (B1 != o.B1) return B1 < o.B1;
       if (mode != o.mode) return mode < o.mode;
       if (inv_temp != o.inv_temp) return inv_temp < o.inv_temp;
       if (top_k != o.top_k) return top_k < o.top_k;
@@ -237,8 +232,6 @@ class Engine {
                       uint64_t sample_seed, double ctx_sum, int attn_ctas, int top_k, float top_p);
   size_t build_rows(const DecodeRow* rows, int B, int Bb, std::vector<int>& h, int& max_ctx, double& ctx_sum);
   void run_graph(const GraphKey& key, const std::function<void()>& body);
-  cudaStream_t s_decode2_ = nullptr;
-  cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
   uint64_t prompts_tag_ = 0;
   CUtensorMap kv_map_{};
   bool has_kv_map_ = false;
@@ -288,12 +281,6 @@ class Engine {
   EngineConfig cfg_;
   ModelW models_[4];
   cudaStream_t s_decode_ = nullptr, s_infer_ = nullptr, s_copy_ = nullptr;
-  cudaStream_t s_infer_green_ = nullptr;  // scoring stream of a green context (SM partition), or null
-  void* green_ctx_ = nullptr;
-  int score_sms_ = 0;
-  bool infer_confined_ = false;
-  cudaEvent_t infer_switch_ = nullptr;
-  void create_green_scoring(int sms);
   // pool
   uint8_t* pool_ = nullptr;
   size_t page_bytes_ = 0, layer_bytes_ = 0;
@@ -315,7 +302,7 @@ class Engine {
   size_t handoff_bytes_ = 0;
   Experience hand_;
   std::vector<int64_t> resp_off_;
-  DecodeWs dec_, dec2_;
+  DecodeWs dec_;
   PinnedRing* ring_ = nullptr;
   void* scratch_ = nullptr;
   size_t scratch_bytes_ = 0;

@@ -500,7 +500,6 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
   const long long launches0 = fpk::launch_count();
   if (!(opts.resident && E.prompts_tag() == ptag)) E.load_prompts(prompts.data(), n, ptag);
   if (opts.probe_attention) E.set_attn_probe(true);
-  E.set_infer_confined(false);
   cudaStream_t sd = E.decode_stream(), si = E.infer_stream();
   FP_CUDA(cudaStreamSynchronize(sd));
   region.barrier();
@@ -646,8 +645,6 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
         res.stats.infer_tokens += batch[sid].prompt_len + rlen[sid];
       }
       res.stats.infer_samples += end - c;
-      E.set_infer_confined(!gen_done_me && fused);
-      si = E.infer_stream();
       // local finishes may still be in flight on the decode stream
       if (!step_end.empty()) FP_CUDA(cudaStreamWaitEvent(si, step_end.back(), 0));
       Batch bt;

@@ -440,38 +440,19 @@ void launch_decode(const bf16* q, int B, int H, int KVH, const KvPoolView& pool,
 }  // namespace
 
 int attn_decode_items(const int* ctx, int B, int KVH, int hd, int G, int* items) {
+  // One item per (sample, 512-token split); splits are not cut into 128-token
+  // sub-chunks (measured slower on gpt2s: the parked sub-partial and its
+  // ticket cost more than the balance gained). Longest first: counting sort
+  // by 32-token units, ties by (sample, split).
+  (void)KVH, (void)hd, (void)G;
   constexpr int kU = kDecodeChunk / 32;  // units per split
-  constexpr int kSubU = 4;                // units per sub-chunk
-  // cut splits longer than the mean work per warp into sub-chunks (wide kernel only)
-  // (measured slower on gpt2s — the parked sub-partial + ticket costs more than
-  // the balance gains — so off unless FUSEPLAN_ATTN_CUT=1)
-  static const bool cut_on = [] {
-    const char* e = std::getenv("FUSEPLAN_ATTN_CUT");
-    return e && std::atoi(e) == 1;
-  }();
-  int warps = 0;
-  const bool wide = cut_on && attn_decode_variant(B, KVH, hd, G, &warps) == 0;
-  int cut = kU + 1;  // no split is longer than kU units: nothing is cut
-  if (wide) {
-    long long units = 0;
-    for (int b = 0; b < B; ++b) units += (ctx[b] + 31) / 32;
-    const long long mean = (units * KVH + 148LL * warps - 1) / (148LL * warps);
-    cut = static_cast<int>(std::max<long long>(kSubU, mean));
-  }
-  // counting sort by units descending
   int n = 0;
   for (int u = kU; u >= 1; --u)
     for (int b = 0; b < B; ++b) {
       const int ns = (ctx[b] + kDecodeChunk - 1) / kDecodeChunk;
       for (int s = 0; s < ns; ++s) {
         const int len = std::min(ctx[b], (s + 1) * kDecodeChunk) - s * kDecodeChunk;
-        const int su = (len + 31) / 32;
-        if (su > cut) {
-          for (int c = 0; c * kSubU < su; ++c)
-            if (std::min(kSubU, su - c * kSubU) == u) items[1 + n++] = b << 11 | s << 3 | c;
-        } else if (su == u) {
-          items[1 + n++] = b << 11 | s << 3 | 7;
-        }
+        if ((len + 31) / 32 == u) items[1 + n++] = b << 11 | s << 3 | 7;
       }
     }
   items[0] = n;

@@ -47,8 +47,10 @@ constexpr int kChainSmem = 225 * 1024;  // + ~0.5 KB static: within the 227 KB p
 
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
+// After a CTA barrier over the writers: the release orders their generic
+// writes (cumulativity through bar.sync); the proxy fence covers the TMA
+// (async proxy) reads of the consumers.
 __device__ __forceinline__ void grid_arrive(int* cnt) {
-  __threadfence();
   fence_proxy_async_global();
   asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(cnt) : "memory");
 }
@@ -89,6 +91,7 @@ struct ChainArgs {
   int B, d;
   int has_qkv;
   int* counters;  // 8 ints: phase counters 0..4, exit; zero at launch, left zero
+  unsigned long long* trace;  // optional: 16 globaltimer stamps per CTA (tools/step_trace.py)
 };
 
 // Item sequence of one CTA: GEMM phases g = 0..3 (P0, P2, P3, P5), tiles
@@ -114,61 +117,88 @@ struct ChainCfg {
   static constexpr int kStageBytes = kTileA + BN * kBK * 2;
   // epilogue staging: EpiSwiGLU (tile + exchange) / EpiRopeKV (tile + cos/sin cache)
   static constexpr int kSwi = EpiSwiGLU<BN>::kTileBytes + 2 * 32 * 128 * 4;
-  static constexpr int kRope = BN * 128 * 2 + EpiRopeKV<BN>::kSmemExtra;
+  // the RoPE epilogue stages [max(BN, 64)][128] bf16 (its zero chunks past BN
+  // land there too), its cos/sin cache follows
+  static constexpr int kRopeTile = (BN < 64 ? 64 : BN) * 128 * 2;
+  static constexpr int kRope = kRopeTile + EpiRopeKV<BN>::kSmemExtra;
   static constexpr int kStaging = ((kSwi > kRope ? kSwi : kRope) + 1023) & ~1023;
   static constexpr int kStages = (kChainSmem - 1024 - kStaging - 1024) / kStageBytes;
-  static constexpr uint32_t kTmemCols = BN <= 16 ? 32 : (BN <= 32 ? 64 : (BN <= 64 ? 128 : (BN <= 128 ? 256 : 512)));
-  static constexpr uint32_t kAccCols = kTmemCols / 2;  // two accumulator buffers
+  // two accumulator buffers of >= 32 columns (an epilogue chunk reads 32)
+  static constexpr uint32_t kAccCols = BN <= 32 ? 32 : BN;
+  static constexpr uint32_t kTmemCols = 2 * kAccCols;
 };
 
-// Residual add + RMSNorm of row `row` with the 256 epilogue threads standing
-// in for add_norm_kernel's blockDim = 32 * ceil(d / 128) threads (virtual
-// thread j = 256 k + t): the same float4 per virtual thread, the same
-// warp-then-warp-order reduction — the same bits.
-__device__ __forceinline__ void chain_norm_row(float* x, const float* parts, int ns, size_t ps, const float* gain,
-                                               __nv_bfloat16* y, int d, int row, float* red) {
+// Residual add + RMSNorm of rows `row0` and (if row1 >= 0) `row1` with the 256
+// epilogue threads standing in for add_norm_kernel's blockDim = 32 * ceil(d /
+// 128) threads (virtual thread j = 256 k + t): the same float4 per virtual
+// thread, the same warp-then-warp-order reduction — the same bits. The loads
+// of both rows are in flight together.
+__device__ __forceinline__ void chain_norm_rows(float* x, const float* parts, int ns, size_t ps, const float* gain,
+                                                __nv_bfloat16* y, int d, int row0, int row1, float (*red)[32]) {
   const int t = static_cast<int>(threadIdx.x) - 64;  // 0..255
   const int d4 = d >> 2;
   const int nthr = ((d4 + 31) / 32) * 32, nw = nthr >> 5;
   const int rounds = (nthr + 255) / 256;
-  float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(row) * d);
-  const float4* pr = reinterpret_cast<const float4*>(parts + static_cast<size_t>(row) * d);
   const size_t ps4 = ps >> 2;
-  float4 v[4];
+  float4 v[2][4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int j = 256 * k + t;
-    if (k < rounds && j < d4) {
-      float4 a = __ldcg(xr + j);
-      float4 p[8];
+  for (int q = 0; q < 2; ++q) {
+    const int row = q ? row1 : row0;
 #pragma unroll
-      for (int s = 0; s < 8; ++s)
-        if (s < ns) p[s] = __ldcg(pr + s * ps4 + j);  // written by other CTAs: L2
+    for (int k = 0; k < 4; ++k) {
+      v[q][k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int j = 256 * k + t;
+      if (row >= 0 && k < rounds && j < d4) {
+        const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(row) * d);
+        const float4* pr = reinterpret_cast<const float4*>(parts + static_cast<size_t>(row) * d);
+        float4 a = __ldcg(xr + j);
+        float4 p[8];
 #pragma unroll
-      for (int s = 0; s < 8; ++s)
-        if (s < ns) a.x += p[s].x, a.y += p[s].y, a.z += p[s].z, a.w += p[s].w;
-      if (ns > 0) xr[j] = a;
-      v[k] = a;
+        for (int s = 0; s < 8; ++s)
+          if (s < ns) p[s] = __ldcg(pr + s * ps4 + j);  // written by other CTAs: L2
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+          if (s < ns) a.x += p[s].x, a.y += p[s].y, a.z += p[s].z, a.w += p[s].w;
+        v[q][k] = a;
+      }
     }
-    if (k < rounds && j < nthr) {
-      const float ws = warp_sum(sumsq4(v[k]));
-      if ((t & 31) == 0) red[(256 * k + t) >> 5] = ws;
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int row = q ? row1 : row0;
+    if (row < 0) continue;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = 256 * k + t;
+      if (k < rounds && j < d4 && ns > 0) reinterpret_cast<float4*>(x + static_cast<size_t>(row) * d)[j] = v[q][k];
+      if (k < rounds && j < nthr) {
+        const float ws = warp_sum(sumsq4(v[q][k]));
+        if ((t & 31) == 0) red[q][(256 * k + t) >> 5] = ws;
+      }
     }
   }
   epi_bar_sync();
-  float tot = (static_cast<int>(lane_id()) < nw) ? red[lane_id()] : 0.f;
-  tot = warp_sum(tot);
-  const float inv = rsqrtf(tot / d + kNormEps);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const int j = 256 * k + t;
-    if (k < rounds && j < d4) {
-      const float4 g = reinterpret_cast<const float4*>(gain)[j];
-      reinterpret_cast<uint2*>(y + static_cast<size_t>(row) * d)[j] = norm_scale4(v[k], inv, g);
+  for (int q = 0; q < 2; ++q) {
+    const int row = q ? row1 : row0;
+    if (row < 0) continue;
+    float tot = (static_cast<int>(lane_id()) < nw) ? red[q][lane_id()] : 0.f;
+    tot = warp_sum(tot);
+    const float inv = rsqrtf(tot / d + kNormEps);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int j = 256 * k + t;
+      if (k < rounds && j < d4) {
+        const float4 g = reinterpret_cast<const float4*>(gain)[j];
+        reinterpret_cast<uint2*>(y + static_cast<size_t>(row) * d)[j] = norm_scale4(v[q][k], inv, g);
+      }
     }
   }
-  epi_bar_sync();  // red[] is reused by the next row
+  epi_bar_sync();  // red[] is reused by the next rows
+}
+
+__device__ __forceinline__ void stamp(unsigned long long* tr, int k) {
+  if (tr) tr[k] = gtime();
 }
 
 template <int BN>
@@ -182,12 +212,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) decode_chain_kernel(const __
   __shared__ __align__(8) uint64_t acc_full[2];
   __shared__ __align__(8) uint64_t acc_empty[2];
   __shared__ uint32_t tmem_base_smem;
-  __shared__ float red[32];
+  __shared__ float red[2][32];
 
   const uint32_t warp = warp_id();
   const int nb = (a.B + BN - 1) / BN;
   const int G = gridDim.x;
   const int n_gemm = a.has_qkv ? 4 : 3;
+  unsigned long long* tr = a.trace ? a.trace + 16ull * blockIdx.x : nullptr;
+  if (threadIdx.x == 0) stamp(tr, 0);
   pdl_trigger();
 
   if (warp == 0 && elect_one()) {
@@ -234,6 +266,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) decode_chain_kernel(const __
           pdl_wait();  // attention output of the previous kernel
         else
           grid_wait(a.counters + (g == 1 ? 1 : g == 2 ? 2 : 4), G);  // P1 / P2 / P4 done everywhere
+        if (g == 1) stamp(tr, 14);
+        if (g == 3) stamp(tr, 15);
         for_tiles(a, g, nb, [&](int, int bt, int, int kb0, int kb1) {
           for (int kb = kb0; kb < kb1; ++kb, ++i) {
             const int s = i % C::kStages;
@@ -277,14 +311,18 @@ __global__ void __launch_bounds__(kChainThreads, 1) decode_chain_kernel(const __
     const size_t ps = static_cast<size_t>(a.B) * a.d;  // split stride of the partials
     pdl_wait();
     int tile = 0;
+    const int acc_stamp[4] = {1, 5, 8, 12};
     auto gemm_phase = [&](int g, const auto& epi, auto&& store_chunk) {
+      bool first = true;
       using Epi = std::remove_cvref_t<decltype(epi)>;
       typename Epi::State st{};
       for_tiles(a, g, nb, [&](int at, int bt, int split, int, int) {
         const int buf = tile & 1;
         const int a0 = at * 128, b0 = bt * BN;
-        if constexpr (EpiHasPrologue<Epi>::value) epi.prologue(st, a0, b0, staging + BN * 128 * 2);
+        if constexpr (EpiHasPrologue<Epi>::value) epi.prologue(st, a0, b0, staging + C::kRopeTile);
         mbar_wait(&acc_full[buf], (tile >> 1) & 1);
+        if (first && threadIdx.x == 64) stamp(tr, acc_stamp[g]);
+        first = false;
         tc_fence_after();
         const uint32_t acc = tmem + buf * C::kAccCols + (static_cast<uint32_t>(quarter * 32) << 16);
 #pragma unroll 1
@@ -324,14 +362,22 @@ __global__ void __launch_bounds__(kChainThreads, 1) decode_chain_kernel(const __
         if (c0 + j < BN && b < a.B) out[static_cast<size_t>(b) * a.d] = v[j];
       }
     };
+    const int arrive_stamp[5] = {2, 4, 6, 9, 11};
     auto arrive = [&](int phase) {
       epi_bar_sync();
-      if (threadIdx.x == 64) grid_arrive(a.counters + phase);
+      if (threadIdx.x == 64) {
+        grid_arrive(a.counters + phase);
+        stamp(tr, arrive_stamp[phase]);
+      }
     };
     auto norm_phase = [&](int phase, int ns, const float* gain) {
-      if (threadIdx.x == 64) grid_wait(a.counters + phase - 1, G);
+      if (threadIdx.x == 64) {
+        grid_wait(a.counters + phase - 1, G);
+        stamp(tr, phase == 1 ? 3 : 10);
+      }
       epi_bar_sync();
-      for (int row = blockIdx.x; row < a.B; row += G) chain_norm_row(a.x, a.parts, ns, ps, gain, a.h, a.d, row, red);
+      for (int row = blockIdx.x; row < a.B; row += 2 * G)
+        chain_norm_rows(a.x, a.parts, ns, ps, gain, a.h, a.d, row, row + G < a.B ? row + G : -1, red);
       arrive(phase);
     };
 
@@ -342,7 +388,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) decode_chain_kernel(const __
     gemm_phase(1, a.swiglu, [&](typename EpiSwiGLU<BN>::State& st, int a0, int b0, int split, int c0,
                                 const float (&v)[32]) { a.swiglu(st, staging, a0, b0, split, r, half, c0, v); });  // P2
     arrive(2);
-    if (threadIdx.x == 64) grid_wait(a.counters + 2, G);  // P3's partials overwrite P0's: P1 has read them
+    if (threadIdx.x == 64) {
+      grid_wait(a.counters + 2, G);  // P3's partials overwrite P0's: P1 has read them
+      stamp(tr, 7);
+    }
     epi_bar_sync();
     gemm_phase(2, none, partial_store);  // P3
     arrive(3);
@@ -350,6 +399,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) decode_chain_kernel(const __
     if (a.has_qkv)
       gemm_phase(3, a.rope, [&](typename EpiRopeKV<BN>::State& st, int a0, int b0, int split, int c0,
                                 const float (&v)[32]) { a.rope(st, staging, a0, b0, split, r, half, c0, v); });  // P5
+    if (threadIdx.x == 64) stamp(tr, 13);
   }
 
   tc_fence_before();
@@ -416,13 +466,19 @@ static void launch_chain(const DecodeChain& c, cudaStream_t st) {
   a.B = c.B;
   a.d = d;
   a.counters = c.counters;
+
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(decode_chain_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, kChainSmem);
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(c.ctas);
+  int tiles = 0;
+  for (int g = 0; g < (a.has_qkv ? 4 : 3); ++g)
+    tiles = std::max(tiles, a.ph[g].a_tiles * a.ph[g].splits * ((c.B + BN - 1) / BN));
+  const int ctas = std::max(1, std::min(c.ctas, tiles));  // idle SMs stay free for the scoring stream
+  a.trace = trace_slot(3, ctas, 16);
+  cfg.gridDim = dim3(ctas);
   cfg.blockDim = dim3(kChainThreads);
   cfg.dynamicSmemBytes = kChainSmem;
   cfg.stream = st;

@@ -98,7 +98,7 @@ unsigned long long* g_trace = nullptr;
 
 template <int BN, class Epi, int ST = 0>
 void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int splits, const Epi& epi,
-            cudaStream_t st, bool weight_is_a = true, bool cluster_split = false) {
+            cudaStream_t st, bool weight_is_a = true) {
   using C = GemmCfg<BN, ST ? ST : EpiStages<Epi>::value>;
   if (K % kBK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
   if (a_rows <= 0 || b_rows <= 0) return;
@@ -124,8 +124,6 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
     g.trace = trace_slot(0, static_cast<int>(ctas), 8);
   }
   const int z = (g.k_blocks + g.kb_per_split - 1) / g.kb_per_split;
-  if (cluster_split && (BN > 64 || z > 8)) throw std::invalid_argument("gemm: cluster split needs BN <= 64, z <= 8");
-  g.cz = cluster_split ? z : 1;
   // Programmatic dependent launch: the prologue and the weight prefetch of this
   // GEMM overlap the tail of the previous kernel (which triggers early).
   cudaLaunchConfig_t cfg{};
@@ -133,15 +131,11 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = C::kSmem + EpiSmemExtra<Epi>::value;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = 1;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = g.cz;
   cfg.attrs = attr;
-  cfg.numAttrs = g.cz > 1 ? 2 : 1;
+  cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<BN, Epi, ST>, ma, mb, g, epi);
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm launch: ") + cudaGetErrorString(e));
   fpk::count_launch();
@@ -168,46 +162,6 @@ int pick_bn(int M, int a_ctas) {
   return best;
 }
 
-// Cluster split of a decode GEMM: a function of the weight shape only (so a
-// row's bits do not depend on the batch): the largest z <= 8 dividing the K
-// blocks with tiles x z <= 148.
-int cluster_splits(int N, int K) {
-  static const int enabled = [] {
-    const char* e = std::getenv("FUSEPLAN_CLUSTER_SPLIT");  // A/B switch
-    return e ? std::atoi(e) : 0;  // off by default: measured slower
-  }();
-  if (!enabled) return 1;
-  const int tiles = (N + 127) / 128, kb = K / kBK;
-  int best = 1;
-  for (int z = 2; z <= 8; ++z)
-    if (kb % z == 0 && tiles * z <= 148) best = z;
-  return best;
-}
-
-// Decode GEMMs with a cluster split use BN <= 64 (the parked partial must fit).
-int pick_bn_small(int M, int a_ctas) {  // pick_bn restricted to BN <= 64
-  static const int kBN[] = {16, 32, 64};
-  int best = 16, best_waves = 1 << 30;
-  for (int bn : kBN) {
-    if (bn != 16 && bn / 2 >= M) break;
-    const int waves = (a_ctas * ((M + bn - 1) / bn) + 147) / 148;
-    if (waves < best_waves) {
-      best = bn;
-      best_waves = waves;
-    }
-  }
-  return best;
-}
-
-template <class F>
-void dispatch_bn_small(int M, int a_ctas, F&& f) {
-  switch (pick_bn_small(M, a_ctas)) {
-    case 16: f.template operator()<16>(); break;
-    case 32: f.template operator()<32>(); break;
-    default: f.template operator()<64>(); break;
-  }
-}
-
 // Decode GEMMs in a lean ring (<= ~110 KB of shared memory) so that the CTAs
 // of the next GEMM in the step fit on an SM beside the current one's: with
 // PDL they become resident early and stream their weights while the previous
@@ -216,38 +170,10 @@ template <int BN>
 struct Lean {
   static constexpr int v = BN <= 16 ? 6 : BN <= 32 ? 5 : BN <= 64 ? 4 : BN <= 128 ? 3 : 2;
 };
-// A ring holding a decode CTA's whole K range (K = 768: 12 stages at BN 16):
-// every weight tile is in flight before griddepcontrol.wait, so the mainloop
-// after it only waits for the activation tiles.
-template <int BN>
-struct Full {
-  static constexpr int kStage = kTileA + BN * kBK * 2;
-  static constexpr int kFit = (216 * 1024 - BN * 64 * 8) / kStage;  // (room for EpiRopeKV's cos/sin cache)
-  static constexpr int v = kFit > 12 ? 12 : kFit;
-};
-bool full_ring(long long ctas) {  // FUSEPLAN_DECODE_FULL: grids of at most this many CTAs take the Full ring
-  static const int max_ctas = [] {
-    const char* e = std::getenv("FUSEPLAN_DECODE_FULL");
-    return e ? std::atoi(e) : 0;
-  }();
-  return ctas <= max_ctas;
-}
-bool lean(int M) {  // (large batches keep the deep ring: their mainloops are bandwidth-hungry)
-  static const int max_m = [] {
-    const char* e = std::getenv("FUSEPLAN_DECODE_LEAN");
-    return e ? std::atoi(e) : 128;
-  }();
-  return M <= max_m;
-}
+bool lean(int M) { return M <= 128; }  // (large batches keep the deep ring: their mainloops are bandwidth-hungry)
 
 // Large GEMMs (several waves of CTAs) take the 2-stage / 2-CTAs-per-SM shape.
-bool many_waves(int M, int N, int BN) {
-  static const int on = [] {
-    const char* e = std::getenv("FUSEPLAN_GEMM_2CTA");
-    return e ? std::atoi(e) : 1;
-  }();
-  return on && static_cast<long long>((N + 127) / 128) * ((M + BN - 1) / BN) >= 2 * 148;
-}
+bool many_waves(int M, int N, int BN) { return static_cast<long long>((N + 127) / 128) * ((M + BN - 1) / BN) >= 2 * 148; }
 
 template <class Epi, class F>
 void dispatch_bn(int M, int a_ctas, F&& f) {
@@ -345,61 +271,11 @@ void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* o
     const uint64_t str[2] = {static_cast<uint64_t>(N) * 4, static_cast<uint64_t>(M) * N * 4};
     const uint32_t box[3] = {128u, static_cast<uint32_t>(BN), 1u};
     EpiStoreF32 e{encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE), 0};
-    if (BN <= 128 && lean(M) && full_ring(static_cast<long long>((N + 127) / 128) * z * ((M + BN - 1) / BN)))
-      launch<BN, EpiStoreF32, Full<BN>::v>(W, N, X, M, K, splits, e, st);
-    else if (BN <= 128 && lean(M))  // (the fp32 staging tile of BN 256 needs the deep ring)
+    if (BN <= 128 && lean(M))  // (the fp32 staging tile of BN 256 needs the deep ring)
       launch<BN, EpiStoreF32, Lean<BN>::v>(W, N, X, M, K, splits, e, st);
     else
       launch<BN>(W, N, X, M, K, splits, e, st);
   });
-}
-
-// CTAs of tc_gemm_kernel<BN, Epi, ST> the device holds at once (1 per SM for
-// the default rings, 2 for the lean / 2-stage ones).
-template <int BN, class Epi, int ST>
-int resident_limit() {
-  static int lim = -1;
-  if (lim < 0) {
-    using C = GemmCfg<BN, ST ? ST : EpiStages<Epi>::value>;
-    const int smem = C::kSmem + EpiSmemExtra<Epi>::value;
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(tc_gemm_kernel<BN, Epi, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, tc_gemm_kernel<BN, Epi, ST>, kGemmThreads, smem);
-    lim = per * sms;
-  }
-  return lim;
-}
-
-bool gemm_f32_splitk_norm(const bf16* W, int N, int K, const bf16* X, int M, float* out, int splits,
-                          const NormFuse& nf, cudaStream_t st) {
-  if (N % 4 || N > 1024 || !nf.x || !nf.gain || !nf.y || !nf.counters) return false;
-  const int kb = K / kBK;
-  splits = std::max(1, std::min(splits, kb));
-  const int per = (kb + splits - 1) / splits;
-  const int z = (kb + per - 1) / per;
-  if (z > 8) return false;
-  bool done = false;
-  dispatch_bn<EpiStoreF32>(M, (N + 127) / 128 * z, [&]<int BN>() {
-    const uint64_t dims[3] = {static_cast<uint64_t>(N), static_cast<uint64_t>(M), static_cast<uint64_t>(z)};
-    const uint64_t str[2] = {static_cast<uint64_t>(N) * 4, static_cast<uint64_t>(M) * N * 4};
-    const uint32_t box[3] = {128u, static_cast<uint32_t>(BN), 1u};
-    EpiStoreF32 e{encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE), 0};
-    e.nf = nf;
-    e.parts = out;
-    e.M = M, e.d = N, e.ns = z;
-    e.total = (N + 127) / 128 * z * ((M + BN - 1) / BN);
-    if (BN <= 128 && lean(M)) {
-      if (e.total > resident_limit<BN, EpiStoreF32, Lean<BN>::v>()) return;
-      launch<BN, EpiStoreF32, Lean<BN>::v>(W, N, X, M, K, splits, e, st);
-    } else {
-      if (e.total > resident_limit<BN, EpiStoreF32, 0>()) return;
-      launch<BN>(W, N, X, M, K, splits, e, st);
-    }
-    done = true;
-  });
-  return done;
 }
 
 void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float* resid, cudaStream_t st) {
@@ -415,20 +291,13 @@ void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float*
 
 void gemm_swiglu_decode(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
   if (F % 64) throw std::invalid_argument("gemm_swiglu: F must be a multiple of 64");
-  const int z = cluster_splits(2 * F, K);
-  auto go = [&]<int BN>() {
+  dispatch_bn<int>(M, (2 * F + 127) / 128, [&]<int BN>() {
     EpiSwiGLU<BN> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, BN)};
-    if (z == 1 && lean(M) && full_ring(static_cast<long long>((2 * F + 127) / 128) * ((M + BN - 1) / BN)))
-      launch<BN, EpiSwiGLU<BN>, Full<BN>::v>(Wgu, 2 * F, X, M, K, z, e, st);
-    else if (z == 1 && lean(M))
-      launch<BN, EpiSwiGLU<BN>, Lean<BN>::v>(Wgu, 2 * F, X, M, K, z, e, st);
+    if (lean(M))
+      launch<BN, EpiSwiGLU<BN>, Lean<BN>::v>(Wgu, 2 * F, X, M, K, 1, e, st);
     else
-      launch<BN>(Wgu, 2 * F, X, M, K, z, e, st, true, z > 1);
-  };
-  if (z > 1)
-    dispatch_bn_small(M, (2 * F + 127) / 128 * z, go);
-  else
-    dispatch_bn<int>(M, (2 * F + 127) / 128, go);
+      launch<BN>(Wgu, 2 * F, X, M, K, 1, e, st);
+  });
 }
 
 void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
@@ -447,21 +316,14 @@ void gemm_qkv_rope(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH
                    cudaStream_t st) {
   if (128 % hd != 0) throw std::invalid_argument("gemm_qkv_rope: head_dim must divide 128");
   const int N = (H + 2 * KVH) * hd;
-  const int z = cluster_splits(N, K);
-  auto go = [&]<int BN>() {
+  dispatch_bn<int>(M, (N + 127) / 128, [&]<int BN>() {
     EpiRopeKV<BN> e{q_out, pool, slot, pos, cs, layer, H, KVH, hd, M};
     e.pool.kv_map = nullptr;  // host pointer: not dereferenced on the device
-    if (z == 1 && lean(M) && full_ring(static_cast<long long>((N + 127) / 128) * ((M + BN - 1) / BN)))
-      launch<BN, EpiRopeKV<BN>, Full<BN>::v>(Wqkv, N, X, M, K, z, e, st);
-    else if (z == 1 && lean(M))
-      launch<BN, EpiRopeKV<BN>, Lean<BN>::v>(Wqkv, N, X, M, K, z, e, st);
+    if (lean(M))
+      launch<BN, EpiRopeKV<BN>, Lean<BN>::v>(Wqkv, N, X, M, K, 1, e, st);
     else
-      launch<BN>(Wqkv, N, X, M, K, z, e, st, true, z > 1);
-  };
-  if (z > 1)
-    dispatch_bn_small(M, (N + 127) / 128 * z, go);
-  else
-    dispatch_bn<int>(M, (N + 127) / 128, go);
+      launch<BN>(Wqkv, N, X, M, K, 1, e, st);
+  });
 }
 
 void gemm_qkv_rope_packed(const bf16* Wqkv, int K, const bf16* X, int M, int H, int KVH, int hd, const int* pos,

@@ -79,7 +79,6 @@ struct GemmGeom {
   int k_blocks;      // total 64-wide K blocks
   int kb_per_split;  // K blocks per gridDim.z slice
   int weight_is_a;   // 1: A is a weight (may be prefetched before griddepcontrol.wait)
-  int cz;            // > 1: the gridDim.z splits form one cluster, reduced through DSMEM (BN <= 64)
   unsigned long long* trace;  // optional per-CTA phase stamps (globaltimer ns), 8 per CTA
 };
 
@@ -222,18 +221,10 @@ __global__ void __launch_bounds__(kGemmThreads, ST == 2 ? 2 : 1)  // the 2-stage
     }
     __syncwarp();
   }
-  // Epilogue warps 2..9 -> TMEM lane quarters (warp % 4), two halves. Without
-  // a cluster split, each reads its accumulator chunks from TMEM. With one
-  // (g.cz > 1: the K splits of a tile are the CTAs of a cluster along z),
-  // every CTA parks its fp32 partial in shared memory, and rank 0 runs the
-  // epilogue on the sum over ranks 0..cz-1 in rank order, read through DSMEM —
-  // a deterministic split-K reduction without a global round trip.
+  // Epilogue warps 2..9 -> TMEM lane quarters (warp % 4), two halves.
   const int quarter = warp & 3;
   const int half = (static_cast<int>(warp) - 2) >> 2;
   const int r = quarter * 32 + lane_id();
-  constexpr int kPStride = (BN < 32 ? 32 : BN) + 4;  // padded fp32 row of the parked partial (32-column chunks)
-  constexpr int kPOff = 64 * 1024;                // parked partial: after any epilogue staging
-  constexpr bool kClusterOK = BN <= 64 && kPOff + 128 * kPStride * 4 <= C::kStages * C::kStageBytes;
   typename Epi::State st{};
   auto run_epi = [&](auto&& load) {
 #pragma unroll 1
@@ -243,15 +234,15 @@ __global__ void __launch_bounds__(kGemmThreads, ST == 2 ? 2 : 1)  // the 2-stage
       for (int c0 = 32 * half; c0 < ((BN + 63) / 64) * 64; c0 += 64) {
         float v[32];
         load(c0, v);
-        epi(st, smem, a_row0, b_row0, g.cz > 1 ? 0 : split, r, half, c0, v);
+        epi(st, smem, a_row0, b_row0, split, r, half, c0, v);
       }
     }
-    epi.finish(st, a_row0, b_row0, g.cz > 1 ? 0 : split, r, half);
+    epi.finish(st, a_row0, b_row0, split, r, half);
     if constexpr (Epi::kTmaStore) {
       fence_async_smem();
       epi_bar_sync();
       if (threadIdx.x == 64) {
-        epi.store(smem, a_row0, b_row0, g.cz > 1 ? 0 : split);
+        epi.store(smem, a_row0, b_row0, split);
         bulk_commit_wait();
       }
     }
@@ -274,47 +265,9 @@ __global__ void __launch_bounds__(kGemmThreads, ST == 2 ? 2 : 1)  // the 2-stage
       if (tr && threadIdx.x == 64) tr[4] = gtime();
       tc_fence_after();
     }
-    if (g.cz > 1) {
-      if constexpr (kClusterOK) {
-        float* P = reinterpret_cast<float*>(smem + kPOff) + r * kPStride;
-        for (int c0 = 32 * half; c0 < BN; c0 += 64) {
-          float v[32];
-          tmem_load(c0, v);
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(P + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        }
-      }
-    } else {
-      run_epi(tmem_load);
-      if (tr && threadIdx.x == 64) tr[5] = gtime();
-      if constexpr (EpiHasPost<Epi>::value) epi.post();
-    }
-  }
-  if constexpr (kClusterOK) {
-    if (g.cz > 1) {
-      cluster_sync();
-      if (warp >= 2 && cluster_ctarank() == 0) {
-        const uint32_t prow = smem_u32(smem + kPOff) + r * kPStride * 4;
-        run_epi([&](int c0, float (&v)[32]) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.f;
-          if (c0 >= BN) return;
-          for (int q = 0; q < g.cz; ++q) {
-            const uint32_t a = mapa_shared(prow + c0 * 4, q);
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 x = ld_dsmem_v4(a + j * 4);
-              v[j] += x.x;
-              v[j + 1] += x.y;
-              v[j + 2] += x.z;
-              v[j + 3] += x.w;
-            }
-          }
-        });
-        if (tr && threadIdx.x == 64) tr[5] = gtime();
-      }
-      cluster_sync();  // peers keep their partials until rank 0 has read them
-    }
+    run_epi(tmem_load);
+    if (tr && threadIdx.x == 64) tr[5] = gtime();
+    if constexpr (EpiHasPost<Epi>::value) epi.post();
   }
   tc_fence_before();
   __syncthreads();
@@ -353,63 +306,6 @@ struct EpiStoreBF16 {
 struct EpiStoreF32 {
   CUtensorMap map;
   int accumulate;
-  // fused add_norm over the partials (x == nullptr: off); M, d = rows, N
-  NormFuse nf{};
-  const float* parts = nullptr;
-  int M = 0, d = 0, ns = 0, total = 0;
-  // After this CTA's partial is in global memory (thread 64 waited for its
-  // bulk store): arrive on counters[0], wait for every CTA of the grid (all
-  // are resident — the host checks), then normalise rows cta, cta + total, ...
-  // with the first 32 * ceil(d / 128) epilogue threads, as add_norm_kernel.
-  __device__ void post() const {
-    if (!nf.x) return;
-    const int t = static_cast<int>(threadIdx.x) - 64;
-    if (t == 0) {
-      asm volatile("fence.proxy.async;" ::: "memory");
-      asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(nf.counters) : "memory");
-      int seen = 0;
-      do {
-        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(nf.counters) : "memory");
-      } while (seen < total);
-    }
-    epi_bar_sync();
-    __shared__ float red[8];
-    const int d4 = d >> 2, nthr = ((d4 + 31) / 32) * 32;
-    const int cta = static_cast<int>(blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z));
-    if (t < nthr) {
-      const int w = t >> 5, l = t & 31, j = t;
-      const bool on = j < d4;
-      const size_t ps4 = static_cast<size_t>(M) * d / 4;
-      for (int row = cta; row < M; row += total) {
-        float4* xr = reinterpret_cast<float4*>(nf.x + static_cast<size_t>(row) * d);
-        const float4* pr = reinterpret_cast<const float4*>(parts + static_cast<size_t>(row) * d);
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (on) {
-          v = xr[j];
-          float4 p[8];
-#pragma unroll
-          for (int s = 0; s < 8; ++s)
-            if (s < ns) p[s] = __ldcg(pr + s * ps4 + j);  // written by other CTAs of this grid: L2
-#pragma unroll
-          for (int s = 0; s < 8; ++s)
-            if (s < ns) v.x += p[s].x, v.y += p[s].y, v.z += p[s].z, v.w += p[s].w;
-          xr[j] = v;
-        }
-        const float ss = group_sum(sumsq4(v), red, w, l, nthr >> 5,
-                                   [&] { asm volatile("bar.sync 3, %0;" ::"r"(nthr) : "memory"); });
-        const float inv = rsqrtf(ss / d + kNormEps);
-        float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (on) {
-          g = reinterpret_cast<const float4*>(nf.gain)[j];
-          reinterpret_cast<uint2*>(nf.y + static_cast<size_t>(row) * d)[j] = norm_scale4(v, inv, g);
-        }
-      }
-    }
-    if (t == 0 && atomicAdd(nf.counters + 1, 1) == total - 1) {  // last out: reset for the next launch
-      atomicExch(nf.counters, 0);
-      atomicExch(nf.counters + 1, 0);
-    }
-  }
   static constexpr bool kTmaStore = true;
   static constexpr int kPasses = 1;
   template <class S> __device__ void next_pass(S&, int, int, int, int) const {}

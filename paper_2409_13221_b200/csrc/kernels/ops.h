@@ -24,26 +24,11 @@ long long launch_count();
 void gemm_bf16(const bf16* W, int N, int K, const bf16* X, int M, bf16* out, int ld_out, cudaStream_t st);
 // fp32 split-K partials: out[s][m][n] for s < splits (see gemm_splits()).
 void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* out, int splits, cudaStream_t st);
-// The residual add + RMSNorm that follows a split-K projection (add_norm over
-// its partials), done by the GEMM's own CTAs once every partial is stored:
-// x[m] += sum_s out[s][m], y[m] = rmsnorm(x[m]) * gain — the same bits as
-// add_norm. counters: 2 ints, zero, left zero.
-struct NormFuse {
-  float* x = nullptr;
-  const float* gain = nullptr;
-  bf16* y = nullptr;
-  int* counters = nullptr;
-};
-// gemm_f32_splitk with the following add_norm fused; false (nothing launched)
-// when the grid cannot be co-resident or d > 1024 — run the two kernels then.
-bool gemm_f32_splitk_norm(const bf16* W, int N, int K, const bf16* X, int M, float* out, int splits,
-                          const NormFuse& nf, cudaStream_t st);
 // resid[m][n] += sum_k X[m][k] W[n][k] (single split; residual add fused).
 void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float* resid, cudaStream_t st);
 // SwiGLU, W_gu [2F, K] interleaved in 64-row gate/up groups: out[m][f], ld = F.
 void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st);
-// Decode variant: the K range split over a thread-block cluster (z CTAs, a
-// function of the weight shape) and reduced through DSMEM in rank order.
+// Decode variant: lean rings for small batches (the next GEMM's CTAs co-reside under PDL).
 void gemm_swiglu_decode(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st);
 // Split count used by gemm_f32_splitk for an (N, K) weight; a function of the
 // weight shape only, so each row's result does not depend on the batch.

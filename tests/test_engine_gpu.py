@@ -193,13 +193,21 @@ def test_fused_rope_prefill_scoring_bit_identical(small64):
 def test_decode_chain_bit_identical(request, fixture):
     """The persistent decode-chain kernel (O -> norm -> gate/up -> down -> norm ->
     next QKV in one launch, the default) gives the same experience bits as the six
-    separate kernels it replaces (FUSEPLAN_DECODE_CHAIN=0), on hd 64 MHA and hd 128
+    separate kernels it replaces (FUSEPLAN_DECODE_CHAIN=0; 512 for the chain at every batch size), on hd 64 MHA and hd 128
     GQA, across batch sizes 1..160 as samples retire."""
     import os
     from paper_2409_13221_b200.configs import gen_config
     from paper_2409_13221_b200.engine import Engine
     w, eng, batch, _ = request.getfixturevalue(fixture)
-    a = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="fused", claim_tokens=4096)
+    os.environ["FUSEPLAN_DECODE_CHAIN"] = "512"
+    try:
+        eng1 = Engine(w, device=0)
+    finally:
+        del os.environ["FUSEPLAN_DECODE_CHAIN"]
+    try:
+        a = eng1.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="fused", claim_tokens=4096)
+    finally:
+        eng1.close()
     os.environ["FUSEPLAN_DECODE_CHAIN"] = "0"
     try:
         eng2 = Engine(w, device=0)

@@ -525,3 +525,59 @@ def test_vocab_filtered_distribution(lib):
     assert freq.sum().item() == pytest.approx(1.0)
     assert (freq[top.indices].sum() - 1.0).abs().item() < 1e-6  # all mass inside the top 5
     assert (freq[top.indices] - p).abs().max().item() < 0.03
+
+
+# ---------------------------------------------------------------------------
+# The persistent decode chain vs the separate kernels it replaces, bit for bit.
+
+@pytest.mark.parametrize("d,H,KVH,hd,F,M", [
+    (256, 4, 4, 64, 512, 37), (768, 12, 12, 64, 3072, 1), (768, 12, 12, 64, 3072, 16),
+    (768, 12, 12, 64, 3072, 100), (768, 12, 12, 64, 3072, 284), (768, 12, 12, 64, 3072, 512),
+    (2048, 16, 16, 128, 5632, 1), (2048, 16, 16, 128, 5632, 64), (2048, 16, 16, 128, 5632, 256),
+    (4096, 32, 8, 128, 14336, 1), (4096, 32, 8, 128, 14336, 64)])
+@pytest.mark.parametrize("last", [False, True])
+def test_decode_chain_matches_separate_kernels(lib, d, H, KVH, hd, F, M, last):
+    L, layer, PT, max_pos, theta = 3, 0, 64, 600, 10000.0
+    ao, qw = H * hd, (H + 2 * KVH) * hd
+    Wo = rand_bf16(d, ao, scale=ao ** -0.5, seed=50)
+    Wgu = rand_bf16(2 * F, d, scale=d ** -0.5, seed=51)
+    Wd = rand_bf16(d, F, scale=F ** -0.5, seed=52)
+    Wqkv = rand_bf16(qw, d, scale=d ** -0.5, seed=53)
+    attn = rand_bf16(M, ao, seed=54)
+    g = torch.Generator(device="cuda").manual_seed(55)
+    x0 = torch.randn(M, d, device="cuda", generator=g)
+    g1 = torch.rand(d, device="cuda", generator=g) + 0.5
+    g2 = torch.rand(d, device="cuda", generator=g) + 0.5
+    pos = torch.randint(0, max_pos, (M,), device="cuda", generator=g, dtype=torch.int32)
+    maxp = (max_pos + PT - 1) // PT
+    npages = M * maxp + 1
+    bt = (torch.randperm(npages - 1, device="cuda", generator=g)[: M * maxp] + 1).to(torch.int32).view(M, maxp)
+    bt = bt.contiguous()
+    slot = torch.randperm(M, device="cuda", generator=g).to(torch.int32)
+
+    def buffers():
+        return dict(x=x0.clone(), h=torch.zeros(M, d, device="cuda", dtype=torch.bfloat16),
+                    act=torch.zeros(M, F, device="cuda", dtype=torch.bfloat16),
+                    parts=torch.zeros(8, M, d, device="cuda"),
+                    q=torch.zeros(M, H, hd, device="cuda", dtype=torch.bfloat16),
+                    pool=torch.zeros(npages, L, KVH, 2, PT, hd, device="cuda", dtype=torch.bfloat16))
+
+    a = buffers()
+    ok(lib, lib.fp_k_decode_chain(ptr(Wo), ptr(Wgu), ptr(Wd), None if last else ptr(Wqkv), ptr(attn), ptr(a["h"]),
+                                  ptr(a["act"]), ptr(a["parts"]), ptr(a["x"]), ptr(g1), ptr(g2), ptr(a["q"]),
+                                  ptr(a["pool"]), L, layer, ptr(bt), maxp, ptr(slot), ptr(pos), max_pos, theta, M, d,
+                                  H, KVH, hd, F, stream()))
+    b = buffers()
+    so, sd = lib.fp_k_gemm_splits(d, ao), lib.fp_k_gemm_splits(d, F)
+    ok(lib, lib.fp_k_gemm_f32(ptr(Wo), d, ao, ptr(attn), M, ptr(b["parts"]), so, stream()))
+    ok(lib, lib.fp_k_add_norm(ptr(b["x"]), ptr(b["parts"]), so, ptr(g1), ptr(b["h"]), M, d, stream()))
+    ok(lib, lib.fp_k_gemm_swiglu_decode(ptr(Wgu), F, d, ptr(b["h"]), M, ptr(b["act"]), stream()))
+    ok(lib, lib.fp_k_gemm_f32(ptr(Wd), d, F, ptr(b["act"]), M, ptr(b["parts"]), sd, stream()))
+    ok(lib, lib.fp_k_add_norm(ptr(b["x"]), ptr(b["parts"]), sd, ptr(g2), ptr(b["h"]), M, d, stream()))
+    if not last:
+        ok(lib, lib.fp_k_qkv_rope(ptr(Wqkv), d, ptr(b["h"]), M, H, KVH, hd, ptr(pos), max_pos, theta, ptr(b["pool"]),
+                                  L, layer + 1, ptr(bt), maxp, ptr(slot), ptr(b["q"]), stream()))
+    torch.cuda.synchronize()
+    for k in ("act", "x", "h", "q", "pool"):
+        assert torch.equal(a[k], b[k]), (k, (a[k].float() - b[k].float()).abs().max().item())
+    assert torch.equal(a["parts"][:sd], b["parts"][:sd])

@@ -13,7 +13,11 @@ import numpy as np
 
 DETAIL = '--detail' in sys.argv
 
-KIND = {0: "gemm", 1: "attn", 2: "attn-team"}
+KIND = {0: "gemm", 1: "attn", 2: "attn-team", 3: "chain"}
+# decode_chain stamps (16 per CTA): see csrc/kernels/chain.cu
+CHAIN = [(1, "P0 acc"), (2, "P0 arrive"), (3, "P1 wait"), (4, "P1 arrive"), (14, "P2 act-in"), (5, "P2 acc"),
+         (6, "P2 arrive"), (7, "P3 wait"), (8, "P3 acc"), (9, "P3 arrive"), (10, "P4 wait"), (11, "P4 arrive"),
+         (15, "P5 act-in"), (12, "P5 acc"), (13, "P5 end")]
 
 
 def run(step, out):
@@ -38,6 +42,16 @@ def show(path):
             beg, end = min(c[0] for c in cta), max(max(c[5], c[4], c[0]) for c in cta)
             first = sorted(c[2] - c[0] for c in cta if c[2])
             extra = f"ctas {len(cta):4d}, first-data median {first[len(first) // 2] / 1e3:5.2f} us" if first else ""
+        elif L["kind"] == 3:  # decode_chain: 16 stamps per CTA
+            cta = [x[k:k + 16] for k in range(0, len(x), 16)]
+            beg = min(c[0] for c in cta if c[0])
+            end = max(max(c) for c in cta)
+            extra = f"ctas {len(cta):4d}"
+            if DETAIL:
+                for col, nm in CHAIN:
+                    v = np.array([c[col] for c in cta if c[col] > 0], dtype=np.float64)
+                    if len(v):
+                        extra += f"\n      {nm:10s} " + " ".join(f"{(q - beg) / 1e3:6.2f}" for q in np.percentile(v, [0, 50, 100]))
         else:  # 4 words per warp / CTA: entry, loop-begin, end, units
             w = [x[k:k + 4] for k in range(0, len(x), 4)]
             w = [v for v in w if v[0] > 0]
