@@ -132,7 +132,7 @@ def main():
             # of its destinations; the queued migrants all move
             queued = {s[0] for s in state if not s[5]} & set(plan.migrated)
             moved = {m[0] for m in out.moves}
-            res["moves_within_plan"] = (plan.no_op == (len(out.moves) == 0) and moved <= set(plan.migrated)
+            res["moves_within_plan"] = ((not plan.no_op or not out.moves) and moved <= set(plan.migrated)
                                         and all(m[2] in plan.destinations for m in out.moves) and queued <= moved)
     dist.barrier()
     # weight sync: rank 0 gets new actor weights, every rank pulls them
