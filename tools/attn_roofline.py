@@ -18,7 +18,10 @@ from paper_2409_13221_b200 import _lib  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 mean_ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 380
-H, KVH, hd, L, layer, PT = 12, 12, 64, 12, 5, 64
+import os
+H, KVH, hd, PT = 12, 12, 64, 64
+L = int(os.environ.get("ATTN_L", "12"))  # layers per page (page bytes scale with L)
+layer = min(5, L - 1)
 lib = _lib.load()
 g = torch.Generator().manual_seed(5)
 ctx = (torch.rand(B, generator=g) * 2 * mean_ctx).clamp(min=1).to(torch.int32)  # uniform on [1, 2 mean)
