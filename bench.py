@@ -114,10 +114,10 @@ PER_GPU = {"gpt2s": 512, "1.3b": 256, "8b": 64}
 DESC = {"gpt2s": "GPT-2-small-shape", "1.3b": "1.3B-shape (Llama-style)", "8b": "Llama-3-8B-shape (GQA 32/8)"}
 
 
-def workload_for(n_gpus, name="gpt2s", zipf_s=None):
+def workload_for(n_gpus, name="gpt2s", zipf_s=None, per_gpu=None):
     from paper_2409_13221_b200.configs import WORKLOADS, scaled
     w = WORKLOADS[name]
-    w = scaled(w, n_prompts=PER_GPU[name] * n_gpus)
+    w = scaled(w, n_prompts=(per_gpu or PER_GPU[name]) * n_gpus)
     return w if zipf_s is None else scaled(w, zipf_s=zipf_s)
 
 
@@ -178,7 +178,7 @@ def run_reference(args, world, rank):
     runtime is reported beside it. Nothing here loads the product library."""
     if rank != 0:
         return
-    w = workload_for(args.gpus, args.workload, args.zipf_s)
+    w = workload_for(args.gpus, args.workload, args.zipf_s, args.prompts_per_gpu)
     batch, batch_src = python_batch(w)
     cores = os.cpu_count() or 1
     n_sub = {"gpt2s": 2, "1.3b": 1, "8b": 1}.get(w.name, 2)
@@ -222,6 +222,7 @@ def config_dict(w, G, args, r_t=None, ratio=None):
     return {"workload": workload_desc(w, G), "prompts": w.n_prompts, "zipf_s": w.zipf_s, "schedule": "fused",
             "r_t": r_t, "r_ratio": ratio, "token_mode": args.token_mode, "claim_tokens": args.claim_tokens,
             "l2": "inputs larger than L2 (KV pool and weights >> 126 MB)",
+            "kv_pool_gb": getattr(args, "kv_pool_gb", 0.0) or None,
             "parallelism": f"dp{G} (one engine per B200)"}
 
 
@@ -245,6 +246,12 @@ def main():
                     help="output-length skew (configs[4] sweep): 0 = uniform on [16, max_new]; default = the "
                          "workload's (1.0)")
     ap.add_argument("--quick", action="store_true", help="value pass only (for profiling)")
+    ap.add_argument("--prompts-per-gpu", type=int, default=None,
+                    help="override the workload's prompts per GPU (e.g. 512 for configs[3] at its stated batch)")
+    ap.add_argument("--kv-pool-gb", type=float, default=0.0,
+                    help="> 0: physical KV pool per GPU (GB); admission is then KV-gated: the decision clock's "
+                         "capacity is the pool in the reference's MHA reservation units (core.cpp:90-93)")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the e2e pass (long configs)")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup()
     if args.impl == "reference":
@@ -259,10 +266,20 @@ def main():
     from paper_2409_13221_b200.engine import Engine
 
     G = world
-    w = workload_for(G, args.workload, args.zipf_s)
-    eng = Engine(w, device=local, max_samples=w.n_prompts, max_live=min(w.n_prompts, 2 * w.n_prompts // G))
+    w = workload_for(G, args.workload, args.zipf_s, args.prompts_per_gpu)
+    max_live = min(w.n_prompts, 2 * w.n_prompts // G)
+    pool = int(args.kv_pool_gb * 1e9)
+    eng = Engine(w, device=local, max_samples=w.n_prompts, max_live=max_live, kv_pool_bytes=pool)
     batch = batch_for(w, eng.sched)
     cfg = gen_config(w, G, calibrated=True)  # decision-clock constants fitted to measured B200 steps
+    if pool > 0:
+        # KV-gated admission (genfuse.cpp:226-236): the clock reserves (prompt + target) x the reference's
+        # MHA bytes per token (core.cpp:90-93, 4 L hidden); the engine holds GQA pages of 64 tokens. Map the
+        # physical pool into the clock's units, less one page per live slot for the page rounding.
+        a = w.actor
+        page = 64 * eng.kv_bytes_per_token()
+        mha_over_phys = 4.0 * a.num_layers * a.hidden / eng.kv_bytes_per_token()
+        cfg.cluster.kv_capacity_per_instance = (pool - max_live * page) * mha_over_phys
     if args.r_ratio == "auto" and G > 1:
         sw = eng.sched.sweep_threshold(batch, cfg)
         ratio = sw.curve[sw.best_index][0]
@@ -341,8 +358,9 @@ def main():
     h2d = len(batch) * w.prompt_len * 4 + len(batch) * 4 * 6
     d2h = int(st["total_resp"]) * 4 * 8 + len(batch) * 4
     if not args.quick:
-        ms_e, outs_e = timed("fused", False, args.steps)
-        e2e = n_total * args.steps / (ms_e / 1000.0)
+        if not args.no_e2e:
+            ms_e, outs_e = timed("fused", False, args.steps)
+            e2e = n_total * args.steps / (ms_e / 1000.0)
         if not args.no_barrier_arm:
             ms_s, outs_s = timed("stage_barrier", True, args.steps)
             sb = n_total * args.steps / (ms_s / 1000.0)
