@@ -166,8 +166,9 @@ int fp_exec_handoff(const fp_exec* x, int32_t* dp, int32_t* group_begin, int32_t
  * packed_off[group_off[begin]] entries, score group_off[end] - group_off[begin]).
  * host[9] in the order of dev[]; NULL entries are skipped. */
 int fp_exec_handoff_download(const fp_exec* x, void** host);
-/* Per decode step of this rank: batch rows and GPU milliseconds (n_steps entries; NULL to query). */
-int fp_exec_steps(const fp_exec* x, int32_t* n_steps, int32_t* rows, float* ms);
+/* Per decode step of this rank: batch rows, GPU milliseconds and visible context tokens summed over the
+ * rows (n_steps entries; NULL to query / skip). */
+int fp_exec_steps(const fp_exec* x, int32_t* n_steps, int32_t* rows, float* ms, int64_t* ctx);
 void fp_exec_free(fp_exec* x);
 
 /* ---- single-kernel entry points (device pointers) ---- */

@@ -149,6 +149,7 @@ struct ExecResult {
   ExecStats stats;
   std::vector<int> step_rows;       // per decode step: batch rows
   std::vector<float> step_ms;       // per decode step: GPU duration (ms)
+  std::vector<std::int64_t> step_ctx;  // per decode step: visible context tokens summed over its rows
   Handoff handoff;
 };
 

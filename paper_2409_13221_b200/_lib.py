@@ -179,7 +179,7 @@ ENGINE_SYMBOLS = {
     "fp_exec_handoff": (C.c_int, [_vp, _i32p, _i32p, _i32p, _i32p, _i32p, _i64p, P(C.c_void_p), _f64p, _i64p,
                                   _i64p]),
     "fp_exec_handoff_download": (C.c_int, [_vp, P(C.c_void_p)]),
-    "fp_exec_steps": (C.c_int, [_vp, _i32p, _i32p, _f32p]),
+    "fp_exec_steps": (C.c_int, [_vp, _i32p, _i32p, _f32p, _i64p]),
     "fp_exec_free": (None, [_vp]),
     "fp_k_init_bf16": (C.c_int, [_vp, C.c_int64, C.c_uint64, C.c_uint64, C.c_float, _vp]),
     "fp_k_gemm_bf16": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, _vp, C.c_int32, _vp]),

@@ -424,13 +424,14 @@ int fp_exec_handoff_download(const fp_exec* x, void** host) {
   });
 }
 
-int fp_exec_steps(const fp_exec* x, int32_t* n_steps, int32_t* rows, float* ms) {
+int fp_exec_steps(const fp_exec* x, int32_t* n_steps, int32_t* rows, float* ms, int64_t* ctx) {
   return guarded([&] {
     need(x, "exec");
     if (n_steps) *n_steps = static_cast<int32_t>(x->r.step_rows.size());
     for (size_t i = 0; i < x->r.step_rows.size(); ++i) {
       if (rows) rows[i] = x->r.step_rows[i];
       if (ms) ms[i] = i < x->r.step_ms.size() ? x->r.step_ms[i] : 0.f;
+      if (ctx) ctx[i] = i < x->r.step_ctx.size() ? x->r.step_ctx[i] : 0;
     }
   });
 }

@@ -764,6 +764,7 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
     res.stats.decode_steps += 1;
     res.stats.decode_rows += static_cast<int64_t>(rows.size());
     res.step_rows.push_back(static_cast<int>(rows.size()));
+    res.step_ctx.push_back(ctx);
     res.stats.decode_ctx_tokens += ctx;
     // bound host run-ahead
     const int kk = k - opts.run_ahead;

@@ -59,6 +59,7 @@ class ExecOutput:
     received: list = None         # (sample, source rank) this rank pulled in at the migration
     trigger_state: tuple = None   # (time, [Remaining...]) the executed plan was taken on
     online: bool = False          # the trigger was taken online
+    step_ctx: np.ndarray = None   # per decode step: visible context tokens summed over its rows
 
 
 class Engine:
@@ -225,11 +226,13 @@ class Engine:
             check(self.lib, self.lib.fp_exec_moves(x, C.byref(nm), ms, mf, mt))
             moves = list(zip(ms[:nm.value], mf[:nm.value], mt[:nm.value]))
             ns = C.c_int32()
-            check(self.lib, self.lib.fp_exec_steps(x, C.byref(ns), None, None))
+            check(self.lib, self.lib.fp_exec_steps(x, C.byref(ns), None, None, None))
             srows = np.zeros(max(ns.value, 1), dtype=np.int32)
             sms = np.zeros(max(ns.value, 1), dtype=np.float32)
+            sctx = np.zeros(max(ns.value, 1), dtype=np.int64)
             check(self.lib, self.lib.fp_exec_steps(x, C.byref(ns), srows.ctypes.data_as(C.POINTER(C.c_int32)),
-                                                   sms.ctypes.data_as(C.POINTER(C.c_float))))
+                                                   sms.ctypes.data_as(C.POINTER(C.c_float)),
+                                                   sctx.ctypes.data_as(C.POINTER(C.c_int64))))
             handoff = self._handoff(x, n) if handoff_dp > 0 else None
             nr = C.c_int32()
             check(self.lib, self.lib.fp_exec_received(x, C.byref(nr), None, None))
@@ -242,6 +245,6 @@ class Engine:
             state = (tt.value, [(r.id, r.instance, r.kv_bytes, r.generated, r.prompt_len, bool(r.admitted))
                                 for r in tst[:nt.value]])
             return ExecOutput(stats, exp, fin, inst, decision, moves, srows[:ns.value], sms[:ns.value], handoff,
-                              list(zip(rs[:nr.value], rf[:nr.value])), state, bool(st.online))
+                              list(zip(rs[:nr.value], rf[:nr.value])), state, bool(st.online), sctx[:ns.value])
         finally:
             self.lib.fp_exec_free(x)

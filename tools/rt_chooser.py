@@ -1,0 +1,216 @@
+"""R_t chooser that models intra-GPU sharing.
+
+The reference chooses the migration threshold with `sweep_threshold`
+(genfuse.cpp:517-534) on its CostModel (core.hpp:31-44): a decode step of
+`decode_step_base * max(1, B / bs_max)` and a fluid scoring drain that starts
+on an instance only when it stops generating. Calibrated to B200 steps
+(tools/calibrate.py) it still predicts a 1.27-1.29x fused gain where 1.03-1.14x
+is measured: on a B200 a decode step is not flat below bs_max (it grows with
+the visible context), and a generating GPU scores too — at low priority, on
+the SMs decode leaves idle — and decodes slower while it does.
+
+This predictor replays the fused and the stage-barrier schedules with three
+fitted terms, all from one 1-GPU profile of the workload
+(tools/step_profile_dump.py):
+  * step time   t(B, C) = a + b B + c C      (B rows, C visible context tokens),
+                least squares on the stage-barrier steps;
+  * sharing     steps of a GPU that is also scoring take (1 + s) t(B, C);
+                scoring on a generating GPU advances at a fraction phi of its
+                dedicated rate (both from the fused 1-GPU run);
+  * scoring     a sample costs flops(T) / F seconds, F = the stage-barrier
+                run's achieved flop rate (bench.py's flop count);
+and the reference's own decisions: round-robin sharding, the trigger when
+fewer than r_t samples remain, plan_migration and apply_migration's in-flight
+placement (through the product scheduler, bit-exact with the reference).
+
+    python tools/rt_chooser.py PROFILE.json [--validate]
+
+prints the fitted model, the predicted fused / stage-barrier ratio for R_t /
+n in 5 % steps at G = 2, 4, 8, the chosen R_t, and (with --validate) the
+prediction next to the measured bench lines in profiles/.
+"""
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from paper_2409_13221_b200.configs import WORKLOADS, batch_for, gen_config, scaled  # noqa: E402
+from paper_2409_13221_b200.sched import Remaining, Sched  # noqa: E402
+
+PER_GPU = {"gpt2s": 512, "1.3b": 256}
+
+
+def fwd_flops(d, T, vocab_head):
+    dense = d.param_count(lm_head=False) - d.vocab * d.hidden
+    return 2 * T * (dense + (d.hidden * d.vocab if vocab_head else d.hidden)) + \
+        2 * T * T * d.num_heads * d.head_dim * d.num_layers
+
+
+def sample_flops(w, T):
+    return fwd_flops(w.ref, T, True) + fwd_flops(w.critic, T, False) + fwd_flops(w.reward, T, False)
+
+
+def fit(profile):
+    w = WORKLOADS[profile["workload"]]
+    sb, fu = profile["stage_barrier"], profile["fused"]
+    X = np.stack([np.ones(len(sb["rows"])), np.array(sb["rows"], float), np.array(sb["ctx"], float)], 1)
+    y = np.array(sb["ms"]) * 1e-3
+    coef, *_ = np.linalg.lstsq(X, y, rcond=None)
+    pred = X @ coef
+    r2 = 1 - np.sum((y - pred) ** 2) / np.sum((y - y.mean()) ** 2)
+    P = profile["prompt_len"]
+    flops = sum(sample_flops(w, P + L) for L in profile["lengths"])
+    F = flops / sb["infer_busy"]  # dedicated scoring rate (flop/s)
+    Xf = np.stack([np.ones(len(fu["rows"])), np.array(fu["rows"], float), np.array(fu["ctx"], float)], 1)
+    share = float(np.sum(np.array(fu["ms"]) * 1e-3) / np.sum(Xf @ coef) - 1.0)
+    # phi: scoring progress on the generating GPU. Fused 1-GPU run: generation
+    # ends at gen_f; the remaining scoring then runs dedicated for wall - gen_f.
+    S = sb["infer_busy"]
+    gen_f = fu["gen_seconds"]
+    first = min(fu["finish"])
+    tail = max(0.0, fu["wall"] - gen_f)
+    phi = float(np.clip((S - tail) / max(gen_f - first, 1e-9), 0.0, 1.0))
+    return {"a": coef[0], "b": coef[1], "c": coef[2], "r2": r2, "F": F, "share": share, "phi": phi}
+
+
+def simulate(w, batch, G, r_t, m, cfg, sched, fused):
+    """Seconds until every sample is generated and scored (fluid scoring drain)."""
+    n = len(batch)
+    P = w.prompt_len
+    L = [s.target_output_len for s in batch]
+    cost = [sample_flops(w, P + l) / m["F"] for l in L]
+    live = [[s for s in range(n) if s % G == g] for g in range(G)]
+    gen = [0] * n
+    clock = [0.0] * G
+    finish = [None] * n
+    triggered = not fused or r_t <= 0
+    remaining = n
+    done_at = [None] * G
+    pool = []  # (ready time, seconds of dedicated scoring work)
+    # per-GPU step loop in global time order
+    while True:
+        active = [g for g in range(G) if live[g]]
+        if not active:
+            break
+        g = min(active, key=lambda k: clock[k])
+        B = len(live[g])
+        C = sum(P + gen[s] for s in live[g])
+        t = m["a"] + m["b"] * B + m["c"] * C
+        if fused and pool:  # this GPU shares its SMs with scoring
+            t *= 1.0 + m["share"]
+        clock[g] += t
+        keep = []
+        for s in live[g]:
+            gen[s] += 1
+            if gen[s] >= L[s]:
+                finish[s] = clock[g]
+                pool.append((clock[g], cost[s]))
+                remaining -= 1
+            else:
+                keep.append(s)
+        live[g] = keep
+        if not live[g]:
+            done_at[g] = clock[g]
+        if not triggered and remaining < r_t:
+            triggered = True
+            t0 = clock[g]
+            state = [Remaining(s, k, float(batch[s].kv_bytes), gen[s], P, True) for k in range(G) for s in live[k]]
+            state.sort(key=lambda r: r.id)
+            plan = sched.plan_migration(t0, state, r_t, cfg)
+            if not plan.no_op:
+                dest = list(plan.destinations)
+                movers = sorted((s for s in plan.migrated), key=lambda s: (-(L[s] - gen[s]), s))
+                moved_bytes = 0.0
+                for s in movers:
+                    src = s % G if s in live[s % G] else next(k for k in range(G) if s in live[k])
+                    k = min(dest, key=lambda d: (len(live[d]), d))
+                    live[src].remove(s)
+                    live[k].append(s)
+                    moved_bytes += (P + gen[s]) * w.actor.kv_bytes_per_token()
+                over = moved_bytes / cfg.cluster.interconnect_bandwidth
+                for k in range(G):
+                    clock[k] = max(clock[k], t0)
+                    if not live[k] and done_at[k] is None:
+                        done_at[k] = t0
+                for d in dest:
+                    clock[d] += over
+    gen_end = max(finish)
+    # fluid scoring drain: GPU g scores at phi while generating (fused), at 1
+    # once it is done; stage barrier: every GPU at 1 from gen_end on
+    pool.sort()
+
+    def rate(t):
+        if not fused:
+            return float(G) if t >= gen_end else 0.0
+        return sum(1.0 if (done_at[k] is not None and done_at[k] <= t) else m["phi"] for k in range(G))
+
+    bps = sorted(set([x[0] for x in pool] + [d for d in done_at if d is not None] + [gen_end]))
+    backlog, pi, end = 0.0, 0, gen_end
+    for i, t0 in enumerate(bps):
+        while pi < len(pool) and pool[pi][0] <= t0:
+            backlog += pool[pi][1]
+            pi += 1
+        t1 = bps[i + 1] if i + 1 < len(bps) else float("inf")
+        r = rate(t0)
+        if r <= 0 or backlog <= 0:
+            continue
+        if backlog <= r * (t1 - t0):
+            end = max(end, t0 + backlog / r)
+            backlog = 0.0
+        else:
+            backlog -= r * (t1 - t0)
+    return end
+
+
+def main():
+    prof = json.loads(Path(sys.argv[1]).read_text())
+    name = prof["workload"]
+    m = fit(prof)
+    print(f"[{name}] step model: t = {m['a'] * 1e3:.3f} ms + {m['b'] * 1e6:.3f} us x B + {m['c'] * 1e9:.3f} ns x C "
+          f"(R^2 {m['r2']:.3f}); scoring {m['F'] / 1e12:.0f} TF/s dedicated; sharing +{m['share'] * 100:.1f} % "
+          f"decode, scoring at phi = {m['phi']:.2f} while generating")
+    sched = Sched()
+    out = {"workload": name, "model": {k: float(v) for k, v in m.items()}, "G": {}}
+    for G in (2, 4, 8):
+        w = scaled(WORKLOADS[name], n_prompts=PER_GPU[name] * G)
+        batch = batch_for(w, sched)
+        cfg = gen_config(w, G, calibrated=True)
+        base = simulate(w, batch, G, 0, m, cfg, sched, fused=False)
+        rows = []
+        for ratio in [0.0] + [x / 100 for x in range(5, 100, 5)]:
+            r_t = round(ratio * len(batch))
+            fz = simulate(w, batch, G, r_t, m, cfg, sched, fused=True)
+            rows.append((ratio, fz, base / fz))
+        best = min(rows, key=lambda r: (r[1], r[0]))
+        ref = sched.sweep_threshold(batch, cfg)
+        serial = ref.serial_total
+        ref_best = (ref.curve[ref.best_index][0], ref.curve[ref.best_index][2])
+        out["G"][G] = {"stage_barrier_s": base, "curve": rows, "best_ratio": best[0], "best_gain": best[2],
+                       "gain_at_0.2": next(r[2] for r in rows if abs(r[0] - 0.2) < 1e-9),
+                       "reference_sweep_best_ratio": ref_best[0], "reference_sweep_gain": serial / ref_best[1]}
+        print(f"  G={G}: barrier {base:.3f} s; predicted fused gain at R_t 20 %: "
+              f"{out['G'][G]['gain_at_0.2']:.3f}; best R_t {best[0]:.2f} ({best[2]:.3f}x); reference sweep "
+              f"(calibrated CostModel) predicts {out['G'][G]['reference_sweep_gain']:.3f}x at {ref_best[0]:.2f}")
+    if "--validate" in sys.argv:
+        meas = {}
+        for G in (2, 4):
+            key = {"gpt2s": f"r02_bench_gpt2s_{G}gpu.json", "1.3b": f"r02_bench_13b_{G}gpu.json"}[name]
+            p = ROOT / "profiles" / key
+            if p.exists():
+                d = json.loads(p.read_text())
+                meas[G] = d["stage_barrier"]["speedup_fused"]
+                pred = out["G"][G]["gain_at_0.2"] if abs(d["config"]["r_ratio"] - 0.2) < 1e-9 else None
+                print(f"  measured G={G} (R_t {d['config']['r_ratio']:.2f}): {meas[G]:.3f}x; predicted "
+                      f"{pred:.3f}x ({(pred / meas[G] - 1) * 100:+.1f} %); reference sweep "
+                      f"{out['G'][G]['reference_sweep_gain']:.3f}x")
+        out["measured"] = meas
+    if len(sys.argv) > 2 and sys.argv[-1].endswith(".json") and sys.argv[-1] != sys.argv[1]:
+        Path(sys.argv[-1]).write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,7 +1,9 @@
-"""Per-decode-step (rows, GPU ms) of one gpt2s bench step (stage barrier and
-fused), for the time-vs-batch-size breakdown in DESIGN.md.
+"""Per-decode-step (rows, visible context, GPU ms) and scoring totals of one
+bench step on 1 B200, stage barrier and fused — the measurements the R_t
+chooser (tools/rt_chooser.py) fits its step and sharing model to, and the
+time-vs-batch-size breakdown in DESIGN.md §8.
 
-    python tools/step_profile_dump.py out.json
+    python tools/step_profile_dump.py gpt2s|1.3b out.json
 """
 import json
 import sys
@@ -10,16 +12,24 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
-from paper_2409_13221_b200.configs import WORKLOADS, batch_for, gen_config  # noqa: E402
+from paper_2409_13221_b200.configs import WORKLOADS, batch_for, gen_config, scaled  # noqa: E402
 from paper_2409_13221_b200.engine import Engine  # noqa: E402
 
-w = WORKLOADS["gpt2s"]
+name = sys.argv[1]
+w = WORKLOADS[name]
+if name == "1.3b":
+    w = scaled(w, n_prompts=256)  # the bench's per-GPU batch
 eng = Engine(w)
 batch = batch_for(w, eng.sched)
-res = {}
-for sched in ("stage_barrier", "fused", "stage_barrier", "fused"):
-    out = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule=sched, resident=True)
-    res[sched] = {"rows": out.step_rows.tolist(), "ms": out.step_ms.tolist(),
-                  "gen_seconds": out.stats["gen_seconds"], "infer_busy": out.stats["infer_busy_seconds"],
-                  "wall": out.stats["wall_seconds"]}
-Path(sys.argv[1]).write_text(json.dumps(res))
+res = {"workload": name, "n": len(batch), "prompt_len": w.prompt_len,
+       "lengths": [b.target_output_len for b in batch]}
+for rep in range(2):
+    for sched in ("stage_barrier", "fused"):
+        out = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule=sched, resident=True)
+        if rep == 0:
+            continue  # warm-up (graphs captured)
+        res[sched] = {"rows": out.step_rows.tolist(), "ms": out.step_ms.tolist(), "ctx": out.step_ctx.tolist(),
+                      "gen_seconds": out.stats["gen_seconds"], "infer_busy": out.stats["infer_busy_seconds"],
+                      "infer_tokens": out.stats["infer_tokens"], "wall": out.stats["wall_seconds"],
+                      "finish": out.finish_seconds.tolist()}
+Path(sys.argv[2]).write_text(json.dumps(res))
