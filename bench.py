@@ -218,9 +218,21 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def chooser_ratio(w, G):
+    """R_t / n picked by tools/rt_chooser.py (committed fit of measured B200 steps), else 0.2."""
+    key = {"gpt2s": "gpt2s", "1.3b": "13b"}.get(w.name)
+    p = ROOT / "profiles" / f"r02_rt_chooser_{key}.json"
+    if key and p.exists():
+        g = json.loads(p.read_text())["G"].get(str(G))
+        if g:
+            return float(g["best_ratio"])
+    return 0.2
+
+
 def config_dict(w, G, args, r_t=None, ratio=None):
     return {"workload": workload_desc(w, G), "prompts": w.n_prompts, "zipf_s": w.zipf_s, "schedule": "fused",
-            "r_t": r_t, "r_ratio": ratio, "token_mode": args.token_mode, "claim_tokens": args.claim_tokens,
+            "r_t": r_t, "r_ratio": ratio, "r_ratio_source": getattr(args, "r_ratio", None),
+            "token_mode": args.token_mode, "claim_tokens": args.claim_tokens,
             "l2": "inputs larger than L2 (KV pool and weights >> 126 MB)",
             "kv_pool_gb": getattr(args, "kv_pool_gb", 0.0) or None,
             "parallelism": f"dp{G} (one engine per B200)"}
@@ -232,9 +244,11 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--r-ratio", default="0.2",
-                    help="migration threshold R_t / n, or 'auto': the best ratio of sweep_threshold under the "
-                         "calibrated CostModel (the paper's workflow, SURVEY §8f row 1)")
+    ap.add_argument("--r-ratio", default="chooser",
+                    help="migration threshold R_t / n; 'chooser': the best ratio of tools/rt_chooser.py's "
+                         "sharing-aware model for this workload and G (profiles/r02_rt_chooser_<w>.json; 0.2 "
+                         "without one); 'auto': the best ratio of the reference's sweep_threshold under the "
+                         "calibrated CostModel")
     ap.add_argument("--token-mode", default="sample", choices=["forced", "greedy", "sample"])
     ap.add_argument("--claim-tokens", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -283,8 +297,10 @@ def main():
     if args.r_ratio == "auto" and G > 1:
         sw = eng.sched.sweep_threshold(batch, cfg)
         ratio = sw.curve[sw.best_index][0]
+    elif args.r_ratio == "chooser":
+        ratio = chooser_ratio(w, G)
     else:
-        ratio = float(args.r_ratio) if args.r_ratio != "auto" else 0.2
+        ratio = float(args.r_ratio)
     r_t = round(ratio * len(batch)) if G > 1 else 0
     shm = None
     if dist:

@@ -1,0 +1,35 @@
+"""The sharing-aware R_t chooser (tools/rt_chooser.py): fitted
+on a committed 1-GPU step profile, its predicted fused / stage-barrier gain at
+2 GPUs is within 5 % of the gain the bench measured on B200s (committed
+profiles/r02_bench_*_2gpu.json, R_t = 20 %), where the reference's own
+sweep_threshold on the calibrated CostModel is 9-23 % off."""
+import json
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT / "tools"))
+
+
+@pytest.mark.parametrize("prof,bench", [("r02_steps_gpt2s.json", "r02_bench_gpt2s_2gpu.json"),
+                                        ("r02_steps_13b.json", "r02_bench_13b_2gpu.json")])
+def test_chooser_predicts_measured_fused_gain(prof, bench):
+    import rt_chooser as rc
+    from paper_2409_13221_b200.configs import WORKLOADS, batch_for, gen_config, scaled
+    from paper_2409_13221_b200.sched import Sched
+    p = json.loads((ROOT / "profiles" / prof).read_text())
+    meas = json.loads((ROOT / "profiles" / bench).read_text())
+    m = rc.fit(p)
+    assert m["r2"] > 0.9
+    G = meas["n_gpus"]
+    name = p["workload"]
+    w = scaled(WORKLOADS[name], n_prompts=rc.PER_GPU[name] * G)
+    s = Sched()
+    batch = batch_for(w, s)
+    cfg = gen_config(w, G, calibrated=True)
+    base = rc.simulate(w, batch, G, 0, m, cfg, s, fused=False)
+    fused = rc.simulate(w, batch, G, meas["config"]["r_t"], m, cfg, s, fused=True)
+    got, want = base / fused, meas["stage_barrier"]["speedup_fused"]
+    assert abs(got / want - 1) < 0.05, (got, want)
