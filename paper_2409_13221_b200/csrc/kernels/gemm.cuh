@@ -97,6 +97,13 @@ __device__ __forceinline__ void bulk_commit_wait() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
+// Only until the bulk store has read its shared-memory source: enough before
+// a CTA exits — the grid's completion (what the next kernel's
+// griddepcontrol.wait observes) covers the global writes themselves.
+__device__ __forceinline__ void bulk_commit_wait_read() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(kGemmThreads, ST == 2 ? 2 : 1)  // the 2-stage
       epi_bar_sync();
       if (threadIdx.x == 64) {
         epi.store(smem, a_row0, b_row0, split);
-        bulk_commit_wait();
+        bulk_commit_wait_read();
       }
     }
   };
