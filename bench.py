@@ -21,7 +21,7 @@ the one-shot long-tail migration at r_t = 20% of the batch.
 `stage_barrier` — the unfused schedule on the same GPUs (same K);
 `roofline` — decode attention (the dominant kernel), algorithmic bytes per
            launch / CUDA-event duration, against MEASURED_PEAKS.json;
-`cpu_baseline` — the CPU oracle (numpy port) on a bounded sample, rank 0.
+`cpu_baseline` — the CPU path (fp32 C++ oracle port, one std::thread per sample) on a bounded sample, rank 0.
 """
 from __future__ import annotations
 
@@ -130,27 +130,25 @@ def workload_desc(w, G):
 _ORACLES = {}
 
 
-def cpu_oracle_rate(w, batch, n_samples: int, time_budget: float = 30.0):
-    """Samples/s of the numpy CPU oracle on the first samples of the batch (all host threads).
-    The oracle's weights are built once, outside the timed region."""
+def cpu_oracle_rate(w, batch, n_samples: int | None = None):
+    """Samples/s of the CPU path — oracle/cpu_oracle.cpp, fp32 C++ with one std::thread per
+    sample over all host cores — on the first n_samples samples of the batch
+    (default: one per host thread), teacher-forced through actor / ref / critic / reward and
+    post-processed. The oracle's weights are built once, outside the timed region.
+    Returns (samples/s, samples, tokens, seconds, threads)."""
     sys.path.insert(0, str(ROOT / "oracle"))
-    from model_oracle import Oracle, forced_response, synthetic_prompts
+    from model_oracle import CppOracle, forced_response, synthetic_prompts
     if w.name not in _ORACLES:
-        _ORACLES[w.name] = Oracle(w)
+        _ORACLES[w.name] = CppOracle(w)
     orc = _ORACLES[w.name]
-    prompts = synthetic_prompts(len(batch), w.prompt_len, w.actor.vocab, 7)
+    n = min(len(batch), n_samples or orc.threads)
+    prompts = synthetic_prompts(n, w.prompt_len, w.actor.vocab, 7)
+    resp = [forced_response(s.id, s.target_output_len, w.max_new, w.actor.vocab, 7) for s in batch[:n]]
     t0 = time.perf_counter()
-    done = 0
-    tokens = 0
-    for s in batch[:n_samples]:
-        resp = forced_response(s.id, s.target_output_len, w.max_new, w.actor.vocab, 7)
-        orc.experience(prompts[s.id, :s.prompt_len], resp, 0.05, 1.0, 0.95)
-        done += 1
-        tokens += s.prompt_len + s.target_output_len
-        if time.perf_counter() - t0 > time_budget:
-            break
+    orc.experience_batch(prompts, [s.prompt_len for s in batch[:n]], resp, 0.05, 1.0, 0.95)
     dt = time.perf_counter() - t0
-    return done / dt, done, tokens, dt
+    tokens = sum(s.prompt_len + s.target_output_len for s in batch[:n])
+    return n / dt, n, tokens, dt, orc.threads
 
 
 def python_batch(w):
@@ -174,19 +172,18 @@ def run_reference(args, world, rank):
     """--impl reference: the reference's CPU path. The reference library only
     simulates this stage (cost formulas, no model math), so the
     CPU implementation of the path that produces experience is the oracle
-    port (numpy fp32, all host threads through BLAS); the simulator's own
+    port (oracle/cpu_oracle.cpp: fp32 C++, one std::thread per sample); the simulator's own
     runtime is reported beside it. Nothing here loads the product library."""
     if rank != 0:
         return
     w = workload_for(args.gpus, args.workload, args.zipf_s, args.prompts_per_gpu)
     batch, batch_src = python_batch(w)
-    cores = os.cpu_count() or 1
-    n_sub = {"gpt2s": 2, "1.3b": 1, "8b": 1}.get(w.name, 2)
+    n_sub = None if w.name in ("toy", "gpt2s") else 1  # one sample per host thread (toy: the first ones)
     rates, walls = [], []
     info = None
     for step in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        r, done, toks, dt = cpu_oracle_rate(w, batch, n_samples=n_sub, time_budget=15.0)
+        r, done, toks, dt, cores = cpu_oracle_rate(w, batch, n_samples=n_sub)
         if step >= args.warmup:
             rates.append(r)
             walls.append(time.perf_counter() - t0)
@@ -203,7 +200,8 @@ def run_reference(args, world, rank):
         rs.simulate_fused(batch, cfg, round(0.2 * len(batch)))
         sim = time.perf_counter() - t0
     sample = (f"{info[0]} of {len(batch)} prompts ({info[1]} tokens) teacher-forced through actor/ref/critic/reward "
-              f"+ KL/GAE post-processing, numpy fp32; step = that subset")
+              f"+ KL/GAE post-processing, fp32 C++ (oracle/cpu_oracle.cpp), one std::thread per sample; "
+              f"step = that subset")
     cfg_line = config_dict(w, args.gpus, args)
     cfg_line["cpu_subset"] = f"{info[0]} of {len(batch)} prompts per step (batch built by {batch_src})"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
@@ -213,8 +211,8 @@ def run_reference(args, world, rank):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "reference_simulator_seconds": sim,
-            "note": "reference path is a discrete-event simulator without model math; CPU arm = oracle port; "
-                    "ms_per_step = measured wall time of the subset"}
+            "note": "reference path is a discrete-event simulator without model math; CPU arm = the oracle port "
+                    "(fp32 C++, std::thread over samples); ms_per_step = measured wall time of the subset"}
     print(json.dumps(line), flush=True)
 
 
@@ -383,10 +381,11 @@ def main():
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline and not args.quick:
-        r, done, toks, dt = cpu_oracle_rate(w, batch, n_samples=2, time_budget=20.0)
-        cpu = {"value": r, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-               "sample": f"{done} of {len(batch)} prompts ({toks} tokens) through the numpy oracle "
-                         f"(teacher-forced actor/ref/critic/reward + post-processing), {dt:.1f}s"}
+        r, done, toks, dt, cores = cpu_oracle_rate(w, batch)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{done} of {len(batch)} prompts ({toks} tokens) through the fp32 C++ oracle "
+                         f"(oracle/cpu_oracle.cpp: teacher-forced actor/ref/critic/reward + post-processing, "
+                         f"one std::thread per sample), {dt:.1f}s"}
 
     # per-rank decode / scoring totals of the value steps, summed over ranks
     # (every rank decodes its own shard; any rank may score any sample)

@@ -490,3 +490,66 @@ class Oracle:
             out_lp.append(float(lp[t]))
             cur, pos = t, pos + 1
         return np.asarray(out_t), np.asarray(out_lp)
+
+
+class CppOracle:
+    """oracle/_ref/liboracle_cpu.so (oracle/cpu_oracle.cpp): the same experience in
+    fp32 C++, std::thread over samples — the timed CPU path of bench.py."""
+
+    def __init__(self, workload, weight_seed: int = 1234, threads: int | None = None):
+        import ctypes as C
+        import os
+        from pathlib import Path
+        p = Path(__file__).resolve().parent / "_ref" / "liboracle_cpu.so"
+        if not p.exists():
+            raise FileNotFoundError(f"{p} not built (make -C oracle liboracle)")
+        self.lib = C.CDLL(str(p))
+        self.lib.cpu_oracle_create.restype = C.c_void_p
+        self.lib.cpu_oracle_create.argtypes = [C.POINTER(C.c_int32), C.c_uint64, C.c_int32]
+        self.lib.cpu_oracle_destroy.argtypes = [C.c_void_p]
+        i32 = C.POINTER(C.c_int32)
+        f32 = C.POINTER(C.c_float)
+        self.lib.cpu_oracle_experience.argtypes = [C.c_void_p, C.c_int32, C.c_int32, i32, i32, i32, i32, C.c_float,
+                                                   C.c_float, C.c_float, C.c_int32, f32, f32]
+        self.threads = threads or len(os.sched_getaffinity(0))
+        dims = []
+        for d in (workload.actor, workload.ref, workload.critic, workload.reward):
+            dims += [d.num_layers, d.hidden, d.num_heads, d.num_kv_heads, d.head_dim, d.ffn, d.vocab]
+        arr = (C.c_int32 * 28)(*dims)
+        self.h = self.lib.cpu_oracle_create(arr, weight_seed, self.threads)
+        self.C = C
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.cpu_oracle_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def experience_batch(self, prompts, prompt_len, responses, beta, gamma, lam):
+        """prompts [n][max_prompt], prompt_len [n], responses: list of arrays -> dict of packed arrays."""
+        C = self.C
+        prompts = np.ascontiguousarray(prompts, dtype=np.int32)
+        n, maxp = prompts.shape
+        pl = np.ascontiguousarray(prompt_len, dtype=np.int32)
+        off = np.zeros(n + 1, dtype=np.int32)
+        off[1:] = np.cumsum([len(r) for r in responses])
+        resp = np.ascontiguousarray(np.concatenate(responses), dtype=np.int32)
+        out = np.zeros(7 * int(off[-1]), dtype=np.float32)
+        score = np.zeros(n, dtype=np.float32)
+        ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))  # noqa: E731
+        fp = lambda a: a.ctypes.data_as(C.POINTER(C.c_float))  # noqa: E731
+        rc = self.lib.cpu_oracle_experience(self.h, n, maxp, ip(pl), ip(prompts), ip(off), ip(resp), beta, gamma, lam,
+                                            self.threads, fp(out), fp(score))
+        if rc != 0:
+            raise ValueError(f"cpu_oracle_experience: status {rc}")
+        T = int(off[-1])
+        names = ("logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret")
+        res = {k: out[i * T:(i + 1) * T] for i, k in enumerate(names)}
+        res["score"] = score
+        res["off"] = off
+        return res

@@ -102,3 +102,29 @@ def test_c_weight_generator_matches_numpy_restatement():
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
         a, b = mo.gain(99, tag, n), mo.gain_np(99, tag, n)
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_cpp_cpu_oracle_matches_numpy_oracle():
+    """oracle/cpu_oracle.cpp (threaded fp32 C++, the timed CPU path) restates the numpy
+    oracle: same experience within fp32 summation-order noise, on the toy config and an
+    hd-128 GQA model."""
+    import model_oracle as mo
+    from paper_2409_13221_b200.configs import Dims, Workload, WORKLOADS, scaled
+    if not (ROOT / "oracle" / "_ref" / "liboracle_cpu.so").exists():
+        pytest.skip("oracle C++ library not built (make -C oracle liboracle)")
+    gq = Dims(2, 256, 4, 2, 64, 512, 1024)
+    for w in (scaled(WORKLOADS["toy"], n_prompts=4, max_new=40, prompt_len=16),
+              Workload("gqa", gq, gq, gq, gq, 3, 12, 30)):
+        cpp = mo.CppOracle(w, threads=4)
+        py = mo.Oracle(w)
+        prompts = mo.synthetic_prompts(w.n_prompts, w.prompt_len, w.actor.vocab, 7)
+        plen = [w.prompt_len - i for i in range(w.n_prompts)]
+        resp = [mo.forced_response(i, 10 + 7 * i, w.max_new, w.actor.vocab, 7) for i in range(w.n_prompts)]
+        got = cpp.experience_batch(prompts, plen, resp, 0.05, 1.0, 0.95)
+        for i in range(w.n_prompts):
+            ref = py.experience(prompts[i, :plen[i]], resp[i], 0.05, 1.0, 0.95)
+            b, e = got["off"][i], got["off"][i + 1]
+            for k in ("logp_actor", "logp_ref", "values", "kl", "adv", "ret"):
+                assert np.max(np.abs(got[k][b:e] - ref[k])) < 2e-3, (w.name, i, k)
+            assert abs(got["score"][i] - ref["score"]) < 2e-3
+        cpp.close()
