@@ -41,7 +41,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2409_13221_b200.configs import WORKLOADS, batch_for, gen_config, scaled  # noqa: E402
 from paper_2409_13221_b200.sched import Remaining, Sched  # noqa: E402
 
-PER_GPU = {"gpt2s": 512, "1.3b": 256}
+PER_GPU = {"gpt2s": 512, "1.3b": 256, "8b": 512}
 
 
 def fwd_flops(d, T, vocab_head):
@@ -83,7 +83,19 @@ def simulate(w, batch, G, r_t, m, cfg, sched, fused):
     P = w.prompt_len
     L = [s.target_output_len for s in batch]
     cost = [sample_flops(w, P + l) / m["F"] for l in L]
-    live = [[s for s in range(n) if s % G == g] for g in range(G)]
+    cap = cfg.cluster.kv_capacity_per_instance
+    queue = [[s for s in range(n) if s % G == g] for g in range(G)]
+    live = [[] for _ in range(G)]
+    kv_used = [0.0] * G
+
+    def admit(g):  # FIFO while the reservation fits (genfuse.cpp:226-236)
+        while queue[g] and (cap <= 0 or kv_used[g] + batch[queue[g][0]].kv_bytes <= cap + 1e-6):
+            s = queue[g].pop(0)
+            kv_used[g] += batch[s].kv_bytes
+            live[g].append(s)
+
+    for g in range(G):
+        admit(g)
     gen = [0] * n
     clock = [0.0] * G
     finish = [None] * n
@@ -93,7 +105,7 @@ def simulate(w, batch, G, r_t, m, cfg, sched, fused):
     pool = []  # (ready time, seconds of dedicated scoring work)
     # per-GPU step loop in global time order
     while True:
-        active = [g for g in range(G) if live[g]]
+        active = [g for g in range(G) if live[g] or queue[g]]
         if not active:
             break
         g = min(active, key=lambda k: clock[k])
@@ -110,15 +122,18 @@ def simulate(w, batch, G, r_t, m, cfg, sched, fused):
                 finish[s] = clock[g]
                 pool.append((clock[g], cost[s]))
                 remaining -= 1
+                kv_used[g] -= batch[s].kv_bytes
             else:
                 keep.append(s)
         live[g] = keep
-        if not live[g]:
+        admit(g)
+        if not live[g] and not queue[g]:
             done_at[g] = clock[g]
         if not triggered and remaining < r_t:
             triggered = True
             t0 = clock[g]
             state = [Remaining(s, k, float(batch[s].kv_bytes), gen[s], P, True) for k in range(G) for s in live[k]]
+            state += [Remaining(s, k, float(batch[s].kv_bytes), 0, P, False) for k in range(G) for s in queue[k]]
             state.sort(key=lambda r: r.id)
             plan = sched.plan_migration(t0, state, r_t, cfg)
             if not plan.no_op:
@@ -126,15 +141,25 @@ def simulate(w, batch, G, r_t, m, cfg, sched, fused):
                 movers = sorted((s for s in plan.migrated), key=lambda s: (-(L[s] - gen[s]), s))
                 moved_bytes = 0.0
                 for s in movers:
-                    src = s % G if s in live[s % G] else next(k for k in range(G) if s in live[k])
-                    k = min(dest, key=lambda d: (len(live[d]), d))
+                    src = next(k for k in range(G) if s in live[k] or s in queue[k])
+                    if s in queue[src]:  # queued: to the shallowest destination queue
+                        k = min(dest, key=lambda d: (len(queue[d]), dest.index(d)))
+                        queue[src].remove(s)
+                        queue[k].append(s)
+                        continue
+                    fits = [d for d in dest if cap <= 0 or kv_used[d] + batch[s].kv_bytes <= cap + 1e-6]
+                    if not fits:
+                        continue  # stays home
+                    k = min(fits, key=lambda d: (len(live[d]), d))
                     live[src].remove(s)
+                    kv_used[src] -= batch[s].kv_bytes
                     live[k].append(s)
+                    kv_used[k] += batch[s].kv_bytes
                     moved_bytes += (P + gen[s]) * w.actor.kv_bytes_per_token()
                 over = moved_bytes / cfg.cluster.interconnect_bandwidth
                 for k in range(G):
                     clock[k] = max(clock[k], t0)
-                    if not live[k] and done_at[k] is None:
+                    if not live[k] and not queue[k] and done_at[k] is None:
                         done_at[k] = t0
                 for d in dest:
                     clock[d] += over
@@ -179,6 +204,7 @@ def main():
         w = scaled(WORKLOADS[name], n_prompts=PER_GPU[name] * G)
         batch = batch_for(w, sched)
         cfg = gen_config(w, G, calibrated=True)
+        cfg.cluster.kv_capacity_per_instance = prof.get("kv_capacity", 0.0)
         base = simulate(w, batch, G, 0, m, cfg, sched, fused=False)
         rows = []
         for ratio in [0.0] + [x / 100 for x in range(5, 100, 5)]:
@@ -198,12 +224,14 @@ def main():
     if "--validate" in sys.argv:
         meas = {}
         for G in (2, 4):
-            key = {"gpt2s": f"r02_bench_gpt2s_{G}gpu.json", "1.3b": f"r02_bench_13b_{G}gpu.json"}[name]
+            key = {"gpt2s": f"r02_bench_gpt2s_{G}gpu.json", "1.3b": f"r02_bench_13b_{G}gpu.json",
+                   "8b": f"r02_bench_8b_full_{G}gpu.json"}[name]
             p = ROOT / "profiles" / key
             if p.exists():
                 d = json.loads(p.read_text())
                 meas[G] = d["stage_barrier"]["speedup_fused"]
-                pred = out["G"][G]["gain_at_0.2"] if abs(d["config"]["r_ratio"] - 0.2) < 1e-9 else None
+                rr = d["config"]["r_ratio"]
+                pred = next(r[2] for r in out["G"][G]["curve"] if abs(r[0] - rr) < 1e-9)
                 print(f"  measured G={G} (R_t {d['config']['r_ratio']:.2f}): {meas[G]:.3f}x; predicted "
                       f"{pred:.3f}x ({(pred / meas[G] - 1) * 100:+.1f} %); reference sweep "
                       f"{out['G'][G]['reference_sweep_gain']:.3f}x")
