@@ -87,14 +87,14 @@ __device__ __forceinline__ uint32_t swz(uint32_t tile_base, int r, int c16) {
 // many warps, 2 stages each — for large batches, where warps per SM hide the
 // per-unit latency; DEEP — few warps, a deep ring each — for small batches,
 // where each warp streams a long item alone and needs many units in flight.
-template <int HD, int DEEP = 0>  // 0 wide, 1 deep, 2 mid (a lean CTA that fits beside a lean GEMM CTA)
+template <int HD, int DEEP = 0>  // 0 wide, 1 deep
 struct DecCfg {
   static constexpr int kSub = HD / 64;                  // 64-column boxes per K (or V) unit
   static constexpr int kBox = 32 * 128;                 // 32 rows x 128 B
   static constexpr int kKV = 2 * kSub * kBox;           // K + V of one 32-token unit
   static constexpr int kQSlot = HD == 64 ? 1024 : 2048; // >= 8 q rows x HD x 2 B, keeps 1 KB alignment
   static constexpr int kStageBytes = kKV + kQSlot;
-  static constexpr int kWarps = DEEP == 1 ? (HD == 64 ? 4 : 3) : DEEP == 2 ? (HD == 64 ? 6 : 3) : (HD == 64 ? 12 : 6);
+  static constexpr int kWarps = DEEP == 1 ? (HD == 64 ? 4 : 3) : (HD == 64 ? 12 : 6);
   static constexpr int kStages = DEEP == 1 ? (HD == 64 ? 6 : 4) : 2;
   static constexpr int kSmem = kWarps * kStages * kStageBytes + 1024;
 };
@@ -888,10 +888,6 @@ void launch_team(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, c
   count_launch();
 }
 
-int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
-}
 
 template <int HD, int G>
 void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const KvPoolView& pool, int layer,
@@ -899,11 +895,6 @@ void launch(const CUtensorMap& map, const bf16* q, int B, int H, int KVH, const 
             cudaStream_t st, int max_ctas) {
   switch (attn_decode_variant(B, KVH, HD, G, nullptr)) {
     case 2: launch_team<4>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st, max_ctas); break;
-    case 3: launch_team<2>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st, max_ctas); break;
-    case 4:
-      launch_cfg<HD, G, 2>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st,
-                           max_ctas);
-      break;
     case 1:
       launch_cfg<HD, G, 1>(map, q, B, H, KVH, pool, layer, slot, ctx, items, nsplit, work, out, counters, st,
                               max_ctas);
@@ -920,23 +911,16 @@ void set_attn_trace(unsigned long long* buf) { g_attn_trace_host = buf; }
 
 // The team kernel (hd 64, G 1) while the (sample, kv head) pairs cannot fill
 // the warp-per-item grid four times over, else deep below that for other
-// shapes, else (optionally) mid, else wide; identical numerics.
-// FUSEPLAN_ATTN_TEAM=0 / FUSEPLAN_ATTN_DEEP=0|1 / FUSEPLAN_ATTN_MID_MAX_B force shapes for A/B runs.
+// shapes, else wide; identical numerics.
+// (The lean "mid" shape and 2-warp teams were measured no faster,
+// profiles/r02_attn_variant_sweep.txt, and are not instantiated.)
 int attn_decode_variant(int B, int KVH, int hd, int G, int* warps) {
-  static const int team_mode = env_int("FUSEPLAN_ATTN_TEAM", 1);
-  static const int deep_mode = env_int("FUSEPLAN_ATTN_DEEP", -1);
   const int wide_warps = hd == 64 ? DecCfg<64, 0>::kWarps : DecCfg<128, 0>::kWarps;
   const bool small = B * KVH * 4 <= 148 * wide_warps;
-  static const int team2_max_b = env_int("FUSEPLAN_ATTN_TEAM2_MAX_B", 0);
-  static const int mid_max_b = env_int("FUSEPLAN_ATTN_MID_MAX_B", 0);  // lean "mid" CTAs up to this batch
   int v = 0;
-  if (hd == 64 && G == 1 && team_mode == 3) v = 3;
-  else if (hd == 64 && G == 1 && team_mode && (team_mode == 2 || small)) v = 2;
-  else if (hd == 64 && G == 1 && team_mode && B <= team2_max_b) v = 3;
-  else if (deep_mode >= 0 ? deep_mode == 1 : small) v = 1;
-  else if (B <= mid_max_b) v = 4;
-  if (warps) *warps = v == 2 || v == 3 ? 12 : v == 1 ? (hd == 64 ? DecCfg<64, 1>::kWarps : DecCfg<128, 1>::kWarps)
-                    : v == 4 ? (hd == 64 ? DecCfg<64, 2>::kWarps : DecCfg<128, 2>::kWarps) : wide_warps;
+  if (hd == 64 && G == 1 && small) v = 2;
+  else if (small) v = 1;
+  if (warps) *warps = v == 2 ? 12 : v == 1 ? (hd == 64 ? DecCfg<64, 1>::kWarps : DecCfg<128, 1>::kWarps) : wide_warps;
   return v;
 }
 
