@@ -189,6 +189,27 @@ def test_fused_rope_prefill_scoring_bit_identical(small64):
         assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
 
 
+def test_eager_decode_bit_identical_to_graphs(small64):
+    """The decode step replayed as a CUDA graph per batch-size bucket (padding rows
+    decode into a scratch slot) gives the eager step's bits (FUSEPLAN_DECODE_GRAPHS=0)."""
+    import os
+    from paper_2409_13221_b200.configs import gen_config
+    from paper_2409_13221_b200.engine import Engine
+    w, eng, batch, _ = small64
+    a = eng.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="fused", claim_tokens=4096)
+    os.environ["FUSEPLAN_DECODE_GRAPHS"] = "0"
+    try:
+        eng2 = Engine(w, device=0)
+    finally:
+        del os.environ["FUSEPLAN_DECODE_GRAPHS"]
+    try:
+        b = eng2.execute(batch, gen_config(w, 1), 0, token_mode="sample", schedule="fused", claim_tokens=4096)
+    finally:
+        eng2.close()
+    for k in ("tokens", "logp_actor", "logp_ref", "values", "kl", "reward", "adv", "ret", "score"):
+        assert np.array_equal(getattr(a.experience, k), getattr(b.experience, k)), k
+
+
 @pytest.mark.parametrize("fixture", ["small64", "gqa128"])
 def test_decode_chain_bit_identical(request, fixture):
     """The persistent decode-chain kernel (O -> norm -> gate/up -> down -> norm ->
