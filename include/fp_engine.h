@@ -235,9 +235,13 @@ int fp_k_attn_decode_ws(const void* q, int32_t B, int32_t H, int32_t KVH, int32_
                         int32_t num_pages, int32_t num_layers, int32_t layer, const int32_t* block_table,
                         int32_t bt_stride, const int32_t* slot, const int32_t* ctx, const int32_t* items_dev,
                         int32_t max_ctx, void* workspace, void* out, void* stream);
-/* Varlen causal attention; cu_host: n_seq+1 offsets (host), cu_dev the same on device. */
+/* Varlen causal attention; cu_host: n_seq+1 offsets (host), cu_dev the same on device.
+ * hd 64 / 128: tcgen05 kernel; other head sizes: mma.sync kernel. */
 int fp_k_attn_varlen(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
                      const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream);
+/* The mma.sync kernel for any supported head size (cross-check of the tcgen05 kernel). */
+int fp_k_attn_varlen_mma(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
+                         const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream);
 int fp_k_postprocess(int32_t n, const int32_t* off, const float* logp_actor, const float* logp_ref,
                      const float* values, const float* score, float beta, float gamma, float lam, float* kl,
                      float* reward, float* adv, float* ret, void* stream);

@@ -666,21 +666,39 @@ int fp_k_attn_decode_ws(const void* q, int32_t B, int32_t H, int32_t KVH, int32_
   });
 }
 
-int fp_k_attn_varlen(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
-                     const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream) {
+namespace {
+int attn_varlen_call(const void* q, const void* k, const void* v, int H, int KVH, int hd, const int32_t* cu_host,
+                     const int32_t* cu_dev, int n_seq, void* out, void* stream, bool mma) {
   return guarded([&] {
-    const int nt = fpk::attn_varlen_tiles(cu_host, n_seq, nullptr);
+    const int rows = mma ? 64 : fpk::attn_varlen_tile_rows(hd);
+    const int nt = fpk::attn_tiles(cu_host, n_seq, rows, nullptr);
     std::vector<int> tiles(2 * static_cast<size_t>(nt));
-    fpk::attn_varlen_tiles(cu_host, n_seq, tiles.data());
+    fpk::attn_tiles(cu_host, n_seq, rows, tiles.data());
     int* dt = nullptr;
     fpe::check(cudaMallocAsync(reinterpret_cast<void**>(&dt), tiles.size() * 4 + 256, S(stream)), "alloc");
     fpe::check(cudaMemcpyAsync(dt, tiles.data(), tiles.size() * 4, cudaMemcpyHostToDevice, S(stream)), "copy");
-    fpk::attn_varlen(static_cast<const bf16*>(q), static_cast<const bf16*>(k), static_cast<const bf16*>(v), H, KVH, hd,
-                     cu_dev, dt, nt, static_cast<bf16*>(out), S(stream));
+    const auto* qb = static_cast<const bf16*>(q);
+    const auto* kb = static_cast<const bf16*>(k);
+    const auto* vb = static_cast<const bf16*>(v);
+    if (mma)
+      fpk::attn_varlen_mma(qb, kb, vb, H, KVH, hd, cu_dev, dt, nt, static_cast<bf16*>(out), S(stream));
+    else
+      fpk::attn_varlen(qb, kb, vb, H, KVH, hd, cu_host[n_seq], cu_dev, dt, nt, static_cast<bf16*>(out), S(stream));
     after_launch();
     fpe::check(cudaStreamSynchronize(S(stream)), "sync");  // tiles lives on the host stack
     fpe::check(cudaFreeAsync(dt, S(stream)), "free");
   });
+}
+}  // namespace
+
+int fp_k_attn_varlen(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
+                     const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream) {
+  return attn_varlen_call(q, k, v, H, KVH, hd, cu_host, cu_dev, n_seq, out, stream, false);
+}
+
+int fp_k_attn_varlen_mma(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
+                         const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream) {
+  return attn_varlen_call(q, k, v, H, KVH, hd, cu_host, cu_dev, n_seq, out, stream, true);
 }
 
 int fp_k_postprocess(int32_t n, const int32_t* off, const float* logp_actor, const float* logp_ref,

@@ -322,6 +322,7 @@ void Engine::alloc_ws() {
     w.slot = static_cast<int*>(dalloc(cap * 4));
     w.cu = static_cast<int*>(dalloc(w.cap_seq * 4));
     w.tiles = static_cast<int*>(dalloc(static_cast<size_t>(2) * (cap / 64 + w.cap_seq) * 4));
+    w.tiles128 = static_cast<int*>(dalloc(static_cast<size_t>(2) * (cap / 128 + w.cap_seq) * 4));
     if (!scoring) return;
     const int cs = w.cap_seq;
     w.sid = static_cast<int*>(dalloc(cs * 4));
@@ -493,10 +494,22 @@ void Engine::release(int slot) {
 
 // ---------------------------------------------------------------------------
 
-void Engine::forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, int n_tiles, bool use_pool,
+void Engine::upload_tiles(PackedWs& ws, const int* cu, int n_seq, int nt[2], cudaStream_t st) {
+  std::vector<int> t;
+  for (int i = 0; i < 2; ++i) {
+    const int rows = i ? 128 : 64;
+    nt[i] = fpk::attn_tiles(cu, n_seq, rows, nullptr);
+    t.assign(2 * static_cast<size_t>(nt[i]), 0);
+    fpk::attn_tiles(cu, n_seq, rows, t.data());
+    upload(i ? ws.tiles128 : ws.tiles, t.data(), t.size() * 4, st);
+  }
+}
+
+void Engine::forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, const int nt[2], bool use_pool,
                             cudaStream_t st) {
   (void)n_seq;
   const Dims& D = w.dims;
+  const bool t128 = fpk::attn_varlen_tile_rows(D.hd) == 128;
   const fpk::KvPoolView pv = pool_view();
   fpk::embed(ws.tokens, nullptr, M, w.embed, D.d, ws.x, st);
   for (int l = 0; l < D.L; ++l) {
@@ -511,7 +524,8 @@ void Engine::forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, int
                     l, ws.slot, st);
     }
     if (use_pool && l == D.L - 1) break;  // prefill only needs the last layer's K/V
-    fpk::attn_varlen(ws.q, ws.k, ws.v, D.H, D.KVH, D.hd, ws.cu, ws.tiles, n_tiles, ws.attn, st);
+    fpk::attn_varlen(ws.q, ws.k, ws.v, D.H, D.KVH, D.hd, M, ws.cu, t128 ? ws.tiles128 : ws.tiles, nt[t128], ws.attn,
+                     st);
     fpk::gemm_f32_residual(L.wo, D.d, D.H * D.hd, ws.attn, M, ws.x, st);
     fpk::add_norm(ws.x, nullptr, 0, 0, L.ln2, ws.h, M, D.d, nullptr, 0, nullptr, nullptr, st);
     fpk::gemm_swiglu(L.wgu, D.F, D.d, ws.h, M, ws.act, st);
@@ -545,13 +559,12 @@ void Engine::prefill(const std::vector<PrefillItem>& items) {
     const int M = static_cast<int>(tok.size());
     const int ns = static_cast<int>(cu.size()) - 1;
     if (M > 0) {
-      tiles.assign(2 * static_cast<size_t>(fpk::attn_varlen_tiles(cu.data(), ns, nullptr)), 0);
-      const int nt = fpk::attn_varlen_tiles(cu.data(), ns, tiles.data());
+      int nt[2];
+      upload_tiles(pre_, cu.data(), ns, nt, st);
       upload(pre_.tokens, tok.data(), M * 4, st);
       upload(pre_.pos, pos.data(), M * 4, st);
       upload(pre_.slot, slot.data(), M * 4, st);
       upload(pre_.cu, cu.data(), cu.size() * 4, st);
-      upload(pre_.tiles, tiles.data(), tiles.size() * 4, st);
       forward_packed(w, pre_, M, ns, nt, true, st);
     }
     i = j;
@@ -818,8 +831,8 @@ void Engine::infer(const std::vector<InferItem>& items, float beta, float gamma,
     const int n = static_cast<int>(sid.size());
     const int M = cu.back();
     const int NR = roff.back();
-    tiles.assign(2 * static_cast<size_t>(fpk::attn_varlen_tiles(cu.data(), n, nullptr)), 0);
-    const int nt = fpk::attn_varlen_tiles(cu.data(), n, tiles.data());
+    int nt[2];
+    upload_tiles(ws, cu.data(), n, nt, st);
     upload(ws.sid, sid.data(), n * 4, st);
     upload(ws.P, P.data(), n * 4, st);
     upload(ws.R, R.data(), n * 4, st);
@@ -828,7 +841,6 @@ void Engine::infer(const std::vector<InferItem>& items, float beta, float gamma,
     upload(ws.off_out, off_out.data(), n * 8, st);
     upload(ws.hist_tok, ht.data(), n * 8, st);
     upload(ws.hist_logp, hl.data(), n * 8, st);
-    upload(ws.tiles, tiles.data(), tiles.size() * 4, st);
     fpk::AssembleArgs a{ws.sid,        ws.P,      ws.R,         ws.cu,           ws.roff,
                         d_prompts_,    cfg_.max_prompt, ws.hist_tok, ws.hist_logp,
                         ws.tokens,     ws.pos,    ws.targets,   ws.logp_actor,   ws.gather_resp,

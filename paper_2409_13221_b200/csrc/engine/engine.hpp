@@ -247,7 +247,7 @@ class Engine {
     int cap = 0, cap_seq = 0;
     float* x = nullptr;
     bf16 *h = nullptr, *qkv = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *attn = nullptr, *act = nullptr;
-    int *tokens = nullptr, *pos = nullptr, *slot = nullptr, *cu = nullptr, *tiles = nullptr;
+    int *tokens = nullptr, *pos = nullptr, *slot = nullptr, *cu = nullptr, *tiles = nullptr, *tiles128 = nullptr;
     // scoring
     int *sid = nullptr, *P = nullptr, *R = nullptr, *roff = nullptr, *targets = nullptr, *gather_resp = nullptr,
         *gather_last = nullptr;
@@ -275,7 +275,10 @@ class Engine {
   void init_model(int m);
   void fill_model(int m, uint64_t seed);
   void alloc_ws();
-  void forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, int n_tiles, bool use_pool,
+  // Both attention tile tables of one packed batch (64- and 128-query tiles);
+  // forward_packed uses the one its model's head size needs. nt[0], nt[1]: counts.
+  void upload_tiles(PackedWs& ws, const int* cu, int n_seq, int nt[2], cudaStream_t st);
+  void forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, const int nt[2], bool use_pool,
                       cudaStream_t st);
 
   EngineConfig cfg_;

@@ -15,6 +15,8 @@
 #include <math.h>
 
 #include <algorithm>
+#include <array>
+#include <vector>
 #include <cstdlib>
 #include <stdexcept>
 
@@ -489,25 +491,39 @@ void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView&
   attn_decode_combine_kernel<<<B * H, std::min(hd, 128), 0, st>>>(part_o, part_ml, ctx, H, hd, ns, out); fpk::count_launch();
 }
 
-int attn_varlen_tiles(const int* cu_host, int n_seq, int* tiles_host) {
-  int n = 0;
+int attn_varlen_tile_rows(int hd) { return attn_prefill_supported(hd) ? 128 : 64; }
+
+int attn_tiles(const int* cu_host, int n_seq, int rows, int* tiles_host) {
+  std::vector<std::array<int, 3>> t;  // (visible keys, seq, q tile)
   for (int s = 0; s < n_seq; ++s) {
     const int len = cu_host[s + 1] - cu_host[s];
-    const int nt = (len + 63) / 64;
-    // Longest tiles (most keys) first: better tail behaviour.
-    for (int t = nt - 1; t >= 0; --t) {
-      if (tiles_host) {
-        tiles_host[2 * n] = s;
-        tiles_host[2 * n + 1] = t;
-      }
-      ++n;
+    for (int q = 0; q * rows < len; ++q) t.push_back({std::min(len, (q + 1) * rows), s, q});
+  }
+  if (tiles_host) {
+    // Most keys first (better tail); ties keep sequence order.
+    std::stable_sort(t.begin(), t.end(), [](const auto& a, const auto& b) { return a[0] > b[0]; });
+    for (size_t i = 0; i < t.size(); ++i) {
+      tiles_host[2 * i] = t[i][1];
+      tiles_host[2 * i + 1] = t[i][2];
     }
   }
-  return n;
+  return static_cast<int>(t.size());
 }
 
-void attn_varlen(const bf16* q, const bf16* k, const bf16* v, int H, int KVH, int hd, const int* cu, const int* tiles,
-                 int n_tiles, bf16* out, cudaStream_t st) {
+int attn_varlen_tiles(const int* cu_host, int n_seq, int hd, int* tiles_host) {
+  return attn_tiles(cu_host, n_seq, attn_varlen_tile_rows(hd), tiles_host);
+}
+
+void attn_varlen(const bf16* q, const bf16* k, const bf16* v, int H, int KVH, int hd, int M, const int* cu,
+                 const int* tiles, int n_tiles, bf16* out, cudaStream_t st) {
+  if (attn_prefill_supported(hd))
+    attn_prefill(q, k, v, H, KVH, hd, M, cu, tiles, n_tiles, out, st);
+  else
+    attn_varlen_mma(q, k, v, H, KVH, hd, cu, tiles, n_tiles, out, st);
+}
+
+void attn_varlen_mma(const bf16* q, const bf16* k, const bf16* v, int H, int KVH, int hd, const int* cu,
+                     const int* tiles, int n_tiles, bf16* out, cudaStream_t st) {
   if (n_tiles <= 0) return;
   const float scale = kLog2e / sqrtf(static_cast<float>(hd));
 #define FP_VL(HD_)                                                                                           \

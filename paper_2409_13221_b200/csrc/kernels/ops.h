@@ -254,10 +254,21 @@ void attn_decode(const bf16* q, int B, int H, int KVH, int hd, const KvPoolView&
                  cudaEvent_t probe_begin = nullptr, cudaEvent_t probe_end = nullptr, int max_ctas = 148);
 // Varlen causal attention over packed q [M, H, hd], k/v [M, KVH, hd];
 // sequences [cu[i], cu[i+1]). tiles: host-built table of (seq, q_tile) pairs
-// (attn_varlen_tiles). out [M, H, hd].
-int attn_varlen_tiles(const int* cu_host, int n_seq, int* tiles_host);
-void attn_varlen(const bf16* q, const bf16* k, const bf16* v, int H, int KVH, int hd, const int* cu, const int* tiles,
-                 int n_tiles, bf16* out, cudaStream_t st);
+// (attn_varlen_tiles; the query-tile height depends on hd). out [M, H, hd].
+// hd 64 / 128 run the tcgen05 kernel (attn_prefill.cu), other head sizes the
+// mma.sync kernel (attention.cu).
+int attn_varlen_tile_rows(int hd);
+int attn_tiles(const int* cu_host, int n_seq, int rows, int* tiles_host);  // (seq, tile) pairs, most keys first
+int attn_varlen_tiles(const int* cu_host, int n_seq, int hd, int* tiles_host);
+void attn_varlen(const bf16* q, const bf16* k, const bf16* v, int H, int KVH, int hd, int M, const int* cu,
+                 const int* tiles, int n_tiles, bf16* out, cudaStream_t st);
+bool attn_prefill_supported(int hd);
+void attn_prefill(const bf16* q, const bf16* k, const bf16* v, int H, int KVH, int hd, int M, const int* cu,
+                  const int* tiles, int n_tiles, bf16* out, cudaStream_t st);
+// The mma.sync kernel for any supported hd (64-row query tiles); kept for
+// hd 32 and as the cross-check of the tcgen05 kernel in the GPU tests.
+void attn_varlen_mma(const bf16* q, const bf16* k, const bf16* v, int H, int KVH, int hd, const int* cu,
+                     const int* tiles, int n_tiles, bf16* out, cudaStream_t st);
 
 // ---- post-processing (post.cu) -----------------------------------------------------
 // Per sample i, inputs at tokens [off[i], off[i+1]): kl, reward, advantage,

@@ -226,6 +226,64 @@ def test_attn_varlen(lib, hd, H, KVH):
         assert err < 3e-2, (i, n, err)
 
 
+def _varlen_ref(q, k, v, cu, H, KVH):
+    g = H // KVH
+    outs = []
+    for i in range(len(cu) - 1):
+        a, b = int(cu[i]), int(cu[i + 1])
+        qq = q[a:b].float().transpose(0, 1)
+        kk = k[a:b].float().transpose(0, 1).repeat_interleave(g, 0)
+        vv = v[a:b].float().transpose(0, 1).repeat_interleave(g, 0)
+        outs.append(torch.nn.functional.scaled_dot_product_attention(qq, kk, vv, is_causal=True).transpose(0, 1))
+    return torch.cat(outs)
+
+
+@pytest.mark.parametrize("hd,H,KVH,lens,grow", [
+    (64, 12, 12, [1, 127, 128, 129, 300, 64, 65, 2], 0.0),
+    (128, 16, 16, [512, 1, 256, 255, 257, 130], 0.0),
+    (128, 32, 8, [1300, 700, 33, 4096], 0.0),
+    (64, 12, 12, [1024, 300], 3.0),     # scores grow along the sequence: forces in-TMEM rescales of O
+    (128, 32, 8, [2000, 129], 3.0),
+])
+def test_attn_prefill_tcgen05(lib, hd, H, KVH, lens, grow):
+    """tcgen05 varlen attention (attn_prefill.cu) vs torch SDPA in fp32 and vs the mma.sync kernel."""
+    torch.manual_seed(len(lens) * 7 + hd)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    M = int(cu[-1])
+    q = torch.randn(M, H, hd, device="cuda")
+    k = torch.randn(M, KVH, hd, device="cuda")
+    if grow:
+        # key magnitude rising with position -> the row max keeps growing by > 2^8 in exp2 units
+        pos = torch.cat([torch.arange(n, device="cuda", dtype=torch.float32) / max(n, 1) for n in lens])
+        k = k + grow * pos[:, None, None] * q.mean(1, keepdim=True)[:, :KVH].sign()
+    q, k = q.to(torch.bfloat16), k.to(torch.bfloat16)
+    v = torch.randn(M, KVH, hd, device="cuda").to(torch.bfloat16)
+    cu_d = torch.from_numpy(cu).cuda()
+    cu_h = cu.ctypes.data_as(C.POINTER(C.c_int32))
+    out = torch.full((M, H, hd), float("nan"), device="cuda", dtype=torch.bfloat16)
+    ok(lib, lib.fp_k_attn_varlen(ptr(q), ptr(k), ptr(v), H, KVH, hd, cu_h, ptr(cu_d), len(lens), ptr(out),
+                                 stream()))
+    alt = torch.full_like(out, float("nan"))
+    ok(lib, lib.fp_k_attn_varlen_mma(ptr(q), ptr(k), ptr(v), H, KVH, hd, cu_h, ptr(cu_d), len(lens), ptr(alt),
+                                     stream()))
+    torch.cuda.synchronize()
+    ref = _varlen_ref(q, k, v, cu, H, KVH)
+    assert torch.isfinite(out.float()).all()
+    err = (out.float() - ref).abs().max().item()
+    assert err < 3e-2, err
+    assert (out.float() - alt.float()).abs().max().item() < 3e-2
+    # batch independence: each sequence alone gives the same bits
+    i = len(lens) - 1
+    a, b = int(cu[i]), int(cu[i + 1])
+    one = torch.empty(b - a, H, hd, device="cuda", dtype=torch.bfloat16)
+    cu1 = np.array([0, b - a], dtype=np.int32)
+    ok(lib, lib.fp_k_attn_varlen(ptr(q[a:b]), ptr(k[a:b]), ptr(v[a:b]), H, KVH, hd,
+                                 cu1.ctypes.data_as(C.POINTER(C.c_int32)), ptr(torch.from_numpy(cu1).cuda()), 1,
+                                 ptr(one), stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(one, out[a:b])
+
+
 def test_postprocess_matches_c_oracle(lib):
     import ctypes
 
