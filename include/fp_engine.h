@@ -178,6 +178,9 @@ int fp_k_gemm_bf16(const void* W, int32_t N, int32_t K, const void* X, int32_t M
 int fp_k_gemm_f32(const void* W, int32_t N, int32_t K, const void* X, int32_t M, float* out, int32_t splits,
                   void* stream); /* splits <= 0: fp_k_gemm_splits(N, K) */
 int fp_k_gemm_splits(int32_t N, int32_t K);
+/* resid[M][N] += X W^T (fp32 residual stream; TMA reduce-add epilogue). */
+int fp_k_gemm_f32_residual(const void* W, int32_t N, int32_t K, const void* X, int32_t M, float* resid,
+                           void* stream);
 /* Debug: record 8 globaltimer stamps per CTA of subsequent GEMMs into buf (device, NULL disables). */
 int fp_k_gemm_trace(void* buf);
 int fp_k_gemm_swiglu(const void* Wgu, int32_t F, int32_t K, const void* X, int32_t M, void* out, void* stream);
@@ -216,6 +219,8 @@ int fp_k_vocab_filtered(const void* X, int32_t M, int32_t K, const void* W, int3
                         float* logp, float* z_out, void* stream);
 int fp_k_add_norm(float* x, const float* parts, int32_t nsplit, const float* gain, void* y, int32_t M, int32_t d,
                   void* stream);
+/* y = bf16(RMSNorm(x) * gain), warp-per-row kernel of the packed (prefill / scoring) forward. */
+int fp_k_rms_norm_rows(const float* x, const float* gain, void* y, int32_t M, int32_t d, void* stream);
 /* Paged decode attention. pool: [num_pages][L][KVH][2][64][hd] bf16; block_table [slots][bt_stride].
  * num_pages > 0 selects the tensor-core TMA kernel (hd 64 / 128); 0 the CUDA-core kernel. */
 int fp_k_attn_decode(const void* q, int32_t B, int32_t H, int32_t KVH, int32_t hd, const void* pool,

@@ -456,6 +456,14 @@ int fp_k_gemm_bf16(const void* W, int32_t N, int32_t K, const void* X, int32_t M
   });
 }
 
+int fp_k_gemm_f32_residual(const void* W, int32_t N, int32_t K, const void* X, int32_t M, float* resid,
+                           void* stream) {
+  return guarded([&] {
+    fpk::gemm_f32_residual(static_cast<const bf16*>(W), N, K, static_cast<const bf16*>(X), M, resid, S(stream));
+    after_launch();
+  });
+}
+
 int fp_k_gemm_splits(int32_t N, int32_t K) { return fpk::gemm_splits(N, K); }
 
 int fp_k_gemm_f32(const void* W, int32_t N, int32_t K, const void* X, int32_t M, float* out, int32_t splits,
@@ -587,6 +595,13 @@ int fp_k_add_norm(float* x, const float* parts, int32_t nsplit, const float* gai
   return guarded([&] {
     fpk::add_norm(x, parts, nsplit, static_cast<size_t>(M) * d, gain, static_cast<bf16*>(y), M, d, nullptr, 0, nullptr,
                   nullptr, S(stream));
+    after_launch();
+  });
+}
+
+int fp_k_rms_norm_rows(const float* x, const float* gain, void* y, int32_t M, int32_t d, void* stream) {
+  return guarded([&] {
+    fpk::rms_norm_rows(x, gain, static_cast<bf16*>(y), M, d, S(stream));
     after_launch();
   });
 }

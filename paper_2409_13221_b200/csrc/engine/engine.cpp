@@ -77,6 +77,11 @@ Engine::Engine(const EngineConfig& cfg) : cfg_(cfg) {
   FP_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
   FP_CUDA(cudaStreamCreateWithPriority(&s_decode_, cudaStreamNonBlocking, prio_hi));
   FP_CUDA(cudaStreamCreateWithPriority(&s_infer_, cudaStreamNonBlocking, prio_lo));
+  for (int i = 0; i < 2; ++i) {
+    FP_CUDA(cudaStreamCreateWithPriority(&s_score_[i], cudaStreamNonBlocking, prio_lo));
+    FP_CUDA(cudaEventCreateWithFlags(&ev_join_[i], cudaEventDisableTiming));
+  }
+  FP_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
   FP_CUDA(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking));
   ring_ = new PinnedRing();
   const Dims& a = cfg_.model[kActor];
@@ -165,12 +170,18 @@ Engine::~Engine() {
   delete ring_;
   cudaStreamDestroy(s_decode_);
   cudaStreamDestroy(s_infer_);
+  for (int i = 0; i < 2; ++i) {
+    cudaStreamDestroy(s_score_[i]);
+    cudaEventDestroy(ev_join_[i]);
+  }
+  cudaEventDestroy(ev_fork_);
   cudaStreamDestroy(s_copy_);
 }
 
 void Engine::synchronize() {
   FP_CUDA(cudaStreamSynchronize(s_decode_));
   FP_CUDA(cudaStreamSynchronize(s_infer_));
+  for (cudaStream_t s : s_score_) FP_CUDA(cudaStreamSynchronize(s));
   FP_CUDA(cudaStreamSynchronize(s_copy_));
 }
 
@@ -309,14 +320,17 @@ void Engine::alloc_ws() {
   auto packed = [&](PackedWs& w, int cap, bool scoring) {
     w.cap = cap;
     w.cap_seq = std::min(cap, cfg_.max_samples) + 1;
-    w.x = static_cast<float*>(dalloc(static_cast<size_t>(cap) * maxd * 4));
-    w.h = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxd * 2));
-    w.qkv = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxq * 2));
-    w.q = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxao * 2));
-    w.k = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxkv * 2));
-    w.v = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxkv * 2));
-    w.attn = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxao * 2));
-    w.act = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxF * 2));
+    for (int i = 0; i < (scoring ? 3 : 1); ++i) {
+      ActWs& a = w.a[i];
+      a.x = static_cast<float*>(dalloc(static_cast<size_t>(cap) * maxd * 4));
+      a.h = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxd * 2));
+      a.qkv = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxq * 2));
+      a.q = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxao * 2));
+      a.k = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxkv * 2));
+      a.v = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxkv * 2));
+      a.attn = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxao * 2));
+      a.act = static_cast<bf16*>(dalloc(static_cast<size_t>(cap) * maxF * 2));
+    }
     w.tokens = static_cast<int*>(dalloc(cap * 4));
     w.pos = static_cast<int*>(dalloc(cap * 4));
     w.slot = static_cast<int*>(dalloc(cap * 4));
@@ -505,31 +519,31 @@ void Engine::upload_tiles(PackedWs& ws, const int* cu, int n_seq, int nt[2], cud
   }
 }
 
-void Engine::forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, const int nt[2], bool use_pool,
-                            cudaStream_t st) {
+void Engine::forward_packed(const ModelW& w, PackedWs& ws, const ActWs& a, int M, int n_seq, const int nt[2],
+                            bool use_pool, cudaStream_t st) {
   (void)n_seq;
   const Dims& D = w.dims;
   const bool t128 = fpk::attn_varlen_tile_rows(D.hd) == 128;
   const fpk::KvPoolView pv = pool_view();
-  fpk::embed(ws.tokens, nullptr, M, w.embed, D.d, ws.x, st);
+  fpk::embed(ws.tokens, nullptr, M, w.embed, D.d, a.x, st);
   for (int l = 0; l < D.L; ++l) {
     const LayerW& L = w.layers[l];
-    fpk::add_norm(ws.x, nullptr, 0, 0, L.ln1, ws.h, M, D.d, nullptr, 0, nullptr, nullptr, st);
+    fpk::rms_norm_rows(a.x, L.ln1, a.h, M, D.d, st);
     if (fuse_rope_ && D.hd == models_[kActor].dims.hd) {  // the cos/sin table is the actor's head_dim
-      fpk::gemm_qkv_rope_packed(L.wqkv, D.d, ws.h, M, D.H, D.KVH, D.hd, ws.pos, rope_cs_, use_pool ? &pv : nullptr, l,
-                                ws.slot, ws.q, ws.k, ws.v, st);
+      fpk::gemm_qkv_rope_packed(L.wqkv, D.d, a.h, M, D.H, D.KVH, D.hd, ws.pos, rope_cs_, use_pool ? &pv : nullptr, l,
+                                ws.slot, a.q, a.k, a.v, st);
     } else {
-      fpk::gemm_bf16(L.wqkv, D.qkv_width(), D.d, ws.h, M, ws.qkv, D.qkv_width(), st);
-      fpk::rope_qkv(ws.qkv, M, D.H, D.KVH, D.hd, ws.pos, cfg_.rope_theta, ws.q, ws.k, ws.v, use_pool ? &pv : nullptr,
+      fpk::gemm_bf16(L.wqkv, D.qkv_width(), D.d, a.h, M, a.qkv, D.qkv_width(), st);
+      fpk::rope_qkv(a.qkv, M, D.H, D.KVH, D.hd, ws.pos, cfg_.rope_theta, a.q, a.k, a.v, use_pool ? &pv : nullptr,
                     l, ws.slot, st);
     }
     if (use_pool && l == D.L - 1) break;  // prefill only needs the last layer's K/V
-    fpk::attn_varlen(ws.q, ws.k, ws.v, D.H, D.KVH, D.hd, M, ws.cu, t128 ? ws.tiles128 : ws.tiles, nt[t128], ws.attn,
+    fpk::attn_varlen(a.q, a.k, a.v, D.H, D.KVH, D.hd, M, ws.cu, t128 ? ws.tiles128 : ws.tiles, nt[t128], a.attn,
                      st);
-    fpk::gemm_f32_residual(L.wo, D.d, D.H * D.hd, ws.attn, M, ws.x, st);
-    fpk::add_norm(ws.x, nullptr, 0, 0, L.ln2, ws.h, M, D.d, nullptr, 0, nullptr, nullptr, st);
-    fpk::gemm_swiglu(L.wgu, D.F, D.d, ws.h, M, ws.act, st);
-    fpk::gemm_f32_residual(L.wd, D.d, D.F, ws.act, M, ws.x, st);
+    fpk::gemm_f32_residual(L.wo, D.d, D.H * D.hd, a.attn, M, a.x, st);
+    fpk::rms_norm_rows(a.x, L.ln2, a.h, M, D.d, st);
+    fpk::gemm_swiglu(L.wgu, D.F, D.d, a.h, M, a.act, st);
+    fpk::gemm_f32_residual(L.wd, D.d, D.F, a.act, M, a.x, st);
   }
 }
 
@@ -565,7 +579,7 @@ void Engine::prefill(const std::vector<PrefillItem>& items) {
       upload(pre_.pos, pos.data(), M * 4, st);
       upload(pre_.slot, slot.data(), M * 4, st);
       upload(pre_.cu, cu.data(), cu.size() * 4, st);
-      forward_packed(w, pre_, M, ns, nt, true, st);
+      forward_packed(w, pre_, pre_.a[0], M, ns, nt, true, st);
     }
     i = j;
   }
@@ -847,22 +861,33 @@ void Engine::infer(const std::vector<InferItem>& items, float beta, float gamma,
                         ws.gather_last};
     fpk::assemble_batch(a, n, st);
 
+    // The three frozen models read the same packed batch and write disjoint
+    // outputs: the critic and the reward model run on streams of their own.
+    FP_CUDA(cudaEventRecord(ev_fork_, st));
+    for (cudaStream_t s2 : s_score_) FP_CUDA(cudaStreamWaitEvent(s2, ev_fork_, 0));
     // reference model: log-prob of every response token
     const ModelW& ref = models_[kRef];
-    forward_packed(ref, ws, M, n, nt, false, st);
-    fpk::add_norm(ws.x, nullptr, 0, 0, ref.lnf, ws.h, M, ref.dims.d, ws.gather_resp, NR, nullptr, nullptr, st);
-    fpk::gemm_vocab(ws.h, NR, ref.dims.d, ref.head, ref.dims.V, 0 /* forced */, 1.0f, ws.targets, nullptr, nullptr, 0,
+    const ActWs& ar = ws.a[0];
+    forward_packed(ref, ws, ar, M, n, nt, false, st);
+    fpk::add_norm(ar.x, nullptr, 0, 0, ref.lnf, ar.h, M, ref.dims.d, ws.gather_resp, NR, nullptr, nullptr, st);
+    fpk::gemm_vocab(ar.h, NR, ref.dims.d, ref.head, ref.dims.V, 0 /* forced */, 1.0f, ws.targets, nullptr, nullptr, 0,
                     ws.vocab_part, ws.tgt_z, st);
     fpk::vocab_finalize(ws.vocab_part, ws.tgt_z, NR, ref.dims.V, 0 /* forced */, ws.targets, nullptr, nullptr, 0, nullptr, ws.logp_ref,
                         nullptr, nullptr, nullptr, nullptr, nullptr, st);
     // critic: value of the state before each response token
     const ModelW& cr = models_[kCritic];
-    forward_packed(cr, ws, M, n, nt, false, st);
-    fpk::add_norm(ws.x, nullptr, 0, 0, cr.lnf, nullptr, M, cr.dims.d, ws.gather_resp, NR, cr.vhead, ws.values, st);
+    forward_packed(cr, ws, ws.a[1], M, n, nt, false, s_score_[0]);
+    fpk::add_norm(ws.a[1].x, nullptr, 0, 0, cr.lnf, nullptr, M, cr.dims.d, ws.gather_resp, NR, cr.vhead, ws.values,
+                  s_score_[0]);
     // reward model: scalar score at the last token
     const ModelW& rw = models_[kReward];
-    forward_packed(rw, ws, M, n, nt, false, st);
-    fpk::add_norm(ws.x, nullptr, 0, 0, rw.lnf, nullptr, M, rw.dims.d, ws.gather_last, n, rw.vhead, ws.score, st);
+    forward_packed(rw, ws, ws.a[2], M, n, nt, false, s_score_[1]);
+    fpk::add_norm(ws.a[2].x, nullptr, 0, 0, rw.lnf, nullptr, M, rw.dims.d, ws.gather_last, n, rw.vhead, ws.score,
+                  s_score_[1]);
+    for (int k = 0; k < 2; ++k) {
+      FP_CUDA(cudaEventRecord(ev_join_[k], s_score_[k]));
+      FP_CUDA(cudaStreamWaitEvent(st, ev_join_[k], 0));
+    }
 
     fpk::PostScatter sc{ws.off_out,   ws.sid,          ws.targets,  exp_.logp_actor, exp_.logp_ref,
                         exp_.values,  exp_.score,      exp_.tokens};

@@ -243,10 +243,15 @@ class Engine {
   std::vector<ProbeRec> probes_;
   std::vector<cudaEvent_t> probe_pool_;
   cudaEvent_t probe_event();
-  struct PackedWs {
-    int cap = 0, cap_seq = 0;
+  // Activations of one packed forward (per model when the scoring models run
+  // concurrently).
+  struct ActWs {
     float* x = nullptr;
     bf16 *h = nullptr, *qkv = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *attn = nullptr, *act = nullptr;
+  };
+  struct PackedWs {
+    int cap = 0, cap_seq = 0;
+    ActWs a[3];  // [0]: prefill / reference; [1], [2]: critic, reward (scoring only)
     int *tokens = nullptr, *pos = nullptr, *slot = nullptr, *cu = nullptr, *tiles = nullptr, *tiles128 = nullptr;
     // scoring
     int *sid = nullptr, *P = nullptr, *R = nullptr, *roff = nullptr, *targets = nullptr, *gather_resp = nullptr,
@@ -278,12 +283,17 @@ class Engine {
   // Both attention tile tables of one packed batch (64- and 128-query tiles);
   // forward_packed uses the one its model's head size needs. nt[0], nt[1]: counts.
   void upload_tiles(PackedWs& ws, const int* cu, int n_seq, int nt[2], cudaStream_t st);
-  void forward_packed(const ModelW& w, PackedWs& ws, int M, int n_seq, const int nt[2], bool use_pool,
-                      cudaStream_t st);
+  void forward_packed(const ModelW& w, PackedWs& ws, const ActWs& a, int M, int n_seq, const int nt[2],
+                      bool use_pool, cudaStream_t st);
 
   EngineConfig cfg_;
   ModelW models_[4];
   cudaStream_t s_decode_ = nullptr, s_infer_ = nullptr, s_copy_ = nullptr;
+  // The critic's and the reward model's forwards run beside the reference
+  // model's (three independent packed forwards over the same batch): one
+  // model's kernel ramp-up / drain overlaps another's mainloops.
+  cudaStream_t s_score_[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork_ = nullptr, ev_join_[2] = {nullptr, nullptr};
   // pool
   uint8_t* pool_ = nullptr;
   size_t page_bytes_ = 0, layer_bytes_ = 0;

@@ -12,6 +12,7 @@
 #include "gemm.cuh"
 #include "launch.cuh"
 #include "ops.h"
+#include "gemm_persist.cuh"
 #include "vocab.cuh"
 
 namespace fpk {
@@ -141,6 +142,53 @@ void launch(const void* A, int a_rows, const void* B, int b_rows, int K, int spl
   fpk::count_launch();
 }
 
+int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
+  return n;
+}
+
+// Packed forwards (prefill / scoring) from this many rows on take the
+// persistent kernel (gemm_persist.cuh); decode batches (<= 512 rows) never do.
+constexpr int kPersistMinRows = 1024;
+
+template <int BN, class Epi>
+void launch_persist(const void* A, int a_rows, const void* B, int b_rows, int K, const Epi& epi, cudaStream_t st) {
+  using C = PersistCfg<BN, Epi>;
+  if (K % kBK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
+  if (a_rows <= 0 || b_rows <= 0) return;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tc_gemm_persist_kernel<BN, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr_set = true;
+  }
+  const CUtensorMap ma = make_map(A, a_rows, K, 128);
+  const CUtensorMap mb = make_map(B, b_rows, K, BN);
+  PersistGeom g;
+  g.a_rows = a_rows;
+  g.b_rows = b_rows;
+  g.k_blocks = K / kBK;
+  g.a_tiles = (a_rows + 127) / 128;
+  g.n_tiles = g.a_tiles * ((b_rows + BN - 1) / BN);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::min(g.n_tiles, sm_count()));
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_persist_kernel<BN, Epi>, ma, mb, g, epi);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("gemm launch: ") + cudaGetErrorString(e));
+  fpk::count_launch();
+}
+
 // Batch-tile width of a swap-AB GEMM with `a_ctas` weight tiles (x splits):
 // the fewest waves over the 148 SMs, then the narrowest tile (most CTAs
 // streaming weights in that wave), never wider than the rows need. A CTA's
@@ -251,6 +299,11 @@ int gemm_splits(int N, int K) {
 
 void gemm_bf16(const bf16* W, int N, int K, const bf16* X, int M, bf16* out, int ld_out, cudaStream_t st) {
   if ((ld_out * 2) % 16) throw std::invalid_argument("gemm_bf16: ld_out must be a multiple of 8");
+  if (M >= kPersistMinRows) {
+    EpiStoreBF16 e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, ld_out, 128, 256)};
+    launch_persist<256>(W, N, X, M, K, e, st);
+    return;
+  }
   dispatch_bn<EpiStoreBF16>(M, (N + 127) / 128, [&]<int BN>() {
     EpiStoreBF16 e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, ld_out, 128, BN)};
     if (many_waves(M, N, BN))
@@ -280,6 +333,11 @@ void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* o
 
 void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float* resid, cudaStream_t st) {
   if (N % 4) throw std::invalid_argument("gemm_f32: N must be a multiple of 4");
+  if (M >= kPersistMinRows) {
+    EpiStoreF32 e{out_map_2d(resid, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, N, N, 128, 128), 1};
+    launch_persist<128>(W, N, X, M, K, e, st);
+    return;
+  }
   dispatch_bn<EpiStoreF32>(M, (N + 127) / 128, [&]<int BN>() {
     EpiStoreF32 e{out_map_2d(resid, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, N, N, 128, BN), 1};
     if (BN <= 128 && many_waves(M, N, BN))  // (the fp32 staging tile of BN 256 needs a deeper ring)
@@ -302,6 +360,11 @@ void gemm_swiglu_decode(const bf16* Wgu, int F, int K, const bf16* X, int M, bf1
 
 void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
   if (F % 64) throw std::invalid_argument("gemm_swiglu: F must be a multiple of 64");
+  if (M >= kPersistMinRows) {
+    EpiSwiGLU<256> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, 256)};
+    launch_persist<256>(Wgu, 2 * F, X, M, K, e, st);
+    return;
+  }
   dispatch_bn<int>(M, (2 * F + 127) / 128, [&]<int BN>() {
     EpiSwiGLU<BN> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, BN)};
     if (many_waves(M, 2 * F, BN))
@@ -331,6 +394,15 @@ void gemm_qkv_rope_packed(const bf16* Wqkv, int K, const bf16* X, int M, int H, 
                           bf16* k_out, bf16* v_out, cudaStream_t st) {
   if (128 % hd != 0) throw std::invalid_argument("gemm_qkv_rope: head_dim must divide 128");
   const int N = (H + 2 * KVH) * hd;
+  if (M >= kPersistMinRows) {
+    EpiRopeKV<256> e{q_out, pool ? *pool : KvPoolView{}, slot, pos, cs, layer, H, KVH, hd, M};
+    e.pool.kv_map = nullptr;
+    e.k_out = k_out;
+    e.v_out = v_out;
+    e.use_pool = pool != nullptr;
+    launch_persist<256>(Wqkv, N, X, M, K, e, st);
+    return;
+  }
   dispatch_bn<int>(M, (N + 127) / 128, [&]<int BN>() {
     EpiRopeKV<BN> e{q_out, pool ? *pool : KvPoolView{}, slot, pos, cs, layer, H, KVH, hd, M};
     e.pool.kv_map = nullptr;

@@ -1,0 +1,184 @@
+// fuseplan-b200 — persistent tcgen05 GEMM for the packed forwards (prefill and
+// the scoring models: thousands of rows).
+//
+// Same math, operands, epilogue functors and per-element K order as
+// tc_gemm_kernel (gemm.cuh) — so every output element has the same bits — but
+// one CTA per SM walks a static list of 128 x BN output tiles:
+//   warp 0      TMA producer: the ring runs across tile boundaries
+//   warp 1      MMA issuer: accumulates tile i into TMEM buffer i & 1
+//   warps 2..9  epilogue of tile i (TMEM buffer i & 1) while the MMA warp
+//               already fills buffer (i + 1) & 1
+// The epilogue stages its output in a shared-memory area of its own (the ring
+// keeps streaming the next tiles), so the ring gets what the budget leaves.
+// This removes the two costs the one-tile-per-CTA kernel pays at large M: the
+// exposed epilogue (no mainloop runs under it) and wave quantisation (e.g.
+// 192 tiles on 148 SMs = two waves for 1.3 waves of work).
+#pragma once
+
+#include "gemm.cuh"
+
+namespace fpk {
+
+// Shared memory the epilogue stages one output tile in (bytes).
+template <int BN, class Epi>
+struct EpiStaging {
+  static constexpr int v = ((BN + 63) / 64) * 64 * 128 * 2;  // bf16 [round64(BN)][128]
+};
+template <int BN>
+struct EpiStaging<BN, EpiStoreF32> {
+  static constexpr int v = ((BN + 63) / 64) * 64 * 128 * 4;  // fp32
+};
+template <int BN>
+struct EpiStaging<BN, EpiSwiGLU<BN>> {
+  static constexpr int v = EpiSwiGLU<BN>::kTileBytes + 2 * 32 * 128 * 4;  // tile + gate/up exchange
+};
+
+constexpr int kPersistSmem = 224 * 1024;
+
+template <int BN, class Epi>
+struct PersistCfg {
+  static constexpr int kStageBytes = kTileA + BN * kBK * 2;
+  static constexpr int kStaging = EpiStaging<BN, Epi>::v + EpiSmemExtra<Epi>::value;
+  static constexpr int kStages = (kPersistSmem - 1024 - kStaging - 256) / kStageBytes;
+  static constexpr int kSmem = kStages * kStageBytes + kStaging + 1024 + 256;
+  static constexpr uint32_t kAccCols = GemmCfg<BN>::kTmemCols;
+  static constexpr uint32_t kTmemCols = 2 * kAccCols;
+  static_assert(kStages >= 2, "persistent GEMM: ring too shallow");
+  static_assert(kTmemCols <= 512, "persistent GEMM: two accumulators must fit TMEM");
+};
+
+struct PersistGeom {
+  int a_rows, b_rows, k_blocks, a_tiles, n_tiles;
+};
+
+template <int BN, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    tc_gemm_persist_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                           const PersistGeom g, const __grid_constant__ Epi epi) {
+  using C = PersistCfg<BN, Epi>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* staging = smem + C::kStages * C::kStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(staging + C::kStaging);
+  uint64_t* full_bar = bars;                    // [kStages]
+  uint64_t* empty_bar = bars + C::kStages;      // [kStages]
+  uint64_t* acc_full = bars + 2 * C::kStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const uint32_t warp = warp_id();
+  pdl_trigger();
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 32 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nkb = g.k_blocks;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int it = 0;  // ring position over the CTA's lifetime
+      bool waited = false;
+      for (int t = blockIdx.x; t < g.n_tiles; t += gridDim.x) {
+        const int a_row0 = (t % g.a_tiles) * 128, b_row0 = (t / g.a_tiles) * BN;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % C::kStages;
+          mbar_wait(&empty_bar[s], ((it / C::kStages) & 1) ^ 1);
+          uint8_t* sa = smem + s * C::kStageBytes;
+          mbar_arrive_expect_tx(&full_bar[s], C::kStageBytes);
+          tma_load_2d(sa, &map_a, &full_bar[s], kb * kBK, a_row0);  // weights: independent of the previous kernel
+          if (!waited) {
+            pdl_wait();  // activations come from the previous kernel
+            waited = true;
+          }
+          tma_load_2d(sa + kTileA, &map_b, &full_bar[s], kb * kBK, b_row0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = idesc_bf16(128, BN);
+      const uint64_t da = sdesc_k128(smem_u32(smem)), db = sdesc_k128(smem_u32(smem) + kTileA);
+      int it = 0, i = 0;
+      for (int t = blockIdx.x; t < g.n_tiles; t += gridDim.x, ++i) {
+        const int buf = i & 1;
+        mbar_wait(&acc_empty[buf], ((i >> 1) & 1) ^ 1);  // epilogue drained this buffer (tile i - 2)
+        tc_fence_after();
+        const uint32_t acc = tmem + buf * C::kAccCols;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % C::kStages;
+          mbar_wait(&full_bar[s], (it / C::kStages) & 1);
+          tc_fence_after();
+          const uint64_t off = static_cast<uint64_t>((s * C::kStageBytes) >> 4);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            tc_mma_bf16(acc, da + off + 2 * k, db + off + 2 * k, idesc, (kb > 0 || k > 0) ? 1u : 0u);
+          tc_commit(&empty_bar[s]);
+        }
+        tc_commit(&acc_full[buf]);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int quarter = warp & 3;
+    const int half = (static_cast<int>(warp) - 2) >> 2;
+    const int r = quarter * 32 + lane_id();
+    pdl_wait();
+    int i = 0;
+    for (int t = blockIdx.x; t < g.n_tiles; t += gridDim.x, ++i) {
+      const int a_row0 = (t % g.a_tiles) * 128, b_row0 = (t / g.a_tiles) * BN;
+      const int buf = i & 1;
+      typename Epi::State st{};
+      if constexpr (EpiHasPrologue<Epi>::value) epi.prologue(st, a_row0, b_row0, staging + EpiStaging<BN, Epi>::v);
+      mbar_wait(&acc_full[buf], (i >> 1) & 1);
+      tc_fence_after();
+      const uint32_t acc = tmem + buf * C::kAccCols + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll 1
+      for (int pass = 0; pass < Epi::kPasses; ++pass) {
+        if (pass) epi.next_pass(st, a_row0, b_row0, r, half);
+#pragma unroll 1
+        for (int c0 = 32 * half; c0 < ((BN + 63) / 64) * 64; c0 += 64) {
+          float v[32];
+          if (c0 < BN) {
+            tmem_ld32(acc + c0, v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          }
+          epi(st, staging, a_row0, b_row0, 0, r, half, c0, v);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[buf]);  // TMEM buffer free: the MMA warp may start tile i + 2 in it
+      epi.finish(st, a_row0, b_row0, 0, r, half);
+      if constexpr (Epi::kTmaStore) {
+        fence_async_smem();
+        epi_bar_sync();
+        if (threadIdx.x == 64) {
+          epi.store(staging, a_row0, b_row0, 0);
+          bulk_commit_wait_read();
+        }
+      }
+      epi_bar_sync();  // staging reusable: the store has read it / finish() is done with it
+    }
+    if constexpr (EpiHasPost<Epi>::value) epi.post();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
+}
+
+}  // namespace fpk

@@ -148,6 +148,33 @@ __global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__
   }
 }
 
+// Packed forward (prefill / scoring, thousands of rows): RMSNorm with one
+// warp per row and 8 rows per block — no block-wide reduction, V float4 of
+// the row per lane, all of them in flight at once. d = 128 V.
+template <int V>
+__global__ void __launch_bounds__(256) rms_norm_rows_kernel(const float* __restrict__ x, const float* __restrict__ gain,
+                                                            bf16* __restrict__ y, int M) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
+  pdl_wait();     // PDL-launched: x comes from the previous kernel
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= M) return;
+  const int lane = threadIdx.x & 31;
+  constexpr int d4 = 32 * V;
+  const float4* xr = reinterpret_cast<const float4*>(x) + static_cast<size_t>(row) * d4;
+  float4 v[V];
+#pragma unroll
+  for (int k = 0; k < V; ++k) v[k] = xr[lane + 32 * k];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < V; ++k) ss += sumsq4(v[k]);
+  ss = warp_sum(ss);
+  const float inv = rsqrtf(ss / (4 * d4) + kNormEps);
+  uint2* yr = reinterpret_cast<uint2*>(y) + static_cast<size_t>(row) * d4;
+  const float4* g4 = reinterpret_cast<const float4*>(gain);
+#pragma unroll
+  for (int k = 0; k < V; ++k) yr[lane + 32 * k] = norm_scale4(v[k], inv, g4[lane + 32 * k]);
+}
+
 // grid: M rows; block: 128. Rotate-half RoPE (pairs i, i + HD/2); cos/sin of
 // the row's position are computed once per pair index and shared by all heads.
 template <int HD>
@@ -343,6 +370,22 @@ void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, con
     default: throw std::invalid_argument("add_norm: at most 8 split-K partials");
   }
 #undef FP_AN
+  fpk::count_launch();
+}
+
+void rms_norm_rows(const float* x, const float* gain, bf16* y, int M, int d, cudaStream_t st) {
+  if (M <= 0) return;
+  const dim3 grid((M + 7) / 8), block(256);
+  switch (d) {
+    case 256: launch_pdl(rms_norm_rows_kernel<2>, grid, block, 0, st, x, gain, y, M); break;
+    case 768: launch_pdl(rms_norm_rows_kernel<6>, grid, block, 0, st, x, gain, y, M); break;
+    case 1024: launch_pdl(rms_norm_rows_kernel<8>, grid, block, 0, st, x, gain, y, M); break;
+    case 2048: launch_pdl(rms_norm_rows_kernel<16>, grid, block, 0, st, x, gain, y, M); break;
+    case 4096: launch_pdl(rms_norm_rows_kernel<32>, grid, block, 0, st, x, gain, y, M); break;
+    default:  // other widths: the block-per-row kernel
+      add_norm(const_cast<float*>(x), nullptr, 0, 0, gain, y, M, d, nullptr, 0, nullptr, nullptr, st);
+      return;
+  }
   fpk::count_launch();
 }
 

@@ -102,6 +102,9 @@ struct L2Prefetch {
 void add_norm(float* x, const float* parts, int nsplit, size_t split_stride, const float* gain, bf16* y, int M,
               int d, const int* gather, int M_out, const bf16* value_w, float* value, cudaStream_t st,
               const L2Prefetch& pf = L2Prefetch{});
+// y = bf16(RMSNorm(x) * gain) for the packed forward (no partials / gather): one
+// warp per row (layers.cu rms_norm_rows_kernel).
+void rms_norm_rows(const float* x, const float* gain, bf16* y, int M, int d, cudaStream_t st);
 
 // RoPE on q, k of a packed qkv [M, (H + 2 KVH) * hd] row block; q -> q_out
 // [M, H, hd]; k, v -> either contiguous k_out/v_out [M, KVH, hd] and/or the

@@ -168,6 +168,23 @@ def test_add_norm(lib):
     assert (y.float() - ref).abs().max().item() < 2e-2 * ref.abs().max().item()
 
 
+@pytest.mark.parametrize("M,d", [(1, 768), (8191, 768), (37, 2048), (1000, 4096), (9, 256), (17, 512)])
+def test_rms_norm_rows(lib, M, d):
+    """Warp-per-row RMSNorm of the packed forward vs fp32 torch (d 512: block-per-row fallback)."""
+    x = torch.randn(M, d, device="cuda") * 3
+    g = torch.rand(d, device="cuda") + 0.5
+    y = torch.zeros(M, d, device="cuda", dtype=torch.bfloat16)
+    ok(lib, lib.fp_k_rms_norm_rows(ptr(x), ptr(g), ptr(y), M, d, stream()))
+    torch.cuda.synchronize()
+    ref = x * torch.rsqrt(x.pow(2).mean(-1, keepdim=True) + 1e-5) * g
+    assert (y.float() - ref).abs().max().item() < 1e-2 * ref.abs().max().item()
+    # rows are independent: a prefix alone gives the same bits
+    y2 = torch.zeros_like(y)
+    ok(lib, lib.fp_k_rms_norm_rows(ptr(x), ptr(g), ptr(y2), max(M // 2, 1), d, stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(y2[: max(M // 2, 1)], y[: max(M // 2, 1)])
+
+
 @pytest.mark.parametrize("hd,H,KVH", [(64, 12, 12), (128, 32, 8), (32, 8, 8), (128, 16, 16), (64, 32, 4)])
 @pytest.mark.parametrize("ctx_list", [[1, 63, 64, 65, 300], [1000, 7, 257], [2000, 513, 512, 511],
                                       list(range(7, 7 + 13 * 80, 13))])  # 80 rows: wide kernel, cut splits
@@ -442,6 +459,50 @@ def test_gemm_swiglu_bench_shapes(lib, M, F, K, decode):
     torch.cuda.synchronize()
     err = (out.float() - ref).abs().max().item()
     assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+
+
+# Packed-forward GEMMs (M >= 1024) run the persistent kernel (gemm_persist.cuh);
+# decode-sized ones the one-tile-per-CTA kernel. Same K order per element: the
+# bits must not depend on which kernel (or how many rows) computed a row.
+@pytest.mark.parametrize("kind,N,K", [("bf16", 2304, 768), ("bf16", 6144, 2048), ("swiglu", 6144, 768),
+                                      ("swiglu", 11264, 2048), ("resid", 768, 3072), ("resid", 2048, 2048),
+                                      ("resid", 4096, 14336)])
+@pytest.mark.parametrize("M", [1024, 3001, 8192])
+def test_gemm_persistent_matches_tiled(lib, kind, N, K, M):
+    if kind == "resid" and N == 4096 and M == 8192:
+        M = 2048  # (bounded runtime)
+    W = rand_bf16(N, K, scale=K ** -0.5, seed=31)
+    if kind == "swiglu":
+        W, X, ref = _swiglu_case(N // 2, K, M, 32)
+    else:
+        X = rand_bf16(M, K, seed=33)
+        ref = X.float() @ W.float().T
+    chunks = [(a, min(M, a + 512)) for a in range(0, M, 512)]
+    if kind == "resid":
+        r0 = torch.randn(M, N, device="cuda")
+        full, part = r0.clone(), r0.clone()
+        ok(lib, lib.fp_k_gemm_f32_residual(ptr(W), N, K, ptr(X), M, ptr(full), stream()))
+        for a, b in chunks:
+            ok(lib, lib.fp_k_gemm_f32_residual(ptr(W), N, K, ptr(X[a:b]), b - a, ptr(part[a:b]), stream()))
+        ref = ref + r0
+        tol = 1e-3
+    else:
+        F = N // 2 if kind == "swiglu" else N
+        full = torch.full((M, F), float("nan"), device="cuda", dtype=torch.bfloat16)
+        part = torch.full_like(full, float("nan"))
+        if kind == "swiglu":
+            ok(lib, lib.fp_k_gemm_swiglu(ptr(W), F, K, ptr(X), M, ptr(full), stream()))
+            for a, b in chunks:
+                ok(lib, lib.fp_k_gemm_swiglu(ptr(W), F, K, ptr(X[a:b]), b - a, ptr(part[a:b]), stream()))
+        else:
+            ok(lib, lib.fp_k_gemm_bf16(ptr(W), N, K, ptr(X), M, ptr(full), N, stream()))
+            for a, b in chunks:
+                ok(lib, lib.fp_k_gemm_bf16(ptr(W), N, K, ptr(X[a:b]), b - a, ptr(part[a:b]), N, stream()))
+        tol = 2e-2
+    torch.cuda.synchronize()
+    err = (full.float() - ref).abs().max().item()
+    assert err <= tol * max(1.0, ref.abs().max().item()), err
+    assert torch.equal(full, part)
 
 
 @pytest.mark.parametrize("M", [1, 64, 300])
