@@ -706,6 +706,10 @@ int attn_varlen_call(const void* q, const void* k, const void* v, int H, int KVH
 }
 }  // namespace
 
+int fp_k_attn_prefill_trace(void* buf) {
+  return guarded([&] { fpk::attn_prefill_set_trace(static_cast<unsigned long long*>(buf)); });
+}
+
 int fp_k_attn_varlen(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
                      const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream) {
   return attn_varlen_call(q, k, v, H, KVH, hd, cu_host, cu_dev, n_seq, out, stream, false);

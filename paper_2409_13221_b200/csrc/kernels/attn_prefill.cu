@@ -173,7 +173,16 @@ __global__ void __launch_bounds__(kThreads, 2)
     attn_prefill_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                         const __grid_constant__ CUtensorMap map_v, int H, int KVH, int n_items,
                         const int* __restrict__ cu, const int* __restrict__ tiles, float scale_log2,
-                        bf16* __restrict__ out) {
+                        bf16* __restrict__ out, unsigned long long* __restrict__ trace) {
+  // debug trace (fp_k_attn_prefill_trace): CTA 0's event times, [kind][64]
+  unsigned long long* tr = blockIdx.x == 0 ? trace : nullptr;
+  auto stamp = [&](int kind, int i) {
+    if (tr && i < 64) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      tr[kind * 64 + i] = t;
+    }
+  };
   using C = PrefillCfg<HD>;
   pdl_trigger();
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -241,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           uint8_t* ks = smem + C::kOffK + s * C::kKBytes;
           uint8_t* vs = smem + C::kOffV + s * C::kKBytes;
           mbar_wait(&k_empty[s], ph);
+          stamp(0, g);
           mbar_arrive_expect_tx(&k_full[s], C::kKBytes);
 #pragma unroll
           for (int c = 0; c < HD / 64; ++c)
@@ -274,6 +284,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                       (first && kk == 0) ? 0u : 1u);
         tc_commit(&pv_done[b]);
         tc_commit(&v_empty[s]);
+        stamp(2, gg);
       };
       int g = 0, n = 0;
       bool prev_first = false;
@@ -295,6 +306,7 @@ __global__ void __launch_bounds__(kThreads, 2)
               tc_mma_bf16(tmem + (g & 1) * kBN, qa + 2 * kk, kb + 2 * kk, idesc_s, (c | kk) ? 1u : 0u);
           }
           tc_commit(&s_full[g & 1]);
+          stamp(1, g);
           tc_commit(&k_empty[s]);
           if (j == x.n_kb - 1) tc_commit(q_free);
           if (g > 0) issue_pv(g - 1, prev_first);
@@ -324,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int j = 0; j < x.n_kb; ++j, ++g) {
         mbar_wait(&s_full[g & 1], (g >> 1) & 1);
         tc_fence_after();
+        if (r == 0) stamp(3, g);
         uint32_t raw[2][32];
         tmem_ld32_async(lane_base + (g & 1) * kBN, raw[0]);
         tmem_ld32_async(lane_base + (g & 1) * kBN + 32, raw[1]);
@@ -360,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           l *= f;
           m_used = m_new;
         }
+        if (r == 0) stamp(4, g);
         const uint32_t pbuf = prow + (g % PB) * C::kPBytes;
         float rs[8];
 #pragma unroll
@@ -379,6 +393,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         fence_async_smem();  // generic-proxy P stores -> visible to the tensor core
         tc_fence_before();
         mbar_arrive(&p_full[g % PB]);
+        if (r == 0) stamp(5, g);
       }
       // epilogue: O / l of this item
       wait_pv(g - 1);
@@ -403,12 +418,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
       tc_fence_before();  // O reads ordered before the next item's first p_full arrive
+      if (r == 0) stamp(6, g);
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
 }
+
+unsigned long long* g_prefill_trace = nullptr;
 
 int sm_count() {
   static int n = [] {
@@ -435,11 +453,14 @@ void launch_prefill(const bf16* q, const bf16* k, const bf16* v, int H, int KVH,
   const float scale = kLog2e / sqrtf(static_cast<float>(HD));
   const int n_items = n_tiles * H;
   const int grid = std::min(n_items, 2 * sm_count());  // two CTAs per SM (TMEM 2 x <= 256 cols, ~113 KB smem)
-  attn_prefill_kernel<HD><<<grid, kThreads, C::kSmem, st>>>(mq, mk, mv, H, KVH, n_items, cu, tiles, scale, out);
+  attn_prefill_kernel<HD><<<grid, kThreads, C::kSmem, st>>>(mq, mk, mv, H, KVH, n_items, cu, tiles, scale, out,
+                                                             g_prefill_trace);
   count_launch();
 }
 
 }  // namespace
+
+void attn_prefill_set_trace(unsigned long long* buf) { g_prefill_trace = buf; }
 
 bool attn_prefill_supported(int hd) { return hd == 64 || hd == 128; }
 

@@ -72,6 +72,21 @@ def main():
               f"union of kernel intervals {busy / 1e3:.1f} ms")
         for k, v in sorted(ks.items(), key=lambda x: -x[1][1])[:14]:
             print(f"   {k:40s} {v[0]:7d} launches {v[1]:9.2f} ms ({v[1] / tot:.1%})")
+    # all streams but the busiest-by-launch-count decode stream: the scoring streams together
+    dec = max(by_stream, key=lambda k: sum(v[0] for v in by_stream[k].values()))
+    iv = sorted(x for sid, xs in spans.items() if sid != dec for x in xs)
+    if iv:
+        busy, cs, ce = 0.0, iv[0][0], iv[0][1]
+        for a, b in iv[1:]:
+            if a > ce:
+                busy += ce - cs
+                cs, ce = a, b
+            else:
+                ce = max(ce, b)
+        busy += ce - cs
+        res["scoring_union_ms"] = busy / 1e3
+        res["scoring_span_ms"] = (iv[-1][1] - iv[0][0]) / 1e3
+        print(f"scoring streams together: union {busy / 1e3:.1f} ms, span {(iv[-1][1] - iv[0][0]) / 1e3:.1f} ms")
     if len(sys.argv) > 2:
         Path(sys.argv[2]).write_text(json.dumps(res, indent=1, default=str))
 

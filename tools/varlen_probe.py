@@ -3,7 +3,7 @@
 (prompt + Zipf response lengths, packed to ~8192 tokens like Engine::infer),
 beside the SwiGLU GEMM of the same M for scale.
 
-    python tools/varlen_probe.py [gpt2s|1.3b|8b ...]   # on a B200 (gpurun)
+    python tools/varlen_probe.py [gpt2s|1.3b|8b ...] [L=<uniform length>]   # on a B200 (gpurun)
 
 Kernel times are CUPTI device durations. Reports causal FLOPs (4 * sum(L^2 / 2) * H * hd) per second.
 """
@@ -67,12 +67,14 @@ def packed_lengths(w, cap=8192):
 
 def main():
     s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-    names = sys.argv[1:] or ["gpt2s", "1.3b", "8b"]
+    args = [a for a in sys.argv[1:] if not a.startswith("L=")]
+    uni = [int(a[2:]) for a in sys.argv[1:] if a.startswith("L=")]
+    names = args or ["gpt2s", "1.3b", "8b"]
     for name in names:
         w = configs.WORKLOADS[name]
         D = w.ref
         H, KVH, hd, d, F = D.num_heads, D.num_kv_heads, D.head_dim, D.hidden, D.ffn
-        lens = packed_lengths(w)
+        lens = [uni[0]] * (8192 // uni[0]) if uni else packed_lengths(w)
         cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
         M = int(cu[-1])
         q = torch.randn(M, H, hd, device="cuda").bfloat16()
@@ -95,5 +97,43 @@ def main():
               f"{fl / tm / 1e9:.0f} TF/s | swiglu GEMM {tg * 1e3:.1f} us = {2 * M * 2 * F * d / tg / 1e9:.0f} TF/s")
 
 
+
+
+def trace(name="gpt2s", L="128"):
+    L = int(L)
+    """CTA 0's per-block event times (us from its first stamp) of one launch."""
+    w = configs.WORKLOADS[name]
+    D = w.ref
+    H, KVH, hd = D.num_heads, D.num_kv_heads, D.head_dim
+    lens = [L] * (8192 // L)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    M = int(cu[-1])
+    q = torch.randn(M, H, hd, device="cuda").bfloat16()
+    k = torch.randn(M, KVH, hd, device="cuda").bfloat16()
+    v = torch.randn(M, KVH, hd, device="cuda").bfloat16()
+    out = torch.empty(M, H, hd, device="cuda", dtype=torch.bfloat16)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    cud = torch.from_numpy(cu).cuda()
+    buf = torch.zeros(7 * 64, dtype=torch.int64, device="cuda")
+    lib.fp_k_attn_varlen(p(q), p(k), p(v), H, KVH, hd, cu.ctypes.data_as(C.POINTER(C.c_int32)), p(cud), len(lens),
+                         p(out), s)
+    lib.fp_k_attn_prefill_trace(p(buf))
+    lib.fp_k_attn_varlen(p(q), p(k), p(v), H, KVH, hd, cu.ctypes.data_as(C.POINTER(C.c_int32)), p(cud), len(lens),
+                         p(out), s)
+    lib.fp_k_attn_prefill_trace(None)
+    torch.cuda.synchronize()
+    t = buf.view(7, 64).cpu().numpy()
+    t0 = t[t > 0].min()
+    names = ["K load", "S issued", "PV issued", "sm: S ready", "sm: PV(g-1) done", "sm: P written", "sm: item done"]
+    print(f"{name} L={L}: CTA 0 timeline (us)")
+    for g in range(24):
+        row = " ".join(f"{(t[kk, g] - t0) / 1e3:7.2f}" if t[kk, g] else "      -" for kk in range(7))
+        print(f"  g={g:2d} {row}")
+    print("  cols:", " | ".join(names))
+
+
 if __name__ == "__main__":
-    main()
+    if "trace" in sys.argv:
+        trace(*(a for a in sys.argv[1:] if a != "trace"))
+    else:
+        main()
