@@ -244,7 +244,7 @@ int fp_k_attn_decode_ws(const void* q, int32_t B, int32_t H, int32_t KVH, int32_
  * hd 64 / 128: tcgen05 kernel; other head sizes: mma.sync kernel. */
 int fp_k_attn_varlen(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
                      const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream);
-/* Debug: record CTA 0's event times of subsequent tcgen05 varlen launches into buf (7 x 64 u64, device). */
+/* Debug: record CTA 0's event times of subsequent tcgen05 varlen launches into buf (8 x 64 u64, device). */
 int fp_k_attn_prefill_trace(void* buf);
 /* The mma.sync kernel for any supported head size (cross-check of the tcgen05 kernel). */
 int fp_k_attn_varlen_mma(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,

@@ -341,24 +341,32 @@ __global__ void __launch_bounds__(kThreads, 2)
         tmem_ld32_async(lane_base + (g & 1) * kBN, raw[0]);
         tmem_ld32_async(lane_base + (g & 1) * kBN + 32, raw[1]);
         tmem_wait_ld();
+        if (r == 0) stamp(7, g);
         tc_fence_before();
         mbar_arrive(&s_free[g & 1]);
         float sv[64];
         const int nvalid = lim - (x.s0 + j * kBN) + 1;  // keys c < nvalid are visible
         float mx[8];
+        if (__all_sync(0xffffffffu, nvalid >= kBN)) {  // below the diagonal for the whole warp: no mask
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          sv[c] = c < nvalid ? __uint_as_float(raw[c >> 5][c & 31]) : -INFINITY;
-          mx[c & 7] = c < 8 ? sv[c] : fmaxf(mx[c & 7], sv[c]);
+          for (int c = 0; c < 64; ++c) {
+            sv[c] = __uint_as_float(raw[c >> 5][c & 31]);
+            mx[c & 7] = c < 8 ? sv[c] : fmaxf(mx[c & 7], sv[c]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            sv[c] = c < nvalid ? __uint_as_float(raw[c >> 5][c & 31]) : -INFINITY;
+            mx[c & 7] = c < 8 ? sv[c] : fmaxf(mx[c & 7], sv[c]);
+          }
         }
         const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * scale_log2;
-        if (g >= PB) wait_pv(g - PB);  // P buffer free
         const float m_new = fmaxf(m_used, mt);
         if (j == 0) {
           m_used = m_new;
         } else if (__any_sync(0xffffffffu, m_new > m_used + kRescaleThresh)) {
-          if (PB > 1) wait_pv(g - 1);  // O settled
+          wait_pv(g - 1);  // O settled
           const float f = ex2(m_used - m_new);
 #pragma unroll 1
           for (int c0 = 0; c0 < HD; c0 += 32) {
@@ -375,21 +383,26 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         if (r == 0) stamp(4, g);
         const uint32_t pbuf = prow + (g % PB) * C::kPBytes;
-        float rs[8];
+        // exponent arguments, row sums and P in packed pairs (FFMA2 / FADD2:
+        // half the FP32 instructions of the issue-bound exp phase)
+        const float2 sc2 = make_float2(scale_log2, scale_log2), nm2 = make_float2(-m_used, -m_used);
+        float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        uint32_t wd[8][4];
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch) {
-          uint32_t wd[4];
-          rs[ch] = 0.f;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float p0 = ex2(fmaf(sv[ch * 8 + 2 * e], scale_log2, -m_used));
-            const float p1 = ex2(fmaf(sv[ch * 8 + 2 * e + 1], scale_log2, -m_used));
-            rs[ch] += p0 + p1;
-            wd[e] = pack_bf16x2(p0, p1);
+            const float2 a = __ffma2_rn(make_float2(sv[ch * 8 + 2 * e], sv[ch * 8 + 2 * e + 1]), sc2, nm2);
+            const float2 pp = make_float2(ex2(a.x), ex2(a.y));
+            rs2[e] = __fadd2_rn(rs2[e], pp);
+            wd[ch][e] = pack_bf16x2(pp.x, pp.y);
           }
-          sts_v4(pbuf + ((ch ^ (r & 7)) << 4), wd[0], wd[1], wd[2], wd[3]);
         }
-        l += ((rs[0] + rs[1]) + (rs[2] + rs[3])) + ((rs[4] + rs[5]) + (rs[6] + rs[7]));
+        if (g >= PB) wait_pv(g - PB);  // P buffer free (checked after the exps: usually long done)
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) sts_v4(pbuf + ((ch ^ (r & 7)) << 4), wd[ch][0], wd[ch][1], wd[ch][2], wd[ch][3]);
+        const float2 rsa = __fadd2_rn(__fadd2_rn(rs2[0], rs2[1]), __fadd2_rn(rs2[2], rs2[3]));
+        l += rsa.x + rsa.y;
         fence_async_smem();  // generic-proxy P stores -> visible to the tensor core
         tc_fence_before();
         mbar_arrive(&p_full[g % PB]);

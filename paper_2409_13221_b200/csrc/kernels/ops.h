@@ -266,7 +266,7 @@ int attn_varlen_tiles(const int* cu_host, int n_seq, int hd, int* tiles_host);
 void attn_varlen(const bf16* q, const bf16* k, const bf16* v, int H, int KVH, int hd, int M, const int* cu,
                  const int* tiles, int n_tiles, bf16* out, cudaStream_t st);
 bool attn_prefill_supported(int hd);
-void attn_prefill_set_trace(unsigned long long* buf);  // debug: CTA 0 event times [7][64] (nullptr: off)
+void attn_prefill_set_trace(unsigned long long* buf);  // debug: CTA 0 event times [8][64] (nullptr: off)
 void attn_prefill(const bf16* q, const bf16* k, const bf16* v, int H, int KVH, int hd, int M, const int* cu,
                   const int* tiles, int n_tiles, bf16* out, cudaStream_t st);
 // The mma.sync kernel for any supported hd (64-row query tiles); kept for

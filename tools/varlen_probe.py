@@ -114,7 +114,7 @@ def trace(name="gpt2s", L="128"):
     out = torch.empty(M, H, hd, device="cuda", dtype=torch.bfloat16)
     s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     cud = torch.from_numpy(cu).cuda()
-    buf = torch.zeros(7 * 64, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(8 * 64, dtype=torch.int64, device="cuda")
     lib.fp_k_attn_varlen(p(q), p(k), p(v), H, KVH, hd, cu.ctypes.data_as(C.POINTER(C.c_int32)), p(cud), len(lens),
                          p(out), s)
     lib.fp_k_attn_prefill_trace(p(buf))
@@ -122,12 +122,13 @@ def trace(name="gpt2s", L="128"):
                          p(out), s)
     lib.fp_k_attn_prefill_trace(None)
     torch.cuda.synchronize()
-    t = buf.view(7, 64).cpu().numpy()
+    t = buf.view(8, 64).cpu().numpy()
     t0 = t[t > 0].min()
-    names = ["K load", "S issued", "PV issued", "sm: S ready", "sm: PV(g-1) done", "sm: P written", "sm: item done"]
+    names = ["K load", "S issued", "PV issued", "sm: S ready", "sm: max done / P buffer free", "sm: P written",
+             "sm: item done", "sm: S in registers"]
     print(f"{name} L={L}: CTA 0 timeline (us)")
     for g in range(24):
-        row = " ".join(f"{(t[kk, g] - t0) / 1e3:7.2f}" if t[kk, g] else "      -" for kk in range(7))
+        row = " ".join(f"{(t[kk, g] - t0) / 1e3:7.2f}" if t[kk, g] else "      -" for kk in range(8))
         print(f"  g={g:2d} {row}")
     print("  cols:", " | ".join(names))
 
