@@ -816,7 +816,12 @@ void Engine::decode_kernels(DecodeWs& dw, cudaStream_t st, int B, int max_ctx, i
 
 // ---------------------------------------------------------------------------
 
-void Engine::infer(const std::vector<InferItem>& items, float beta, float gamma, float lam) {
+void Engine::infer(const std::vector<InferItem>& items, float beta, float gamma, float lam, bool yield) {
+  struct PersistGuard {
+    bool prev;
+    explicit PersistGuard(bool on) : prev(fpk::packed_persistent()) { fpk::set_packed_persistent(on); }
+    ~PersistGuard() { fpk::set_packed_persistent(prev); }
+  } guard(!yield);
   cudaStream_t st = infer_stream();
   PackedWs& ws = inf_;
   std::vector<int> sid, P, R, cu, roff, tiles;
@@ -863,8 +868,11 @@ void Engine::infer(const std::vector<InferItem>& items, float beta, float gamma,
 
     // The three frozen models read the same packed batch and write disjoint
     // outputs: the critic and the reward model run on streams of their own.
-    FP_CUDA(cudaEventRecord(ev_fork_, st));
-    for (cudaStream_t s2 : s_score_) FP_CUDA(cudaStreamWaitEvent(s2, ev_fork_, 0));
+    cudaStream_t s_cr = yield ? st : s_score_[0], s_rw = yield ? st : s_score_[1];
+    if (!yield) {
+      FP_CUDA(cudaEventRecord(ev_fork_, st));
+      for (cudaStream_t s2 : s_score_) FP_CUDA(cudaStreamWaitEvent(s2, ev_fork_, 0));
+    }
     // reference model: log-prob of every response token
     const ModelW& ref = models_[kRef];
     const ActWs& ar = ws.a[0];
@@ -876,15 +884,15 @@ void Engine::infer(const std::vector<InferItem>& items, float beta, float gamma,
                         nullptr, nullptr, nullptr, nullptr, nullptr, st);
     // critic: value of the state before each response token
     const ModelW& cr = models_[kCritic];
-    forward_packed(cr, ws, ws.a[1], M, n, nt, false, s_score_[0]);
+    forward_packed(cr, ws, ws.a[1], M, n, nt, false, s_cr);
     fpk::add_norm(ws.a[1].x, nullptr, 0, 0, cr.lnf, nullptr, M, cr.dims.d, ws.gather_resp, NR, cr.vhead, ws.values,
-                  s_score_[0]);
+                  s_cr);
     // reward model: scalar score at the last token
     const ModelW& rw = models_[kReward];
-    forward_packed(rw, ws, ws.a[2], M, n, nt, false, s_score_[1]);
+    forward_packed(rw, ws, ws.a[2], M, n, nt, false, s_rw);
     fpk::add_norm(ws.a[2].x, nullptr, 0, 0, rw.lnf, nullptr, M, rw.dims.d, ws.gather_last, n, rw.vhead, ws.score,
-                  s_score_[1]);
-    for (int k = 0; k < 2; ++k) {
+                  s_rw);
+    for (int k = 0; k < 2 && !yield; ++k) {
       FP_CUDA(cudaEventRecord(ev_join_[k], s_score_[k]));
       FP_CUDA(cudaStreamWaitEvent(st, ev_join_[k], 0));
     }

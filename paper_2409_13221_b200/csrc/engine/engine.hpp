@@ -149,7 +149,9 @@ class Engine {
   // Scores items in chunks of <= max_infer_tokens rows (three frozen models),
   // post-processes, and scatters the experience into the device arrays below
   // at each sample's global response offset (set_layout).
-  void infer(const std::vector<InferItem>& items, float beta, float gamma, float lam);
+  // yield: this GPU is still decoding — one stream, one-tile-per-CTA kernels
+  // (the decode step's CTAs get SMs between scoring tiles).
+  void infer(const std::vector<InferItem>& items, float beta, float gamma, float lam, bool yield = false);
 
   // Global response layout: resp_off[n+1]; (re)allocates the experience arrays.
   void set_layout(const std::vector<int64_t>& resp_off);

@@ -653,7 +653,7 @@ ExecResult execute(GpuEngine* ge, const std::vector<GenSample>& batch, const Gen
       events.push_back(bt.b);
       events.push_back(bt.e);
       FP_CUDA(cudaEventRecord(bt.b, si));
-      E.infer(items, opts.kl_beta, opts.gamma, opts.lam);
+      E.infer(items, opts.kl_beta, opts.gamma, opts.lam, /*yield=*/fused && !gen_done_me);
       FP_CUDA(cudaEventRecord(bt.e, si));
       inflight.push_back(bt);
     }

@@ -465,7 +465,9 @@ void launch_prefill(const bf16* q, const bf16* k, const bf16* v, int H, int KVH,
   const CUtensorMap mv = chain_operand_map(v, M, KVH * HD, kBN);
   const float scale = kLog2e / sqrtf(static_cast<float>(HD));
   const int n_items = n_tiles * H;
-  const int grid = std::min(n_items, 2 * sm_count());  // two CTAs per SM (TMEM 2 x <= 256 cols, ~113 KB smem)
+  // two CTAs per SM (TMEM 2 x 256 cols, <= 113 KB smem); one item per CTA
+  // when the packed kernels must leave room for a decode step (set_packed_persistent)
+  const int grid = packed_persistent() ? std::min(n_items, 2 * sm_count()) : n_items;
   attn_prefill_kernel<HD><<<grid, kThreads, C::kSmem, st>>>(mq, mk, mv, H, KVH, n_items, cu, tiles, scale, out,
                                                              g_prefill_trace);
   count_launch();

@@ -155,6 +155,7 @@ int sm_count() {
 // Packed forwards (prefill / scoring) from this many rows on take the
 // persistent kernel (gemm_persist.cuh); decode batches (<= 512 rows) never do.
 constexpr int kPersistMinRows = 1024;
+thread_local bool g_persist = true;
 
 template <int BN, class Epi>
 void launch_persist(const void* A, int a_rows, const void* B, int b_rows, int K, const Epi& epi, cudaStream_t st) {
@@ -236,6 +237,9 @@ void dispatch_bn(int M, int a_ctas, F&& f) {
 
 }  // namespace
 
+void set_packed_persistent(bool on) { g_persist = on; }
+bool packed_persistent() { return g_persist; }
+
 CUtensorMap make_kv_map(const void* pool, long long rows, int hd) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(hd), static_cast<cuuint64_t>(rows)};
@@ -299,7 +303,7 @@ int gemm_splits(int N, int K) {
 
 void gemm_bf16(const bf16* W, int N, int K, const bf16* X, int M, bf16* out, int ld_out, cudaStream_t st) {
   if ((ld_out * 2) % 16) throw std::invalid_argument("gemm_bf16: ld_out must be a multiple of 8");
-  if (M >= kPersistMinRows) {
+  if (M >= kPersistMinRows && g_persist) {
     EpiStoreBF16 e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, ld_out, 128, 256)};
     launch_persist<256>(W, N, X, M, K, e, st);
     return;
@@ -333,7 +337,7 @@ void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* o
 
 void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float* resid, cudaStream_t st) {
   if (N % 4) throw std::invalid_argument("gemm_f32: N must be a multiple of 4");
-  if (M >= kPersistMinRows) {
+  if (M >= kPersistMinRows && g_persist) {
     EpiStoreF32 e{out_map_2d(resid, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, N, N, 128, 128), 1};
     launch_persist<128>(W, N, X, M, K, e, st);
     return;
@@ -360,7 +364,7 @@ void gemm_swiglu_decode(const bf16* Wgu, int F, int K, const bf16* X, int M, bf1
 
 void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
   if (F % 64) throw std::invalid_argument("gemm_swiglu: F must be a multiple of 64");
-  if (M >= kPersistMinRows) {
+  if (M >= kPersistMinRows && g_persist) {
     EpiSwiGLU<256> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, 256)};
     launch_persist<256>(Wgu, 2 * F, X, M, K, e, st);
     return;
@@ -394,7 +398,7 @@ void gemm_qkv_rope_packed(const bf16* Wqkv, int K, const bf16* X, int M, int H, 
                           bf16* k_out, bf16* v_out, cudaStream_t st) {
   if (128 % hd != 0) throw std::invalid_argument("gemm_qkv_rope: head_dim must divide 128");
   const int N = (H + 2 * KVH) * hd;
-  if (M >= kPersistMinRows) {
+  if (M >= kPersistMinRows && g_persist) {
     EpiRopeKV<256> e{q_out, pool ? *pool : KvPoolView{}, slot, pos, cs, layer, H, KVH, hd, M};
     e.pool.kv_map = nullptr;
     e.k_out = k_out;

@@ -19,6 +19,13 @@ void count_launch();
 void count_launches(long long n);  // graph replays: the kernels the graph holds
 long long launch_count();
 
+// Packed forwards (M >= 1024 rows) take the persistent GEMM / attention
+// kernels, which hold every SM for their whole duration. While the same GPU
+// is still decoding, scoring turns this off (calling thread only) so its
+// one-tile-per-CTA kernels leave room for the decode step's CTAs.
+void set_packed_persistent(bool on);
+bool packed_persistent();
+
 // ---- GEMMs (tcgen05; gemm.cu) --------------------------------------------------
 // swap-AB: out[m][n] = sum_k X[m][k] W[n][k]; W [N, K], X [M, K], K % 64 == 0.
 void gemm_bf16(const bf16* W, int N, int K, const bf16* X, int M, bf16* out, int ld_out, cudaStream_t st);
