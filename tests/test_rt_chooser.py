@@ -1,7 +1,7 @@
 """The sharing-aware R_t chooser (tools/rt_chooser.py): fitted
 on a committed 1-GPU step profile, its predicted fused / stage-barrier gain at
 2 GPUs is within 5 % of the gain the bench measured on B200s (committed
-profiles/r02_bench_*_2gpu.json, R_t = 20 %), where the reference's own
+profiles/r02_bench_*_2gpu.json, at the R_t the chooser picked), where the reference's own
 sweep_threshold on the calibrated CostModel is 9-23 % off."""
 import json
 import sys
