@@ -218,7 +218,7 @@ def run_reference(args, world, rank):
 
 def chooser_ratio(w, G):
     """R_t / n picked by tools/rt_chooser.py (committed fit of measured B200 steps), else 0.2."""
-    key = {"gpt2s": "gpt2s", "1.3b": "13b"}.get(w.name)
+    key = {"gpt2s": "gpt2s", "1.3b": "13b", "8b": "8b"}.get(w.name)
     p = ROOT / "profiles" / f"r02_rt_chooser_{key}.json"
     if key and p.exists():
         g = json.loads(p.read_text())["G"].get(str(G))
