@@ -338,8 +338,13 @@ void gemm_f32_splitk(const bf16* W, int N, int K, const bf16* X, int M, float* o
 void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float* resid, cudaStream_t st) {
   if (N % 4) throw std::invalid_argument("gemm_f32: N must be a multiple of 4");
   if (M >= kPersistMinRows && g_persist) {
-    EpiStoreF32 e{out_map_2d(resid, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, N, N, 128, 128), 1};
-    launch_persist<128>(W, N, X, M, K, e, st);
+    // 256-token tiles (more bytes per flop, 4-stage ring) when there are
+    // enough of them to keep the 148 SMs evenly loaded, else 128 (6 stages)
+    const long long tiles256 = static_cast<long long>((N + 127) / 128) * ((M + 255) / 256);
+    if (tiles256 >= 4 * sm_count())
+      launch_persist<256>(W, N, X, M, K, EpiResidDirect{resid, N, M}, st);
+    else
+      launch_persist<128>(W, N, X, M, K, EpiResidDirect{resid, N, M}, st);
     return;
   }
   dispatch_bn<EpiStoreF32>(M, (N + 127) / 128, [&]<int BN>() {
@@ -365,8 +370,12 @@ void gemm_swiglu_decode(const bf16* Wgu, int F, int K, const bf16* X, int M, bf1
 void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
   if (F % 64) throw std::invalid_argument("gemm_swiglu: F must be a multiple of 64");
   if (M >= kPersistMinRows && g_persist) {
-    EpiSwiGLU<256> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, 256)};
-    launch_persist<256>(Wgu, 2 * F, X, M, K, e, st);
+    if (K >= 2048) {  // long mainloops: the deeper ring pays; short ones are epilogue-bound (TMA store)
+      launch_persist<256>(Wgu, 2 * F, X, M, K, EpiSwiGLUDirect<256>{out, F, M}, st);
+    } else {
+      EpiSwiGLU<256> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, 256)};
+      launch_persist<256>(Wgu, 2 * F, X, M, K, e, st);
+    }
     return;
   }
   dispatch_bn<int>(M, (2 * F + 127) / 128, [&]<int BN>() {

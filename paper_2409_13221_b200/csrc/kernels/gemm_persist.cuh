@@ -33,7 +33,88 @@ struct EpiStaging<BN, EpiSwiGLU<BN>> {
   static constexpr int v = EpiSwiGLU<BN>::kTileBytes + 2 * 32 * 128 * 4;  // tile + gate/up exchange
 };
 
-constexpr int kPersistSmem = 224 * 1024;
+// Residual add without staging: resid[m][n] += D[n][m] straight from the
+// accumulator registers. Each element belongs to exactly one tile (no split-K),
+// so a plain load-add-store gives the bits of the TMA reduce-add (one fp32 add,
+// round to nearest) — and the staging smem goes to a deeper TMA ring: the
+// small-K scoring GEMMs are bound by the operand bytes a CTA keeps in flight.
+// A warp covers 32 consecutive features of one token per access (128 B).
+struct EpiResidDirect {
+  float* resid;
+  int N, M;
+  static constexpr bool kTmaStore = false;
+  static constexpr int kPasses = 1;
+  template <class S> __device__ void next_pass(S&, int, int, int, int) const {}
+  struct State {};
+  __device__ void operator()(State&, uint8_t*, int a0, int b0, int, int r, int, int c0, const float (&v)[32]) const {
+    const int n = a0 + r;
+    const int m0 = b0 + c0;
+    if (n >= N || m0 >= M) return;
+    float* p = resid + static_cast<size_t>(m0) * N + n;
+    const int cnt = min(32, M - m0);
+    float old[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < cnt) old[j] = p[static_cast<size_t>(j) * N];
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < cnt) p[static_cast<size_t>(j) * N] = old[j] + v[j];
+  }
+  __device__ void finish(State&, int, int, int, int, int) const {}
+  __device__ void store(const uint8_t*, int, int, int) const {}
+};
+template <int BN>
+struct EpiStaging<BN, EpiResidDirect> {
+  static constexpr int v = 0;
+};
+
+// SwiGLU with the same gate/up pairing and arithmetic as EpiSwiGLU (so the
+// same bits) but the outputs go straight to global memory: per store a warp
+// writes 32 consecutive features of one token (64 B). Only the gate/up
+// exchange buffer stays in shared memory, which leaves room for a 4-stage ring
+// at BN = 256.
+template <int BN>
+struct EpiSwiGLUDirect {
+  __nv_bfloat16* out;
+  int F, M;
+  static constexpr bool kTmaStore = false;
+  static constexpr int kPasses = 1;
+  template <class S> __device__ void next_pass(S&, int, int, int, int) const {}
+  struct State {};
+  __device__ void operator()(State&, uint8_t* smem, int a0, int b0, int, int r, int half, int c0,
+                             const float (&v)[32]) const {
+    float* xch = reinterpret_cast<float*>(smem) + half * 32 * 128;  // [32][128]
+    const uint32_t xa = smem_u32(xch) + r * 4;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) sts_f32(xa + j * 512, v[j]);
+    half_bar_sync(half);
+    const int t = r;
+    const int f = t & 63, j0 = (t >> 6) * 16;
+    if (c0 < BN) {
+      float gte[16], up[16];
+      const uint32_t xr = smem_u32(xch) + (j0 * 128 + f) * 4;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        gte[j] = lds_f32(xr + j * 512);
+        up[j] = lds_f32(xr + j * 512 + 256);
+      }
+      const int m0 = b0 + c0 + j0;
+      __nv_bfloat16* o = out + static_cast<size_t>(m0) * F + a0 / 2 + f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (m0 + j < M) o[static_cast<size_t>(j) * F] = f2bf(__fdividef(gte[j], 1.0f + __expf(-gte[j])) * up[j]);
+    }
+    half_bar_sync(half);
+  }
+  __device__ void finish(State&, int, int, int, int, int) const {}
+  __device__ void store(const uint8_t*, int, int, int) const {}
+};
+template <int BN>
+struct EpiStaging<BN, EpiSwiGLUDirect<BN>> {
+  static constexpr int v = 2 * 32 * 128 * 4;  // gate/up exchange only
+};
+
+constexpr int kPersistSmem = 227 * 1024;
 
 template <int BN, class Epi>
 struct PersistCfg {
