@@ -608,11 +608,6 @@ int Engine::bucket_of(int B) {
   return ((B + 127) / 128) * 128;
 }
 
-// One decode step. Rows are padded to a batch-size bucket (padding rows decode
-// a dummy token into the scratch slot / page / history row) so that the whole
-// step — ~10 kernels per layer with PDL edges — replays as one CUDA graph per
-// (bucket, mode, temperature, seed): host launch cost and inter-kernel gaps
-// vanish. The probe mode (per-launch CUDA events) runs the step eagerly.
 // Host row table of one decode group, padded to Bb rows (padding rows decode a
 // dummy token into the scratch slot / page / history row): [7][Bb] columns +
 // the attention work-item table. Returns the ints to upload.
@@ -642,12 +637,10 @@ size_t Engine::build_rows(const DecodeRow* rows, int B, int Bb, std::vector<int>
 
 // One decode step. Rows are padded to a batch-size bucket so that the whole
 // step — ~7 kernels per layer with PDL edges — replays as one CUDA graph per
-// (bucket, mode, temperature, seed): host launch cost and inter-kernel gaps
-// vanish. Large batches are cut into two halves that run as two dependent-
-// kernel chains on two streams in the same graph (the rows are independent and
-// every kernel is batch-independent, so the bits do not change): one half's
-// latency-bound GEMM chain overlaps the other half's bandwidth-bound attention,
-// which is capped to part of the SMs. The probe mode (per-launch CUDA events)
+// (bucket, mode, temperature, seed, top-k, top-p): host launch cost and
+// inter-kernel gaps vanish. (Cutting large batches into two halves on two
+// graph branches, so one half's GEMM chain overlaps the other's attention,
+// measured no faster and was removed.) The probe mode (per-launch CUDA events)
 // and the traced step run eagerly.
 void Engine::decode(const std::vector<DecodeRow>& rows, int mode, float inv_temp, uint64_t sample_seed, int top_k,
                     float top_p) {
