@@ -184,7 +184,7 @@ int fp_k_gemm_f32_residual(const void* W, int32_t N, int32_t K, const void* X, i
 /* Debug: record 8 globaltimer stamps per CTA of subsequent GEMMs into buf (device, NULL disables). */
 int fp_k_gemm_trace(void* buf);
 int fp_k_gemm_swiglu(const void* Wgu, int32_t F, int32_t K, const void* X, int32_t M, void* out, void* stream);
-/* The decode-step SwiGLU GEMM (lean rings, cluster split-K over K for small M). */
+/* The decode-step SwiGLU GEMM (lean shared-memory rings for small M, so the next GEMM's CTAs co-reside under PDL). */
 int fp_k_gemm_swiglu_decode(const void* Wgu, int32_t F, int32_t K, const void* X, int32_t M, void* out,
                             void* stream);
 /* Decode QKV projection with RoPE and the KV append fused (one kernel):
