@@ -175,6 +175,7 @@ void launch_persist(const void* A, int a_rows, const void* B, int b_rows, int K,
   g.k_blocks = K / kBK;
   g.a_tiles = (a_rows + 127) / 128;
   g.n_tiles = g.a_tiles * ((b_rows + BN - 1) / BN);
+  g.trace = g_trace;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(std::min(g.n_tiles, sm_count()));
   cfg.blockDim = dim3(kGemmThreads);

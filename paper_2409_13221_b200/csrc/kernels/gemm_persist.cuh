@@ -130,7 +130,16 @@ struct PersistCfg {
 
 struct PersistGeom {
   int a_rows, b_rows, k_blocks, a_tiles, n_tiles;
+  unsigned long long* trace;  // debug (fp_k_gemm_trace): per CTA, per local tile i < 8: 4 globaltimer stamps
 };
+
+__device__ __forceinline__ void persist_stamp(const PersistGeom& g, int i, int k) {
+  if (g.trace && i < 8) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g.trace[(blockIdx.x * 8 + i) * 4 + k] = t;
+  }
+}
 
 template <int BN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -202,6 +211,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % C::kStages;
           mbar_wait(&full_bar[s], (it / C::kStages) & 1);
+          if (kb == 0) persist_stamp(g, i, 0);
           tc_fence_after();
           const uint64_t off = static_cast<uint64_t>((s * C::kStageBytes) >> 4);
 #pragma unroll
@@ -210,6 +220,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tc_commit(&empty_bar[s]);
         }
         tc_commit(&acc_full[buf]);
+        persist_stamp(g, i, 1);
       }
     }
     __syncwarp();
@@ -225,6 +236,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       typename Epi::State st{};
       if constexpr (EpiHasPrologue<Epi>::value) epi.prologue(st, a_row0, b_row0, staging + EpiStaging<BN, Epi>::v);
       mbar_wait(&acc_full[buf], (i >> 1) & 1);
+      if (threadIdx.x == 64) persist_stamp(g, i, 2);
       tc_fence_after();
       const uint32_t acc = tmem + buf * C::kAccCols + (static_cast<uint32_t>(quarter * 32) << 16);
 #pragma unroll 1
@@ -254,6 +266,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       epi_bar_sync();  // staging reusable: the store has read it / finish() is done with it
+      if (threadIdx.x == 64) persist_stamp(g, i, 3);
     }
     if constexpr (EpiHasPost<Epi>::value) epi.post();
   }
