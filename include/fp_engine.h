@@ -244,6 +244,9 @@ int fp_k_attn_decode_ws(const void* q, int32_t B, int32_t H, int32_t KVH, int32_
  * hd 64 / 128: tcgen05 kernel; other head sizes: mma.sync kernel. */
 int fp_k_attn_varlen(const void* q, const void* k, const void* v, int32_t H, int32_t KVH, int32_t hd,
                      const int32_t* cu_host, const int32_t* cu_dev, int32_t n_seq, void* out, void* stream);
+/* Packed-forward kernel policy of the calling thread: 1 (default) persistent GEMM / attention
+ * kernels from 1024 rows, 0 one-tile-per-CTA kernels (what scoring uses while its GPU decodes). */
+int fp_k_set_packed_persistent(int on);
 /* Debug: record CTA 0's event times of subsequent tcgen05 varlen launches into buf (8 x 64 u64, device). */
 int fp_k_attn_prefill_trace(void* buf);
 /* The mma.sync kernel for any supported head size (cross-check of the tcgen05 kernel). */

@@ -706,6 +706,10 @@ int attn_varlen_call(const void* q, const void* k, const void* v, int H, int KVH
 }
 }  // namespace
 
+int fp_k_set_packed_persistent(int on) {
+  return guarded([&] { fpk::set_packed_persistent(on != 0); });
+}
+
 int fp_k_attn_prefill_trace(void* buf) {
   return guarded([&] { fpk::attn_prefill_set_trace(static_cast<unsigned long long*>(buf)); });
 }

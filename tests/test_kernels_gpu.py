@@ -301,6 +301,54 @@ def test_attn_prefill_tcgen05(lib, hd, H, KVH, lens, grow):
     assert torch.equal(one, out[a:b])
 
 
+@pytest.mark.parametrize("hd,H,KVH,lens", [(64, 12, 12, [300, 955, 17, 128, 4]), (128, 32, 8, [1300, 700, 129])])
+def test_attn_prefill_yield_mode_identical(lib, hd, H, KVH, lens):
+    """Scoring on a GPU that still decodes launches one item per CTA instead of the
+    persistent grid (fp_k_set_packed_persistent(0)): same bits."""
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    M = int(cu[-1])
+    q = torch.randn(M, H, hd, device="cuda").to(torch.bfloat16)
+    k = torch.randn(M, KVH, hd, device="cuda").to(torch.bfloat16)
+    v = torch.randn(M, KVH, hd, device="cuda").to(torch.bfloat16)
+    cu_d = torch.from_numpy(cu).cuda()
+    cu_h = cu.ctypes.data_as(C.POINTER(C.c_int32))
+    outs = []
+    for on in (1, 0):
+        ok(lib, lib.fp_k_set_packed_persistent(on))
+        o = torch.full((M, H, hd), float("nan"), device="cuda", dtype=torch.bfloat16)
+        ok(lib, lib.fp_k_attn_varlen(ptr(q), ptr(k), ptr(v), H, KVH, hd, cu_h, ptr(cu_d), len(lens), ptr(o), stream()))
+        outs.append(o)
+    ok(lib, lib.fp_k_set_packed_persistent(1))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("kind,N,K", [("resid", 768, 768), ("resid", 4096, 4096), ("swiglu", 6144, 768),
+                                      ("swiglu", 4096, 2048), ("bf16", 2304, 768)])
+def test_gemm_yield_mode_identical(lib, kind, N, K):
+    """M >= 1024: persistent kernel vs the one-tile-per-CTA kernel at the same M — same bits."""
+    M = 2500
+    W = rand_bf16(N, K, scale=K ** -0.5, seed=41)
+    X = rand_bf16(M, K, seed=42)
+    outs = []
+    r0 = torch.randn(M, N, device="cuda")
+    for on in (1, 0):
+        ok(lib, lib.fp_k_set_packed_persistent(on))
+        if kind == "resid":
+            o = r0.clone()
+            ok(lib, lib.fp_k_gemm_f32_residual(ptr(W), N, K, ptr(X), M, ptr(o), stream()))
+        elif kind == "swiglu":
+            o = torch.full((M, N // 2), float("nan"), device="cuda", dtype=torch.bfloat16)
+            ok(lib, lib.fp_k_gemm_swiglu(ptr(W), N // 2, K, ptr(X), M, ptr(o), stream()))
+        else:
+            o = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+            ok(lib, lib.fp_k_gemm_bf16(ptr(W), N, K, ptr(X), M, ptr(o), N, stream()))
+        outs.append(o)
+    ok(lib, lib.fp_k_set_packed_persistent(1))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+
+
 def test_postprocess_matches_c_oracle(lib):
     import ctypes
 
