@@ -247,6 +247,9 @@ int fp_k_attn_varlen(const void* q, const void* k, const void* v, int32_t H, int
 /* Packed-forward kernel policy of the calling thread: 1 (default) persistent GEMM / attention
  * kernels from 1024 rows, 0 one-tile-per-CTA kernels (what scoring uses while its GPU decodes). */
 int fp_k_set_packed_persistent(int on);
+/* Packed GEMMs on SM pairs (tcgen05 cta_group::2, 256 x 256 tiles) for the calling thread:
+ * -1 (default) when the tiles spread evenly, 0 never, 1 always. Same bits either way. */
+int fp_k_set_pair_gemm(int mode);
 /* Debug: record CTA 0's event times of subsequent tcgen05 varlen launches into buf (8 x 64 u64, device). */
 int fp_k_attn_prefill_trace(void* buf);
 /* The mma.sync kernel for any supported head size (cross-check of the tcgen05 kernel). */

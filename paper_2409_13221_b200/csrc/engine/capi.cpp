@@ -710,6 +710,10 @@ int fp_k_set_packed_persistent(int on) {
   return guarded([&] { fpk::set_packed_persistent(on != 0); });
 }
 
+int fp_k_set_pair_gemm(int mode) {
+  return guarded([&] { fpk::set_pair_gemm(mode); });
+}
+
 int fp_k_attn_prefill_trace(void* buf) {
   return guarded([&] { fpk::attn_prefill_set_trace(static_cast<unsigned long long*>(buf)); });
 }

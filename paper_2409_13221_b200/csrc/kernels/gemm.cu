@@ -12,6 +12,7 @@
 #include "gemm.cuh"
 #include "launch.cuh"
 #include "ops.h"
+#include "gemm_pair.cuh"
 #include "gemm_persist.cuh"
 #include "vocab.cuh"
 
@@ -191,6 +192,56 @@ void launch_persist(const void* A, int a_rows, const void* B, int b_rows, int K,
   fpk::count_launch();
 }
 
+// The SM-pair kernel (gemm_pair.cuh): 256 x 256 tiles, cluster of two CTAs.
+template <class Epi>
+void launch_pair(const void* A, int a_rows, const void* B, int b_rows, int K, const Epi& epi, cudaStream_t st) {
+  using C = PairCfg<Epi>;
+  if (K % kBK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
+  if (a_rows <= 0 || b_rows <= 0) return;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tc_gemm_pair_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    cudaFuncSetAttribute(tc_gemm_pair_kernel<Epi>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    attr_set = true;
+  }
+  const CUtensorMap ma = make_map(A, a_rows, K, 128);
+  const CUtensorMap mb = make_map(B, b_rows, K, 128);
+  PersistGeom g;
+  g.a_rows = a_rows;
+  g.b_rows = b_rows;
+  g.k_blocks = K / kBK;
+  g.a_tiles = (a_rows + 255) / 256;
+  g.n_tiles = g.a_tiles * ((b_rows + 255) / 256);
+  g.trace = g_trace;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * std::min(g.n_tiles, sm_count() / 2));
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_pair_kernel<Epi>, ma, mb, g, epi);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("gemm pair launch: ") + cudaGetErrorString(e));
+  fpk::count_launch();
+}
+
+// SM pairs for the packed GEMMs when their 256 x 256 tiles still spread
+// evenly (>= 3 per pair; fewer, e.g. gpt2s' N = 768 projections, lose more to
+// the last round than the pairs gain); set_pair_gemm forces either kernel.
+thread_local int g_pair = -1;  // -1 auto, 0 one-SM, 1 pairs
+bool use_pair(int N, int M) {
+  if (g_pair >= 0) return g_pair == 1;
+  const long long tiles = static_cast<long long>((N + 255) / 256) * ((M + 255) / 256);
+  return tiles >= 3 * (sm_count() / 2);
+}
+
 // Batch-tile width of a swap-AB GEMM with `a_ctas` weight tiles (x splits):
 // the fewest waves over the 148 SMs, then the narrowest tile (most CTAs
 // streaming weights in that wave), never wider than the rows need. A CTA's
@@ -239,6 +290,7 @@ void dispatch_bn(int M, int a_ctas, F&& f) {
 }  // namespace
 
 void set_packed_persistent(bool on) { g_persist = on; }
+void set_pair_gemm(int mode) { g_pair = mode < 0 ? -1 : (mode ? 1 : 0); }
 bool packed_persistent() { return g_persist; }
 
 CUtensorMap make_kv_map(const void* pool, long long rows, int hd) {
@@ -306,7 +358,10 @@ void gemm_bf16(const bf16* W, int N, int K, const bf16* X, int M, bf16* out, int
   if ((ld_out * 2) % 16) throw std::invalid_argument("gemm_bf16: ld_out must be a multiple of 8");
   if (M >= kPersistMinRows && g_persist) {
     EpiStoreBF16 e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, ld_out, 128, 256)};
-    launch_persist<256>(W, N, X, M, K, e, st);
+    if (use_pair(N, M))
+      launch_pair(W, N, X, M, K, e, st);
+    else
+      launch_persist<256>(W, N, X, M, K, e, st);
     return;
   }
   dispatch_bn<EpiStoreBF16>(M, (N + 127) / 128, [&]<int BN>() {
@@ -341,6 +396,10 @@ void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float*
   if (M >= kPersistMinRows && g_persist) {
     // 256-token tiles (more bytes per flop, 4-stage ring) when there are
     // enough of them to keep the 148 SMs evenly loaded, else 128 (6 stages)
+    if (use_pair(N, M)) {
+      launch_pair(W, N, X, M, K, EpiResidDirect{resid, N, M}, st);
+      return;
+    }
     const long long tiles256 = static_cast<long long>((N + 127) / 128) * ((M + 255) / 256);
     if (tiles256 >= 4 * sm_count())
       launch_persist<256>(W, N, X, M, K, EpiResidDirect{resid, N, M}, st);
@@ -371,6 +430,15 @@ void gemm_swiglu_decode(const bf16* Wgu, int F, int K, const bf16* X, int M, bf1
 void gemm_swiglu(const bf16* Wgu, int F, int K, const bf16* X, int M, bf16* out, cudaStream_t st) {
   if (F % 64) throw std::invalid_argument("gemm_swiglu: F must be a multiple of 64");
   if (M >= kPersistMinRows && g_persist) {
+    if (use_pair(2 * F, M)) {
+      if (K >= 2048) {
+        launch_pair(Wgu, 2 * F, X, M, K, EpiSwiGLUDirect<256>{out, F, M}, st);
+      } else {
+        EpiSwiGLU<256> e{out_map_2d(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, F, F, 64, 256)};
+        launch_pair(Wgu, 2 * F, X, M, K, e, st);
+      }
+      return;
+    }
     if (K >= 2048) {  // long mainloops: the deeper ring pays; short ones are epilogue-bound (TMA store)
       launch_persist<256>(Wgu, 2 * F, X, M, K, EpiSwiGLUDirect<256>{out, F, M}, st);
     } else {
@@ -414,7 +482,10 @@ void gemm_qkv_rope_packed(const bf16* Wqkv, int K, const bf16* X, int M, int H, 
     e.k_out = k_out;
     e.v_out = v_out;
     e.use_pool = pool != nullptr;
-    launch_persist<256>(Wqkv, N, X, M, K, e, st);
+    if (use_pair(N, M))
+      launch_pair(Wqkv, N, X, M, K, e, st);
+    else
+      launch_persist<256>(Wqkv, N, X, M, K, e, st);
     return;
   }
   dispatch_bn<int>(M, (N + 127) / 128, [&]<int BN>() {

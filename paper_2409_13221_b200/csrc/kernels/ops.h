@@ -25,6 +25,7 @@ long long launch_count();
 // one-tile-per-CTA kernels leave room for the decode step's CTAs.
 void set_packed_persistent(bool on);
 bool packed_persistent();
+void set_pair_gemm(int mode);  // packed GEMMs on SM pairs (cta_group::2): -1 auto (default), 0 never, 1 always
 
 // ---- GEMMs (tcgen05; gemm.cu) --------------------------------------------------
 // swap-AB: out[m][n] = sum_k X[m][k] W[n][k]; W [N, K], X [M, K], K % 64 == 0.

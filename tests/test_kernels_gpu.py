@@ -301,6 +301,35 @@ def test_attn_prefill_tcgen05(lib, hd, H, KVH, lens, grow):
     assert torch.equal(one, out[a:b])
 
 
+@pytest.mark.parametrize("kind,N,K", [("resid", 768, 768), ("resid", 2048, 5632), ("resid", 4096, 4096),
+                                      ("swiglu", 6144, 768), ("swiglu", 11264, 2048), ("bf16", 2304, 768),
+                                      ("bf16", 6144, 2048)])
+@pytest.mark.parametrize("M", [1024, 3001, 8192])
+def test_gemm_pair_matches_one_sm(lib, kind, N, K, M):
+    """SM-pair kernel (tcgen05 cta_group::2, gemm_pair.cuh) vs the one-SM persistent kernel: same bits,
+    including partial 256-row weight / token tiles."""
+    W = rand_bf16(N, K, scale=K ** -0.5, seed=51)
+    X = rand_bf16(M, K, seed=52)
+    r0 = torch.randn(M, N, device="cuda")
+    outs = []
+    for mode in (0, 1):
+        ok(lib, lib.fp_k_set_pair_gemm(mode))
+        if kind == "resid":
+            o = r0.clone()
+            ok(lib, lib.fp_k_gemm_f32_residual(ptr(W), N, K, ptr(X), M, ptr(o), stream()))
+        elif kind == "swiglu":
+            o = torch.full((M, N // 2), float("nan"), device="cuda", dtype=torch.bfloat16)
+            ok(lib, lib.fp_k_gemm_swiglu(ptr(W), N // 2, K, ptr(X), M, ptr(o), stream()))
+        else:
+            o = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+            ok(lib, lib.fp_k_gemm_bf16(ptr(W), N, K, ptr(X), M, ptr(o), N, stream()))
+        outs.append(o)
+    ok(lib, lib.fp_k_set_pair_gemm(-1))
+    torch.cuda.synchronize()
+    assert not torch.isnan(outs[1].float()).any()
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("hd,H,KVH,lens", [(64, 12, 12, [300, 955, 17, 128, 4]), (128, 32, 8, [1300, 700, 129])])
 def test_attn_prefill_yield_mode_identical(lib, hd, H, KVH, lens):
     """Scoring on a GPU that still decodes launches one item per CTA instead of the
