@@ -193,25 +193,24 @@ void launch_persist(const void* A, int a_rows, const void* B, int b_rows, int K,
 }
 
 // The SM-pair kernel (gemm_pair.cuh): 256 x 256 tiles, cluster of two CTAs.
-template <class Epi>
+template <int BN = 256, class Epi>
 void launch_pair(const void* A, int a_rows, const void* B, int b_rows, int K, const Epi& epi, cudaStream_t st) {
-  using C = PairCfg<Epi>;
+  using C = PairCfg<Epi, BN>;
   if (K % kBK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
   if (a_rows <= 0 || b_rows <= 0) return;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tc_gemm_pair_kernel<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    cudaFuncSetAttribute(tc_gemm_pair_kernel<Epi>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    cudaFuncSetAttribute(tc_gemm_pair_kernel<Epi, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
     attr_set = true;
   }
   const CUtensorMap ma = make_map(A, a_rows, K, 128);
-  const CUtensorMap mb = make_map(B, b_rows, K, 128);
+  const CUtensorMap mb = make_map(B, b_rows, K, BN / 2);
   PersistGeom g;
   g.a_rows = a_rows;
   g.b_rows = b_rows;
   g.k_blocks = K / kBK;
   g.a_tiles = (a_rows + 255) / 256;
-  g.n_tiles = g.a_tiles * ((b_rows + 255) / 256);
+  g.n_tiles = g.a_tiles * ((b_rows + BN - 1) / BN);
   g.trace = g_trace;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * std::min(g.n_tiles, sm_count() / 2));
@@ -227,7 +226,7 @@ void launch_pair(const void* A, int a_rows, const void* B, int b_rows, int K, co
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_pair_kernel<Epi>, ma, mb, g, epi);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_pair_kernel<Epi, BN>, ma, mb, g, epi);
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm pair launch: ") + cudaGetErrorString(e));
   fpk::count_launch();
 }
@@ -397,7 +396,11 @@ void gemm_f32_residual(const bf16* W, int N, int K, const bf16* X, int M, float*
     // 256-token tiles (more bytes per flop, 4-stage ring) when there are
     // enough of them to keep the 148 SMs evenly loaded, else 128 (6 stages)
     if (use_pair(N, M)) {
-      launch_pair(W, N, X, M, K, EpiResidDirect{resid, N, M}, st);
+      launch_pair<256>(W, N, X, M, K, EpiResidDirect{resid, N, M}, st);
+      return;
+    }
+    if (g_pair < 0 && K >= 2048) {  // few 256 x 256 tiles (N = 768) but a long mainloop: 256 x 128 pair tiles
+      launch_pair<128>(W, N, X, M, K, EpiResidDirect{resid, N, M}, st);
       return;
     }
     const long long tiles256 = static_cast<long long>((N + 127) / 128) * ((M + 255) / 256);

@@ -74,24 +74,25 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
-template <class Epi>
+template <class Epi, int BN_ = 256>
 struct PairCfg {
-  static constexpr int BN = 256;                            // MMA N (tokens per pair tile)
-  static constexpr int kStageBytes = kTileA + 128 * kBK * 2;  // this CTA's A half + B half
+  static constexpr int BN = BN_;                             // MMA N (tokens per pair tile)
+  static constexpr int kStageBytes = kTileA + (BN / 2) * kBK * 2;  // this CTA's A half + B half
   static constexpr int kStaging = EpiStaging<BN, Epi>::v + EpiSmemExtra<Epi>::value;
   static constexpr int kStages = (kPersistSmem - 1024 - kStaging - 256) / kStageBytes;
   static constexpr int kSmem = kStages * kStageBytes + kStaging + 1024 + 256;
-  static constexpr uint32_t kAccCols = 256;
-  static constexpr uint32_t kTmemCols = 512;
+  static constexpr uint32_t kAccCols = BN;
+  static constexpr uint32_t kTmemCols = 2 * BN;
   static_assert(kStages >= 2, "pair GEMM: ring too shallow");
 };
 
-// Tiles: a_tiles = ceil(a_rows / 256) weight-row pairs, tokens in 256s.
-template <class Epi>
+// Tiles: a_tiles = ceil(a_rows / 256) weight-row pairs, tokens in BNs.
+template <class Epi, int BN_ = 256>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                         const PersistGeom g, const __grid_constant__ Epi epi) {
-  using C = PairCfg<Epi>;
+  using C = PairCfg<Epi, BN_>;
+  constexpr int BN = C::BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* staging = smem + C::kStages * C::kStageBytes;
@@ -131,7 +132,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int it = 0;
       bool waited = false;
       for (int t = pair; t < g.n_tiles; t += n_pairs) {
-        const int a_row0 = (t % g.a_tiles) * 256 + 128 * rank, b_row0 = (t / g.a_tiles) * 256 + 128 * rank;
+        const int a_row0 = (t % g.a_tiles) * 256 + 128 * rank, b_row0 = (t / g.a_tiles) * BN + (BN / 2) * rank;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % C::kStages;
           mbar_wait(&empty_bar[s], ((it / C::kStages) & 1) ^ 1);
@@ -149,7 +150,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else if (warp == 1) {
     if (rank == 0 && elect_one()) {
-      constexpr uint32_t idesc = idesc_bf16(256, C::BN);
+      constexpr uint32_t idesc = idesc_bf16(256, BN);
       const uint64_t da = sdesc_k128(smem_u32(smem)), db = sdesc_k128(smem_u32(smem) + kTileA);
       int it = 0, i = 0;
       for (int t = pair; t < g.n_tiles; t += n_pairs, ++i) {
@@ -180,10 +181,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     pdl_wait();
     int i = 0;
     for (int t = pair; t < g.n_tiles; t += n_pairs, ++i) {
-      const int a_row0 = (t % g.a_tiles) * 256 + 128 * rank, b_row0 = (t / g.a_tiles) * 256;
+      const int a_row0 = (t % g.a_tiles) * 256 + 128 * rank, b_row0 = (t / g.a_tiles) * BN;
       const int buf = i & 1;
       typename Epi::State st{};
-      if constexpr (EpiHasPrologue<Epi>::value) epi.prologue(st, a_row0, b_row0, staging + EpiStaging<256, Epi>::v);
+      if constexpr (EpiHasPrologue<Epi>::value) epi.prologue(st, a_row0, b_row0, staging + EpiStaging<BN, Epi>::v);
       mbar_wait(&acc_full[buf], (i >> 1) & 1);
       if (threadIdx.x == 64) persist_stamp(g, i, 2);
       tc_fence_after();
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       for (int pass = 0; pass < Epi::kPasses; ++pass) {
         if (pass) epi.next_pass(st, a_row0, b_row0, r, half);
 #pragma unroll 1
-        for (int c0 = 32 * half; c0 < C::BN; c0 += 64) {
+        for (int c0 = 32 * half; c0 < BN; c0 += 64) {
           float v[32];
           tmem_ld32(acc + c0, v);
           epi(st, staging, a_row0, b_row0, 0, r, half, c0, v);

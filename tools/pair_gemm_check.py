@@ -1,4 +1,5 @@
-"""SM-pair (cta_group::2) packed GEMM vs the one-SM persistent kernel: bits and time.
+"""SM-pair (cta_group::2) packed GEMM vs the one-SM persistent kernel vs the automatic
+choice (fp_k_set_pair_gemm 0 / 1 / -1): bits and time.
 
     python tools/pair_gemm_check.py [gpt2s|1.3b|8b]
 """
@@ -36,7 +37,7 @@ def main():
         Xk = X[:, :K].contiguous()
         r0 = torch.randn(M, N, device="cuda")
         outs, ts = [], []
-        for pair in (0, 1):
+        for pair in (0, 1, -1):
             lib.fp_k_set_pair_gemm(pair)
             if "resid" in kind:
                 o = r0.clone()
@@ -55,8 +56,11 @@ def main():
         same = torch.equal(outs[0], outs[1])
         diff = (outs[0].float() - outs[1].float()).abs().max().item()
         fl = 2 * M * N * K
+        extra = ""
+        if len(ts) > 2:
+            extra = f", auto {ts[2]:.1f} us (same bits {torch.equal(outs[0], outs[2])})"
         print(f"{name} {kind} M={M} N={N} K={K}: one-SM {ts[0]:.1f} us ({fl / ts[0] / 1e6:.0f} TF/s), "
-              f"pair {ts[1]:.1f} us ({fl / ts[1] / 1e6:.0f} TF/s); bit-identical {same} (max |diff| {diff:.3g})")
+              f"pair {ts[1]:.1f} us ({fl / ts[1] / 1e6:.0f} TF/s){extra}; bit-identical {same} (max |diff| {diff:.3g})")
 
 
 if __name__ == "__main__":
