@@ -330,6 +330,24 @@ def test_gemm_pair_matches_one_sm(lib, kind, N, K, M):
     assert torch.equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("M", [256, 300, 512])
+def test_swiglu_decode_pair_batch_independent(lib, M):
+    """8B-shape decode SwiGLU: large batches take the SM-pair kernel, small ones the tiled kernel — a row's
+    bits must not depend on the batch it decodes in."""
+    F, K = 14336, 4096
+    Wgu, X, ref = _swiglu_case(F, K, M, 61)
+    full = torch.full((M, F), float("nan"), device="cuda", dtype=torch.bfloat16)
+    part = torch.full_like(full, float("nan"))
+    ok(lib, lib.fp_k_gemm_swiglu_decode(ptr(Wgu), F, K, ptr(X), M, ptr(full), stream()))
+    for a in range(0, M, 64):
+        b = min(M, a + 64)
+        ok(lib, lib.fp_k_gemm_swiglu_decode(ptr(Wgu), F, K, ptr(X[a:b]), b - a, ptr(part[a:b]), stream()))
+    torch.cuda.synchronize()
+    err = (full.float() - ref).abs().max().item()
+    assert err <= 2e-2 * max(1.0, ref.abs().max().item()), err
+    assert torch.equal(full, part)
+
+
 @pytest.mark.parametrize("hd,H,KVH,lens", [(64, 12, 12, [300, 955, 17, 128, 4]), (128, 32, 8, [1300, 700, 129])])
 def test_attn_prefill_yield_mode_identical(lib, hd, H, KVH, lens):
     """Scoring on a GPU that still decodes launches one item per CTA instead of the
