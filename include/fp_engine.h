@@ -250,6 +250,9 @@ int fp_k_set_packed_persistent(int on);
 /* Packed GEMMs on SM pairs (tcgen05 cta_group::2, 256 x 256 tiles) for the calling thread:
  * -1 (default) when the tiles spread evenly, 0 never, 1 always. Same bits either way. */
 int fp_k_set_pair_gemm(int mode);
+/* Decode-attention work table (fp_k_attn_items) for the calling thread: 0 (default) whole 512-token
+ * splits, 1 cut into 128-token sub-chunks, -1 cut only for small wide-kernel batches. Same bits. */
+int fp_k_set_attn_cut(int mode);
 /* Debug: record CTA 0's event times of subsequent tcgen05 varlen launches into buf (8 x 64 u64, device). */
 int fp_k_attn_prefill_trace(void* buf);
 /* The mma.sync kernel for any supported head size (cross-check of the tcgen05 kernel). */

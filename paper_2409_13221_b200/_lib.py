@@ -211,6 +211,7 @@ ENGINE_SYMBOLS = {
     "fp_k_attn_prefill_trace": (C.c_int, [_vp]),
     "fp_k_set_packed_persistent": (C.c_int, [C.c_int]),
     "fp_k_set_pair_gemm": (C.c_int, [C.c_int]),
+    "fp_k_set_attn_cut": (C.c_int, [C.c_int]),
     "fp_k_attn_varlen_mma": (C.c_int, [_vp, _vp, _vp, C.c_int32, C.c_int32, C.c_int32, _i32p, _vp, C.c_int32,
                                        _vp, _vp]),
     "fp_k_postprocess": (C.c_int, [C.c_int32, _vp, _vp, _vp, _vp, _vp, C.c_float, C.c_float, C.c_float, _vp, _vp,

@@ -710,6 +710,10 @@ int fp_k_set_packed_persistent(int on) {
   return guarded([&] { fpk::set_packed_persistent(on != 0); });
 }
 
+int fp_k_set_attn_cut(int mode) {
+  return guarded([&] { fpk::set_attn_cut(mode); });
+}
+
 int fp_k_set_pair_gemm(int mode) {
   return guarded([&] { fpk::set_pair_gemm(mode); });
 }

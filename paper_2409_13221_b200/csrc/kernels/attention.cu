@@ -441,20 +441,40 @@ void launch_decode(const bf16* q, int B, int H, int KVH, const KvPoolView& pool,
 
 }  // namespace
 
+namespace {
+thread_local int g_attn_cut = 0;  // 0 never (default), 1 always, -1 the small-batch rule below (warp-per-item kernels)
+}
+void set_attn_cut(int mode) { g_attn_cut = mode < 0 ? -1 : (mode ? 1 : 0); }  // fp_k_set_attn_cut
+
 int attn_decode_items(const int* ctx, int B, int KVH, int hd, int G, int* items) {
-  // One item per (sample, 512-token split); splits are not cut into 128-token
-  // sub-chunks (measured slower on gpt2s: the parked sub-partial and its
-  // ticket cost more than the balance gained). Longest first: counting sort
-  // by 32-token units, ties by (sample, split).
-  (void)KVH, (void)hd, (void)G;
+  // One item per (sample, 512-token split), longest first (counting sort by
+  // 32-token units, ties by (sample, split, sub)). Cutting splits into
+  // 128-token sub-chunks (partials folded in order: the same bits) is a policy
+  // (set_attn_cut): isolated, the wide kernel gains at small batches (gpt2s
+  // B 48 / 96: 18.5 / 24.6 vs 26.6 / 26.6 us) and the deep kernel loses (8B
+  // B 16-64: 1.2-1.8x slower); in the bench the rule below (cut when the whole
+  // splits cannot give every wide-kernel warp an item) measured 549.0 vs 554.2
+  // samples/s, so the default is never. The team kernel never takes cuts.
   constexpr int kU = kDecodeChunk / 32;  // units per split
+  constexpr int kSubU = 4;               // units per sub-chunk (attn_decode.cu kSubUnits)
+  int warps = 0;
+  const int v = attn_decode_variant(B, KVH, hd, G, &warps);
+  int pairs = 0;
+  for (int b = 0; b < B; ++b) pairs += (ctx[b] + kDecodeChunk - 1) / kDecodeChunk;
+  const bool cut = v != 2 && (g_attn_cut == 1 || (g_attn_cut < 0 && v == 0 && pairs * KVH < 148 * warps));
   int n = 0;
   for (int u = kU; u >= 1; --u)
     for (int b = 0; b < B; ++b) {
       const int ns = (ctx[b] + kDecodeChunk - 1) / kDecodeChunk;
       for (int s = 0; s < ns; ++s) {
         const int len = std::min(ctx[b], (s + 1) * kDecodeChunk) - s * kDecodeChunk;
-        if ((len + 31) / 32 == u) items[1 + n++] = b << 11 | s << 3 | 7;
+        const int units = (len + 31) / 32;
+        if (!cut || units <= kSubU) {
+          if (units == u) items[1 + n++] = b << 11 | s << 3 | 7;
+        } else {
+          for (int c = 0; c * kSubU < units; ++c)
+            if (std::min(kSubU, units - c * kSubU) == u) items[1 + n++] = b << 11 | s << 3 | c;
+        }
       }
     }
   items[0] = n;

@@ -244,10 +244,12 @@ inline int attn_decode_counters(int B, int KVH, int max_ctx) {
 int attn_decode_variant(int B, int KVH, int hd, int G, int* warps);
 // Host: the item table from the contexts: items[0] = n, items[1..n] =
 // b << 11 | split << 3 | sub (sub 7: the whole split), longest first (an LPT
-// order for the dynamic schedule); ties by (b, split, sub). Splits longer than
-// the mean work per warp are cut into sub-chunks when the wide kernel runs.
+// order for the dynamic schedule); ties by (b, split, sub). Splits are cut
+// into 128-token sub-chunks only under set_attn_cut (default never); same bits
+// either way.
 // Capacity: 1 + B * ceil(max_ctx / 128) ints.
 int attn_decode_items(const int* ctx, int B, int KVH, int hd, int G, int* items);
+void set_attn_cut(int mode);  // calling thread: 0 never cut (default), 1 always, -1 small-batch rule
 void rope_qkv(const bf16* qkv, int M, int H, int KVH, int hd, const int* pos, float rope_theta, bf16* q_out,
               bf16* k_out, bf16* v_out, const KvPoolView* pool, int layer, const int* slot, cudaStream_t st);
 

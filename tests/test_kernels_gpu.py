@@ -218,6 +218,34 @@ def test_attn_decode(lib, hd, H, KVH, ctx_list, tma):
         assert err < 2e-2, (b, err)
 
 
+@pytest.mark.parametrize("hd,H,KVH", [(64, 12, 12), (128, 32, 8), (128, 16, 16), (64, 32, 4)])
+@pytest.mark.parametrize("ctx_list", [[3000, 17, 2500, 700], [1, 63, 64, 65, 300, 1200],
+                                      list(range(100, 100 + 97 * 40, 97))])
+def test_attn_decode_cut_splits_identical(lib, hd, H, KVH, ctx_list):
+    """Decode attention with 512-token splits cut into 128-token sub-chunks (small batches) gives the same
+    bits as whole splits (sub-chunk partials folded in order)."""
+    L, layer, PT = 3, 1, 64
+    B = len(ctx_list)
+    maxp = (max(ctx_list) + PT - 1) // PT
+    npages = B * maxp + 1
+    pool = (torch.randn(npages, L, KVH, 2, PT, hd, device="cuda") * 0.5).to(torch.bfloat16)
+    bt = (torch.randperm(npages - 1, device="cuda").to(torch.int32) + 1)[: B * maxp].view(B, maxp).contiguous()
+    slot = torch.arange(B, device="cuda", dtype=torch.int32)
+    ctx = torch.tensor(ctx_list, device="cuda", dtype=torch.int32)
+    q = torch.randn(B, H, hd, device="cuda").to(torch.bfloat16)
+    outs = []
+    for mode in (0, 1):
+        ok(lib, lib.fp_k_set_attn_cut(mode))
+        o = torch.full((B, H, hd), float("nan"), device="cuda", dtype=torch.bfloat16)
+        ok(lib, lib.fp_k_attn_decode(ptr(q), B, H, KVH, hd, ptr(pool), npages, L, layer, ptr(bt), maxp, ptr(slot),
+                                     ptr(ctx), max(ctx_list), ptr(o), stream()))
+        outs.append(o)
+    ok(lib, lib.fp_k_set_attn_cut(0))
+    torch.cuda.synchronize()
+    assert not torch.isnan(outs[1].float()).any()
+    assert torch.equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("hd,H,KVH", [(64, 12, 12), (128, 16, 4), (32, 8, 8)])
 def test_attn_varlen(lib, hd, H, KVH):
     lens = [1, 63, 64, 65, 200, 7]

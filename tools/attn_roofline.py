@@ -1,4 +1,5 @@
-"""Decode-attention roofline on a bench-shaped launch (gpt2s: H = KVH = 12, hd 64).
+"""Decode-attention roofline on a bench-shaped launch (gpt2s: H = KVH = 12, hd 64;
+ATTN_SHAPE=8b: H 32, KVH 8, hd 128).
 
     python tools/attn_roofline.py [B] [mean_ctx]        # CUDA-event timing, L2 flushed per launch
     ncu --set full -k regex:attn_decode_mma -s 5 -c 1 python tools/attn_roofline.py ...
@@ -19,10 +20,13 @@ from paper_2409_13221_b200 import _lib  # noqa: E402
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 mean_ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 380
 import os
-H, KVH, hd, PT = 12, 12, 64, 64
+# ATTN_SHAPE=8b: Llama-3-8B's GQA 32 / 8 heads of 128 (default: gpt2s MHA 12 x 64)
+H, KVH, hd, PT = (32, 8, 128, 64) if os.environ.get("ATTN_SHAPE") == "8b" else (12, 12, 64, 64)
 L = int(os.environ.get("ATTN_L", "12"))  # layers per page (page bytes scale with L)
 layer = min(5, L - 1)
 lib = _lib.load()
+if os.environ.get("ATTN_CUT") is not None:  # 0 whole splits (default), 1 128-token sub-chunks, -1 rule
+    lib.fp_k_set_attn_cut(int(os.environ["ATTN_CUT"]))
 g = torch.Generator().manual_seed(5)
 ctx = (torch.rand(B, generator=g) * 2 * mean_ctx).clamp(min=1).to(torch.int32)  # uniform on [1, 2 mean)
 maxp = (int(ctx.max()) + PT - 1) // PT
