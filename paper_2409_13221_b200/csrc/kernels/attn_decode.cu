@@ -919,7 +919,11 @@ int attn_decode_variant(int B, int KVH, int hd, int G, int* warps) {
   const bool small = B * KVH * 4 <= 148 * wide_warps;
   int v = 0;
   if (hd == 64 && G == 1 && small) v = 2;
-  else if (small) v = 1;
+  // GQA at hd 128 (Llama-3-8B, 4 query heads per KV head): the wide shape wins
+  // once B * KVH > 40 (8B B 8 / 16 / 24, long contexts: 59 / 68 / 94 vs
+  // 74 / 78 / 100 us, ATTN_SHAPE=8b tools/attn_roofline.py); MHA at hd 128
+  // (1.3B) keeps the deep shape (29-31 vs 35 us at B 4-12).
+  else if (small && !(hd == 128 && G >= 4 && B * KVH > 40)) v = 1;
   if (warps) *warps = v == 2 ? 12 : v == 1 ? (hd == 64 ? DecCfg<64, 1>::kWarps : DecCfg<128, 1>::kWarps) : wide_warps;
   return v;
 }

@@ -1,5 +1,5 @@
 """Decode-attention roofline on a bench-shaped launch (gpt2s: H = KVH = 12, hd 64;
-ATTN_SHAPE=8b: H 32, KVH 8, hd 128).
+ATTN_SHAPE=8b: H 32, KVH 8, hd 128; 13b: H = KVH = 16, hd 128).
 
     python tools/attn_roofline.py [B] [mean_ctx]        # CUDA-event timing, L2 flushed per launch
     ncu --set full -k regex:attn_decode_mma -s 5 -c 1 python tools/attn_roofline.py ...
@@ -21,7 +21,7 @@ B = int(sys.argv[1]) if len(sys.argv) > 1 else 128
 mean_ctx = int(sys.argv[2]) if len(sys.argv) > 2 else 380
 import os
 # ATTN_SHAPE=8b: Llama-3-8B's GQA 32 / 8 heads of 128 (default: gpt2s MHA 12 x 64)
-H, KVH, hd, PT = (32, 8, 128, 64) if os.environ.get("ATTN_SHAPE") == "8b" else (12, 12, 64, 64)
+H, KVH, hd, PT = {"8b": (32, 8, 128, 64), "13b": (16, 16, 128, 64)}.get(os.environ.get("ATTN_SHAPE"), (12, 12, 64, 64))
 L = int(os.environ.get("ATTN_L", "12"))  # layers per page (page bytes scale with L)
 layer = min(5, L - 1)
 lib = _lib.load()
