@@ -159,7 +159,8 @@ constexpr int kPersistMinRows = 1024;
 thread_local bool g_persist = true;
 
 template <int BN, class Epi>
-void launch_persist(const void* A, int a_rows, const void* B, int b_rows, int K, const Epi& epi, cudaStream_t st) {
+void launch_persist(const void* A, int a_rows, const void* B, int b_rows, int K, const Epi& epi, cudaStream_t st,
+                    bool weight_is_a = true) {
   using C = PersistCfg<BN, Epi>;
   if (K % kBK != 0) throw std::invalid_argument("gemm: K must be a multiple of 64");
   if (a_rows <= 0 || b_rows <= 0) return;
@@ -176,6 +177,7 @@ void launch_persist(const void* A, int a_rows, const void* B, int b_rows, int K,
   g.k_blocks = K / kBK;
   g.a_tiles = (a_rows + 127) / 128;
   g.n_tiles = g.a_tiles * ((b_rows + BN - 1) / BN);
+  g.weight_is_a = weight_is_a ? 1 : 0;
   g.trace = g_trace;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(std::min(g.n_tiles, sm_count()));
@@ -211,6 +213,7 @@ void launch_pair(const void* A, int a_rows, const void* B, int b_rows, int K, co
   g.k_blocks = K / kBK;
   g.a_tiles = (a_rows + 255) / 256;
   g.n_tiles = g.a_tiles * ((b_rows + BN - 1) / BN);
+  g.weight_is_a = 1;
   g.trace = g_trace;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * std::min(g.n_tiles, sm_count() / 2));
@@ -528,7 +531,10 @@ void gemm_vocab(const bf16* X, int M, int K, const bf16* Whead, int V, int mode,
     e.n_tiles = vocab_tiles(V);
     e.seed_lo = static_cast<uint32_t>(seed);
     e.seed_hi = static_cast<uint32_t>(seed >> 32);
-    launch<kVocabBN>(X, M, Whead, V, K, 1, e, st, /*weight_is_a=*/false);
+    if (M >= kPersistMinRows && g_persist)  // scoring: the reference model's log-probs over thousands of rows
+      launch_persist<kVocabBN>(X, M, Whead, V, K, e, st, /*weight_is_a=*/false);
+    else
+      launch<kVocabBN>(X, M, Whead, V, K, 1, e, st, /*weight_is_a=*/false);
   };
   if (mode == kForced) go(EpiVocab<kForced>{});
   else if (mode == kGreedy) go(EpiVocab<kGreedy>{});

@@ -139,6 +139,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* sa = smem + s * C::kStageBytes;
           const uint32_t fb = peer0(&full_bar[s]);
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * C::kStageBytes);
+          if (!waited && !g.weight_is_a) {
+            pdl_wait();
+            waited = true;
+          }
           tma_load_2d_pair(sa, &map_a, fb, kb * kBK, a_row0);
           if (!waited) {
             pdl_wait();

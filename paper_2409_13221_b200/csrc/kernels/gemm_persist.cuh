@@ -16,6 +16,7 @@
 #pragma once
 
 #include "gemm.cuh"
+#include "vocab.cuh"
 
 namespace fpk {
 
@@ -65,6 +66,10 @@ struct EpiResidDirect {
 };
 template <int BN>
 struct EpiStaging<BN, EpiResidDirect> {
+  static constexpr int v = 0;
+};
+template <int BN, int MODE>
+struct EpiStaging<BN, EpiVocab<MODE>> {  // writes its partials straight to global memory
   static constexpr int v = 0;
 };
 
@@ -130,6 +135,7 @@ struct PersistCfg {
 
 struct PersistGeom {
   int a_rows, b_rows, k_blocks, a_tiles, n_tiles;
+  int weight_is_a;  // 1: A (prefetched before griddepcontrol.wait) is the weight; 0: B is
   unsigned long long* trace;  // debug (fp_k_gemm_trace): per CTA, per local tile i < 8: 4 globaltimer stamps
 };
 
@@ -189,9 +195,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&empty_bar[s], ((it / C::kStages) & 1) ^ 1);
           uint8_t* sa = smem + s * C::kStageBytes;
           mbar_arrive_expect_tx(&full_bar[s], C::kStageBytes);
-          tma_load_2d(sa, &map_a, &full_bar[s], kb * kBK, a_row0);  // weights: independent of the previous kernel
+          // the weight operand is independent of the previous kernel: it goes
+          // first, the activations after griddepcontrol.wait
+          if (!waited && !g.weight_is_a) {
+            pdl_wait();
+            waited = true;
+          }
+          tma_load_2d(sa, &map_a, &full_bar[s], kb * kBK, a_row0);
           if (!waited) {
-            pdl_wait();  // activations come from the previous kernel
+            pdl_wait();
             waited = true;
           }
           tma_load_2d(sa + kTileA, &map_b, &full_bar[s], kb * kBK, b_row0);

@@ -1,4 +1,4 @@
-"""One LM-head launch (fp_k_vocab) for ncu / timing: python tools/vocab_profile.py M mode(0 forced,1 greedy,2 sample)"""
+"""One LM-head launch (fp_k_vocab) for ncu / timing: python tools/vocab_profile.py M mode(0 forced,1 greedy,2 sample) [persistent 0|1]"""
 import ctypes as C
 import sys
 
@@ -11,6 +11,8 @@ M = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
 mode = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 V, K = 50257, 768
 lib = _lib.load()
+if len(sys.argv) > 3:  # 0: one tile per CTA instead of the persistent kernel (M >= 1024)
+    lib.fp_k_set_packed_persistent(int(sys.argv[3]))
 p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
 W = (torch.randn(V, K, device="cuda") * 0.05).to(torch.bfloat16)
 X = torch.randn(M, K, device="cuda").to(torch.bfloat16)
