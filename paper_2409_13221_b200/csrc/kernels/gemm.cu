@@ -531,7 +531,10 @@ void gemm_vocab(const bf16* X, int M, int K, const bf16* Whead, int V, int mode,
     e.n_tiles = vocab_tiles(V);
     e.seed_lo = static_cast<uint32_t>(seed);
     e.seed_hi = static_cast<uint32_t>(seed >> 32);
-    if (M >= kPersistMinRows && g_persist)  // scoring: the reference model's log-probs over thousands of rows
+    // persistent at every M: 197 vocab tiles (V 50257) on 148 SMs load-balance
+    // and stream through a 4-deep ring; the weight streams before
+    // griddepcontrol.wait
+    if (g_persist)
       launch_persist<kVocabBN>(X, M, Whead, V, K, e, st, /*weight_is_a=*/false);
     else
       launch<kVocabBN>(X, M, Whead, V, K, 1, e, st, /*weight_is_a=*/false);

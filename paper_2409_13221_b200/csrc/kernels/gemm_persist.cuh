@@ -186,28 +186,48 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (warp == 0) {
     if (elect_one()) {
-      int it = 0;  // ring position over the CTA's lifetime
-      bool waited = false;
-      for (int t = blockIdx.x; t < g.n_tiles; t += gridDim.x) {
-        const int a_row0 = (t % g.a_tiles) * 128, b_row0 = (t / g.a_tiles) * BN;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % C::kStages;
-          mbar_wait(&empty_bar[s], ((it / C::kStages) & 1) ^ 1);
-          uint8_t* sa = smem + s * C::kStageBytes;
-          mbar_arrive_expect_tx(&full_bar[s], C::kStageBytes);
-          // the weight operand is independent of the previous kernel: it goes
-          // first, the activations after griddepcontrol.wait
-          if (!waited && !g.weight_is_a) {
-            pdl_wait();
-            waited = true;
-          }
+      // ring position it -> (local tile it / nkb, k-block it % nkb). The weight
+      // operand does not depend on the previous kernel: the first kStages
+      // stages of it are issued before griddepcontrol.wait, the activations
+      // after it.
+      const int local_tiles = g.n_tiles > static_cast<int>(blockIdx.x)
+                                  ? (g.n_tiles - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+                                  : 0;
+      const int total = local_tiles * nkb;
+      const int pre = min(total, C::kStages);
+      auto rows_of = [&](int it, int& a_row0, int& b_row0) {
+        const int t = blockIdx.x + (it / nkb) * gridDim.x;
+        a_row0 = (t % g.a_tiles) * 128;
+        b_row0 = (t / g.a_tiles) * BN;
+      };
+      auto load_weight = [&](uint8_t* sa, int it, int a_row0, int b_row0) {
+        const int s = it % C::kStages, kb = it % nkb;
+        if (g.weight_is_a)
           tma_load_2d(sa, &map_a, &full_bar[s], kb * kBK, a_row0);
-          if (!waited) {
-            pdl_wait();
-            waited = true;
-          }
+        else
           tma_load_2d(sa + kTileA, &map_b, &full_bar[s], kb * kBK, b_row0);
+      };
+      for (int it = 0; it < pre; ++it) {
+        int a_row0, b_row0;
+        rows_of(it, a_row0, b_row0);
+        mbar_arrive_expect_tx(&full_bar[it], C::kStageBytes);
+        load_weight(smem + it * C::kStageBytes, it, a_row0, b_row0);
+      }
+      pdl_wait();
+      for (int it = 0; it < total; ++it) {
+        const int s = it % C::kStages, kb = it % nkb;
+        int a_row0, b_row0;
+        rows_of(it, a_row0, b_row0);
+        uint8_t* sa = smem + s * C::kStageBytes;
+        if (it >= pre) {
+          mbar_wait(&empty_bar[s], ((it / C::kStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full_bar[s], C::kStageBytes);
+          load_weight(sa, it, a_row0, b_row0);
         }
+        if (g.weight_is_a)
+          tma_load_2d(sa + kTileA, &map_b, &full_bar[s], kb * kBK, b_row0);
+        else
+          tma_load_2d(sa, &map_a, &full_bar[s], kb * kBK, a_row0);
       }
     }
   } else if (warp == 1) {

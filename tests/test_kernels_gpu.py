@@ -650,27 +650,33 @@ def test_vocab_bench_shapes(lib, M, V, K):
     assert torch.equal(tok.long()[clear], logits.argmax(-1)[clear])
 
 
-@pytest.mark.parametrize("M,V,K", [(1024, 50257, 768), (3001, 50257, 768), (1500, 32000, 2048),
+@pytest.mark.parametrize("M,V,K", [(1, 50257, 768), (37, 50257, 768), (284, 50257, 768), (1024, 50257, 768),
+                                   (3001, 50257, 768), (1500, 32000, 2048), (130, 128256, 4096),
                                    (1100, 128256, 4096)])
-def test_vocab_persistent_scoring_identical(lib, M, V, K):
-    """Scoring-sized forced log-probs (M >= 1024) run the persistent LM-head kernel; the
-    one-tile-per-CTA kernel (fp_k_set_packed_persistent(0)) gives the same bits, both match torch."""
+@pytest.mark.parametrize("mode", [0, 2])
+def test_vocab_persistent_identical(lib, M, V, K, mode):
+    """The LM head runs the persistent kernel (gemm_persist.cuh) at every M; the one-tile-per-CTA
+    kernel (fp_k_set_packed_persistent(0)) gives the same bits — forced log-probs and sampled
+    tokens — and forced log-probs match torch."""
     X = rand_bf16(M, K, seed=43)
     W = rand_bf16(V, K, scale=3 * K ** -0.5, seed=44)
     tgt = torch.randint(0, V, (M,), device="cuda", dtype=torch.int32)
+    sid = torch.arange(M, device="cuda", dtype=torch.int32) * 7 + 3
+    stp = torch.arange(M, device="cuda", dtype=torch.int32) % 11
     outs = []
     for on in (1, 0):
         ok(lib, lib.fp_k_set_packed_persistent(on))
         tok = torch.zeros(M, device="cuda", dtype=torch.int32)
         lp = torch.full((M,), float("nan"), device="cuda", dtype=torch.float32)
-        ok(lib, lib.fp_k_vocab(ptr(X), M, K, ptr(W), V, 0, 1.0, ptr(tgt), None, None, 0, ptr(tok), ptr(lp),
-                               stream()))
-        outs.append(lp)
+        ok(lib, lib.fp_k_vocab(ptr(X), M, K, ptr(W), V, mode, 1.0, ptr(tgt), ptr(sid), ptr(stp), 1234, ptr(tok),
+                               ptr(lp), stream()))
+        outs.append((tok, lp))
     ok(lib, lib.fp_k_set_packed_persistent(1))
     torch.cuda.synchronize()
-    assert torch.equal(outs[0], outs[1])
-    ref = torch.log_softmax(X.float() @ W.float().T, -1).gather(1, tgt.long()[:, None])[:, 0]
-    assert (outs[0] - ref).abs().max().item() < 2e-3
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    if mode == 0:
+        ref = torch.log_softmax(X.float() @ W.float().T, -1).gather(1, tgt.long()[:, None])[:, 0]
+        assert (outs[0][1] - ref).abs().max().item() < 2e-3
 
 
 @pytest.mark.parametrize("M", [1, 64, 300])
