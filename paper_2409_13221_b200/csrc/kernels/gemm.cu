@@ -573,7 +573,19 @@ __global__ void vocab_finalize_kernel(const VocabPartial* __restrict__ part, con
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
-  const VocabPartial* p = part + static_cast<size_t>(row) * n_tiles;
+  // the row's partials are contiguous: stage them in shared memory with
+  // independent coalesced 16-byte loads (n_tiles is even, so the row is a
+  // multiple of 48 bytes), then walk them there
+  extern __shared__ float4 fin_smem[];
+  const int n4 = n_tiles * static_cast<int>(sizeof(VocabPartial)) / 16;
+  float4* srow = fin_smem + static_cast<size_t>(threadIdx.x >> 5) * n4;
+  {
+    const float4* g4 = reinterpret_cast<const float4*>(part + static_cast<size_t>(row) * n_tiles);
+#pragma unroll 4
+    for (int i = lane; i < n4; i += 32) srow[i] = g4[i];
+  }
+  __syncwarp();
+  const VocabPartial* p = reinterpret_cast<const VocabPartial*>(srow);
   // lane l owns the contiguous half-tiles [t0, t1); the mass is summed in
   // that fixed order (per lane, then lane 0..31 sequentially) so the oracle
   // (model_oracle.sample_token) replays it bit-for-bit
@@ -668,8 +680,14 @@ void vocab_finalize(const void* part, const float* tgt_z, int M, int V, int mode
                     const int* sample_id, const int* step, uint64_t seed, int* token, float* logp, const int* dst,
                     int* out_tok, float* out_logp, const int* cur_idx, int* cur_tok, cudaStream_t st) {
   if (M <= 0) return;
-  const int warps = 8;
-  launch_pdl(vocab_finalize_kernel, dim3((M + warps - 1) / warps), dim3(warps * 32), 0, st,
+  const size_t row_bytes = static_cast<size_t>(vocab_tiles(V)) * sizeof(VocabPartial);
+  const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / row_bytes)));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(vocab_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  launch_pdl(vocab_finalize_kernel, dim3((M + warps - 1) / warps), dim3(warps * 32), warps * row_bytes, st,
              static_cast<const VocabPartial*>(part), tgt_z, M, vocab_tiles(V), mode, target, sample_id, step,
              static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32), token, logp, dst, out_tok, out_logp,
              cur_idx, cur_tok);

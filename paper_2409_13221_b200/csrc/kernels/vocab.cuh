@@ -41,6 +41,7 @@ struct VocabPartial {
   int idx;
   float pad0, pad1;
 };
+static_assert(sizeof(VocabPartial) == 24, "vocab_finalize stages a row of partials as 16-byte words");
 
 struct VocabRowInfo {
   const int* target;     // [rows] forced target id (kForced) or nullptr
