@@ -573,18 +573,21 @@ __global__ void vocab_finalize_kernel(const VocabPartial* __restrict__ part, con
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= M) return;
-  // the row's partials are contiguous: stage them in shared memory with
-  // independent coalesced 16-byte loads (n_tiles is even, so the row is a
-  // multiple of 48 bytes), then walk them there
+  // the row's partials are contiguous (n_tiles is even: a multiple of 48
+  // bytes): one bulk copy per row into shared memory, then walk them there
   extern __shared__ float4 fin_smem[];
-  const int n4 = n_tiles * static_cast<int>(sizeof(VocabPartial)) / 16;
-  float4* srow = fin_smem + static_cast<size_t>(threadIdx.x >> 5) * n4;
-  {
-    const float4* g4 = reinterpret_cast<const float4*>(part + static_cast<size_t>(row) * n_tiles);
-#pragma unroll 4
-    for (int i = lane; i < n4; i += 32) srow[i] = g4[i];
+  __shared__ __align__(8) uint64_t fin_bar[8];
+  const uint32_t row_bytes = static_cast<uint32_t>(n_tiles * sizeof(VocabPartial));
+  float4* srow = fin_smem + static_cast<size_t>(threadIdx.x >> 5) * (row_bytes / 16);
+  uint64_t* bar = &fin_bar[threadIdx.x >> 5];
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+    mbar_arrive_expect_tx(bar, row_bytes);
+    bulk_load(srow, part + static_cast<size_t>(row) * n_tiles, row_bytes, bar);
   }
   __syncwarp();
+  mbar_wait(bar, 0);
   const VocabPartial* p = reinterpret_cast<const VocabPartial*>(srow);
   // lane l owns the contiguous half-tiles [t0, t1); the mass is summed in
   // that fixed order (per lane, then lane 0..31 sequentially) so the oracle
@@ -681,7 +684,8 @@ void vocab_finalize(const void* part, const float* tgt_z, int M, int V, int mode
                     int* out_tok, float* out_logp, const int* cur_idx, int* cur_tok, cudaStream_t st) {
   if (M <= 0) return;
   const size_t row_bytes = static_cast<size_t>(vocab_tiles(V)) * sizeof(VocabPartial);
-  const int warps = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / row_bytes)));
+  // small batches (decode): one row per CTA, spread over the SMs
+  const int warps = M <= 2 * 148 ? 1 : static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / row_bytes)));
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(vocab_finalize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
