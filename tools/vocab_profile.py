@@ -9,7 +9,8 @@ from paper_2409_13221_b200 import _lib  # noqa: E402
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
 mode = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-V, K = 50257, 768
+import os  # noqa: E402
+V, K = map(int, os.environ.get("VOCAB_VK", "50257,768").split(","))
 lib = _lib.load()
 if len(sys.argv) > 3:  # 0: one tile per CTA instead of the persistent kernel (M >= 1024)
     lib.fp_k_set_packed_persistent(int(sys.argv[3]))
