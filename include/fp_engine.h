@@ -217,6 +217,10 @@ int fp_k_decode_chain(const void* Wo, const void* Wgu, const void* Wd, const voi
 int fp_k_vocab_filtered(const void* X, int32_t M, int32_t K, const void* W, int32_t V, float inv_temp, int32_t top_k,
                         float top_p, const int32_t* sample_id, const int32_t* step, uint64_t seed, int32_t* token,
                         float* logp, float* z_out, void* stream);
+/* Decode step head: x[m] = E[tokens[idx[m]]] (fp32) and y = RMSNorm(x) * gain in one launch
+ * (idx may be NULL: row m gathers tokens[m]); the bits of an embedding gather then fp_k_add_norm with nsplit 0. */
+int fp_k_embed_norm(const int32_t* tokens, const int32_t* idx, int32_t M, const void* E, int32_t d, float* x,
+                    const float* gain, void* y, void* stream);
 int fp_k_add_norm(float* x, const float* parts, int32_t nsplit, const float* gain, void* y, int32_t M, int32_t d,
                   void* stream);
 /* y = bf16(RMSNorm(x) * gain), warp-per-row kernel of the packed (prefill / scoring) forward. */

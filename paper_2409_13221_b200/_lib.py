@@ -198,6 +198,7 @@ ENGINE_SYMBOLS = {
     "fp_k_vocab_filtered": (C.c_int, [_vp, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_float, C.c_int32, C.c_float,
                                       _vp, _vp, C.c_uint64, _vp, _vp, _vp, _vp]),
     "fp_k_add_norm": (C.c_int, [_vp, _vp, C.c_int32, _vp, _vp, C.c_int32, C.c_int32, _vp]),
+    "fp_k_embed_norm": (C.c_int, [_vp, _vp, C.c_int32, _vp, C.c_int32, _vp, _vp, _vp, _vp]),
     "fp_k_rms_norm_rows": (C.c_int, [_vp, _vp, _vp, C.c_int32, C.c_int32, _vp]),
     "fp_k_attn_decode": (C.c_int, [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int32, C.c_int32,
                                    C.c_int32, _vp, C.c_int32, _vp, _vp, C.c_int32, _vp, _vp]),

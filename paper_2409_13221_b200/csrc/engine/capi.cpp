@@ -590,6 +590,14 @@ int fp_k_vocab_filtered(const void* X, int32_t M, int32_t K, const void* W, int3
   });
 }
 
+int fp_k_embed_norm(const int32_t* tokens, const int32_t* idx, int32_t M, const void* E, int32_t d, float* x,
+                    const float* gain, void* y, void* stream) {
+  return guarded([&] {
+    fpk::embed_norm(tokens, idx, M, static_cast<const bf16*>(E), d, x, gain, static_cast<bf16*>(y), S(stream));
+    after_launch();
+  });
+}
+
 int fp_k_add_norm(float* x, const float* parts, int32_t nsplit, const float* gain, void* y, int32_t M, int32_t d,
                   void* stream) {
   return guarded([&] {

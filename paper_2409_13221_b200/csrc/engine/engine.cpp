@@ -749,8 +749,7 @@ void Engine::decode_kernels(DecodeWs& dw, cudaStream_t st, int B, int max_ctx, i
   const int so = fpk::gemm_splits(D.d, D.H * D.hd);
   const int sd = fpk::gemm_splits(D.d, D.F);
 
-  fpk::embed(d_cur_tok_, slot, B, w.embed, D.d, dw.x, st);
-  fpk::add_norm(dw.x, nullptr, 0, stride, w.layers[0].ln1, dw.h, B, D.d, nullptr, 0, nullptr, nullptr, st);
+  fpk::embed_norm(d_cur_tok_, slot, B, w.embed, D.d, dw.x, w.layers[0].ln1, dw.h, st);
   fpk::gemm_qkv_rope(w.layers[0].wqkv, D.d, dw.h, B, D.H, D.KVH, D.hd, pos, rope_cs_, pv, 0, slot, dw.q, st);
   for (int l = 0; l < D.L; ++l) {
     const LayerW& L = w.layers[l];

@@ -148,6 +148,38 @@ __global__ void add_norm_kernel(float* __restrict__ x, const float* __restrict__
   }
 }
 
+// Decode step head: the embedding gather and the first layer's RMSNorm in one
+// launch — x = E[tok] (exact bf16 -> fp32) and y = RMSNorm(x) with
+// add_norm_kernel<0>'s thread mapping and reduction tree, so the same bits as
+// embed + add_norm.
+__global__ void embed_norm_kernel(const int* __restrict__ tok, const int* __restrict__ idx,
+                                  const bf16* __restrict__ E, int d, float* __restrict__ x,
+                                  const float* __restrict__ gain, bf16* __restrict__ y) {
+  pdl_trigger();  // let the next (PDL-launched) GEMM start its prologue / weight prefetch
+  __shared__ float red[32];
+  const int i = blockIdx.x;
+  const int j = threadIdx.x;
+  const bool on = j < (d >> 2);
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (on) {
+    const bf16* e = E + static_cast<size_t>(tok[idx ? idx[i] : i]) * d;
+    const uint2 w = reinterpret_cast<const uint2*>(e)[j];
+    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&w.x);
+    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&w.y);
+    v = make_float4(__bfloat162float(a.x), __bfloat162float(a.y), __bfloat162float(b.x), __bfloat162float(b.y));
+    reinterpret_cast<float4*>(x + static_cast<size_t>(i) * d)[j] = v;
+  }
+  float ss = sumsq4(v);
+  ss = block_sum(ss, red);
+  const float inv = rsqrtf(ss / d + kNormEps);
+  float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (on) g = reinterpret_cast<const float4*>(gain)[j];
+  if (on) {
+    uint2* yr = reinterpret_cast<uint2*>(y + static_cast<size_t>(i) * d);
+    yr[j] = norm_scale4(v, inv, g);
+  }
+}
+
 // Packed forward (prefill / scoring, thousands of rows): RMSNorm with one
 // warp per row and 8 rows per block — no block-wide reduction, V float4 of
 // the row per lane, all of them in flight at once. d = 128 V.
@@ -301,6 +333,15 @@ void init_gain(float* g, size_t n, uint64_t seed, uint64_t tag, cudaStream_t st)
 
 void init_bf16_gu(bf16* w, int F, int d, uint64_t seed, uint64_t tag, float scale, cudaStream_t st) {
   init_bf16_gu_kernel<<<grid_for(static_cast<size_t>(2) * F * d), 256, 0, st>>>(w, F, d, seed, tag, scale); fpk::count_launch();
+}
+
+void embed_norm(const int* tokens, const int* idx, int M, const bf16* E, int d, float* x, const float* gain, bf16* y,
+                cudaStream_t st) {
+  if (M <= 0) return;
+  if (d % 4 || d > 4096) throw std::invalid_argument("embed_norm: d must be a multiple of 4 and <= 4096");
+  // a plain launch, like embed(): the step's first kernel fully orders the step
+  embed_norm_kernel<<<M, ((d / 4 + 31) / 32) * 32, 0, st>>>(tokens, idx, E, d, x, gain, y);
+  fpk::count_launch();
 }
 
 void embed(const int* tokens, const int* idx, int M, const bf16* E, int d, float* x, cudaStream_t st) {

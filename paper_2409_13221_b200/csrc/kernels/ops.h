@@ -86,6 +86,9 @@ void init_gain(float* g, size_t n, uint64_t seed, uint64_t tag, cudaStream_t st)
 void init_bf16_gu(bf16* w, int F, int d, uint64_t seed, uint64_t tag, float scale, cudaStream_t st);
 // x[m] = E[tokens[idx ? idx[m] : m]] (fp32 residual stream).
 void embed(const int* tokens, const int* idx, int M, const bf16* E, int d, float* x, cudaStream_t st);
+// embed + the first RMSNorm in one launch (decode step head): same bits as embed then add_norm (no partials).
+void embed_norm(const int* tokens, const int* idx, int M, const bf16* E, int d, float* x, const float* gain, bf16* y,
+                cudaStream_t st);
 // Packed scoring batch: for sample j (global id sid[j], prompt P[j], response
 // R[j], rows [cu[j], cu[j+1])): tokens = prompt ++ response, pos = 0..T-1;
 // response-aligned outputs at [roff[j], roff[j] + R[j]): targets (response

@@ -168,6 +168,27 @@ def test_add_norm(lib):
     assert (y.float() - ref).abs().max().item() < 2e-2 * ref.abs().max().item()
 
 
+@pytest.mark.parametrize("M,d", [(1, 768), (37, 768), (300, 2048), (64, 4096), (5, 256)])
+def test_embed_norm_matches_embed_then_add_norm(lib, M, d):
+    """The decode step's fused embedding gather + first RMSNorm gives the bits of the gather followed by
+    add_norm (no partials): x exactly E[tok] in fp32, y bit-identical."""
+    V = 1000
+    E = rand_bf16(V, d, seed=47)
+    tokens = torch.randint(0, V, (2 * M,), device="cuda", dtype=torch.int32)
+    idx = torch.randperm(2 * M, device="cuda")[:M].to(torch.int32)
+    g = torch.rand(d, device="cuda") + 0.5
+    x = torch.full((M, d), float("nan"), device="cuda")
+    y = torch.zeros(M, d, device="cuda", dtype=torch.bfloat16)
+    ok(lib, lib.fp_k_embed_norm(ptr(tokens), ptr(idx), M, ptr(E), d, ptr(x), ptr(g), ptr(y), stream()))
+    x_ref = E[tokens[idx.long()].long()].float()
+    y_ref = torch.zeros_like(y)
+    x2 = x_ref.clone()
+    ok(lib, lib.fp_k_add_norm(ptr(x2), None, 0, ptr(g), ptr(y_ref), M, d, stream()))
+    torch.cuda.synchronize()
+    assert torch.equal(x, x_ref)
+    assert torch.equal(y, y_ref)
+
+
 @pytest.mark.parametrize("M,d", [(1, 768), (8191, 768), (37, 2048), (1000, 4096), (9, 256), (17, 512)])
 def test_rms_norm_rows(lib, M, d):
     """Warp-per-row RMSNorm of the packed forward vs fp32 torch (d 512: block-per-row fallback)."""
