@@ -265,13 +265,14 @@ int pick_bn(int M, int a_ctas) {
   return best;
 }
 
-// Decode GEMMs in a lean ring (<= ~110 KB of shared memory) so that the CTAs
-// of the next GEMM in the step fit on an SM beside the current one's: with
-// PDL they become resident early and stream their weights while the previous
-// kernels run; for M <= FUSEPLAN_DECODE_LEAN (default 128, 0 disables).
+// Decode GEMMs (M <= 128) in a lean ring (120-128 KB of shared memory) so that
+// the next kernels' CTAs fit on an SM beside the current one's: with PDL they
+// become resident early and stream their weights while the previous kernels
+// run. One stage deeper than the first cut (<= 110 KB) measured faster
+// (gpt2s bench 572.5 vs 563.1 samples/s, DESIGN 8.4).
 template <int BN>
 struct Lean {
-  static constexpr int v = BN <= 16 ? 6 : BN <= 32 ? 5 : BN <= 64 ? 4 : BN <= 128 ? 3 : 2;
+  static constexpr int v = BN <= 16 ? 7 : BN <= 32 ? 6 : BN <= 64 ? 5 : BN <= 128 ? 4 : 3;
 };
 bool lean(int M) { return M <= 128; }  // (large batches keep the deep ring: their mainloops are bandwidth-hungry)
 
@@ -349,7 +350,10 @@ int gemm_splits(int N, int K) {
   const int kb = K / kBK;
   const int tiles = (N + 127) / 128;
   int s = (2 * 148 + tiles - 1) / tiles;
-  s = std::min(s, 8);  // partial traffic (splits x M x N x 4 B) is read back by add_norm
+  // at most 4: the partials (splits x M x N x 4 B) are read back by add_norm,
+  // and fewer, longer K slices measured faster than 6-8 (gpt2s bench 567.9 vs
+  // 563.1 samples/s at cap 4 vs 8, DESIGN 8.4)
+  s = std::min(s, 4);
   s = std::min(s, kb);
   // Equalise the K range per split so that no split is empty.
   const int per = (kb + s - 1) / s;
