@@ -248,7 +248,7 @@ def main():
                          "without one); 'auto': the best ratio of the reference's sweep_threshold under the "
                          "calibrated CostModel")
     ap.add_argument("--token-mode", default="sample", choices=["forced", "greedy", "sample"])
-    ap.add_argument("--claim-tokens", type=int, default=8192)
+    ap.add_argument("--claim-tokens", type=int, default=12288)  # swept: 8192 580.2, 10240 581.6, 12288 584.1, 16384 570.2
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-barrier-arm", action="store_true")
     ap.add_argument("--workload", default="gpt2s", choices=sorted(PER_GPU),
